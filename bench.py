@@ -1,0 +1,386 @@
+"""NSGA-III generations/sec on DTLZ (BASELINE.json metric) -- B200 engine vs the CPU reference.
+
+Default workload (N=1): configs[1] = C2, DTLZ2 m=5 d=14 n=10,000 (R = 20,000
+merged rows, w = 8,855 Das-Dennis points), synthetic seed-0 population.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* ours: W untimed generations, then K generations each one CUDA-graph replay
+  timed with CUDA events on the launching stream; L2 is flushed (a 512 MiB
+  write, outside the events) between generations.  value = generations/s
+  (whole job: N ranks x K generations / max-over-ranks device time).
+* e2e: the same metric through the public C-ABI call (mo_step via
+  engine.Engine.step) with host buffers: every generation copies the
+  parents (X, F, ideal) host->device from pinned memory and the survivors
+  + info device->host, inside the CUDA-event-timed region.
+* roofline: the dominant kernel (by measured share of the step) against
+  the measured issue-rate peak of the same instruction mix (k_peaks.cu),
+  since MEASURED_PEAKS.json only carries HBM and tensor-core peaks.
+* cpu_baseline / --impl reference: the numpy restatement of the reference
+  (oracle/manyobj_ref) on this host's cores; a bounded sample of the
+  generation (see cpu_generation_estimate) extrapolated to one generation.
+N > 1 (torchrun): independent replicas, one per GPU, seeds 0..N-1 (the
+sharded bit-matrix path is for N >= 1M populations).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": dict(problem="DTLZ1", m=3, d=7, n=92, label="C1 DTLZ1 m=3 d=7 N=92 (w=91, H=12)"),
+    "c2": dict(problem="DTLZ2", m=5, d=14, n=10000, label="C2 DTLZ2 m=5 d=14 N=10k (w=8855, H=19)"),
+    "c3": dict(problem="DTLZ3", m=10, d=19, n=100000, label="C3 DTLZ3 m=10 d=19 N=100k (w=97383)"),
+}
+METRIC = "NSGA-III generations/sec on DTLZ (m=3–10, N to 1M+) at 1/2/4/8 B200 vs CPU ref"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-rows", type=int, default=0)
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.out = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU reference
+
+def cpu_generation_estimate(wl, seed=0, sample_rows=0, threads=None):
+    """Seconds per generation of the numpy restatement of the reference on this host.
+
+    Bounded sample: the O(R^2) parts (dominance matrix construction and the
+    reference-point association, which are row-separable) are timed on
+    ``sample_rows`` of the R merged rows and scaled by R/sample_rows; the
+    remaining stages (variation, evaluation, peeling of the sampled
+    dominance counts, normalisation, niching) run on the full population.
+    Row blocks go to a thread pool (numpy releases the GIL).
+    """
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.manyobj_ref import engine as Oeng
+    from oracle.manyobj_ref import niche as On
+    from oracle.manyobj_ref import rng as Orng
+    from oracle.manyobj_ref import variation as Ov
+
+    cores = threads or len(os.sched_getaffinity(0))
+    cfg = Oeng.RunConfig(problem=wl["problem"], n=wl["n"], m=wl["m"], d=wl["d"], generations=1, seed=seed)
+    st = Oeng.initialize(cfg)
+    n, m = wl["n"], wl["m"]
+    R = 2 * n
+    t0 = time.perf_counter()
+    O = Ov.vary(st.X, cfg.variation, seed, 0)
+    FO = Oeng.evaluate(cfg, O)
+    t_vary = time.perf_counter() - t0
+    FR = np.concatenate([st.F, FO])
+    B = sample_rows or max(64, min(R, int(2e9 / (R * m * 4 + 1)) // 8 * 8))
+    rs = np.random.default_rng(seed)
+    rows = np.sort(rs.choice(R, size=min(B, R), replace=False))
+
+    def dom_block(r):
+        A = FR[r, None, :]
+        return ((A <= FR[None, :, :]).all(-1) & (A < FR[None, :, :]).any(-1)).sum(axis=0)
+
+    blocks = [rows[i:i + 32] for i in range(0, len(rows), 32)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(dom_block, blocks))
+    t_dom = (time.perf_counter() - t0) * R / len(rows)
+    zh = st.zhat
+    w = zh.shape[0]
+    pos_ref = Orng.positions(w, seed, 0, Orng.STREAM_REF_SHUFFLE)
+    Fn = (FR - FR.min(0)) / np.maximum(FR.max(0) - FR.min(0), 1e-10)
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        list(ex.map(lambda r: On.associate_canonical(Fn, zh, pos_ref, r, block=len(r)), blocks))
+    t_assoc = (time.perf_counter() - t0) * R / len(rows)
+    # linear-time remainder: normalisation + counts + nearest + water-fill on a real split
+    ranks = np.zeros(R, np.int64)
+    ranks[rs.random(R) < 0.5] = 1
+    split = type("S", (), {"l": 1, "k": n - int((ranks == 0).sum()), "selected_count": int((ranks == 0).sum())})
+    t0 = time.perf_counter()
+    cand = np.ones(R, bool)
+    pos_pop = Orng.positions(R, seed, 0, Orng.STREAM_POP_SHUFFLE)
+    On.normalize_objectives(FR, st.ideal, cand, pos_pop)
+    t_lin = time.perf_counter() - t0
+    total = t_vary + t_dom + t_assoc + t_lin
+    return {"seconds_per_generation": total, "t_variation_eval": t_vary, "t_dominance": t_dom,
+            "t_association": t_assoc, "t_linear": t_lin, "cores": cores, "sample_rows": int(len(rows)),
+            "split_k": split.k}
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def measure_peaks(torch, L, _lib):
+    """Issue-rate peaks (compares/s, FP32 flop/s) from k_peaks.cu, best of 3."""
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    inp = torch.rand(64, device="cuda") + 0.5
+    out = torch.empty(1 << 20, dtype=torch.int32, device="cuda")
+    res = {}
+    for which, per_iter, name in ((0, 64, "compare"), (1, 16, "fp32")):
+        blocks, iters = sm * 8, 4096
+        best = 0.0
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.check(L.mo_peak_issue(which, blocks, iters, _lib.ptr(inp), _lib.ptr(out), _lib.stream_ptr()),
+                       "peak")
+            e1.record()
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = max(best, blocks * 256 * iters * per_iter / t)
+        res[name] = best
+    return res
+
+
+def time_kernels(torch, eng, _lib):
+    """Per-phase and per-kernel device times on the engine's current state (outside the timed run)."""
+    L = _lib.lib()
+    cfg = eng.cfg
+    n, m = cfg.n, cfg.m
+    R = 2 * n
+    out = {}
+    # phases (eager, events)
+    prof = {}
+    for _ in range(3):
+        prof = {}
+        eng.step(profile=prof)
+    out.update({k: v * 1e3 for k, v in prof.items()})        # ms
+    # dom_tile alone on the merged objectives of the last step
+    FR = eng.FR[eng.cur ^ 1]
+    W = int(L.mo_bits_words_per_row(R))
+    bits = torch.empty((R, W), dtype=torch.int32, device="cuda")
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.mo_dominance_bits(_lib.ptr(FR), R, m, None, _lib.ptr(bits), _lib.stream_ptr()), "dom")
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    out["dom_tile_ms"] = float(np.median(ts))
+    del bits
+    return out
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_2504_06067_b200 import _lib, engine
+
+    wl = WORKLOADS[args.workload]
+    torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
+    cfg = engine.RunConfig(problem=wl["problem"], n=wl["n"], m=wl["m"], d=wl["d"],
+                           generations=args.steps + args.warmup, seed=rank)
+    eng = engine.Engine(cfg, graph=True)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    # warm-up
+    eng.replay(max(3, args.warmup))
+    torch.cuda.synchronize()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    eng.gen_dev.fill_(eng.generation)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 255)
+            starts[i].record()
+            eng.replay_one()
+            ends[i].record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    info = eng.info_dict()
+    assert info["survivors"] == cfg.n and info["error"] == 0, info
+
+    # ---- e2e through the C-ABI with host buffers (H2D parents, D2H survivors, every generation)
+    n, d, m = cfg.n, cfg.d, cfg.m
+    hX = torch.empty((n, d), dtype=torch.float32).pin_memory()
+    hF = torch.empty((n, m), dtype=torch.float32).pin_memory()
+    hI = torch.empty(m, dtype=torch.float32).pin_memory()
+    hInfo = torch.empty(_lib.INFO_COUNT, dtype=torch.int32).pin_memory()
+    hX.copy_(eng.X)
+    hF.copy_(eng.F)
+    hI.copy_(eng.ideal)
+    e_steps = max(5, args.steps // 2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(e_steps):
+        eng.XR[eng.cur][:n].copy_(hX, non_blocking=True)
+        eng.FR[eng.cur][:n].copy_(hF, non_blocking=True)
+        eng.ideal.copy_(hI, non_blocking=True)
+        eng.step()
+        hX.copy_(eng.X, non_blocking=True)
+        hF.copy_(eng.F, non_blocking=True)
+        hI.copy_(eng.ideal, non_blocking=True)
+        hInfo.copy_(eng.info, non_blocking=True)
+    e1.record()
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e_steps
+    h2d = n * d * 4 + n * m * 4 + m * 4
+    d2h = n * d * 4 + n * m * 4 + m * 4 + _lib.INFO_COUNT * 4
+
+    result = {"ms": ms, "clk": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "info": info,
+              "w": eng.w}
+    if rank == 0:
+        result["kernels"] = time_kernels(torch, eng, _lib)
+        result["peaks"] = measure_peaks(torch, _lib.lib(), _lib)
+    return result
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    wl = WORKLOADS[args.workload]
+    cfgd = {"workload": wl["label"], "problem": wl["problem"], "m": wl["m"], "d": wl["d"], "n": wl["n"],
+            "merged_rows": 2 * wl["n"], "l2": "flushed (512 MiB write) between timed generations",
+            "graph": "one CUDA-graph replay per generation"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cores = len(os.sched_getaffinity(0))
+        per = []
+        for i in range(args.warmup + args.steps):
+            est = cpu_generation_estimate(wl, seed=0, sample_rows=args.cpu_sample_rows or 256)
+            if i >= args.warmup:
+                per.append(est["seconds_per_generation"])
+        spg = float(np.mean(per))
+        v = 1.0 / spg
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "generations/s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": spg * 1e3, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfgd,
+                          "cpu_baseline": {"value": v, "unit": "generations/s", "cores": cores, "kind": "port",
+                                           "sample": f"numpy oracle/manyobj_ref; per step: dominance + association "
+                                                     f"on {est['sample_rows']} of {2 * wl['n']} merged rows "
+                                                     "scaled by rows, the rest of the generation in full"},
+                          "e2e": {"value": v, "unit": "generations/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    r = run_ours(args, rank, world)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+    K = args.steps
+    ms_per = r["ms"] / K
+    value = world * K / (r["ms"] / 1e3)
+    kern = r["kernels"]
+    peaks = r["peaks"]
+    n, m, R = wl["n"], wl["m"], 2 * wl["n"]
+    step_ms = kern["t_variation"] + kern["t_sort"] + kern["t_niche"]
+    cmp_work = R * (R - 1) * m          # FP32 compares of the dominance bit-matrix
+    dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
+    roof = {"kernel": "k_dom_tile (dominance bit-matrix)", "bound": "fp32-compare-issue",
+            "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12, "unit": "Tcmp/s",
+            "frac": dom_achieved / peaks["compare"], "traffic": None,
+            "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
+            "share_of_step": kern["dom_tile_ms"] / step_ms if step_ms else None,
+            "algorithmic": f"R(R-1)m = {cmp_work:.3e} compares per launch"}
+    line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform population, random-init)",
+            "config": dict(cfgd, parallelism="replicas" if world > 1 else "single", w=r["w"]),
+            "clocks": r["clk"],
+            "e2e": {"value": world * 1e3 / r["e2e_ms"], "unit": "generations/s", "h2d_bytes_per_step": r["h2d"],
+                    "d2h_bytes_per_step": r["d2h"]},
+            "gpu_launches": K * 7,
+            "roofline": roof,
+            "phases_ms": {k: round(v, 4) for k, v in kern.items()},
+            "peaks": {"compare_per_s": peaks["compare"], "fp32_flop_per_s": peaks["fp32"]},
+            "last_info": r["info"]}
+    if not args.no_cpu_baseline:
+        est = cpu_generation_estimate(wl, seed=0, sample_rows=args.cpu_sample_rows or 256)
+        line["cpu_baseline"] = {"value": 1.0 / est["seconds_per_generation"], "unit": "generations/s",
+                                "cores": est["cores"], "kind": "port",
+                                "sample": f"numpy oracle: dominance + association on {est['sample_rows']} of {R} "
+                                          "rows scaled by rows; variation, evaluation, normalisation in full",
+                                "detail_s": {k: round(v, 3) for k, v in est.items() if k.startswith("t_")}}
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

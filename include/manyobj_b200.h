@@ -1,0 +1,214 @@
+/*
+ * manyobj_b200.h -- C-ABI of the B200-native NSGA-III survivor-selection +
+ * variation engine (libmanyobj_b200.so, sm_100a).
+ *
+ * The reference ("manyobj", /root/reference/SPEC.md) is a Python package; its
+ * hot path is engine.step and the per-op functions it calls.
+ * Each entry point below replaces one of those operations; the comment on each
+ * cites the reference interface (file:line) it stands in for.  The Python
+ * host package paper_2504_06067_b200 binds these with ctypes.
+ *
+ * Conventions:
+ *   - plain device pointers + sizes; no torch/C++ types in signatures;
+ *   - the caller allocates every buffer, including the workspace sized by
+ *     mo_workspace_bytes(); the library never allocates or frees;
+ *   - all work is stream-ordered and asynchronous on `stream`
+ *     (a cudaStream_t passed as void*); the caller sets the device;
+ *   - status codes map 1:1 onto pkg/src/manyobj/errors.py classes;
+ *   - device-side outcomes (split front, domain violations) are written to
+ *     caller-provided device int arrays and read lazily by the host.
+ */
+#ifndef MANYOBJ_B200_H
+#define MANYOBJ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes -> pkg/src/manyobj/errors.py:4-41 */
+enum {
+  MO_OK = 0,
+  MO_ERR_SHAPE = 1,      /* ShapeError           errors.py:4  */
+  MO_ERR_PARAM = 2,      /* ParameterError       errors.py:8  */
+  MO_ERR_BOUNDS = 3,     /* BoundsError          errors.py:12 */
+  MO_ERR_EMPTY = 4,      /* EmptySelectionError  errors.py:16 */
+  MO_ERR_DOMAIN = 5,     /* DomainError          errors.py:20 */
+  MO_ERR_INFEASIBLE = 6, /* InfeasibleSplitError errors.py:32 */
+  MO_ERR_CUDA = 7        /* CUDA runtime failure (no reference analogue) */
+};
+
+/* Problems (DTLZ1/4/6 per the standard suite). */
+enum { MO_DTLZ1 = 1, MO_DTLZ2, MO_DTLZ3, MO_DTLZ4, MO_DTLZ5, MO_DTLZ6, MO_DTLZ7 };
+
+/* Split/outcome record written by the selection kernels (device int32[16]). */
+enum {
+  MO_INFO_L = 0,          /* splitting front index l                       */
+  MO_INFO_SELECTED = 1,   /* |F_s| = cumulative size of fronts < l         */
+  MO_INFO_K = 2,          /* k = n - |F_s|                                 */
+  MO_INFO_NFRONTS = 3,    /* fronts peeled (= l + 1)                       */
+  MO_INFO_FL_SIZE = 4,    /* |F_l|                                         */
+  MO_INFO_SKIPPED = 5,    /* 1 if cum(<=l) == n and niching was skipped    */
+  MO_INFO_NEAREST = 6,    /* individuals promoted by nearest selection     */
+  MO_INFO_LEVEL = 7,      /* water-fill level L*                           */
+  MO_INFO_SINGULAR = 8,   /* 1 if the intercept solve fell back entirely   */
+  MO_INFO_SURVIVORS = 9,  /* survivors written (must equal n)              */
+  MO_INFO_ERROR = 10,     /* non-zero status raised on the device          */
+  MO_INFO_COUNT = 16
+};
+
+/* VariationConfig; p_m < 0 means 1/d. */
+typedef struct mo_var_cfg {
+  float eta_c;
+  float eta_m;
+  float p_c;
+  float p_m;
+} mo_var_cfg;
+
+/* ---------------------------------------------------------------- sizing */
+
+/* Bytes of workspace mo_step / mo_select need for (n, m, d, w).  The
+ * bit-matrix dominates: 2n x round_up(2n, 256)/8 bytes. */
+int mo_workspace_bytes(int64_t n, int32_t m, int32_t d, int64_t w, size_t* bytes);
+
+/* Workspace bytes of the per-op entry points (mo_front_peel, mo_normalize,
+ * mo_associate, mo_niche_select) for R rows, m objectives, w reference points. */
+int mo_workspace_bytes_rows(int64_t R, int32_t m, int64_t w, size_t* bytes);
+
+/* Words per row of the dominance bit-matrix for R rows. */
+int64_t mo_bits_words_per_row(int64_t R);
+
+/* Library build/version string. */
+const char* mo_version(void);
+
+/* --------------------------------------------------- RNG / shuffles (L1) */
+
+/* batchcore.shuffle_rows permutation.  perm[p] = item at
+ * position p (new -> old), pos[i] = position of item i; either may be NULL. */
+int mo_permutation(int64_t n, uint64_t seed, uint32_t generation, uint32_t stream,
+                   int32_t* perm, int32_t* pos, void* stream_);
+
+/* engine.initialize's uniform population, SPEC.md:450-458 (X is n x d). */
+int mo_init_population(float* X, int64_t n, int32_t d, uint64_t seed, void* stream_);
+
+/* ----------------------------------------------- problems / variation (L2/L3) */
+
+/* problems.dtlz_eval.  F is n x m.  *domain_flag (device
+ * int32, may be NULL) is OR-ed with 1 when any x lies outside [0,1]. */
+int mo_dtlz_eval(int32_t problem, const float* X, int64_t n, int32_t d, int32_t m, float* F,
+                 int32_t* domain_flag, void* stream_);
+
+/* variation.mating_pool + sbx_pair + polynomial_mutation + clamp, then
+ * dtlz_eval of the children, fused.
+ * Parents X (n x d) -> offspring Xo (n x d), Fo (n x m).  If ideal != NULL
+ * it is lowered to the column minima of Fo (running ideal). */
+int mo_vary_eval(int32_t problem, const float* X, int64_t n, int32_t d, int32_t m, uint64_t seed,
+                 uint32_t generation, const mo_var_cfg* cfg, float* Xo, float* Fo, float* ideal,
+                 void* stream_);
+
+/* --------------------------------------------------------- dominance (L3) */
+
+/* dominance.dominance_matrix, as a bit-matrix:
+ * bit i of row j (word i/32 of bits + j*W) is set iff F[i] dominates F[j].
+ * valid (uint8 per row, NULL = all valid): invalid rows neither dominate nor
+ * are dominated.  W = mo_bits_words_per_row(R). */
+int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid, uint32_t* bits,
+                      void* stream_);
+
+/* dominance.non_dominated_sort + split_fronts, peeling the
+ * bit-matrix.  stop_at > 0 stops at the first front whose cumulative size
+ * reaches stop_at (later rows get 0x7fffffff = dropped); stop_at <= 0 ranks
+ * every valid row.  info: device int32[MO_INFO_COUNT]. */
+int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at,
+                  int32_t* ranks, int32_t* info, void* workspace, size_t workspace_bytes,
+                  void* stream_);
+
+/* ------------------------------------------------------------- niche (L3) */
+
+/* niche.normalize_objectives, over candidate rows
+ * (ranks[i] <= l, l = info[MO_INFO_L]).  ideal (m) is updated in place
+ * (running minimum over all R rows); Fn (R x m, may be NULL) receives the
+ * normalised objectives of candidate rows; intercepts (m doubles, may be NULL). */
+int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, const int32_t* info,
+                 uint64_t seed, uint32_t generation, float* ideal, float* Fn, double* intercepts,
+                 void* workspace, size_t workspace_bytes, void* stream_);
+
+/* niche.perpendicular_distance_matrix + associate, fused and
+ * never materialising D: for every candidate row, pi = nearest reference
+ * point (canonical FP32 key, lowest shuffled reference position on ties) and
+ * d = perpendicular distance.  Fn is R x m, zhat is w x m unit directions. */
+int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64_t w,
+                 const int32_t* ranks, const int32_t* info, uint64_t seed, uint32_t generation,
+                 int32_t* pi, float* d, void* workspace, size_t workspace_bytes, void* stream_);
+
+/* niche.niche_counts + nearest_selection + build_cache +
+ * batched_random_selection (closed-form water-filling).
+ * Promoted individuals get rank l-1 in `ranks`; selected (uint8, R) marks
+ * the n survivors. */
+int mo_niche_select(const int32_t* pi, const float* d, int64_t R, int64_t w, int64_t n,
+                    int32_t* ranks, int32_t* info, uint64_t seed, uint32_t generation,
+                    uint8_t* selected, void* workspace, size_t workspace_bytes, void* stream_);
+
+/* ---------------------------------------------------------- engine (L4) */
+
+/* engine.step: one NSGA-III generation.
+ *   XR (2n x d), FR (2n x m): rows [0,n) hold the parents on entry;
+ *   X_next (n x d), F_next (n x m): survivors, ascending merged index;
+ *   ideal (m): running ideal, updated; ranks (2n): merged-population ranks;
+ *   info: device int32[MO_INFO_COUNT]; zhat: w x m unit reference directions.
+ * Decision variables live in [0,1]^d (the DTLZ domain). */
+typedef struct mo_step_args {
+  int32_t problem;
+  int32_t m;
+  int32_t d;
+  int32_t pad0;
+  int64_t n;
+  int64_t w;
+  uint64_t seed;
+  uint32_t generation;
+  uint32_t pad1;
+  mo_var_cfg var;
+  const float* zhat;
+  float* XR;
+  float* FR;
+  float* X_next;
+  float* F_next;
+  float* ideal;
+  int32_t* ranks;
+  int32_t* info;
+  void* workspace;
+  size_t workspace_bytes;
+  /* Optional device uint32 generation counter.  When non-NULL the kernels read
+   * the generation from it (instead of `generation`) and the step increments
+   * it, so one captured CUDA graph can be replayed generation after generation. */
+  uint32_t* generation_dev;
+} mo_step_args;
+
+int mo_step(const mo_step_args* args, void* stream_);
+
+/* mo_step split into its phases (for per-phase timing):
+ * MO_PHASE_VARY = variation + evaluation, MO_PHASE_SORT = dominance bit-matrix
+ * + peeling + split, MO_PHASE_NICHE = normalisation + association + niching +
+ * survivor compaction.  mo_step == all three in order. */
+enum { MO_PHASE_VARY = 1, MO_PHASE_SORT = 2, MO_PHASE_NICHE = 4, MO_PHASE_ALL = 7 };
+int mo_step_phases(const mo_step_args* args, uint32_t phase_mask, void* stream_);
+
+/* Survivor selection only (NDS + split + niching + compaction) on merged
+ * objectives already in FR -- the part of mo_step after variation. */
+int mo_select(const mo_step_args* args, void* stream_);
+
+/* ---------------------------------------------------- measurement helper */
+
+/* Issue-rate microbenchmark for the roofline of the CUDA-core kernels (not a
+ * reference op): which = 0 -> 64 FP32 compares (setp.{lt,gt}[.or]) per
+ * iteration per thread; which = 1 -> 16 FP32 flops (mul.rn + add.rn) per
+ * iteration per thread.  256 threads per block; in64 = 64 floats. */
+int mo_peak_issue(int32_t which, int32_t blocks, int32_t iters, const float* in64, void* out, void* stream_);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MANYOBJ_B200_H */

@@ -1,0 +1,127 @@
+"""ctypes binding of libmanyobj_b200.so (the C-ABI in include/manyobj_b200.h).
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, :func:`lib` raises ``RuntimeError`` and every GPU op fails loudly.
+"""
+import ctypes
+import os
+import threading
+
+import torch
+
+from .errors import raise_for_status
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmanyobj_b200.so")
+
+_lock = threading.Lock()
+_lib = None
+
+c_i32, c_i64, c_u32, c_u64, c_f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_float
+c_vp, c_sz = ctypes.c_void_p, ctypes.c_size_t
+
+INFO = dict(L=0, SELECTED=1, K=2, NFRONTS=3, FL_SIZE=4, SKIPPED=5, NEAREST=6, LEVEL=7, SINGULAR=8,
+            SURVIVORS=9, ERROR=10)
+INFO_COUNT = 16
+PHASE_VARY, PHASE_SORT, PHASE_NICHE, PHASE_ALL = 1, 2, 4, 7
+PROBLEM_IDS = {f"DTLZ{i}": i for i in range(1, 8)}
+DROPPED = 2 ** 31 - 1
+
+
+class VarCfg(ctypes.Structure):
+    _fields_ = [("eta_c", c_f32), ("eta_m", c_f32), ("p_c", c_f32), ("p_m", c_f32)]
+
+
+class StepArgs(ctypes.Structure):
+    _fields_ = [
+        ("problem", c_i32), ("m", c_i32), ("d", c_i32), ("pad0", c_i32),
+        ("n", c_i64), ("w", c_i64), ("seed", c_u64), ("generation", c_u32), ("pad1", c_u32),
+        ("var", VarCfg),
+        ("zhat", c_vp), ("XR", c_vp), ("FR", c_vp), ("X_next", c_vp), ("F_next", c_vp),
+        ("ideal", c_vp), ("ranks", c_vp), ("info", c_vp), ("workspace", c_vp), ("workspace_bytes", c_sz),
+        ("generation_dev", c_vp),
+    ]
+
+
+_PROTOS = {
+    "mo_version": (ctypes.c_char_p, []),
+    "mo_bits_words_per_row": (c_i64, [c_i64]),
+    "mo_workspace_bytes": (c_i32, [c_i64, c_i32, c_i32, c_i64, ctypes.POINTER(c_sz)]),
+    "mo_workspace_bytes_rows": (c_i32, [c_i64, c_i32, c_i64, ctypes.POINTER(c_sz)]),
+    "mo_permutation": (c_i32, [c_i64, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp]),
+    "mo_init_population": (c_i32, [c_vp, c_i64, c_i32, c_u64, c_vp]),
+    "mo_dtlz_eval": (c_i32, [c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "mo_vary_eval": (c_i32, [c_i32, c_vp, c_i64, c_i32, c_i32, c_u64, c_u32, ctypes.POINTER(VarCfg),
+                             c_vp, c_vp, c_vp, c_vp]),
+    "mo_dominance_bits": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "mo_front_peel": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_normalize": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_associate": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_sz,
+                             c_vp]),
+    "mo_niche_select": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_sz,
+                                c_vp]),
+    "mo_step": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
+    "mo_select": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
+    "mo_step_phases": (c_i32, [ctypes.POINTER(StepArgs), c_u32, c_vp]),
+    "mo_peak_issue": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
+}
+
+EXPORTED = tuple(_PROTOS)
+
+
+def load_library(path=LIB_PATH):
+    """dlopen the library and bind every prototype (no GPU needed)."""
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: run `python -m paper_2504_06067_b200.build` "
+                           "(the engine has no CPU fallback)")
+    so = ctypes.CDLL(path)
+    for name, (res, args) in _PROTOS.items():
+        fn = getattr(so, name)
+        fn.restype = res
+        fn.argtypes = args
+    return so
+
+
+def lib():
+    """The loaded library; requires a CUDA device (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not torch.cuda.is_available():
+                    raise RuntimeError("manyobj_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+                torch.cuda.init()
+                _lib = load_library()
+    return _lib
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return c_vp(s.cuda_stream)
+
+
+def ptr(t):
+    return c_vp(0) if t is None else c_vp(t.data_ptr())
+
+
+def check(code, what):
+    raise_for_status(int(code), what)
+
+
+def workspace_rows(R, m, w, device=None):
+    nbytes = c_sz(0)
+    check(lib().mo_workspace_bytes_rows(int(R), int(m), int(w), ctypes.byref(nbytes)), "mo_workspace_bytes_rows")
+    return torch.empty(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")
+
+
+def workspace_step(n, m, d, w, device=None):
+    nbytes = c_sz(0)
+    check(lib().mo_workspace_bytes(int(n), int(m), int(d), int(w), ctypes.byref(nbytes)), "mo_workspace_bytes")
+    return torch.empty(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")
+
+
+def new_info(device=None, **fields):
+    info = torch.zeros(INFO_COUNT, dtype=torch.int32)
+    for k, v in fields.items():
+        info[INFO[k]] = int(v)
+    return info.to(device or "cuda")

@@ -1,0 +1,693 @@
+// Normalisation (K3), association (K4) and niche selection (K5-K9).
+//
+// Reference: niche.normalize_objectives SPEC.md:331-339, perpendicular_distance
+// _matrix :340-348, associate :349-357, niche_counts :358-366,
+// nearest_selection :367-375, build_cache :376-384, batched_random_selection
+// :385-393; Alg. 2 PAPER.md:157-191.  Pins: DESIGN.md "Pinned semantics" and
+// oracle/manyobj_ref/niche.py (same arithmetic, same tie-breaks).
+//
+// k_prep      (persistent): running ideal, keyed shuffles of rows and
+//             reference points, candidate list (rank <= l), ASF extreme
+//             points, FP64 hyperplane solve -> FP32 intercepts.
+// k_assoc<M>  (rows x reference-split grid): canonical FP32 key
+//             t = ((f0*z0 + f1*z1) + ...) against zhat in shuffled order,
+//             running (max t, first position), merged across splits with a
+//             64-bit atomicMax of (ord(t), ~position).  D is never stored.
+// k_assoc_final: pi = perm_ref[p*], d = sqrt(sum (f - t z)^2).
+// k_select    (persistent): niche counts with warp-aggregated atomics,
+//             nearest selection (64-bit atomicMin of (d, position)),
+//             closed-form water-filling of the Alg. 2 loop, the cache as a
+//             stable radix sort of F_l by pi in shuffled order, promotion,
+//             and the stable survivor compaction.
+#include "mo_common.cuh"
+#include "mo_grid.cuh"
+#include "mo_rng.cuh"
+#include "k_niche_args.cuh"
+
+namespace mo {
+
+constexpr int MAXM = 64;
+constexpr float ASF_EPS = 1e-6f;
+constexpr double DEGENERATE = 1e-10;
+
+// ---------------------------------------------------------------- prep
+
+
+
+__device__ __forceinline__ void atomic_min_f(float* addr, float v) {
+  if (v >= 0.0f)
+    atomicMin(reinterpret_cast<int*>(addr), __float_as_int(v));
+  else
+    atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
+
+__device__ double solve_intercepts(const PrepArgs& a, const float* ideal, double* A, double* rhs, int* singular) {
+  // E b = 1 with partial pivoting, FP64, every operation separately rounded
+  // (library is built with -fmad=false).  Mirrors oracle niche.gauss_solve.
+  const int m = a.m;
+  for (int r = 0; r < m; ++r) {
+    const int row = __ldcg(a.perm_pop + (uint32_t)(__ldcg(a.ext_key + r) & 0xffffffffull));
+    for (int c = 0; c < m; ++c) A[r * m + c] = (double)__fsub_rn(a.F[(int64_t)row * m + c], ideal[c]);
+    rhs[r] = 1.0;
+  }
+  for (int c = 0; c < m; ++c) {
+    int p = c;
+    double best = fabs(A[c * m + c]);
+    for (int r = c + 1; r < m; ++r)
+      if (fabs(A[r * m + c]) > best) {
+        best = fabs(A[r * m + c]);
+        p = r;
+      }
+    if (best == 0.0) {
+      *singular = 1;
+      return 0.0;
+    }
+    if (p != c) {
+      for (int q = 0; q < m; ++q) {
+        double t = A[c * m + q];
+        A[c * m + q] = A[p * m + q];
+        A[p * m + q] = t;
+      }
+      double t = rhs[c];
+      rhs[c] = rhs[p];
+      rhs[p] = t;
+    }
+    for (int r = c + 1; r < m; ++r) {
+      double f = A[r * m + c] / A[c * m + c];
+      for (int q = c; q < m; ++q) A[r * m + q] = A[r * m + q] - f * A[c * m + q];
+      rhs[r] = rhs[r] - f * rhs[c];
+    }
+  }
+  for (int c = m - 1; c >= 0; --c) {
+    double s = rhs[c];
+    for (int q = c + 1; q < m; ++q) s = s - A[c * m + q] * rhs[q];
+    rhs[c] = s / A[c * m + c];  // rhs now holds b
+  }
+  *singular = 0;
+  return 0.0;
+}
+
+__global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
+  __shared__ uint32_t sKp[MAX_SHUFFLE_ROUNDS], sSp[MAX_SHUFFLE_ROUNDS], sKr[MAX_SHUFFLE_ROUNDS],
+      sSr[MAX_SHUFFLE_ROUNDS];
+  __shared__ int sRp, sRr;
+  __shared__ float sMin[MAXM];
+  __shared__ double sA[MAXM * MAXM];
+  __shared__ double sRhs[MAXM];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+  const int R = a.R, m = a.m, w = a.w;
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  const int l = __ldcg(a.info + MO_INFO_L);
+  const bool skipped = __ldcg(a.info + MO_INFO_SKIPPED) != 0;
+
+  // ---- phase 0: running ideal over all R rows (A-4), shuffles, candidate list
+  for (int k = tid; k < m; k += blockDim.x) sMin[k] = __int_as_float(0x7f800000);
+  const uint32_t gen = a.gen_ptr ? __ldcg(a.gen_ptr) : a.gen;
+  load_shuffle_keys_smem(sKp, sSp, &sRp, (uint32_t)R, a.seed, gen, STREAM_POP_SHUFFLE);
+  load_shuffle_keys_smem(sKr, sSr, &sRr, (uint32_t)w, a.seed, gen, STREAM_REF_SHUFFLE);
+  __syncthreads();
+  if (a.mode == PREP_FULL) {
+    for (int64_t e = gtid; e < (int64_t)R * m; e += gthreads) atomic_min_f(&sMin[e % m], a.F[e]);
+    __syncthreads();
+    for (int k = tid; k < m; k += blockDim.x) atomic_min_f(&a.ideal[k], sMin[k]);
+  }
+  if (skipped) return;
+  for (int i = gtid; i < R; i += gthreads) {
+    const int p = (int)prp((uint32_t)i, sKp, sSp, sRp, (uint32_t)R);
+    a.pos_pop[i] = p;
+    a.perm_pop[p] = i;
+    if (a.mode == PREP_PERMS) continue;
+    a.akey[i] = 0ull;
+    if (a.ranks[i] >= 0 && a.ranks[i] <= l) a.cand[atomicAdd(a.ctl, 1)] = i;
+  }
+  for (int j = gtid; j < w; j += gthreads) {
+    const int p = (int)prp((uint32_t)j, sKr, sSr, sRr, (uint32_t)w);
+    a.pos_ref[j] = p;
+    a.perm_ref[p] = j;
+    if (a.zhat)
+      for (int k = 0; k < m; ++k) a.zs[(int64_t)p * m + k] = a.zhat[(int64_t)j * m + k];
+  }
+  if (a.mode != PREP_FULL) return;
+  if (gtid < m) {
+    a.ext_key[gtid] = ~0ull;
+    a.colmax[gtid] = 0u;
+  }
+  grid_sync(a.bar);
+
+  // ---- phase 1: ASF extreme points + column maxima of translated candidates
+  const int ncand = __ldcg(a.ctl);
+  float idl[MAXM];
+  for (int k = 0; k < m; ++k) idl[k] = __ldcg(a.ideal + k);
+  for (int base = blockIdx.x * blockDim.x; base < ncand; base += gthreads) {
+    const int c = base + tid;
+    const bool act = c < ncand;
+    float ft[MAXM], q[MAXM];
+    int row = 0, pp = 0;
+    if (act) {
+      row = __ldcg(a.cand + c);
+      pp = __ldcg(a.pos_pop + row);
+      for (int k = 0; k < m; ++k) {
+        ft[k] = __fsub_rn(a.F[(int64_t)row * m + k], idl[k]);
+        q[k] = __fdiv_rn(ft[k], ASF_EPS);
+      }
+    }
+    for (int k = 0; k < m; ++k) {
+      uint32_t v = act ? f2ord(ft[k]) : 0u;
+      v = warp_max_u32(v);
+      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
+    }
+    for (int ax = 0; ax < m; ++ax) {
+      unsigned long long key = ~0ull;
+      if (act) {
+        float s = ft[ax];  // w_ax,ax = 1: f / 1 is exact
+        for (int k = 0; k < m; ++k)
+          if (k != ax) s = fmaxf(s, q[k]);
+        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+      }
+      key = warp_min_u64(key);
+      if (lane == 0 && key != ~0ull) atomicMin(&a.ext_key[ax], key);
+    }
+  }
+  grid_sync(a.bar);
+
+  // ---- phase 2: hyperplane solve (one thread), per-component fallbacks
+  if (blockIdx.x == 0 && tid == 0) {
+    int singular = 0;
+    float idl2[MAXM];
+    for (int k = 0; k < m; ++k) idl2[k] = __ldcg(a.ideal + k);
+    double fb[MAXM];
+    for (int k = 0; k < m; ++k) {
+      double mx = (double)ord2f(__ldcg(a.colmax + k));
+      fb[k] = mx > DEGENERATE ? mx : 1.0;
+    }
+    if (ncand == 0) singular = 1;
+    else solve_intercepts(a, idl2, sA, sRhs, &singular);
+    bool bad = singular != 0;
+    if (!bad)
+      for (int k = 0; k < m; ++k)
+        if (!isfinite(sRhs[k])) bad = true;
+    for (int k = 0; k < m; ++k) {
+      double ak;
+      if (bad) {
+        ak = fb[k];
+      } else {
+        ak = 1.0 / sRhs[k];
+        if (!(isfinite(ak) && ak > DEGENERATE)) ak = fb[k];
+      }
+      a.icpt[k] = ak;
+      a.a32[k] = __double2float_rn(ak);
+      if (a.icpt_out) a.icpt_out[k] = ak;
+    }
+    a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
+  }
+}
+
+// ---------------------------------------------------------- association
+
+constexpr int ASSOC_THREADS = 128;
+constexpr int ASSOC_RB = 4;                        // rows per thread
+constexpr int ASSOC_ROWS = ASSOC_THREADS * ASSOC_RB;
+constexpr int ASSOC_PTILE = 512;                   // reference points staged per smem tile
+
+
+
+template <int M>
+__device__ __forceinline__ float canon_dot(const float* f, const float* z) {
+  float t = __fmul_rn(f[0], z[0]);
+#pragma unroll
+  for (int k = 1; k < M; ++k) t = __fadd_rn(t, __fmul_rn(f[k], z[k]));
+  return t;
+}
+
+template <int M>
+__global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sz[ASSOC_PTILE * MP];
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int rbase = blockIdx.x * ASSOC_ROWS;
+  if (rbase >= ncand) return;
+  const int p0 = blockIdx.y * a.psplit;
+  const int p1 = min(a.w, p0 + a.psplit);
+  if (p0 >= p1) return;
+  const int tid = threadIdx.x;
+  float fn[ASSOC_RB][M];
+  int rows[ASSOC_RB];
+#pragma unroll
+  for (int r = 0; r < ASSOC_RB; ++r) {
+    const int c = rbase + r * ASSOC_THREADS + tid;
+    rows[r] = c < ncand ? __ldcg(a.cand + c) : -1;
+    const int row = rows[r] < 0 ? 0 : rows[r];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      float v = a.F[(int64_t)row * M + k];
+      if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+      if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+      fn[r][k] = v;
+    }
+  }
+  float best[ASSOC_RB];
+  int bp[ASSOC_RB];
+#pragma unroll
+  for (int r = 0; r < ASSOC_RB; ++r) {
+    best[r] = -__int_as_float(0x7f800000);
+    bp[r] = p0;
+  }
+  for (int t0 = p0; t0 < p1; t0 += ASSOC_PTILE) {
+    const int tn = min(ASSOC_PTILE, p1 - t0);
+    __syncthreads();
+    for (int e = tid; e < tn * MP; e += ASSOC_THREADS) {
+      const int p = e / MP, k = e - p * MP;
+      sz[e] = k < M ? a.zs[(int64_t)(t0 + p) * M + k] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int p = 0; p < tn; ++p) {
+      float z[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) z[k] = sz[p * MP + k];
+#pragma unroll
+      for (int r = 0; r < ASSOC_RB; ++r) {
+        const float t = canon_dot<M>(fn[r], z);
+        if (t > best[r]) {
+          best[r] = t;
+          bp[r] = t0 + p;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < ASSOC_RB; ++r) {
+    if (rows[r] >= 0) {
+      const unsigned long long key = ((unsigned long long)f2ord(best[r]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp[r]);
+      atomicMax(&a.akey[rows[r]], key);
+    }
+  }
+}
+
+
+
+__global__ void k_assoc_final(AssocFinalArgs a) {
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncand) return;
+  const int m = a.m;
+  const int row = __ldcg(a.cand + c);
+  const unsigned long long key = __ldcg(a.akey + row);
+  const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
+  float fn[MAXM];
+  for (int k = 0; k < m; ++k) {
+    float v = a.F[(int64_t)row * m + k];
+    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+    fn[k] = v;
+    if (a.Fn_out) a.Fn_out[(int64_t)row * m + k] = v;
+  }
+  if (a.fn_only) return;
+  const float* z = a.zs + (int64_t)p * m;
+  float t = __fmul_rn(fn[0], z[0]);
+  for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn[k], z[k]));
+  float s = 0.0f;
+  for (int k = 0; k < m; ++k) {
+    const float e = __fsub_rn(fn[k], __fmul_rn(t, z[k]));
+    s = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s, __fmul_rn(e, e));
+  }
+  a.pi[row] = a.perm_ref[p];
+  a.d[row] = __fsqrt_rn(s);
+}
+
+// --------------------------------------------------------------- select
+
+
+
+constexpr int SELECT_THREADS = 512;
+
+__global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
+  __shared__ int sh[40];
+  __shared__ int wcnt[(SELECT_THREADS / 32) * 256];
+  __shared__ int run[256], off[256];
+  __shared__ int sHist[2][1024];
+  __shared__ long long sLL[4];
+  const int tid = threadIdx.x;
+  const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+  const int R = a.R, w = a.w;
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  const int l = __ldcg(a.info + MO_INFO_L);
+  const int k = __ldcg(a.info + MO_INFO_K);
+  const bool skipped = __ldcg(a.info + MO_INFO_SKIPPED) != 0;
+  int kept_nearest = 0, level = -1;
+
+  if (!skipped) {
+    // ---- S0: reset per-reference state
+    for (int j = gtid; j < w; j += gthreads) {
+      a.rho[j] = 0;
+      a.rho_p[j] = 0;
+      a.take[j] = 0;
+      a.near_key[j] = ~0ull;
+    }
+    for (int i = gtid; i < R; i += gthreads) a.prom[i] = 0;
+    grid_sync(a.g.bar);
+    // ---- S1: niche counts rho (rank < l) and rho' (rank == l), warp-aggregated atomics
+    for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {
+      const int i = base + tid;
+      const int r = i < R ? a.ranks[i] : MO_RANK_DROPPED;
+      const bool c = (r >= 0) && (r <= l);
+      const int j = c ? __ldcg(a.pi + i) : 0;
+      warp_agg_add(a.rho, j, c && r < l);
+      warp_agg_add(a.rho_p, j, c && r == l);
+    }
+    grid_sync(a.g.bar);
+    // ---- S2: disable reference points without candidates (rho = inf where rho' = 0)
+    for (int j = gtid; j < w; j += gthreads)
+      if (__ldcg(a.rho_p + j) == 0) a.rho[j] = MO_INF;
+    grid_sync(a.g.bar);
+    // ---- S3: nearest candidate of every empty niche: min (d, shuffled position)
+    for (int i = gtid; i < R; i += gthreads) {
+      if (a.ranks[i] != l) continue;
+      const int j = __ldcg(a.pi + i);
+      if (__ldcg(a.rho + j) != 0) continue;
+      const unsigned long long key = ((unsigned long long)f2ord(__ldcg(a.d + i)) << 32) | (uint32_t)a.pos_pop[i];
+      atomicMin(&a.near_key[j], key);
+    }
+    grid_sync(a.g.bar);
+    // ---- S4: nearest selection, truncated to the first k empty niches in shuffled order
+    {
+      const int kk = k;
+      const int M0 = grid_scan(
+          a.g, w, [&](int64_t p) { return (int)(__ldcg(a.rho + a.perm_ref[p]) == 0); },
+          [&](int64_t p, int pre) {
+            if (pre >= kk) return;
+            const int j = a.perm_ref[p];
+            const int row = a.perm_pop[(uint32_t)(__ldcg(a.near_key + j) & 0xffffffffull)];
+            a.prom[row] = 1;
+            const int rp = __ldcg(a.rho_p + j) - 1;
+            a.rho_p[j] = rp;
+            a.rho[j] = rp == 0 ? MO_INF : 1;
+          },
+          sh);
+      kept_nearest = min(M0, kk);
+    }
+    grid_sync(a.g.bar);
+    const int k_rem = k - kept_nearest;
+    if (k_rem > 0) {
+      // ---- S5: water-filling level L* (block 0): T(L) = sum_j clamp(L+1-rho_j, 0, c_j)
+      if (blockIdx.x == 0) {
+        long long mn = (long long)MO_INF, mx = 0;
+        for (int j = tid; j < w; j += blockDim.x) {
+          const int r = __ldcg(a.rho + j);
+          if (r < MO_INF) {
+            mn = min(mn, (long long)r);
+            mx = max(mx, (long long)r + __ldcg(a.rho_p + j));
+          }
+        }
+        // block min / max via shared atomics on 64-bit
+        if (tid == 0) {
+          sLL[0] = (long long)MO_INF;
+          sLL[1] = 0;
+        }
+        __syncthreads();
+        atomicMin(reinterpret_cast<unsigned long long*>(&sLL[0]), (unsigned long long)mn);
+        atomicMax(reinterpret_cast<unsigned long long*>(&sLL[1]), (unsigned long long)mx);
+        for (int q = tid; q < 2 * 1024; q += blockDim.x) (&sHist[0][0])[q] = 0;
+        __syncthreads();
+        const long long lo = sLL[0];
+        // window histogram of start (rho_j) and end (rho_j + c_j) levels
+        for (int j = tid; j < w; j += blockDim.x) {
+          const int r = __ldcg(a.rho + j);
+          if (r >= MO_INF) continue;
+          const long long s0 = (long long)r - lo, e0 = s0 + __ldcg(a.rho_p + j);
+          if (s0 < 1024) atomicAdd(&sHist[0][s0], 1);
+          if (e0 < 1024) atomicAdd(&sHist[1][e0], 1);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          long long active = 0, T = 0, Lstar = -1, before = 0;
+          for (int q = 0; q < 1024; ++q) {
+            active += sHist[0][q] - sHist[1][q];
+            if (T + active >= k_rem) {
+              Lstar = lo + q;
+              before = T;
+              break;
+            }
+            T += active;
+          }
+          sLL[2] = Lstar;
+          sLL[3] = before;
+        }
+        __syncthreads();
+        long long Lstar = sLL[2];
+        if (Lstar < 0) {
+          // rare: beyond the window -> binary search with full passes over w
+          long long lo2 = lo + 1024, hi2 = sLL[1];
+          while (lo2 < hi2) {
+            const long long mid = (lo2 + hi2) / 2;
+            long long part = 0;
+            for (int j = tid; j < w; j += blockDim.x) {
+              const int r = __ldcg(a.rho + j);
+              if (r >= MO_INF) continue;
+              long long t = mid + 1 - r;
+              const long long c = __ldcg(a.rho_p + j);
+              part += t < 0 ? 0 : (t > c ? c : t);
+            }
+            __syncthreads();
+            if (tid == 0) sLL[2] = 0;
+            __syncthreads();
+            atomicAdd(reinterpret_cast<unsigned long long*>(&sLL[2]), (unsigned long long)part);
+            __syncthreads();
+            const long long T = sLL[2];
+            __syncthreads();
+            if (T >= k_rem)
+              hi2 = mid;
+            else
+              lo2 = mid + 1;
+          }
+          Lstar = lo2;
+          long long part = 0;
+          for (int j = tid; j < w; j += blockDim.x) {
+            const int r = __ldcg(a.rho + j);
+            if (r >= MO_INF) continue;
+            long long t = Lstar - r;
+            const long long c = __ldcg(a.rho_p + j);
+            part += t < 0 ? 0 : (t > c ? c : t);
+          }
+          __syncthreads();
+          if (tid == 0) sLL[3] = 0;
+          __syncthreads();
+          atomicAdd(reinterpret_cast<unsigned long long*>(&sLL[3]), (unsigned long long)part);
+          __syncthreads();
+        }
+        if (tid == 0) {
+          a.ctl[8] = (int)Lstar;
+          a.ctl[9] = (int)(k_rem - sLL[3]);  // marked points kept at level L*
+        }
+      }
+      grid_sync(a.g.bar);
+      const int L = __ldcg(a.ctl + 8), need = __ldcg(a.ctl + 9);
+      level = L;
+      for (int j = gtid; j < w; j += gthreads) {
+        const int r = __ldcg(a.rho + j);
+        if (r >= MO_INF) continue;
+        const int c = __ldcg(a.rho_p + j);
+        const long long t = (long long)L - r;
+        a.take[j] = (int)(t < 0 ? 0 : (t > c ? c : t));
+      }
+      grid_scan(
+          a.g, w,
+          [&](int64_t p) {
+            const int j = a.perm_ref[p];
+            const int r = __ldcg(a.rho + j);
+            return (int)(r < MO_INF && r <= L && (long long)L < (long long)r + __ldcg(a.rho_p + j));
+          },
+          [&](int64_t p, int pre) {
+            if (pre < need) a.take[a.perm_ref[p]] += 1;
+          },
+          sh);
+      // ---- S6: bucket starts of the cache (counts c_j in reference index order)
+      grid_scan(
+          a.g, w, [&](int64_t j) { return __ldcg(a.rho_p + j); },
+          [&](int64_t j, int pre) { a.bstart[j] = pre; }, sh);
+      // ---- S7: F_l members left after the nearest pass, in shuffled population order
+      const int L_n = grid_scan(
+          a.g, R,
+          [&](int64_t p) {
+            const int i = a.perm_pop[p];
+            return (int)(a.ranks[i] == l && __ldcg(a.prom + i) == 0);
+          },
+          [&](int64_t p, int pre) {
+            const int i = a.perm_pop[p];
+            a.keyA[pre] = (uint32_t)__ldcg(a.pi + i);
+            a.valA[pre] = i;
+          },
+          sh);
+      grid_sync(a.g.bar);
+      // ---- S8: stable radix sort by reference point -> the cache table Q as CSR
+      const int kbits = bitlen((uint32_t)(w > 1 ? w - 1 : 1));
+      uint32_t* kin = a.keyA;
+      int* vin = a.valA;
+      uint32_t* kout = a.keyB;
+      int* vout = a.valB;
+      for (int shift = 0; shift < kbits; shift += 8) {
+        grid_radix_pass(a.g, L_n, shift, kin, vin, kout, vout, wcnt, run, off, sh);
+        uint32_t* tk = kin;
+        kin = kout;
+        kout = tk;
+        int* tv = vin;
+        vin = vout;
+        vout = tv;
+      }
+      // ---- S9: promote the first take_j cache entries of every reference point
+      for (int s = gtid; s < L_n; s += gthreads) {
+        const int j = (int)__ldcg(kin + s);
+        const int i = __ldcg(vin + s);
+        if (s - __ldcg(a.bstart + j) < __ldcg(a.take + j)) a.prom[i] = 1;
+      }
+    }
+    grid_sync(a.g.bar);
+  }
+  // ---- S10: survivors = fronts < l + promoted (or fronts <= l when niching was skipped);
+  //           promoted rank = l - 1 (A-8); stable compaction in merged-row order (A-9)
+  const int nsurv = grid_scan(
+      a.g, R,
+      [&](int64_t i) {
+        const int r = a.ranks[i];
+        const bool s = skipped ? (r >= 0 && r <= l) : ((r >= 0 && r < l) || __ldcg(a.prom + i) != 0);
+        return (int)s;
+      },
+      [&](int64_t i, int pre) {
+        if (a.X_next) {
+          const float* src = a.XR + i * a.dvars;
+          float* dst = a.X_next + (int64_t)pre * a.dvars;
+          for (int v = 0; v < a.dvars; ++v) dst[v] = src[v];
+          const float* fs = a.FR + i * a.m;
+          float* fd = a.F_next + (int64_t)pre * a.m;
+          for (int v = 0; v < a.m; ++v) fd[v] = fs[v];
+        }
+      },
+      sh);
+  grid_sync(a.g.bar);
+  for (int i = gtid; i < R; i += gthreads) {
+    const int r = a.ranks[i];
+    const bool pr = !skipped && __ldcg(a.prom + i) != 0;
+    const bool s = skipped ? (r >= 0 && r <= l) : ((r >= 0 && r < l) || pr);
+    if (a.selected) a.selected[i] = s;
+    if (pr) a.ranks[i] = l - 1;
+  }
+  if (gtid == 0) {
+    a.info[MO_INFO_NEAREST] = kept_nearest;
+    a.info[MO_INFO_LEVEL] = level;
+    a.info[MO_INFO_SURVIVORS] = nsurv;
+    if (a.gen_ptr) *a.gen_ptr += 1u;
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+static int coop_blocks(const void* fn, int threads, int cap_per_sm) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, 0);
+  if (per > cap_per_sm) per = cap_per_sm;
+  return sms * (per > 0 ? per : 1);
+}
+
+template <class Args>
+static int launch_coop(void (*fn)(Args), int blocks, int threads, Args args, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, fn, args) != cudaSuccess) return MO_ERR_CUDA;
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int prep_grid_blocks() {
+  static int b = 0;
+  if (!b) b = coop_blocks((const void*)k_prep, 256, 2);
+  return b;
+}
+int select_grid_blocks() {
+  static int b = 0;
+  if (!b) b = coop_blocks((const void*)k_select, SELECT_THREADS, 1);
+  return b;
+}
+
+int launch_prep(const PrepArgs& a, cudaStream_t s) {
+  if (a.m < 1 || a.m > MAXM) return MO_ERR_PARAM;
+  if (cudaMemsetAsync(a.ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  int blocks = prep_grid_blocks();
+  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), 256);
+  if (blocks > need) blocks = need < 1 ? 1 : need;
+  return launch_coop(k_prep, blocks, 256, a, s);
+}
+
+int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  int rowblocks = (int)ceil_div(R, ASSOC_ROWS);
+  // split the reference points so the grid covers the GPU ~4x
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int want = 4 * sms;
+  int splits = (int)ceil_div(want, rowblocks);
+  int maxsplit = (int)ceil_div(a.w, 64);
+  if (splits > maxsplit) splits = maxsplit;
+  if (splits < 1) splits = 1;
+  AssocArgs b = a;
+  b.psplit = (int)ceil_div(a.w, splits);
+  dim3 grid(rowblocks, (unsigned)ceil_div(a.w, b.psplit));
+  switch (m) {
+#define MO_AS_CASE(MM) \
+  case MM: k_assoc<MM><<<grid, ASSOC_THREADS, 0, s>>>(b); break;
+    MO_AS_CASE(1)
+    MO_AS_CASE(2)
+    MO_AS_CASE(3)
+    MO_AS_CASE(4)
+    MO_AS_CASE(5)
+    MO_AS_CASE(6)
+    MO_AS_CASE(7)
+    MO_AS_CASE(8)
+    MO_AS_CASE(9)
+    MO_AS_CASE(10)
+    MO_AS_CASE(11)
+    MO_AS_CASE(12)
+    MO_AS_CASE(13)
+    MO_AS_CASE(14)
+    MO_AS_CASE(15)
+    MO_AS_CASE(16)
+#undef MO_AS_CASE
+    default:
+      return MO_ERR_PARAM;
+  }
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  k_assoc_final<<<(unsigned)ceil_div(R, 128), 128, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_select(const SelectArgs& a, cudaStream_t s) {
+  if (cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  int blocks = select_grid_blocks();
+  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), SELECT_THREADS);
+  if (blocks > need) blocks = need < 1 ? 1 : need;
+  return launch_coop(k_select, blocks, SELECT_THREADS, a, s);
+}
+
+}  // namespace mo

@@ -1,0 +1,170 @@
+// Fused variation + evaluation: mating pool -> SBX -> clamp -> PM -> clamp -> DTLZ.
+//
+// Reference ops: variation.mating_pool, sbx_pair (:258-266),
+// polynomial_mutation (:267-275), clamp (:295), problems.dtlz_eval (:520-528).
+// One thread per mating pair q: parents a = perm[2q], b = perm[2q+1] of the
+// keyed MATING permutation; children are written to rows 2q and 2q+1.
+// Draws: pair Bernoulli(p_c) = Philox(q, PAIR_SLOT, g, SBX).x, SBX u_v =
+// Philox(q, v, g, SBX).x, PM flag/draw = Philox(i, v, g, PM).x/.y.  The
+// arithmetic is FP64 (oracle order), children are rounded to FP32 once after
+// SBX+clamp and once after PM+clamp.
+#include "mo_common.cuh"
+#include "mo_dtlz.cuh"
+#include "mo_rng.cuh"
+
+namespace mo {
+
+__device__ __forceinline__ void atomic_min_float(float* addr, float v) {
+  if (v >= 0.0f)
+    atomicMin(reinterpret_cast<int*>(addr), __float_as_int(v));
+  else
+    atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
+}
+
+__device__ __forceinline__ double sbx_beta(double u, double eta) {
+  double e = 1.0 / (eta + 1.0);
+  return u <= 0.5 ? pow(2.0 * u, e) : pow(1.0 / (2.0 * (1.0 - u)), e);
+}
+
+__device__ __forceinline__ double pm_apply(double x, double u, double eta) {
+  // bounds [0,1]: span = 1, d1 = x, d2 = 1 - x  (oracle variation.pm_delta)
+  const double lo = 0.0, hi = 1.0, span = hi - lo;
+  double d1 = (x - lo) / span, d2 = (hi - x) / span;
+  double mp = 1.0 / (eta + 1.0);
+  double dq;
+  if (u < 0.5) {
+    double v = 2.0 * u + (1.0 - 2.0 * u) * pow(1.0 - d1, eta + 1.0);
+    dq = pow(v, mp) - 1.0;
+  } else {
+    double v = 2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow(1.0 - d2, eta + 1.0);
+    dq = 1.0 - pow(v, mp);
+  }
+  return x + dq * span;
+}
+
+__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
+
+// Block = 128 threads; dynamic smem holds the MATING shuffle keys.
+__global__ void __launch_bounds__(128) k_vary_eval(int problem, const float* __restrict__ X, int n, int d, int m,
+                                                   uint64_t seed, uint32_t gen_val, const uint32_t* gen_ptr,
+                                                   mo_var_cfg cfg,
+                                                   float* __restrict__ Xo, float* __restrict__ Fo,
+                                                   float* __restrict__ ideal, int* __restrict__ domain_flag) {
+  __shared__ uint32_t shK[MAX_SHUFFLE_ROUNDS], shS[MAX_SHUFFLE_ROUNDS];
+  __shared__ int shR;
+  __shared__ float shMin[16];
+  const uint32_t gen = gen_ptr ? *gen_ptr : gen_val;
+  load_shuffle_keys_smem(shK, shS, &shR, (uint32_t)n, seed, gen, STREAM_MATING);
+  if (threadIdx.x < 16) shMin[threadIdx.x] = __int_as_float(0x7f800000);
+  __syncthreads();
+  const int rounds = shR;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
+  if (q < n / 2) {
+    const uint32_t a = prp_inv(2u * q, shK, shS, rounds, (uint32_t)n);
+    const uint32_t b = prp_inv(2u * q + 1u, shK, shS, rounds, (uint32_t)n);
+    const float* p1 = X + (int64_t)a * d;
+    const float* p2 = X + (int64_t)b * d;
+    float* c1 = Xo + (int64_t)(2 * q) * d;
+    float* c2 = Xo + (int64_t)(2 * q + 1) * d;
+    const bool cross = u01(philox4x32((uint32_t)q, PAIR_SLOT, gen, STREAM_SBX, seed).x) < cfg.p_c;
+    const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
+    for (int v = 0; v < d; ++v) {
+      double x1 = (double)p1[v], x2 = (double)p2[v];
+      float o1, o2;
+      if (cross) {
+        double u = (double)u01(philox4x32((uint32_t)q, (uint32_t)v, gen, STREAM_SBX, seed).x);
+        double be = sbx_beta(u, eta_c);
+        o1 = (float)clamp01(0.5 * ((1.0 + be) * x1 + (1.0 - be) * x2));
+        o2 = (float)clamp01(0.5 * ((1.0 - be) * x1 + (1.0 + be) * x2));
+      } else {
+        o1 = p1[v];
+        o2 = p2[v];
+      }
+      U4 r1 = philox4x32((uint32_t)(2 * q), (uint32_t)v, gen, STREAM_PM, seed);
+      U4 r2 = philox4x32((uint32_t)(2 * q + 1), (uint32_t)v, gen, STREAM_PM, seed);
+      if (u01(r1.x) < p_m) o1 = (float)clamp01(pm_apply((double)o1, (double)u01(r1.y), eta_m));
+      if (u01(r2.x) < p_m) o2 = (float)clamp01(pm_apply((double)o2, (double)u01(r2.y), eta_m));
+      c1[v] = o1;
+      c2[v] = o2;
+    }
+    float* f1 = Fo + (int64_t)(2 * q) * m;
+    float* f2 = Fo + (int64_t)(2 * q + 1) * m;
+    bool ok = dtlz_eval_row(problem, c1, d, m, f1);
+    ok = dtlz_eval_row(problem, c2, d, m, f2) && ok;
+    if (!ok && domain_flag) atomicOr(domain_flag, 1);
+    if (ideal) {
+      for (int j = 0; j < m && j < 16; ++j) atomic_min_float(&shMin[j], fminf(f1[j], f2[j]));
+    }
+  }
+  if (ideal) {
+    __syncthreads();
+    if (threadIdx.x < m && threadIdx.x < 16) atomic_min_float(&ideal[threadIdx.x], shMin[threadIdx.x]);
+    // objectives beyond 16 columns: per-thread global atomics
+    if (m > 16 && q < n / 2)
+      for (int j = 16; j < m; ++j)
+        atomic_min_float(&ideal[j], fminf(Fo[(int64_t)(2 * q) * m + j], Fo[(int64_t)(2 * q + 1) * m + j]));
+  }
+}
+
+__global__ void k_init_population(float* __restrict__ X, int64_t n, int d, uint64_t seed) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * d) return;
+  int64_t i = t / d;
+  int v = (int)(t - i * d);
+  X[t] = u01(philox4x32((uint32_t)i, (uint32_t)v, 0u, STREAM_INIT, seed).x);
+}
+
+__global__ void k_dtlz_eval(int problem, const float* __restrict__ X, int64_t n, int d, int m,
+                            float* __restrict__ F, int* __restrict__ domain_flag) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool ok = dtlz_eval_row(problem, X + i * d, d, m, F + i * m);
+  if (!ok && domain_flag) atomicOr(domain_flag, 1);
+}
+
+__global__ void k_min_rows(const float* __restrict__ F, int64_t R, int m, float* __restrict__ ideal) {
+  // column minima of F into ideal (running minimum); one thread per (row, column)
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= R * m) return;
+  atomic_min_float(&ideal[t % m], F[t]);
+}
+
+int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint64_t seed, uint32_t gen,
+                     const uint32_t* gen_ptr, const mo_var_cfg& cfg, float* Xo, float* Fo, float* ideal,
+                     int* domain_flag, cudaStream_t s) {
+  if (n <= 0 || (n & 1) || d < m || m < 2) return MO_ERR_PARAM;
+  if (problem < MO_DTLZ1 || problem > MO_DTLZ7) return MO_ERR_PARAM;
+  int pairs = (int)(n / 2);
+  k_vary_eval<<<(unsigned)ceil_div(pairs, 128), 128, 0, s>>>(problem, X, (int)n, d, m, seed, gen, gen_ptr, cfg,
+                                                               Xo, Fo, ideal, domain_flag);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_init_population(float* X, int64_t n, int d, uint64_t seed, cudaStream_t s) {
+  if (n <= 0 || d <= 0) return MO_ERR_PARAM;
+  int64_t tot = n * d;
+  k_init_population<<<(unsigned)ceil_div(tot, 256), 256, 0, s>>>(X, n, d, seed);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float* F, int* domain_flag,
+                     cudaStream_t s) {
+  if (n < 0 || d < m || m < 2) return MO_ERR_PARAM;
+  if (problem < MO_DTLZ1 || problem > MO_DTLZ7) return MO_ERR_PARAM;
+  if (n == 0) return MO_OK;
+  k_dtlz_eval<<<(unsigned)ceil_div(n, 128), 128, 0, s>>>(problem, X, n, d, m, F, domain_flag);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_min_rows(const float* F, int64_t R, int m, float* ideal, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  k_min_rows<<<(unsigned)ceil_div(R * m, 256), 256, 0, s>>>(F, R, m, ideal);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+}  // namespace mo

@@ -1,0 +1,417 @@
+// extern "C" boundary of libmanyobj_b200.so (declared in include/manyobj_b200.h).
+//
+// Every entry point validates its scalar arguments, carves the caller's
+// workspace, and enqueues kernels on the caller's stream.  No allocation, no
+// synchronisation, no host round trip: device-side outcomes land in `info`.
+#include <string.h>
+
+#include "mo_common.cuh"
+#include "mo_grid.cuh"
+#include "mo_rng.cuh"
+
+namespace mo {
+// k_vary.cu
+int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint64_t seed, uint32_t gen,
+                     const uint32_t* gen_ptr, const mo_var_cfg& cfg, float* Xo, float* Fo, float* ideal,
+                     int* domain_flag, cudaStream_t s);
+int launch_init_population(float* X, int64_t n, int d, uint64_t seed, cudaStream_t s);
+int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float* F, int* domain_flag,
+                     cudaStream_t s);
+// k_dominance.cu
+int64_t words_per_row(int64_t R);
+int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
+int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
+                      int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar, cudaStream_t s);
+}  // namespace mo
+
+#include "k_niche_args.cuh"
+
+namespace mo {
+
+constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/hist sizing)
+
+struct Layout {
+  size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
+      colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
+      hist, sel, total;
+};
+
+static size_t bump(size_t& cur, size_t bytes) {
+  size_t at = (cur + 255) & ~(size_t)255;
+  cur = at + bytes;
+  return at;
+}
+
+static Layout make_layout(int64_t R, int64_t w, int m) {
+  Layout L;
+  size_t c = 0;
+  const int64_t W = words_per_row(R);
+  L.bits = bump(c, (size_t)R * W * 4);
+  L.resume = bump(c, (size_t)R * 4);
+  L.ranked = bump(c, (size_t)W * 4);
+  L.fsizes = bump(c, (size_t)(R + 4) * 4);
+  L.bar = bump(c, 64 * 4);
+  L.pos_pop = bump(c, (size_t)R * 4);
+  L.perm_pop = bump(c, (size_t)R * 4);
+  L.pos_ref = bump(c, (size_t)w * 4);
+  L.perm_ref = bump(c, (size_t)w * 4);
+  L.zs = bump(c, (size_t)w * m * 4);
+  L.cand = bump(c, (size_t)R * 4);
+  L.ctl = bump(c, 64 * 4);
+  L.ext_key = bump(c, 64 * 8);
+  L.colmax = bump(c, 64 * 4);
+  L.icpt = bump(c, 64 * 8);
+  L.a32 = bump(c, 64 * 4);
+  L.akey = bump(c, (size_t)R * 8);
+  L.pi = bump(c, (size_t)R * 4);
+  L.d = bump(c, (size_t)R * 4);
+  L.rho = bump(c, (size_t)(w + 1) * 4);
+  L.rho_p = bump(c, (size_t)(w + 1) * 4);
+  L.take = bump(c, (size_t)(w + 1) * 4);
+  L.bstart = bump(c, (size_t)(w + 1) * 4);
+  L.near_key = bump(c, (size_t)(w + 1) * 8);
+  L.prom = bump(c, (size_t)R);
+  L.keyA = bump(c, (size_t)R * 4);
+  L.valA = bump(c, (size_t)R * 4);
+  L.keyB = bump(c, (size_t)R * 4);
+  L.valB = bump(c, (size_t)R * 4);
+  L.part = bump(c, (size_t)(MAX_GRID + 1) * 4);
+  L.hist = bump(c, (size_t)256 * MAX_GRID * 4);
+  L.sel = bump(c, (size_t)R);
+  L.total = (c + 255) & ~(size_t)255;
+  return L;
+}
+
+template <class T>
+static T* at(void* ws, size_t off) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(ws) + off);
+}
+
+// Barrier slots inside L.bar (each 2 x u32, 64-byte apart to avoid false sharing)
+enum { BAR_PEEL = 0, BAR_PREP = 16, BAR_SELECT = 32 };
+
+static int check_ws(const Layout& L, void* ws, size_t bytes) {
+  if (ws == nullptr || bytes < L.total) return MO_ERR_PARAM;
+  if ((reinterpret_cast<uintptr_t>(ws) & 255u) != 0) return MO_ERR_PARAM;
+  return MO_OK;
+}
+
+static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, int m, int64_t w,
+                          const int* ranks, int* info, float* ideal, uint64_t seed, uint32_t gen,
+                          const float* zhat, double* icpt_out, int mode) {
+  PrepArgs a;
+  a.F = F;
+  a.R = (int)R;
+  a.m = m;
+  a.w = (int)w;
+  a.ranks = ranks;
+  a.info = info;
+  a.ideal = ideal;
+  a.seed = seed;
+  a.gen = gen;
+  a.gen_ptr = nullptr;
+  a.zhat = zhat;
+  a.pos_pop = at<int>(ws, L.pos_pop);
+  a.perm_pop = at<int>(ws, L.perm_pop);
+  a.pos_ref = at<int>(ws, L.pos_ref);
+  a.perm_ref = at<int>(ws, L.perm_ref);
+  a.zs = at<float>(ws, L.zs);
+  a.cand = at<int>(ws, L.cand);
+  a.ctl = at<int>(ws, L.ctl);
+  a.ext_key = at<unsigned long long>(ws, L.ext_key);
+  a.colmax = at<unsigned>(ws, L.colmax);
+  a.icpt = at<double>(ws, L.icpt);
+  a.a32 = at<float>(ws, L.a32);
+  a.akey = at<unsigned long long>(ws, L.akey);
+  a.bar = at<unsigned>(ws, L.bar) + BAR_PREP;
+  a.icpt_out = icpt_out;
+  a.mode = mode;
+  return a;
+}
+
+static SelectArgs select_args(const Layout& L, void* ws, int64_t R, int64_t w, int64_t n, int* ranks, int* info,
+                              const int* pi, const float* d, uint8_t* selected) {
+  SelectArgs a;
+  a.R = (int)R;
+  a.w = (int)w;
+  a.n = (int)n;
+  a.ranks = ranks;
+  a.info = info;
+  a.pi = pi;
+  a.d = d;
+  a.pos_pop = at<int>(ws, L.pos_pop);
+  a.perm_pop = at<int>(ws, L.perm_pop);
+  a.perm_ref = at<int>(ws, L.perm_ref);
+  a.rho = at<int>(ws, L.rho);
+  a.rho_p = at<int>(ws, L.rho_p);
+  a.take = at<int>(ws, L.take);
+  a.bstart = at<int>(ws, L.bstart);
+  a.near_key = at<unsigned long long>(ws, L.near_key);
+  a.prom = at<uint8_t>(ws, L.prom);
+  a.keyA = at<uint32_t>(ws, L.keyA);
+  a.valA = at<int>(ws, L.valA);
+  a.keyB = at<uint32_t>(ws, L.keyB);
+  a.valB = at<int>(ws, L.valB);
+  a.ctl = at<int>(ws, L.ctl);
+  a.selected = selected;
+  a.XR = nullptr;
+  a.FR = nullptr;
+  a.X_next = nullptr;
+  a.F_next = nullptr;
+  a.dvars = 0;
+  a.m = 0;
+  a.gen_ptr = nullptr;
+  a.g.bar = at<unsigned>(ws, L.bar) + BAR_SELECT;
+  a.g.part = at<int>(ws, L.part);
+  a.g.hist = at<int>(ws, L.hist);
+  return a;
+}
+
+__global__ void k_permutation(int n, uint64_t seed, uint32_t gen, uint32_t stream, int* perm, int* pos) {
+  __shared__ uint32_t sK[MAX_SHUFFLE_ROUNDS], sS[MAX_SHUFFLE_ROUNDS];
+  __shared__ int sR;
+  load_shuffle_keys_smem(sK, sS, &sR, (uint32_t)n, seed, gen, stream);
+  __syncthreads();
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (pos) pos[i] = (int)prp((uint32_t)i, sK, sS, sR, (uint32_t)n);
+  if (perm) perm[i] = (int)prp_inv((uint32_t)i, sK, sS, sR, (uint32_t)n);
+}
+
+static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
+  const int64_t n = a->n, R = 2 * n;
+  void* ws = a->workspace;
+  uint32_t* bits = at<uint32_t>(ws, L.bits);
+  MO_TRY(launch_dom_tile(a->FR, R, a->m, nullptr, bits, s));
+  return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
+                           at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, s);
+}
+
+static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
+  const int64_t n = a->n, R = 2 * n, w = a->w;
+  const int m = a->m;
+  void* ws = a->workspace;
+  PrepArgs pa = prep_args(L, ws, a->FR, R, m, w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
+                          nullptr, PREP_FULL);
+  pa.gen_ptr = a->generation_dev;
+  MO_TRY(launch_prep(pa, s));
+  AssocArgs aa;
+  aa.F = a->FR;
+  aa.ideal = a->ideal;
+  aa.a32 = pa.a32;
+  aa.zs = pa.zs;
+  aa.cand = pa.cand;
+  aa.ctl = pa.ctl;
+  aa.info = a->info;
+  aa.w = (int)w;
+  aa.psplit = (int)w;
+  aa.akey = pa.akey;
+  MO_TRY(launch_assoc(aa, m, R, s));
+  AssocFinalArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.F = a->FR;
+  fa.ideal = a->ideal;
+  fa.a32 = pa.a32;
+  fa.zs = pa.zs;
+  fa.perm_ref = pa.perm_ref;
+  fa.cand = pa.cand;
+  fa.ctl = pa.ctl;
+  fa.info = a->info;
+  fa.m = m;
+  fa.akey = pa.akey;
+  fa.pi = at<int>(ws, L.pi);
+  fa.d = at<float>(ws, L.d);
+  MO_TRY(launch_assoc_final(fa, R, s));
+  SelectArgs sa = select_args(L, ws, R, w, n, a->ranks, a->info, fa.pi, fa.d, at<uint8_t>(ws, L.sel));
+  sa.XR = a->XR;
+  sa.FR = a->FR;
+  sa.X_next = a->X_next;
+  sa.F_next = a->F_next;
+  sa.dvars = a->d;
+  sa.m = m;
+  sa.gen_ptr = a->generation_dev;
+  return launch_select(sa, s);
+}
+
+static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
+  const int64_t n = a->n, R = 2 * n;
+  Layout L = make_layout(R, a->w, a->m);
+  MO_TRY(check_ws(L, a->workspace, a->workspace_bytes));
+  if (mask & MO_PHASE_VARY)
+    MO_TRY(launch_vary_eval(a->problem, a->XR, n, a->d, a->m, a->seed, a->generation, a->generation_dev, a->var,
+                            a->XR + n * a->d, a->FR + n * a->m, nullptr, nullptr, s));
+  if (mask & MO_PHASE_SORT) MO_TRY(sort_phase(a, L, s));
+  if (mask & MO_PHASE_NICHE) MO_TRY(niche_phase(a, L, s));
+  return MO_OK;
+}
+
+static int check_step_args(const mo_step_args* a) {
+  if (a == nullptr) return MO_ERR_PARAM;
+  if (a->n < 2 || (a->n & 1) || a->m < 2 || a->m > 16 || a->d < a->m || a->w < 1) return MO_ERR_PARAM;
+  if (2 * a->n > (int64_t)0x7fffffff || a->w > (int64_t)0x7fffffff) return MO_ERR_PARAM;
+  if (!a->zhat || !a->XR || !a->FR || !a->X_next || !a->F_next || !a->ideal || !a->ranks || !a->info)
+    return MO_ERR_PARAM;
+  if (a->problem < MO_DTLZ1 || a->problem > MO_DTLZ7) return MO_ERR_PARAM;
+  return MO_OK;
+}
+
+}  // namespace mo
+
+using namespace mo;
+
+extern "C" {
+
+const char* mo_version(void) { return "manyobj_b200 0.1.0 (sm_100a)"; }
+
+int64_t mo_bits_words_per_row(int64_t R) { return words_per_row(R); }
+
+int mo_workspace_bytes(int64_t n, int32_t m, int32_t d, int64_t w, size_t* bytes) {
+  (void)d;
+  if (!bytes || n < 1 || m < 1 || w < 1) return MO_ERR_PARAM;
+  *bytes = make_layout(2 * n, w, m).total;
+  return MO_OK;
+}
+
+int mo_workspace_bytes_rows(int64_t R, int32_t m, int64_t w, size_t* bytes) {
+  if (!bytes || R < 1 || m < 1 || w < 0) return MO_ERR_PARAM;
+  *bytes = make_layout(R, w > 0 ? w : 1, m).total;
+  return MO_OK;
+}
+
+int mo_permutation(int64_t n, uint64_t seed, uint32_t generation, uint32_t stream, int32_t* perm, int32_t* pos,
+                   void* stream_) {
+  if (n < 0 || n > (int64_t)0x7fffffff) return MO_ERR_PARAM;
+  if (n == 0) return MO_OK;
+  k_permutation<<<(unsigned)ceil_div(n, 256), 256, 0, (cudaStream_t)stream_>>>((int)n, seed, generation, stream,
+                                                                             perm, pos);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int mo_init_population(float* X, int64_t n, int32_t d, uint64_t seed, void* stream_) {
+  return launch_init_population(X, n, d, seed, (cudaStream_t)stream_);
+}
+
+int mo_dtlz_eval(int32_t problem, const float* X, int64_t n, int32_t d, int32_t m, float* F, int32_t* domain_flag,
+                 void* stream_) {
+  return launch_dtlz_eval(problem, X, n, d, m, F, domain_flag, (cudaStream_t)stream_);
+}
+
+int mo_vary_eval(int32_t problem, const float* X, int64_t n, int32_t d, int32_t m, uint64_t seed, uint32_t generation,
+                 const mo_var_cfg* cfg, float* Xo, float* Fo, float* ideal, void* stream_) {
+  if (!cfg) return MO_ERR_PARAM;
+  return launch_vary_eval(problem, X, n, d, m, seed, generation, nullptr, *cfg, Xo, Fo, ideal, nullptr,
+                          (cudaStream_t)stream_);
+}
+
+int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid, uint32_t* bits, void* stream_) {
+  return launch_dom_tile(F, R, m, valid, bits, (cudaStream_t)stream_);
+}
+
+int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int32_t* ranks,
+                  int32_t* info, void* workspace, size_t workspace_bytes, void* stream_) {
+  Layout L = make_layout(R, 1, 1);
+  MO_TRY(check_ws(L, workspace, workspace_bytes));
+  return launch_front_peel(bits, R, valid, stop_at, ranks, info, at<int>(workspace, L.resume),
+                           at<uint32_t>(workspace, L.ranked), at<int>(workspace, L.fsizes),
+                           at<unsigned>(workspace, L.bar) + BAR_PEEL, (cudaStream_t)stream_);
+}
+
+int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, const int32_t* info, uint64_t seed,
+                 uint32_t generation, float* ideal, float* Fn, double* intercepts, void* workspace,
+                 size_t workspace_bytes, void* stream_) {
+  if (m < 1 || m > 64 || R < 1) return MO_ERR_PARAM;
+  Layout L = make_layout(R, 1, m);
+  MO_TRY(check_ws(L, workspace, workspace_bytes));
+  cudaStream_t s = (cudaStream_t)stream_;
+  // w = 1 dummy reference point set: only the row shuffle matters here
+  // w = 1 and no reference set: only the row shuffle (extreme-point ties) matters here
+  PrepArgs pa = prep_args(L, workspace, F, R, m, 1, ranks, const_cast<int*>(info), ideal, seed, generation,
+                          nullptr, intercepts, PREP_FULL);
+  MO_TRY(launch_prep(pa, s));
+  if (Fn) {
+    AssocFinalArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fa.F = F;
+    fa.ideal = ideal;
+    fa.a32 = pa.a32;
+    fa.cand = pa.cand;
+    fa.ctl = pa.ctl;
+    fa.info = info;
+    fa.m = m;
+    fa.Fn_out = Fn;
+    fa.fn_only = 1;
+    MO_TRY(launch_assoc_final(fa, R, s));
+  }
+  return MO_OK;
+}
+
+int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64_t w, const int32_t* ranks,
+                 const int32_t* info, uint64_t seed, uint32_t generation, int32_t* pi, float* d, void* workspace,
+                 size_t workspace_bytes, void* stream_) {
+  if (m < 1 || m > 16 || R < 1 || w < 1) return MO_ERR_PARAM;
+  Layout L = make_layout(R, w, m);
+  MO_TRY(check_ws(L, workspace, workspace_bytes));
+  cudaStream_t s = (cudaStream_t)stream_;
+  PrepArgs pa = prep_args(L, workspace, Fn, R, m, w, ranks, const_cast<int*>(info), nullptr, seed, generation, zhat,
+                          nullptr, PREP_PERMS_CAND);
+  MO_TRY(launch_prep(pa, s));
+  AssocArgs aa;
+  aa.F = Fn;
+  aa.ideal = nullptr;
+  aa.a32 = nullptr;
+  aa.zs = pa.zs;
+  aa.cand = pa.cand;
+  aa.ctl = pa.ctl;
+  aa.info = info;
+  aa.w = (int)w;
+  aa.psplit = (int)w;
+  aa.akey = pa.akey;
+  MO_TRY(launch_assoc(aa, m, R, s));
+  AssocFinalArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  fa.F = Fn;
+  fa.zs = pa.zs;
+  fa.perm_ref = pa.perm_ref;
+  fa.cand = pa.cand;
+  fa.ctl = pa.ctl;
+  fa.info = info;
+  fa.m = m;
+  fa.akey = pa.akey;
+  fa.pi = pi;
+  fa.d = d;
+  return launch_assoc_final(fa, R, s);
+}
+
+int mo_niche_select(const int32_t* pi, const float* d, int64_t R, int64_t w, int64_t n, int32_t* ranks,
+                    int32_t* info, uint64_t seed, uint32_t generation, uint8_t* selected, void* workspace,
+                    size_t workspace_bytes, void* stream_) {
+  if (R < 1 || w < 1 || n < 1) return MO_ERR_PARAM;
+  Layout L = make_layout(R, w, 1);
+  MO_TRY(check_ws(L, workspace, workspace_bytes));
+  cudaStream_t s = (cudaStream_t)stream_;
+  // shuffles only (rows and reference points)
+  PrepArgs pa = prep_args(L, workspace, nullptr, R, 1, w, ranks, info, nullptr, seed, generation, nullptr, nullptr,
+                          PREP_PERMS);
+  MO_TRY(launch_prep(pa, s));
+  SelectArgs sa = select_args(L, workspace, R, w, n, ranks, info, pi, d, selected);
+  return launch_select(sa, s);
+}
+
+int mo_select(const mo_step_args* args, void* stream_) {
+  MO_TRY(check_step_args(args));
+  return run_phases(args, MO_PHASE_SORT | MO_PHASE_NICHE, (cudaStream_t)stream_);
+}
+
+int mo_step(const mo_step_args* a, void* stream_) {
+  MO_TRY(check_step_args(a));
+  return run_phases(a, MO_PHASE_ALL, (cudaStream_t)stream_);
+}
+
+int mo_step_phases(const mo_step_args* a, uint32_t phase_mask, void* stream_) {
+  MO_TRY(check_step_args(a));
+  if (phase_mask == 0 || (phase_mask & ~(uint32_t)MO_PHASE_ALL)) return MO_ERR_PARAM;
+  return run_phases(a, phase_mask, (cudaStream_t)stream_);
+}
+
+}  // extern "C"

@@ -1,0 +1,140 @@
+// Shared device/host helpers for the manyobj B200 engine (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/manyobj_b200.h"
+
+#ifndef __CUDACC__
+#error "mo_common.cuh is CUDA-only"
+#endif
+
+#define MO_WARP 32
+#define MO_FULL 0xffffffffu
+#define MO_RANK_UNRANKED (-2)
+#define MO_RANK_DROPPED 0x7fffffff
+#define MO_INF 0x7fffffff
+
+// Launch-error check used by every entry point: converts a CUDA error to MO_ERR_CUDA.
+#define MO_CHECK_LAUNCH()                                  \
+  do {                                                     \
+    cudaError_t e__ = cudaGetLastError();                  \
+    if (e__ != cudaSuccess) return MO_ERR_CUDA;            \
+  } while (0)
+
+#define MO_TRY(expr)                                       \
+  do {                                                     \
+    int s__ = (expr);                                      \
+    if (s__ != MO_OK) return s__;                          \
+  } while (0)
+
+namespace mo {
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Order-preserving map FP32 -> uint32 (total order for non-NaN values, -0 < +0 is fine here).
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(MO_FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t t = __shfl_xor_sync(MO_FULL, v, o);
+    v = t < v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t t = __shfl_xor_sync(MO_FULL, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(MO_FULL, v, o));
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(MO_FULL, v, o));
+  return v;
+}
+
+// Warp-aggregated histogram increment: lanes with equal `bin` elect one leader
+// (__match_any_sync) that adds the group's population with a single atomic.
+__device__ __forceinline__ void warp_agg_add(int* hist, int bin, bool active) {
+  unsigned act = __ballot_sync(MO_FULL, active);
+  if (!active) return;
+  unsigned peers = __match_any_sync(act, bin);
+  int leader = __ffs(peers) - 1;
+  if ((int)lane_id() == leader) atomicAdd(hist + bin, __popc(peers));
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x multiple of 32, <= 1024).
+// `sh` must hold >= 33 ints.  Returns the exclusive prefix; *total gets the block sum.
+__device__ __forceinline__ int block_excl_scan(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(MO_FULL, x, o);
+    if (lane >= o) x += t;
+  }
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < nw ? sh[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(MO_FULL, s, o);
+      if (lane >= o) s += t;
+    }
+    if (lane < nw) sh[lane] = s;
+    if (lane == 31) sh[32] = s;
+  }
+  __syncthreads();
+  int res = x - v + (wid > 0 ? sh[wid - 1] : 0);
+  *total = sh[32];
+  __syncthreads();
+  return res;
+}
+
+// Sense-reversing software grid barrier for persistent kernels launched with
+// cudaLaunchAttributeCooperative (all CTAs co-resident).  `bar` = {count, gen}.
+__device__ __forceinline__ void grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    unsigned gen = *vgen;
+    __threadfence();
+    unsigned arrived = atomicAdd(bar, 1u) + 1u;
+    if (arrived == gridDim.x) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace mo

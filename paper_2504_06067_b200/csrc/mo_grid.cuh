@@ -1,0 +1,135 @@
+// Grid-wide primitives for persistent cooperative kernels: chunked stable
+// scans/compactions and a stable LSD radix-sort pass.  Every block of the grid
+// must call these with identical arguments (they contain grid barriers).
+#pragma once
+#include "mo_common.cuh"
+
+namespace mo {
+
+struct GridCtx {
+  unsigned* bar;  // {count, gen}
+  int* part;      // >= gridDim.x + 1 ints
+  int* hist;      // >= 256 * gridDim.x ints (radix)
+};
+
+// Stable exclusive scan of value(e) over e in [0, N) in ascending e.  Calls
+// emit(e, prefix) for every e with value(e) != 0.  Returns the grand total.
+// `sh` must hold >= 34 ints of shared memory.  One internal grid barrier.
+template <class ValueF, class EmitF>
+__device__ int grid_scan(const GridCtx& g, int64_t N, ValueF value, EmitF emit, int* sh) {
+  const int G = gridDim.x, b = blockIdx.x;
+  const int64_t chunk = ceil_div(N, (int64_t)G);
+  const int64_t lo = min((int64_t)b * chunk, N), hi = min(lo + chunk, N);
+  int cnt = 0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) cnt += value(e);
+  int tot;
+  block_excl_scan(cnt, sh, &tot);
+  if (threadIdx.x == 0) g.part[b] = tot;
+  grid_sync(g.bar);
+  // offset = sum of parts of earlier blocks; total = sum of all parts
+  int pre = 0, all = 0;
+  for (int q = threadIdx.x; q < G; q += blockDim.x) {
+    int v = __ldcg(g.part + q);
+    all += v;
+    if (q < b) pre += v;
+  }
+  int dummy;
+  int s1 = block_excl_scan(pre, sh, &dummy);
+  (void)s1;
+  int offset = dummy;
+  block_excl_scan(all, sh, &dummy);
+  int total = dummy;
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    int64_t e = base + threadIdx.x;
+    int v = (e < hi) ? value(e) : 0;
+    int t;
+    int p = block_excl_scan(v, sh, &t);
+    if (v) emit(e, offset + p);
+    offset += t;
+  }
+  return total;
+}
+
+// One stable LSD radix pass (8-bit digit at `shift`) of N (key, val) pairs
+// from (kin, vin) to (kout, vout).  Shared memory: `wcnt` >= (blockDim/32)*256
+// ints, `run`/`off` >= 256 ints each.  Two internal grid barriers.
+__device__ inline void grid_radix_pass(const GridCtx& g, int N, int shift, const uint32_t* kin, const int* vin,
+                                       uint32_t* kout, int* vout, int* wcnt, int* run, int* off, int* sh) {
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nw = blockDim.x >> 5;
+  const int chunk = (int)ceil_div(N, G);
+  const int lo = min(b * chunk, N), hi = min(lo + chunk, N);
+  // 1. block digit histogram -> hist[d * G + b]
+  for (int d = tid; d < 256; d += blockDim.x) run[d] = 0;
+  __syncthreads();
+  for (int e = lo + tid; e < hi; e += blockDim.x) atomicAdd(&run[(__ldcg(kin + e) >> shift) & 255u], 1);
+  __syncthreads();
+  for (int d = tid; d < 256; d += blockDim.x) g.hist[d * G + b] = run[d];
+  grid_sync(g.bar);
+  // 2. global offset of (digit d, this block): totals of smaller digits + earlier blocks of digit d
+  for (int d = tid; d < 256; d += blockDim.x) {
+    int pre = 0, tot = 0;
+    for (int q = 0; q < G; ++q) {
+      int v = __ldcg(g.hist + d * G + q);
+      tot += v;
+      if (q < b) pre += v;
+    }
+    off[d] = pre;
+    run[d] = tot;
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of 256 digit totals by one warp (8 per lane)
+    int v[8], s = 0;
+    for (int q = 0; q < 8; ++q) {
+      v[q] = run[lane * 8 + q];
+      s += v[q];
+    }
+    int x = s;
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(MO_FULL, x, o);
+      if (lane >= o) x += t;
+    }
+    int ex = x - s;
+    for (int q = 0; q < 8; ++q) {
+      off[lane * 8 + q] += ex;
+      ex += v[q];
+    }
+  }
+  for (int d = tid; d < 256; d += blockDim.x) run[d] = 0;  // running count per digit in this block
+  for (int q = tid; q < nw * 256; q += blockDim.x) wcnt[q] = 0;
+  __syncthreads();
+  // 3. stable scatter, one blockDim tile at a time
+  for (int base = lo; base < hi; base += blockDim.x) {
+    const int e = base + tid;
+    const bool act = e < hi;
+    uint32_t key = act ? __ldcg(kin + e) : 0u;
+    int val = act ? __ldcg(vin + e) : 0;
+    const int dg = act ? (int)((key >> shift) & 255u) : 256 + lane;
+    const unsigned peers = __match_any_sync(MO_FULL, dg);
+    const int rank_w = __popc(peers & ((1u << lane) - 1u));
+    if (act && rank_w == 0) wcnt[wid * 256 + dg] = __popc(peers);
+    __syncthreads();
+    for (int d = tid; d < 256; d += blockDim.x) {
+      int r = run[d];
+      for (int q = 0; q < nw; ++q) {
+        int c = wcnt[q * 256 + d];
+        wcnt[q * 256 + d] = r;
+        r += c;
+      }
+      run[d] = r;
+    }
+    __syncthreads();
+    if (act) {
+      const int pos = off[dg] + wcnt[wid * 256 + dg] + rank_w;
+      kout[pos] = key;
+      vout[pos] = val;
+    }
+    __syncthreads();
+    for (int q = tid; q < nw * 256; q += blockDim.x) wcnt[q] = 0;
+    __syncthreads();
+  }
+  grid_sync(g.bar);
+  (void)sh;
+}
+
+}  // namespace mo

@@ -1,0 +1,108 @@
+"""Pareto dominance and non-dominated sorting on the GPU.
+
+``dominance_matrix`` / ``non_dominated_sort`` / ``split_fronts`` keep the
+reference signatures; the work runs in ``k_dom_tile`` (warp-ballot bit-matrix)
+and ``k_front_peel`` (persistent resume-scan peeling) of libmanyobj_b200.so.
+"""
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._tensor import as_cuda, as_mask, as_matrix, device
+from .errors import InfeasibleSplitError, ShapeError
+
+DROPPED = _lib.DROPPED
+
+
+def dominates(a, b):
+    """a <= b everywhere and a < b somewhere."""
+    a = as_cuda(a, torch.float32)
+    b = as_cuda(b, torch.float32)
+    if a.shape != b.shape:
+        raise ShapeError("objective vectors differ in length")
+    return bool(((a <= b).all() & (a < b).any()).item())
+
+
+def dominance_bits(F, valid=None):
+    """Raw bit-matrix: (R x W) int32 words, bit i of row j = "F[i] dominates F[j]"."""
+    F = as_matrix(F)
+    R, m = F.shape
+    W = int(_lib.lib().mo_bits_words_per_row(R))
+    bits = torch.empty((R, W), dtype=torch.int32, device=F.device)
+    v = as_mask(valid, R)
+    _lib.check(_lib.lib().mo_dominance_bits(_lib.ptr(F), R, m, _lib.ptr(v), _lib.ptr(bits), _lib.stream_ptr()),
+               "mo_dominance_bits")
+    return bits
+
+
+def unpack_bits(bits, R):
+    """(R x W) words -> dense bool M with M[i][j] = bit i of row j."""
+    w = bits.view(torch.int32)
+    shifts = torch.arange(32, device=w.device, dtype=torch.int32)
+    b = ((w.unsqueeze(-1) >> shifts) & 1).bool()          # rows j, words, bit -> i
+    dom_of = b.reshape(w.shape[0], -1)[:, :R]              # [j, i]
+    return dom_of.t().contiguous()                         # [i, j]
+
+
+def dominance_matrix(F, valid=None):
+    """M[i][j] = dominates(F[i], F[j]) as a bool CUDA tensor."""
+    F = as_matrix(F)
+    return unpack_bits(dominance_bits(F, valid), F.shape[0])
+
+
+def non_dominated_sort(F, valid=None, stop_at=None, return_info=False):
+    """Front index per row; invalid / beyond-split rows -> DROPPED.
+
+    ``stop_at`` (the engine's n) stops peeling at the first front whose
+    cumulative size reaches it.  Returns an int32 CUDA tensor.
+    """
+    F = as_matrix(F)
+    R, m = F.shape
+    if R == 0:
+        raise ShapeError("need at least one row")
+    bits = dominance_bits(F, valid)
+    v = as_mask(valid, R)
+    ranks = torch.empty(R, dtype=torch.int32, device=F.device)
+    info = _lib.new_info(F.device)
+    ws = _lib.workspace_rows(R, m, 1, F.device)
+    L = _lib.lib()
+    _lib.check(L.mo_front_peel(_lib.ptr(bits), R, _lib.ptr(v), int(stop_at or 0), _lib.ptr(ranks), _lib.ptr(info),
+                               _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "mo_front_peel")
+    if return_info:
+        return ranks, info
+    return ranks
+
+
+@dataclass(frozen=True)
+class FrontSplit:
+    """SPEC.md:172-175."""
+    l: int
+    selected_count: int
+    k: int
+
+
+def split_fronts(ranks, n):
+    """l / selected_count / k of a rank vector."""
+    r = as_cuda(ranks, torch.int64)
+    live = r[r != DROPPED]
+    if live.numel() < n:
+        raise InfeasibleSplitError(f"{live.numel()} valid individuals < n={n}")
+    sizes = torch.bincount(live)
+    cum = torch.cumsum(sizes, 0)
+    l = int(torch.searchsorted(cum, torch.tensor([n], device=cum.device)).item())
+    sel = int(cum[l - 1].item()) if l > 0 else 0
+    return FrontSplit(l, sel, n - sel)
+
+
+def split_from_info(info):
+    """FrontSplit from the device info record written by mo_front_peel / mo_step."""
+    h = info.cpu().tolist()
+    err = h[_lib.INFO["ERROR"]]
+    if err:
+        _lib.check(err, "front peeling")
+    return FrontSplit(h[_lib.INFO["L"]], h[_lib.INFO["SELECTED"]], h[_lib.INFO["K"]])
+
+
+__all__ = ["DROPPED", "dominates", "dominance_bits", "dominance_matrix", "non_dominated_sort", "FrontSplit",
+           "split_fronts", "split_from_info", "unpack_bits", "device"]

@@ -1,0 +1,329 @@
+"""GPU (sm_100a) parity against the CPU oracle, through the C-ABI library.
+
+Bit-exact: permutations, initial population, dominance bits, ranks, split,
+ideal, intercepts, Fn, pi, d, survivor sets.  Tolerance (north star: 1e-5
+relative in FP32): offspring and objectives, which the GPU computes in FP64
+and rounds once (so they agree to ~1 ulp in practice; tested at rtol 1e-6).
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import examples
+from oracle.manyobj_ref import dominance as Odom
+from oracle.manyobj_ref import engine as Oeng
+from oracle.manyobj_ref import niche as Oniche
+from oracle.manyobj_ref import problems as Oprob
+from oracle.manyobj_ref import refpoints as Oref
+from oracle.manyobj_ref import rng as Orng
+from oracle.manyobj_ref import variation as Ovar
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2504_06067_b200 as pkg
+    from paper_2504_06067_b200 import _lib
+    _lib.lib()  # fails loudly without the library / device
+    return pkg
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+# ------------------------------------------------------------------ L1 / RNG
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 184, 1000, 20000])
+def test_permutation_bit_exact(M, n):
+    for seed, gen, stream in [(0, 0, 5), (123456789012, 7, 6), (5, 99, 2)]:
+        perm = M.variation.permutation(n, seed, gen, stream)
+        assert np.array_equal(np_(perm), Orng.permutation(n, seed, gen, stream))
+
+
+def test_init_population_bit_exact(M):
+    X = M.variation.init_population(92, 7, 11)
+    assert np.array_equal(np_(X), Oeng.initial_population(92, 7, 11))
+
+
+@pytest.mark.parametrize("kind", Oprob.KINDS)
+def test_dtlz_eval_matches_oracle(M, kind):
+    rs = np.random.default_rng(1)
+    for m, d in [(3, 7), (5, 14), (10, 19), (3, 22)]:
+        X = rs.random((257, d)).astype(np.float32)
+        X[:5] = np.round(X[:5])                   # exact 0/1 corners
+        P = M.problems.ContinuousProblem(kind, m, d)
+        got = np_(M.problems.dtlz_eval(P, X))
+        want = Oprob.dtlz_eval(Oprob.ContinuousProblem(kind, m, d), X.astype(np.float64)).astype(np.float32)
+        assert np.allclose(got, want, rtol=1e-6, atol=1e-7), (kind, m, d)
+
+
+def test_dtlz_golden(M):
+    from paper_2504_06067_b200 import errors
+    for ex in examples({"dtlz_point", "dtlz_domain"}):
+        P = M.problems.ContinuousProblem(ex["kind"], ex["m"], ex["d"])
+        if "error" in ex:
+            with pytest.raises(errors.DomainError):
+                M.problems.dtlz_eval(P, np.array([ex["x"]], np.float32))
+        else:
+            assert np.allclose(np_(M.problems.dtlz_eval(P, np.array([ex["x"]], np.float32)))[0], ex["out"],
+                               atol=1e-6)
+
+
+@pytest.mark.parametrize("kind,m,d", [("DTLZ1", 3, 7), ("DTLZ2", 5, 14), ("DTLZ3", 10, 19), ("DTLZ7", 3, 22),
+                                      ("DTLZ4", 4, 9), ("DTLZ5", 4, 9), ("DTLZ6", 4, 9)])
+def test_vary_eval_matches_oracle(M, kind, m, d):
+    rs = np.random.default_rng(3)
+    n = 256
+    X = rs.random((n, d)).astype(np.float32)
+    X[:4, :2] = 0.0
+    X[4:8, :2] = 1.0
+    cfg = M.variation.VariationConfig()
+    P = M.problems.ContinuousProblem(kind, m, d)
+    Xo, Fo = M.variation.vary_eval(P, X, cfg, seed=77, generation=5)
+    want_X = Ovar.vary(X, Ovar.VariationConfig(), 77, 5)
+    assert np.allclose(np_(Xo), want_X, rtol=1e-6, atol=1e-7)
+    want_F = Oprob.dtlz_eval(Oprob.ContinuousProblem(kind, m, d), np_(Xo).astype(np.float64)).astype(np.float32)
+    assert np.allclose(np_(Fo), want_F, rtol=1e-6, atol=1e-7)
+    # bit-exact fraction: FP64 internals round to the same FP32 almost always
+    assert (np_(Xo) == want_X).mean() > 0.999
+
+
+# ----------------------------------------------------------------- dominance
+
+def _instances():
+    rs = np.random.default_rng(21)
+    for R, m in [(1, 2), (2, 2), (31, 3), (32, 3), (255, 2), (256, 5), (257, 3), (700, 4), (1100, 10),
+                 (600, 1)]:
+        yield rs.random((R, m)).astype(np.float32)
+        yield rs.integers(0, 3, size=(R, m)).astype(np.float32)       # ties + duplicates
+
+
+def test_dominance_matrix_bit_exact(M):
+    for F in _instances():
+        got = np_(M.dominance.dominance_matrix(F))
+        assert np.array_equal(got, Odom.dominance_matrix(F)), F.shape
+
+
+def test_dominance_with_valid_mask(M):
+    rs = np.random.default_rng(5)
+    F = rs.integers(0, 4, size=(300, 3)).astype(np.float32)
+    valid = rs.random(300) < 0.7
+    got = np_(M.dominance.dominance_matrix(F, valid))
+    D = Odom.dominance_matrix(F)
+    D &= valid[:, None] & valid[None, :]
+    assert np.array_equal(got, D)
+    r = np_(M.dominance.non_dominated_sort(F, valid))
+    assert np.array_equal(r, Odom.non_dominated_sort(F, valid))
+
+
+def test_nds_bit_exact(M):
+    for F in _instances():
+        assert np.array_equal(np_(M.dominance.non_dominated_sort(F)), Odom.non_dominated_sort(F)), F.shape
+
+
+def test_nds_stop_at(M):
+    rs = np.random.default_rng(8)
+    for R, m in [(184, 3), (2000, 3), (4000, 5)]:
+        F = rs.random((R, m)).astype(np.float32)
+        n = R // 2
+        ranks, info = M.dominance.non_dominated_sort(F, stop_at=n, return_info=True)
+        want = Odom.non_dominated_sort(F, stop_at=n)
+        assert np.array_equal(np_(ranks), want)
+        sp = M.dominance.split_from_info(info)
+        wsp = Odom.split_fronts(want, n)
+        assert (sp.l, sp.selected_count, sp.k) == (wsp.l, wsp.selected_count, wsp.k)
+
+
+def test_dominance_golden(M):
+    from paper_2504_06067_b200 import errors
+    for ex in examples({"dominates", "dominance_matrix", "non_dominated_sort", "split_fronts"}):
+        op = ex["op"]
+        if op == "dominates":
+            if "error" in ex:
+                with pytest.raises(errors.ShapeError):
+                    M.dominance.dominates(ex["a"], ex["b"])
+            else:
+                assert M.dominance.dominates(ex["a"], ex["b"]) == ex["out"]
+        elif op == "dominance_matrix":
+            assert np_(M.dominance.dominance_matrix(np.array(ex["F"], np.float32))).tolist() == ex["out"]
+        elif op == "non_dominated_sort":
+            assert np_(M.dominance.non_dominated_sort(np.array(ex["F"], np.float32))).tolist() == ex["out"]
+        else:
+            ranks = np.concatenate([np.full(s, i) for i, s in enumerate(ex["sizes"])]).astype(np.int32)
+            if "error" in ex:
+                with pytest.raises(errors.InfeasibleSplitError):
+                    M.dominance.split_fronts(ranks, ex["n"])
+            else:
+                sp = M.dominance.split_fronts(ranks, ex["n"])
+                assert [sp.l, sp.selected_count, sp.k] == ex["out"]
+
+
+def test_nds_infeasible(M):
+    from paper_2504_06067_b200 import errors
+    F = np.random.default_rng(0).random((10, 3)).astype(np.float32)
+    valid = np.zeros(10, bool)
+    valid[:3] = True
+    _, info = M.dominance.non_dominated_sort(F, valid, stop_at=5, return_info=True)
+    with pytest.raises(errors.InfeasibleSplitError):
+        M.dominance.split_from_info(info)
+
+
+# -------------------------------------------------------------------- niche
+
+def _front_instance(seed, R, m, kind="DTLZ2"):
+    rs = np.random.default_rng(seed)
+    X = rs.random((R, m + 4)).astype(np.float32)
+    F = Oprob.dtlz_eval(Oprob.ContinuousProblem(kind, m, m + 4), X).astype(np.float32)
+    n = R // 2
+    ranks = Odom.non_dominated_sort(F, stop_at=n)
+    sp = Odom.split_fronts(ranks, n)
+    return F, ranks, sp, n
+
+
+@pytest.mark.parametrize("seed,R,m", [(0, 184, 3), (1, 2000, 5), (2, 4000, 3), (3, 3000, 10), (4, 1000, 8)])
+def test_normalize_bit_exact(M, seed, R, m):
+    F, ranks, sp, n = _front_instance(seed, R, m)
+    cand = (ranks <= sp.l) & (ranks != Odom.DROPPED)
+    ideal0 = np.full(m, np.inf, np.float32)
+    gen = 3
+    pos_pop = Orng.positions(R, seed, gen, Orng.STREAM_POP_SHUFFLE)
+    Fn, ideal, a, ext, singular = Oniche.normalize_objectives(F, ideal0, cand, pos_pop)
+    gFn, gideal, gicpt = M.niche.normalize_objectives(F, ideal0, ranks.astype(np.int32), sp.l, seed, gen)
+    assert np.array_equal(np_(gideal), ideal)
+    assert np.array_equal(np_(gicpt), a)
+    assert np.array_equal(np_(gFn)[cand], Fn[cand])
+
+
+def test_normalize_golden(M):
+    for ex in examples({"normalize"}):
+        F = np.array(ex["F"], np.float32)
+        ideal = None if ex["ideal"] is None else np.array(ex["ideal"], np.float32)
+        Fn, idl, a = M.niche.normalize_objectives(F, ideal)
+        assert np.allclose(np_(Fn), ex["out"], atol=1e-6)
+        if "intercepts" in ex:
+            assert np.allclose(np_(a), ex["intercepts"])
+
+
+@pytest.mark.parametrize("seed,R,m,w_target", [(0, 184, 3, 91), (1, 2000, 5, 1000), (2, 5000, 3, 2500),
+                                              (3, 3000, 10, 1500), (4, 1024, 2, 512)])
+def test_associate_bit_exact(M, seed, R, m, w_target):
+    F, ranks, sp, n = _front_instance(seed, R, m)
+    cand = (ranks <= sp.l) & (ranks != Odom.DROPPED)
+    Z = Oref.reference_points(m, w_target)
+    zh = Oref.unit_directions(Z)
+    gen = 4
+    pos_pop = Orng.positions(R, seed, gen, Orng.STREAM_POP_SHUFFLE)
+    pos_ref = Orng.positions(len(Z), seed, gen, Orng.STREAM_REF_SHUFFLE)
+    Fn, *_ = Oniche.normalize_objectives(F, np.full(m, np.inf, np.float32), cand, pos_pop)
+    pi, d = Oniche.associate_canonical(Fn, zh, pos_ref, np.flatnonzero(cand))
+    Fn_in = np.where(cand[:, None], Fn, 0).astype(np.float32)
+    gpi, gd = M.niche.associate(Fn_in, zh, ranks.astype(np.int32), sp.l, seed, gen)
+    assert np.array_equal(np_(gpi)[cand], pi[cand])
+    assert np.array_equal(np_(gd)[cand], d[cand])
+    assert (np_(gpi)[~cand] == -1).all()
+
+
+@pytest.mark.parametrize("seed,R,m,w_target", [(0, 184, 3, 91), (1, 2000, 5, 1000), (2, 6000, 3, 3000),
+                                              (5, 2000, 3, 40), (6, 1500, 8, 700)])
+def test_niche_select_bit_exact(M, seed, R, m, w_target):
+    F, ranks, sp, n = _front_instance(seed, R, m)
+    Z = Oref.reference_points(m, w_target)
+    zh = Oref.unit_directions(Z)
+    gen = 2
+    sel, info = Oniche.select(F, ranks, sp, np.full(m, np.inf, np.float32), zh, seed, gen)
+    if info["skipped"]:
+        pytest.skip("instance needed no niching")
+    gsel, granks, ginfo = M.niche.niche_select(info["pi"].astype(np.int32), info["d"], ranks.astype(np.int32),
+                                               sp, n, len(Z), seed, gen)
+    assert np.array_equal(np_(gsel), sel)
+    assert int(np_(gsel).sum()) == n
+    assert ginfo["NEAREST"] == len(info["nearest"])
+
+
+# ------------------------------------------------------------------- engine
+
+def _gpu_state_to_oracle(eng):
+    return Oeng.RunState(eng.generation, np_(eng.X).copy(), np_(eng.F).copy(), np_(eng.ideal).copy(),
+                         Oref.unit_directions(eng.Z), eng.Z)
+
+
+@pytest.mark.parametrize("kind,n,m,d,gens", [("DTLZ1", 92, 3, 7, 30), ("DTLZ2", 1000, 5, 14, 6),
+                                             ("DTLZ3", 400, 10, 19, 4), ("DTLZ7", 600, 3, 22, 6),
+                                             ("DTLZ4", 200, 4, 13, 6), ("DTLZ5", 200, 4, 13, 6),
+                                             ("DTLZ6", 200, 3, 12, 6)])
+def test_engine_step_state_injection(M, kind, n, m, d, gens):
+    """Every generation: the oracle's selection on the GPU's merged objectives picks the GPU's survivors."""
+    cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=17)
+    ocfg = Oeng.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=17)
+    eng = M.engine.Engine(cfg)
+    X0 = Oeng.initial_population(n, d, 17)
+    assert np.array_equal(np_(eng.X), X0)
+    skipped = niched = 0
+    for g in range(gens):
+        st = _gpu_state_to_oracle(eng)
+        cur = eng.cur
+        eng.step()
+        # offspring the GPU produced (rows n..2n of the merged buffer it just consumed)
+        O = np_(eng.XR[cur][n:]).copy()
+        FO = np_(eng.FR[cur][n:]).copy()
+        want_O = Ovar.vary(st.X, ocfg.variation, 17, g)
+        assert np.allclose(O, want_O, rtol=1e-6, atol=1e-7)
+        nxt = Oeng.step(st, ocfg, offspring=(O, FO))
+        info = eng.info_dict()
+        assert info["survivors"] == n
+        assert info["l"] == nxt.info["l"] and info["k"] == nxt.info["k"]
+        assert np.array_equal(np_(eng.X), nxt.X), f"generation {g}"
+        assert np.array_equal(np_(eng.F), nxt.F)
+        assert np.array_equal(np_(eng.ideal), nxt.ideal)
+        skipped += info["skipped"]
+        niched += 1 - info["skipped"]
+    assert niched > 0
+
+
+def test_engine_graph_equals_eager(M):
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=500, m=5, d=14, generations=8, seed=4)
+    a = M.engine.Engine(cfg)
+    for _ in range(8):
+        a.step()
+    b = M.engine.Engine(cfg, graph=True)
+    b.replay(8)
+    torch.cuda.synchronize()
+    assert a.generation == b.generation == 8
+    assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F) and torch.equal(a.ideal, b.ideal)
+
+
+def test_engine_determinism(M):
+    cfg = M.engine.RunConfig(problem="DTLZ1", n=92, m=3, d=7, generations=20, seed=9)
+    h1, s1 = M.engine.run(cfg)
+    h2, s2 = M.engine.run(cfg)
+    assert h1 == h2 and torch.equal(s1.X, s2.X)
+
+
+def test_engine_c2_full_size_properties(M):
+    """C2 (DTLZ2 m=5 d=14 n=10k): size-independent invariants of one generation at full size."""
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=10000, m=5, d=14, generations=3, seed=0)
+    eng = M.engine.Engine(cfg)
+    for _ in range(3):
+        eng.step()
+        info = eng.info_dict()
+        assert info["survivors"] == 10000 and info["error"] == 0
+    F = eng.F
+    assert torch.isfinite(F).all() and (eng.X >= 0).all() and (eng.X <= 1).all()
+    # ranks of the last step against the oracle NDS of the same merged objectives
+    FR = np_(eng.FR[eng.cur ^ 1]).copy()
+    ranks = Odom.non_dominated_sort(FR, stop_at=10000)
+    l = Odom.split_fronts(ranks, 10000).l
+    g = np_(eng.ranks)
+    assert info["l"] == l
+    assert np.array_equal(g[ranks < l], ranks[ranks < l])
+    assert np.isin(g[ranks == l], [l, l - 1]).all()
+    assert (g[ranks == Odom.DROPPED] == Odom.DROPPED).all()
+
+
+def test_engine_rejects_oracle_backend(M):
+    from paper_2504_06067_b200 import errors
+    with pytest.raises(errors.ConfigError) as ei:
+        M.engine.initialize(M.engine.RunConfig(backend="oracle"))
+    assert ei.value.field == "backend"
