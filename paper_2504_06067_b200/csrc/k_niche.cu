@@ -297,8 +297,6 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
   if (c >= ncand) return;
   const int m = a.m;
   const int row = __ldcg(a.cand + c);
-  const unsigned long long key = __ldcg(a.akey + row);
-  const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
   float fn[MAXM];
   for (int k = 0; k < m; ++k) {
     float v = a.F[(int64_t)row * m + k];
@@ -308,6 +306,8 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
     if (a.Fn_out) a.Fn_out[(int64_t)row * m + k] = v;
   }
   if (a.fn_only) return;
+  const unsigned long long key = __ldcg(a.akey + row);
+  const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
   const float* z = a.zs + (int64_t)p * m;
   float t = __fmul_rn(fn[0], z[0]);
   for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn[k], z[k]));

@@ -75,7 +75,7 @@ static Layout make_layout(int64_t R, int64_t w, int m) {
   L.valA = bump(c, (size_t)R * 4);
   L.keyB = bump(c, (size_t)R * 4);
   L.valB = bump(c, (size_t)R * 4);
-  L.part = bump(c, (size_t)(MAX_GRID + 1) * 4);
+  L.part = bump(c, (size_t)2 * (MAX_GRID + 1) * 4);
   L.hist = bump(c, (size_t)256 * MAX_GRID * 4);
   L.sel = bump(c, (size_t)R);
   L.total = (c + 255) & ~(size_t)255;
@@ -164,6 +164,7 @@ static SelectArgs select_args(const Layout& L, void* ws, int64_t R, int64_t w, i
   a.g.bar = at<unsigned>(ws, L.bar) + BAR_SELECT;
   a.g.part = at<int>(ws, L.part);
   a.g.hist = at<int>(ws, L.hist);
+  a.g.parity = 0;
   return a;
 }
 

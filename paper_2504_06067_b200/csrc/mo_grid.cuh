@@ -8,28 +8,33 @@ namespace mo {
 
 struct GridCtx {
   unsigned* bar;  // {count, gen}
-  int* part;      // >= gridDim.x + 1 ints
+  int* part;      // >= 2 * (gridDim.x + 1) ints: double-buffered block partials
   int* hist;      // >= 256 * gridDim.x ints (radix)
+  int parity;     // which half of `part` the next grid_scan uses (same on every block)
 };
 
 // Stable exclusive scan of value(e) over e in [0, N) in ascending e.  Calls
 // emit(e, prefix) for every e with value(e) != 0.  Returns the grand total.
 // `sh` must hold >= 34 ints of shared memory.  One internal grid barrier.
 template <class ValueF, class EmitF>
-__device__ int grid_scan(const GridCtx& g, int64_t N, ValueF value, EmitF emit, int* sh) {
+__device__ int grid_scan(GridCtx& g, int64_t N, ValueF value, EmitF emit, int* sh) {
   const int G = gridDim.x, b = blockIdx.x;
+  // alternate halves of `part`: a fast block may enter the next scan and write
+  // its partial while a slow block still reads this scan's partials
+  int* part = g.part + g.parity * (G + 1);
+  g.parity ^= 1;
   const int64_t chunk = ceil_div(N, (int64_t)G);
   const int64_t lo = min((int64_t)b * chunk, N), hi = min(lo + chunk, N);
   int cnt = 0;
   for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) cnt += value(e);
   int tot;
   block_excl_scan(cnt, sh, &tot);
-  if (threadIdx.x == 0) g.part[b] = tot;
+  if (threadIdx.x == 0) part[b] = tot;
   grid_sync(g.bar);
   // offset = sum of parts of earlier blocks; total = sum of all parts
   int pre = 0, all = 0;
   for (int q = threadIdx.x; q < G; q += blockDim.x) {
-    int v = __ldcg(g.part + q);
+    int v = __ldcg(part + q);
     all += v;
     if (q < b) pre += v;
   }
@@ -53,7 +58,7 @@ __device__ int grid_scan(const GridCtx& g, int64_t N, ValueF value, EmitF emit, 
 // One stable LSD radix pass (8-bit digit at `shift`) of N (key, val) pairs
 // from (kin, vin) to (kout, vout).  Shared memory: `wcnt` >= (blockDim/32)*256
 // ints, `run`/`off` >= 256 ints each.  Two internal grid barriers.
-__device__ inline void grid_radix_pass(const GridCtx& g, int N, int shift, const uint32_t* kin, const int* vin,
+__device__ inline void grid_radix_pass(GridCtx& g, int N, int shift, const uint32_t* kin, const int* vin,
                                        uint32_t* kout, int* vout, int* wcnt, int* run, int* off, int* sh) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nw = blockDim.x >> 5;
@@ -95,6 +100,7 @@ __device__ inline void grid_radix_pass(const GridCtx& g, int N, int shift, const
       ex += v[q];
     }
   }
+  __syncthreads();
   for (int d = tid; d < 256; d += blockDim.x) run[d] = 0;  // running count per digit in this block
   for (int q = tid; q < nw * 256; q += blockDim.x) wcnt[q] = 0;
   __syncthreads();
