@@ -27,7 +27,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 
 import numpy as np
@@ -46,7 +45,7 @@ METRIC = "NSGA-III generations/sec on DTLZ (m=3–10, N to 1M+) at 1/2/4/8 B200 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=500)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
@@ -68,24 +67,28 @@ class ClockSampler:
         self.out = []
 
     def __enter__(self):
+        import tempfile
+        self.path = tempfile.mktemp(suffix=".csv")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+                                          "--format=csv,noheader,nounits", "-lms", "20", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)   # let the sampler start before the timed region
         except FileNotFoundError:
             self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.out.append(line.strip())
-
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.05)
             self.proc.terminate()
             self.proc.wait()
+            try:
+                with open(self.path) as f:
+                    self.out = [ln.strip() for ln in f if ln.strip()]
+                os.unlink(self.path)
+            except OSError:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
@@ -198,6 +201,7 @@ def measure_peaks(torch, L, _lib):
 
 def time_kernels(torch, eng, _lib):
     """Per-phase and per-kernel device times on the engine's current state (outside the timed run)."""
+    from paper_2504_06067_b200 import dominance
     L = _lib.lib()
     cfg = eng.cfg
     n, m = cfg.n, cfg.m
@@ -209,15 +213,18 @@ def time_kernels(torch, eng, _lib):
         prof = {}
         eng.step(profile=prof)
     out.update({k: v * 1e3 for k, v in prof.items()})        # ms
-    # dom_tile alone on the merged objectives of the last step
+    # the engine's dominance kernel alone (presorted rows of the last merged population)
     FR = eng.FR[eng.cur ^ 1]
+    perm, FS, SS, wend = dominance.presort(FR)
     W = int(L.mo_bits_words_per_row(R))
     bits = torch.empty((R, W), dtype=torch.int32, device="cuda")
+    hasdom = torch.empty(R, dtype=torch.uint8, device="cuda")
     ts = []
-    for _ in range(5):
+    for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.mo_dominance_bits(_lib.ptr(FR), R, m, None, _lib.ptr(bits), _lib.stream_ptr()), "dom")
+        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(SS), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
+                                              _lib.stream_ptr()), "dom")
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -349,14 +356,14 @@ def main():
     peaks = r["peaks"]
     n, m, R = wl["n"], wl["m"], 2 * wl["n"]
     step_ms = kern["t_variation"] + kern["t_sort"] + kern["t_niche"]
-    cmp_work = R * (R - 1) * m          # FP32 compares of the dominance bit-matrix
+    cmp_work = R * (R - 1) // 2 * m     # unordered pairs x m FP32 compares (one direction after the S-sort)
     dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
-    roof = {"kernel": "k_dom_tile (dominance bit-matrix)", "bound": "fp32-compare-issue",
+    roof = {"kernel": "k_dom_tile_sorted (dominance bit-matrix)", "bound": "fp32-compare-issue",
             "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12, "unit": "Tcmp/s",
             "frac": dom_achieved / peaks["compare"], "traffic": None,
             "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
             "share_of_step": kern["dom_tile_ms"] / step_ms if step_ms else None,
-            "algorithmic": f"R(R-1)m = {cmp_work:.3e} compares per launch"}
+            "algorithmic": f"R(R-1)/2 * m = {cmp_work:.3e} compares per launch"}
     line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform population, random-init)",
@@ -364,7 +371,7 @@ def main():
             "clocks": r["clk"],
             "e2e": {"value": world * 1e3 / r["e2e_ms"], "unit": "generations/s", "h2d_bytes_per_step": r["h2d"],
                     "d2h_bytes_per_step": r["d2h"]},
-            "gpu_launches": K * 7,
+            "gpu_launches": K * 8,
             "roofline": roof,
             "phases_ms": {k: round(v, 4) for k, v in kern.items()},
             "peaks": {"compare_per_s": peaks["compare"], "fp32_flop_per_s": peaks["fp32"]},

@@ -80,6 +80,11 @@ int mo_workspace_bytes_rows(int64_t R, int32_t m, int64_t w, size_t* bytes);
 /* Words per row of the dominance bit-matrix for R rows. */
 int64_t mo_bits_words_per_row(int64_t R);
 
+/* Byte offset, inside an mo_step workspace for (n, m, w), of the 64-slot
+ * uint64 phase trace (globaltimer ns stamped at phase boundaries of the
+ * persistent kernels; diagnostic only). */
+int64_t mo_trace_offset(int64_t n, int32_t m, int64_t w);
+
 /* Library build/version string. */
 const char* mo_version(void);
 
@@ -116,6 +121,21 @@ int mo_vary_eval(int32_t problem, const float* X, int64_t n, int32_t d, int32_t 
  * are dominated.  W = mo_bits_words_per_row(R). */
 int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid, uint32_t* bits,
                       void* stream_);
+
+/* The engine's sort path (used inside mo_step), exposed for testing and
+ * measurement: mo_presort buckets the R rows by a 16-bit quantisation of
+ * S = FP32 left-to-right sum of their objectives (S-ordered buckets, arbitrary
+ * order inside a bucket) and writes perm[p] (row at position p), FS (R x m
+ * rows in that order), SS (their sums), wend[p] (one past the last bit-matrix
+ * word that can hold a dominator of p) and blkmin/blkmax (min/max S of every
+ * 256-position block, ceil(R/256) floats each).  mo_dominance_bits_sorted then
+ * fills `bits` in position space (rows p, words < wend[p] only) and
+ * hasdom[p] = 1 iff p has a dominator.  Same reference op as
+ * mo_dominance_bits. */
+int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, float* SS, int32_t* wend,
+               float* blkmin, float* blkmax, void* workspace, size_t workspace_bytes, void* stream_);
+int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int32_t m,
+                             uint32_t* bits, uint8_t* hasdom, void* stream_);
 
 /* dominance.non_dominated_sort + split_fronts, peeling the
  * bit-matrix.  stop_at > 0 stops at the first front whose cumulative size

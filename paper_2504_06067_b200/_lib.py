@@ -46,6 +46,7 @@ class StepArgs(ctypes.Structure):
 _PROTOS = {
     "mo_version": (ctypes.c_char_p, []),
     "mo_bits_words_per_row": (c_i64, [c_i64]),
+    "mo_trace_offset": (c_i64, [c_i64, c_i32, c_i64]),
     "mo_workspace_bytes": (c_i32, [c_i64, c_i32, c_i32, c_i64, ctypes.POINTER(c_sz)]),
     "mo_workspace_bytes_rows": (c_i32, [c_i64, c_i32, c_i64, ctypes.POINTER(c_sz)]),
     "mo_permutation": (c_i32, [c_i64, c_u64, c_u32, c_u32, c_vp, c_vp, c_vp]),
@@ -55,6 +56,8 @@ _PROTOS = {
                              c_vp, c_vp, c_vp, c_vp]),
     "mo_dominance_bits": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_front_peel": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_presort": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_dominance_bits_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_normalize": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_associate": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_sz,
                              c_vp]),

@@ -18,7 +18,10 @@
 // known to contain only ranked dominators, and the ranked set only grows, so
 // across all fronts every word of a row is read once plus one re-check per
 // front.  Eight lanes scan one row 128 bytes at a time.
+#include "mo_chains.cuh"
 #include "mo_common.cuh"
+#include "mo_grid.cuh"
+#include "k_dominance_args.cuh"
 
 namespace mo {
 
@@ -162,6 +165,85 @@ __global__ void __launch_bounds__(DOM_TILE) k_dom_tile_generic(const float* __re
   }
 }
 
+// ---------------------------------------------------------------- sorted path
+//
+// Engine path (mo_step): rows are presorted by S = FP32 left-to-right sum of
+// their objectives.  S is monotone under component-wise <= (rounding is
+// monotone), so j dominates i only if S_j <= S_i.  In an off-diagonal tile
+// (bi < bj) with max S(bi) < min S(bj) no lane j can dominate any i
+// and, S differing, "i dominates j" reduces to an m-long FSETP.LE AND chain:
+// m compares per unordered pair instead of 2m plus ballots.  Tiles touching an
+// S tie and the diagonal tiles run the symmetric code above.  The rows of bits
+// are then indexed by sorted position; words past a row's S-tie group are
+// never written (the peel is bounded by wend[p]).  hasdom[p] = 1 iff row p
+// has at least one dominator, so front 0 needs no scan at all.
+
+template <int M>
+__global__ void __launch_bounds__(DOM_TILE) k_dom_tile_sorted(const float* __restrict__ FS,
+                                                              const float* __restrict__ blkmin,
+                                                              const float* __restrict__ blkmax, int R,
+                                                              uint32_t* __restrict__ bits, int64_t W,
+                                                              uint8_t* __restrict__ hasdom) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sFi[DOM_TILE * MP];
+  __shared__ uint32_t sB2[DOM_TILE * 9];
+  int bi, bj;
+  tri_decode(blockIdx.x, bi, bj);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = bi * DOM_TILE, j0 = bj * DOM_TILE;
+  // rows past R are padded with +FLT_MAX: they dominate nothing and are never stored
+  for (int e = tid; e < DOM_TILE * MP; e += DOM_TILE) {
+    int r = e / MP, k = e - r * MP;
+    int i = i0 + r;
+    sFi[e] = (k < M && i < R) ? FS[(int64_t)i * M + k] : 3.402823466e38f;
+  }
+  const int j = j0 + tid;
+  float fj[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) fj[k] = j < R ? FS[(int64_t)j * M + k] : 3.402823466e38f;
+  const bool fast = (bi < bj) && (__ldg(blkmax + bi) < __ldg(blkmin + bj));
+  __syncthreads();
+  uint32_t accw[8];
+  if (fast) {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) Chain<M>::le(sFi + (c * 32 + b) * MP, fj, acc, 1u << b);
+      accw[c] = acc;
+    }
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t acc = 0, mybal = 0;
+#pragma unroll
+      for (int b = 0; b < 32; ++b) {
+        const uint32_t bal = Chain<M>::sym(sFi + (c * 32 + b) * MP, fj, acc, 1u << b);
+        mybal = (lane == b) ? bal : mybal;
+      }
+      accw[c] = acc;
+      sB2[(c * 32 + lane) * 9 + warp] = mybal;
+    }
+  }
+  if (j < R) {
+    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)j * W + (int64_t)bi * 8);
+    dst[0] = make_uint4(accw[0], accw[1], accw[2], accw[3]);
+    dst[1] = make_uint4(accw[4], accw[5], accw[6], accw[7]);
+    if ((accw[0] | accw[1] | accw[2] | accw[3] | accw[4] | accw[5] | accw[6] | accw[7]) != 0u) hasdom[j] = 1;
+  }
+  if (!fast && bi != bj) {
+    __syncthreads();
+    const int i = i0 + tid;
+    if (i < R) {
+      const uint32_t* s = sB2 + tid * 9;
+      uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)i * W + (int64_t)bj * 8);
+      dst[0] = make_uint4(s[0], s[1], s[2], s[3]);
+      dst[1] = make_uint4(s[4], s[5], s[6], s[7]);
+      if ((s[0] | s[1] | s[2] | s[3] | s[4] | s[5] | s[6] | s[7]) != 0u) hasdom[i] = 1;
+    }
+  }
+}
+
 int64_t words_per_row(int64_t R) { return round_up(R, DOM_TILE) / 32; }
 
 int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s) {
@@ -197,20 +279,214 @@ int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint
   return MO_OK;
 }
 
+
+int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int m,
+                           uint32_t* bits, uint8_t* hasdom, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  const int64_t W = words_per_row(R);
+  const int64_t nb = W / 8;
+  const int64_t tiles = nb * (nb + 1) / 2;
+  if (tiles > 0x7fffffffll) return MO_ERR_PARAM;
+  if (cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
+  dim3 grid((unsigned)tiles);
+  switch (m) {
+#define MO_DOMS_CASE(MM) \
+  case MM: k_dom_tile_sorted<MM><<<grid, DOM_TILE, 0, s>>>(FS, blkmin, blkmax, (int)R, bits, W, hasdom); break;
+    MO_DOMS_CASE(2)
+    MO_DOMS_CASE(3)
+    MO_DOMS_CASE(4)
+    MO_DOMS_CASE(5)
+    MO_DOMS_CASE(6)
+    MO_DOMS_CASE(7)
+    MO_DOMS_CASE(8)
+    MO_DOMS_CASE(9)
+    MO_DOMS_CASE(10)
+    MO_DOMS_CASE(11)
+    MO_DOMS_CASE(12)
+    MO_DOMS_CASE(13)
+    MO_DOMS_CASE(14)
+    MO_DOMS_CASE(15)
+    MO_DOMS_CASE(16)
+#undef MO_DOMS_CASE
+    default:
+      return MO_ERR_PARAM;
+  }
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+// ---------------------------------------------------------------- presort
+//
+// k_presort (persistent, all SMs): S_i = ((f_i0 + f_i1) + ...) in FP32 and
+// key_i = ord(S_i); rows are bucketed by a 16-bit quantisation of key_i over
+// [min key, max key] (monotone in S), i.e. one counting-sort pass:
+//   P0 S, key, key range      P1 bucket histogram     P2 bucket starts (scan)
+//   P3 scatter rows to FS/SS  P4 wend + per-256-row block min/max of S.
+// Order inside a bucket is arbitrary (the bit layout may differ run to run,
+// the ranks cannot: fronts are a function of the point set).  Because buckets
+// are S-ordered, a row's dominators lie at earlier positions or in its own
+// bucket, so wend[p] = one past the word of its bucket's last position, and a
+// tile (bi < bj) is free of reverse dominance when max S(bi) < min S(bj).
+constexpr int PRESORT_THREADS = 512;
+
+__global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
+  __shared__ int sh[40];
+  __shared__ unsigned sMin, sMax;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+  const int R = a.R, m = a.m;
+  trace_mark(a.trace, 0);
+  // P0: sums, keys, key range; clear bucket counts and fill cursors
+  if (tid == 0) {
+    sMin = 0xffffffffu;
+    sMax = 0u;
+  }
+  for (int q = gtid; q < PRESORT_BUCKETS; q += gthreads) {
+    a.valB[q] = 0;
+    a.fill[q] = 0;
+  }
+  __syncthreads();
+  unsigned kmin = 0xffffffffu, kmax = 0u;
+  for (int i = gtid; i < R; i += gthreads) {
+    const float* f = a.F + (int64_t)i * m;
+    float s = f[0];
+    for (int k = 1; k < m; ++k) s = __fadd_rn(s, f[k]);
+    const uint32_t key = f2ord(s);
+    a.keyB[i] = key;
+    kmin = min(kmin, key);
+    kmax = max(kmax, key);
+  }
+  kmin = warp_min_u32(kmin);
+  kmax = warp_max_u32(kmax);
+  if (lane == 0) {
+    atomicMin(&sMin, kmin);
+    atomicMax(&sMax, kmax);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    atomicMin(&a.ctl[0], sMin);
+    atomicMax(&a.ctl[1], sMax);
+  }
+  grid_sync(a.g.bar);
+  trace_mark(a.trace, 1);
+  // P1: bucket of every row + histogram
+  const uint32_t lo = __ldcg(a.ctl), hi = __ldcg(a.ctl + 1);
+  const uint64_t span = (uint64_t)(hi - lo) + 1ull;
+  for (int i = gtid; i < R; i += gthreads) {
+    const uint32_t key = __ldcg(a.keyB + i);
+    const uint32_t q = (uint32_t)(((uint64_t)(key - lo) * (uint64_t)PRESORT_BUCKETS) / span);
+    a.keyA[i] = q;
+    atomicAdd(&a.valB[q], 1);
+  }
+  grid_sync(a.g.bar);
+  trace_mark(a.trace, 2);
+  // P2: exclusive scan of the bucket counts -> bucket starts (in fill[] to keep counts)
+  grid_scan(
+      a.g, PRESORT_BUCKETS, [&](int64_t q) { return __ldcg(a.valB + q); },
+      [&](int64_t q, int pre) { a.fill[q] = pre; }, sh);
+  grid_sync(a.g.bar);
+  trace_mark(a.trace, 3);
+  // P3: scatter rows into their buckets
+  for (int i = gtid; i < R; i += gthreads) {
+    const uint32_t q = __ldcg(a.keyA + i);
+    const int pos = atomicAdd(&a.fill[q], 1);
+    a.perm[pos] = i;
+    a.SS[pos] = ord2f(__ldcg(a.keyB + i));
+    for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+  }
+  grid_sync(a.g.bar);
+  trace_mark(a.trace, 4);
+  // P4: wend (after P3 fill[q] = end of bucket q) and per-256-row S range
+  for (int p = gtid; p < R; p += gthreads) {
+    const int i = __ldcg(a.perm + p);
+    const uint32_t q = __ldcg(a.keyA + i);
+    const int last = __ldcg(a.fill + q) - 1;
+    a.wend[p] = last / 32 + 1;
+  }
+  const int nblk = (R + 255) / 256;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    float mn = 3.402823466e38f, mx = -3.402823466e38f;
+    for (int p = b * 256 + tid; p < min(R, b * 256 + 256); p += blockDim.x) {
+      const float v = __ldcg(a.SS + p);
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+    }
+    __shared__ float wmn[PRESORT_THREADS / 32], wmx[PRESORT_THREADS / 32];
+    if (lane == 0) {
+      wmn[tid >> 5] = mn;
+      wmx[tid >> 5] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < PRESORT_THREADS / 32; ++w) {
+        mn = fminf(mn, wmn[w]);
+        mx = fmaxf(mx, wmx[w]);
+      }
+      a.blkmin[b] = fminf(mn, wmn[0]);
+      a.blkmax[b] = fmaxf(mx, wmx[0]);
+    }
+    __syncthreads();
+  }
+  trace_mark(a.trace, 5);
+}
+
+int launch_presort(const PresortArgs& args, cudaStream_t s) {
+  static int maxb = 0;
+  if (!maxb) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_presort, PRESORT_THREADS, 0);
+    maxb = sms * (per > 0 ? (per > 1 ? 1 : per) : 1);
+  }
+  int blocks = (int)ceil_div(args.R > PRESORT_BUCKETS ? args.R : PRESORT_BUCKETS, PRESORT_THREADS * 2);
+  if (blocks > maxb) blocks = maxb;
+  if (blocks < 1) blocks = 1;
+  const unsigned init[2] = {0xffffffffu, 0u};
+  if (cudaMemsetAsync(args.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(args.ctl, 0xff, sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(args.ctl + 1, 0, sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  (void)init;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(PRESORT_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k_presort, args) != cudaSuccess) return MO_ERR_CUDA;
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
 // ------------------------------------------------------------------ peeling
 
 struct PeelArgs {
   const uint32_t* bits;
   int R;
   int64_t W;
-  const uint8_t* valid;
+  const uint8_t* valid;    // nullable (per row, position space)
   int64_t stop_at;
-  int* ranks;
+  int* ranks;              // output, original row order
   int* info;
   int* resume;
   uint32_t* ranked;
   int* front_sizes;
   unsigned* bar;
+  // sorted engine path (all nullable): position -> row map, rows' "has any
+  // dominator" flags, exclusive word bound of each row's possible dominators,
+  // and the position-space rank scratch
+  const int* perm;
+  const uint8_t* hasdom;
+  const int* wend;
+  int* rank_pos;
+  unsigned long long* trace;  // nullable phase trace (slots 8..11)
 };
 
 constexpr int PEEL_THREADS = 256;
@@ -223,12 +499,14 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   const int R = a.R;
   const int64_t W = a.W;
   const int nwords_used = (R + 31) / 32;
+  int* rk = a.perm ? a.rank_pos : a.ranks;   // ranks indexed by bit-matrix row
+  trace_mark(a.trace, 8);
 
   // prologue: ranks / resume / ranked mask (invalid rows count as ranked so they never block)
   int nvalid_local = 0;
   for (int j = gtid; j < R; j += gthreads) {
     bool v = a.valid == nullptr || a.valid[j];
-    a.ranks[j] = v ? MO_RANK_UNRANKED : MO_RANK_DROPPED;
+    rk[j] = v ? MO_RANK_UNRANKED : MO_RANK_DROPPED;
     a.resume[j] = 0;
     nvalid_local += v;
   }
@@ -245,11 +523,11 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
     }
     a.ranked[w] = m;
   }
-  // valid-row count -> front_sizes[-1] slot (front_sizes[0] of the array is reserved)
   nvalid_local = warp_sum(nvalid_local);
   if (lane == 0) atomicAdd(&a.front_sizes[0], nvalid_local);
   if (gtid == 0) a.front_sizes[1] = 0;
   grid_sync(a.bar);
+  trace_mark(a.trace, 9);
   const int nvalid = __ldcg(a.front_sizes);
   const int64_t target = a.stop_at > 0 ? a.stop_at : (int64_t)nvalid;
   if (a.stop_at > 0 && nvalid < a.stop_at) {
@@ -268,37 +546,52 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   for (;;) {
     // ---- phase A: find front k
     int ready_local = 0;
-    for (int rb = gwarp * 4; rb < R; rb += nwarps * 4) {
-      const int j = rb + g8;
-      bool active = (j < R) && (__ldcg(a.ranks + j) == MO_RANK_UNRANKED);
-      int64_t base = active ? (int64_t)a.resume[j] : W;
-      bool blocked = false;
-      for (;;) {
-        const bool scanning = active && !blocked && base < W;
-        if (__ballot_sync(MO_FULL, scanning) == 0) break;
-        bool hit = false;
-        if (scanning) {
-          const int64_t idx = base + l8 * 4;
-          if (idx < W) {
-            uint4 b4 = __ldg(reinterpret_cast<const uint4*>(a.bits + (int64_t)j * W + idx));
-            uint4 r4 = __ldcg(reinterpret_cast<const uint4*>(a.ranked + idx));
-            hit = ((b4.x & ~r4.x) | (b4.y & ~r4.y) | (b4.z & ~r4.z) | (b4.w & ~r4.w)) != 0u;
-          }
-        }
-        const uint32_t hb = __ballot_sync(MO_FULL, hit);
-        if (scanning) {
-          if (hb & gmask)
-            blocked = true;
-          else
-            base += 32;
+    if (k == 0 && a.hasdom) {
+      // front 0 = rows without any dominator, known from the tile kernel
+      for (int j = gtid; j < R; j += gthreads) {
+        if (rk[j] == MO_RANK_UNRANKED && a.hasdom[j] == 0) {
+          rk[j] = 0;
+          ready_local++;
         }
       }
-      if (active && l8 == 0) {
-        if (blocked) {
-          a.resume[j] = (int)base;
-        } else {
-          a.ranks[j] = k;
-          ready_local++;
+    } else {
+      for (int rb = gwarp * 4; rb < R; rb += nwarps * 4) {
+        const int j = rb + g8;
+        bool active = (j < R) && (__ldcg(rk + j) == MO_RANK_UNRANKED);
+        const int64_t wlim = (active && a.wend) ? (int64_t)a.wend[j] : W;
+        int64_t base = active ? (int64_t)a.resume[j] : W;
+        bool blocked = false;
+        for (;;) {
+          const bool scanning = active && !blocked && base < wlim;
+          if (__ballot_sync(MO_FULL, scanning) == 0) break;
+          bool hit = false;
+          if (scanning) {
+            const int64_t idx = base + l8 * 4;
+            if (idx < wlim) {
+              uint4 b4 = __ldg(reinterpret_cast<const uint4*>(a.bits + (int64_t)j * W + idx));
+              uint4 r4 = __ldcg(reinterpret_cast<const uint4*>(a.ranked + idx));
+              uint32_t h = b4.x & ~r4.x;
+              if (idx + 1 < wlim) h |= b4.y & ~r4.y;
+              if (idx + 2 < wlim) h |= b4.z & ~r4.z;
+              if (idx + 3 < wlim) h |= b4.w & ~r4.w;
+              hit = h != 0u;
+            }
+          }
+          const uint32_t hb = __ballot_sync(MO_FULL, hit);
+          if (scanning) {
+            if (hb & gmask)
+              blocked = true;
+            else
+              base += 32;
+          }
+        }
+        if (active && l8 == 0) {
+          if (blocked) {
+            a.resume[j] = (int)base;
+          } else {
+            rk[j] = k;
+            ready_local++;
+          }
         }
       }
     }
@@ -317,8 +610,14 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
     cum += fk;
     const bool done = (cum >= target) || (fk == 0);
     if (done) {
-      for (int j = gtid; j < R; j += gthreads)
-        if (__ldcg(a.ranks + j) == MO_RANK_UNRANKED) a.ranks[j] = MO_RANK_DROPPED;
+      for (int j = gtid; j < R; j += gthreads) {
+        int r = __ldcg(rk + j);
+        if (r == MO_RANK_UNRANKED) {
+          r = MO_RANK_DROPPED;
+          if (!a.perm) rk[j] = r;
+        }
+        if (a.perm) a.ranks[a.perm[j]] = r;
+      }
       if (gtid == 0) {
         const int64_t sel = cum - fk;
         a.info[MO_INFO_L] = k;
@@ -329,11 +628,12 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
         a.info[MO_INFO_SKIPPED] = (a.stop_at > 0 && sel + fk == a.stop_at) ? 1 : 0;
         a.info[MO_INFO_ERROR] = 0;
       }
+      trace_mark(a.trace, 10);
       return;
     }
     for (int64_t w = gwarp; w < nwords_used; w += nwarps) {
       const int64_t j = w * 32 + lane;
-      const bool in = (j < R) && (__ldcg(a.ranks + j) == k);
+      const bool in = (j < R) && (__ldcg(rk + j) == k);
       const uint32_t m = __ballot_sync(MO_FULL, in);
       if (lane == 0 && m) a.ranked[w] |= m;
     }
@@ -357,13 +657,16 @@ int peel_grid_blocks() {
 
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
-                      cudaStream_t s) {
+                      const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
+                      unsigned long long* trace, cudaStream_t s) {
   if (R <= 0) return MO_ERR_PARAM;
-  PeelArgs a{bits, (int)R, words_per_row(R), valid, stop_at, ranks, info, resume, ranked, front_sizes, bar};
+  PeelArgs a{bits, (int)R, words_per_row(R), valid, stop_at, ranks, info, resume, ranked, front_sizes, bar,
+             perm, hasdom, wend, rank_pos, trace};
   if (cudaMemsetAsync(front_sizes, 0, 2 * sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
   if (cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   int blocks = peel_grid_blocks();
-  int needed = (int)ceil_div(R, (PEEL_THREADS / 32) * 4);
+  // two grid barriers per front: ~32 rows per warp keeps the barriers cheap
+  int needed = (int)ceil_div(R, (PEEL_THREADS / 32) * 32);
   if (blocks > needed) blocks = needed < 1 ? 1 : needed;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);

@@ -1,0 +1,38 @@
+// Argument records + launchers of k_dominance.cu, shared with mo_capi.cu.
+#pragma once
+#include "mo_grid.cuh"
+
+namespace mo {
+
+constexpr int PRESORT_BUCKETS = 65536;
+
+struct PresortArgs {
+  const float* F;
+  int R, m;
+  uint32_t* keyA;   // R: per-row bucket
+  int* valA;        // unused (kept for the workspace layout)
+  uint32_t* keyB;   // R: per-row S key
+  int* valB;        // PRESORT_BUCKETS + 1: bucket counts -> starts
+  int* perm;        // sorted position -> row
+  float* FS;        // R x m, sorted
+  float* SS;        // R, sorted sums
+  int* wend;        // R
+  float* blkmin;    // ceil(R/256)
+  float* blkmax;
+  unsigned* ctl;    // [0] min key, [1] max key (reset by the launcher), [2..] fill cursors base
+  int* fill;        // PRESORT_BUCKETS
+  GridCtx g;
+  unsigned long long* trace;
+};
+
+int64_t words_per_row(int64_t R);
+int launch_presort(const PresortArgs& args, cudaStream_t s);
+int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
+int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int m,
+                           uint32_t* bits, uint8_t* hasdom, cudaStream_t s);
+int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
+                      int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
+                      const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
+                      unsigned long long* trace, cudaStream_t s);
+
+}  // namespace mo

@@ -14,11 +14,12 @@
 //             running (max t, first position), merged across splits with a
 //             64-bit atomicMax of (ord(t), ~position).  D is never stored.
 // k_assoc_final: pi = perm_ref[p*], d = sqrt(sum (f - t z)^2).
-// k_select    (persistent): niche counts with warp-aggregated atomics,
-//             nearest selection (64-bit atomicMin of (d, position)),
-//             closed-form water-filling of the Alg. 2 loop, the cache as a
-//             stable radix sort of F_l by pi in shuffled order, promotion,
-//             and the stable survivor compaction.
+// k_select    (persistent): nearest selection (64-bit atomicMin of
+//             (d, position)), closed-form water-filling of the Alg. 2 loop,
+//             the cache table as per-point buckets whose take_j smallest
+//             shuffled positions are promoted, and the stable survivor
+//             compaction.  (Niche counts are warp-aggregated atomics fused
+//             into k_assoc_final.)
 #include "mo_common.cuh"
 #include "mo_grid.cuh"
 #include "mo_rng.cuh"
@@ -100,6 +101,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   const int l = __ldcg(a.info + MO_INFO_L);
   const bool skipped = __ldcg(a.info + MO_INFO_SKIPPED) != 0;
+  trace_mark(a.trace, 16);
 
   // ---- phase 0: running ideal over all R rows (A-4), shuffles, candidate list
   for (int k = tid; k < m; k += blockDim.x) sMin[k] = __int_as_float(0x7f800000);
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     const int p = (int)prp((uint32_t)i, sKp, sSp, sRp, (uint32_t)R);
     a.pos_pop[i] = p;
     a.perm_pop[p] = i;
+    if (a.prom) a.prom[i] = 0;
     if (a.mode == PREP_PERMS) continue;
     a.akey[i] = 0ull;
     if (a.ranks[i] >= 0 && a.ranks[i] <= l) a.cand[atomicAdd(a.ctl, 1)] = i;
@@ -125,15 +128,27 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     const int p = (int)prp((uint32_t)j, sKr, sSr, sRr, (uint32_t)w);
     a.pos_ref[j] = p;
     a.perm_ref[p] = j;
+    if (a.rho) {
+      a.rho[j] = 0;
+      a.rho_p[j] = 0;
+      a.take[j] = 0;
+      a.kept[j] = 0;
+      a.fill[j] = 0;
+      a.near_key[j] = ~0ull;
+    }
     if (a.zhat)
       for (int k = 0; k < m; ++k) a.zs[(int64_t)p * m + k] = a.zhat[(int64_t)j * m + k];
   }
+  if (a.lvl)
+    for (int q = gtid; q < 2 * LVL_BINS; q += gthreads) a.lvl[q] = 0;
+  if (a.sctl && gtid < 16) a.sctl[gtid] = 0;
   if (a.mode != PREP_FULL) return;
   if (gtid < m) {
     a.ext_key[gtid] = ~0ull;
     a.colmax[gtid] = 0u;
   }
   grid_sync(a.bar);
+  trace_mark(a.trace, 17);
 
   // ---- phase 1: ASF extreme points + column maxima of translated candidates
   const int ncand = __ldcg(a.ctl);
@@ -170,6 +185,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     }
   }
   grid_sync(a.bar);
+  trace_mark(a.trace, 18);
 
   // ---- phase 2: hyperplane solve (one thread), per-component fallbacks
   if (blockIdx.x == 0 && tid == 0) {
@@ -201,6 +217,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     }
     a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
   }
+  trace_mark(a.trace, 19);
 }
 
 // ---------------------------------------------------------- association
@@ -293,31 +310,45 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
   const int ncand = __ldcg(a.ctl);
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncand) return;
+  const int base = blockIdx.x * blockDim.x;
+  if (base >= ncand) return;  // whole block idle (uniform)
+  const int c = base + threadIdx.x;
+  const bool act = c < ncand;
   const int m = a.m;
-  const int row = __ldcg(a.cand + c);
+  const int row = act ? __ldcg(a.cand + c) : 0;
   float fn[MAXM];
-  for (int k = 0; k < m; ++k) {
-    float v = a.F[(int64_t)row * m + k];
-    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
-    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
-    fn[k] = v;
-    if (a.Fn_out) a.Fn_out[(int64_t)row * m + k] = v;
+  if (act) {
+    for (int k = 0; k < m; ++k) {
+      float v = a.F[(int64_t)row * m + k];
+      if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+      if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+      fn[k] = v;
+      if (a.Fn_out) a.Fn_out[(int64_t)row * m + k] = v;
+    }
   }
   if (a.fn_only) return;
-  const unsigned long long key = __ldcg(a.akey + row);
-  const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
-  const float* z = a.zs + (int64_t)p * m;
-  float t = __fmul_rn(fn[0], z[0]);
-  for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn[k], z[k]));
-  float s = 0.0f;
-  for (int k = 0; k < m; ++k) {
-    const float e = __fsub_rn(fn[k], __fmul_rn(t, z[k]));
-    s = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s, __fmul_rn(e, e));
+  int j = 0;
+  if (act) {
+    const unsigned long long key = __ldcg(a.akey + row);
+    const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
+    const float* z = a.zs + (int64_t)p * m;
+    float t = __fmul_rn(fn[0], z[0]);
+    for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn[k], z[k]));
+    float s2 = 0.0f;
+    for (int k = 0; k < m; ++k) {
+      const float e = __fsub_rn(fn[k], __fmul_rn(t, z[k]));
+      s2 = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s2, __fmul_rn(e, e));
+    }
+    j = a.perm_ref[p];
+    a.pi[row] = j;
+    a.d[row] = __fsqrt_rn(s2);
   }
-  a.pi[row] = a.perm_ref[p];
-  a.d[row] = __fsqrt_rn(s);
+  if (a.ranks) {  // niche counts, warp-aggregated
+    const int l = __ldcg(a.info + MO_INFO_L);
+    const int r = act ? a.ranks[row] : -1;
+    warp_agg_add(a.rho, j, act && r < l);
+    warp_agg_add(a.rho_p, j, act && r == l);
+  }
 }
 
 // --------------------------------------------------------------- select
@@ -326,46 +357,60 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
 
 constexpr int SELECT_THREADS = 512;
 
+__device__ __forceinline__ int warp_bitonic_asc(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int o = __shfl_xor_sync(MO_FULL, v, j);
+      const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+      v = (lower == up) ? min(v, o) : max(v, o);
+    }
+  return v;
+}
+
+// Niche selection after association (Alg. 2 lines 5-26).
+//   P0 (op-level only) niche counts
+//   P1 nearest-candidate keys of empty niches; M0 = #empty niches
+//   P2 M0 > k: promote the nearest of the first k empty niches in shuffled
+//      reference order (done).  Else promote every empty niche's nearest,
+//      post-nearest counts, level histogram of [rho_j, rho_j + c_j)
+//   P3 every block: water level L* = min{L : T(L) >= k'} and `need`
+//   P4 marked points at L*, first `need` in shuffled reference order
+//   P5 take_j; buckets for partially taken points
+//   P6 cache members: all taken, or bucketed by position
+//   P7 per bucket: the take_j smallest shuffled positions (warp bitonic /
+//      threshold search) -- equal to the cursor order of the cache table
+//   P8 survivors: stable compaction in merged-row order
 __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
   __shared__ int sh[40];
-  __shared__ int wcnt[(SELECT_THREADS / 32) * 256];
-  __shared__ int run[256], off[256];
-  __shared__ int sHist[2][1024];
-  __shared__ long long sLL[4];
-  const int tid = threadIdx.x;
+  __shared__ int sHist[2][LVL_BINS];
+  __shared__ int sRes[4];
+  const int tid = threadIdx.x, lane = tid & 31;
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+  const int gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const int R = a.R, w = a.w;
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   const int l = __ldcg(a.info + MO_INFO_L);
   const int k = __ldcg(a.info + MO_INFO_K);
   const bool skipped = __ldcg(a.info + MO_INFO_SKIPPED) != 0;
   int kept_nearest = 0, level = -1;
+  trace_mark(a.trace, 24);
 
   if (!skipped) {
-    // ---- S0: reset per-reference state
-    for (int j = gtid; j < w; j += gthreads) {
-      a.rho[j] = 0;
-      a.rho_p[j] = 0;
-      a.take[j] = 0;
-      a.near_key[j] = ~0ull;
+    if (a.count_inside) {
+      for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {
+        const int i = base + tid;
+        const int r = i < R ? a.ranks[i] : MO_RANK_DROPPED;
+        const bool c = (r >= 0) && (r <= l);
+        const int j = c ? __ldcg(a.pi + i) : 0;
+        warp_agg_add(a.rho, j, c && r < l);
+        warp_agg_add(a.rho_p, j, c && r == l);
+      }
+      grid_sync(a.g.bar);
     }
-    for (int i = gtid; i < R; i += gthreads) a.prom[i] = 0;
-    grid_sync(a.g.bar);
-    // ---- S1: niche counts rho (rank < l) and rho' (rank == l), warp-aggregated atomics
-    for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {
-      const int i = base + tid;
-      const int r = i < R ? a.ranks[i] : MO_RANK_DROPPED;
-      const bool c = (r >= 0) && (r <= l);
-      const int j = c ? __ldcg(a.pi + i) : 0;
-      warp_agg_add(a.rho, j, c && r < l);
-      warp_agg_add(a.rho_p, j, c && r == l);
-    }
-    grid_sync(a.g.bar);
-    // ---- S2: disable reference points without candidates (rho = inf where rho' = 0)
-    for (int j = gtid; j < w; j += gthreads)
-      if (__ldcg(a.rho_p + j) == 0) a.rho[j] = MO_INF;
-    grid_sync(a.g.bar);
-    // ---- S3: nearest candidate of every empty niche: min (d, shuffled position)
+    // ---- P1
     for (int i = gtid; i < R; i += gthreads) {
       if (a.ranks[i] != l) continue;
       const int j = __ldcg(a.pi + i);
@@ -373,183 +418,206 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       const unsigned long long key = ((unsigned long long)f2ord(__ldcg(a.d + i)) << 32) | (uint32_t)a.pos_pop[i];
       atomicMin(&a.near_key[j], key);
     }
-    grid_sync(a.g.bar);
-    // ---- S4: nearest selection, truncated to the first k empty niches in shuffled order
     {
-      const int kk = k;
-      const int M0 = grid_scan(
-          a.g, w, [&](int64_t p) { return (int)(__ldcg(a.rho + a.perm_ref[p]) == 0); },
-          [&](int64_t p, int pre) {
-            if (pre >= kk) return;
-            const int j = a.perm_ref[p];
-            const int row = a.perm_pop[(uint32_t)(__ldcg(a.near_key + j) & 0xffffffffull)];
-            a.prom[row] = 1;
-            const int rp = __ldcg(a.rho_p + j) - 1;
-            a.rho_p[j] = rp;
-            a.rho[j] = rp == 0 ? MO_INF : 1;
-          },
-          sh);
-      kept_nearest = min(M0, kk);
+      int e = 0;
+      for (int j = gtid; j < w; j += gthreads) e += (__ldcg(a.rho + j) == 0) & (__ldcg(a.rho_p + j) > 0);
+      e = warp_sum(e);
+      if (lane == 0 && e) atomicAdd(&a.sctl[SCTL_M0], e);
     }
     grid_sync(a.g.bar);
-    const int k_rem = k - kept_nearest;
-    if (k_rem > 0) {
-      // ---- S5: water-filling level L* (block 0): T(L) = sum_j clamp(L+1-rho_j, 0, c_j)
-      if (blockIdx.x == 0) {
-        long long mn = (long long)MO_INF, mx = 0;
-        for (int j = tid; j < w; j += blockDim.x) {
-          const int r = __ldcg(a.rho + j);
-          if (r < MO_INF) {
-            mn = min(mn, (long long)r);
-            mx = max(mx, (long long)r + __ldcg(a.rho_p + j));
-          }
-        }
-        // block min / max via shared atomics on 64-bit
-        if (tid == 0) {
-          sLL[0] = (long long)MO_INF;
-          sLL[1] = 0;
-        }
-        __syncthreads();
-        atomicMin(reinterpret_cast<unsigned long long*>(&sLL[0]), (unsigned long long)mn);
-        atomicMax(reinterpret_cast<unsigned long long*>(&sLL[1]), (unsigned long long)mx);
-        for (int q = tid; q < 2 * 1024; q += blockDim.x) (&sHist[0][0])[q] = 0;
-        __syncthreads();
-        const long long lo = sLL[0];
-        // window histogram of start (rho_j) and end (rho_j + c_j) levels
-        for (int j = tid; j < w; j += blockDim.x) {
-          const int r = __ldcg(a.rho + j);
-          if (r >= MO_INF) continue;
-          const long long s0 = (long long)r - lo, e0 = s0 + __ldcg(a.rho_p + j);
-          if (s0 < 1024) atomicAdd(&sHist[0][s0], 1);
-          if (e0 < 1024) atomicAdd(&sHist[1][e0], 1);
-        }
-        __syncthreads();
-        if (tid == 0) {
-          long long active = 0, T = 0, Lstar = -1, before = 0;
-          for (int q = 0; q < 1024; ++q) {
-            active += sHist[0][q] - sHist[1][q];
-            if (T + active >= k_rem) {
-              Lstar = lo + q;
-              before = T;
-              break;
-            }
-            T += active;
-          }
-          sLL[2] = Lstar;
-          sLL[3] = before;
-        }
-        __syncthreads();
-        long long Lstar = sLL[2];
-        if (Lstar < 0) {
-          // rare: beyond the window -> binary search with full passes over w
-          long long lo2 = lo + 1024, hi2 = sLL[1];
-          while (lo2 < hi2) {
-            const long long mid = (lo2 + hi2) / 2;
-            long long part = 0;
-            for (int j = tid; j < w; j += blockDim.x) {
-              const int r = __ldcg(a.rho + j);
-              if (r >= MO_INF) continue;
-              long long t = mid + 1 - r;
-              const long long c = __ldcg(a.rho_p + j);
-              part += t < 0 ? 0 : (t > c ? c : t);
-            }
-            __syncthreads();
-            if (tid == 0) sLL[2] = 0;
-            __syncthreads();
-            atomicAdd(reinterpret_cast<unsigned long long*>(&sLL[2]), (unsigned long long)part);
-            __syncthreads();
-            const long long T = sLL[2];
-            __syncthreads();
-            if (T >= k_rem)
-              hi2 = mid;
-            else
-              lo2 = mid + 1;
-          }
-          Lstar = lo2;
-          long long part = 0;
-          for (int j = tid; j < w; j += blockDim.x) {
-            const int r = __ldcg(a.rho + j);
-            if (r >= MO_INF) continue;
-            long long t = Lstar - r;
-            const long long c = __ldcg(a.rho_p + j);
-            part += t < 0 ? 0 : (t > c ? c : t);
-          }
-          __syncthreads();
-          if (tid == 0) sLL[3] = 0;
-          __syncthreads();
-          atomicAdd(reinterpret_cast<unsigned long long*>(&sLL[3]), (unsigned long long)part);
-          __syncthreads();
-        }
-        if (tid == 0) {
-          a.ctl[8] = (int)Lstar;
-          a.ctl[9] = (int)(k_rem - sLL[3]);  // marked points kept at level L*
-        }
-      }
-      grid_sync(a.g.bar);
-      const int L = __ldcg(a.ctl + 8), need = __ldcg(a.ctl + 9);
-      level = L;
-      for (int j = gtid; j < w; j += gthreads) {
-        const int r = __ldcg(a.rho + j);
-        if (r >= MO_INF) continue;
-        const int c = __ldcg(a.rho_p + j);
-        const long long t = (long long)L - r;
-        a.take[j] = (int)(t < 0 ? 0 : (t > c ? c : t));
-      }
+    trace_mark(a.trace, 25);
+    const int M0 = __ldcg(a.sctl + SCTL_M0);
+    int k_rem = 0;
+    if (M0 > k) {
+      // ---- P2 (truncated): the first k empty niches in shuffled reference order
       grid_scan(
           a.g, w,
           [&](int64_t p) {
             const int j = a.perm_ref[p];
-            const int r = __ldcg(a.rho + j);
-            return (int)(r < MO_INF && r <= L && (long long)L < (long long)r + __ldcg(a.rho_p + j));
+            return (int)((__ldcg(a.rho + j) == 0) & (__ldcg(a.rho_p + j) > 0));
           },
           [&](int64_t p, int pre) {
-            if (pre < need) a.take[a.perm_ref[p]] += 1;
+            if (pre >= k) return;
+            const int j = a.perm_ref[p];
+            a.prom[a.perm_pop[(uint32_t)(__ldcg(a.near_key + j) & 0xffffffffull)]] = 1;
           },
           sh);
-      // ---- S6: bucket starts of the cache (counts c_j in reference index order)
+      kept_nearest = k;
+      grid_sync(a.g.bar);
+    } else {
+      // ---- P2: all empty niches take their nearest; post-nearest counts; level histogram
+      for (int q = tid; q < 2 * LVL_BINS; q += blockDim.x) (&sHist[0][0])[q] = 0;
+      __syncthreads();
+      for (int j = gtid; j < w; j += gthreads) {
+        int r = __ldcg(a.rho + j), c = __ldcg(a.rho_p + j);
+        if (c == 0) continue;
+        if (r == 0) {
+          a.prom[a.perm_pop[(uint32_t)(__ldcg(a.near_key + j) & 0xffffffffull)]] = 1;
+          r = 1;
+          c -= 1;
+          a.rho[j] = r;
+          a.rho_p[j] = c;
+        }
+        if (c == 0) continue;
+        if (r < LVL_BINS) atomicAdd(&sHist[0][r], 1);
+        if (r + c < LVL_BINS) atomicAdd(&sHist[1][r + c], 1);
+      }
+      __syncthreads();
+      for (int q = tid; q < 2 * LVL_BINS; q += blockDim.x) {
+        const int v = (&sHist[0][0])[q];
+        if (v) atomicAdd(a.lvl + q, v);
+      }
+      kept_nearest = M0;
+      k_rem = k - M0;
+      grid_sync(a.g.bar);
+    }
+    trace_mark(a.trace, 26);
+    if (k_rem > 0) {
+      // ---- P3: L* from the level histogram, redundantly in every block (no barrier)
+      if (tid < 32) {
+        long long carryA = 0, carryT = 0, Lstar = -1, before = 0;
+        for (int base = 0; base < LVL_BINS && Lstar < 0; base += 32) {
+          const int q = base + lane;
+          long long x = (long long)__ldcg(a.lvl + q) - (long long)__ldcg(a.lvl + LVL_BINS + q);
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(MO_FULL, x, o);
+            if (lane >= o) x += t;
+          }
+          long long A = x + carryA;  // active points at level q
+          long long y = A;
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(MO_FULL, y, o);
+            if (lane >= o) y += t;
+          }
+          const long long T = y + carryT;  // takes once level q is processed
+          const unsigned hit = __ballot_sync(MO_FULL, T >= k_rem);
+          if (hit) {
+            const int f = __ffs(hit) - 1;
+            Lstar = base + f;
+            before = __shfl_sync(MO_FULL, T - A, f);
+          }
+          carryA = __shfl_sync(MO_FULL, A, 31);
+          carryT = __shfl_sync(MO_FULL, T, 31);
+        }
+        if (lane == 0) {
+          sRes[0] = (int)Lstar;
+          sRes[1] = (int)before;
+        }
+      }
+      __syncthreads();
+      int L = sRes[0];
+      long long before = sRes[1];
+      if (L < 0) {
+        // rare: level beyond the window -> block-cooperative binary search over all j
+        __shared__ unsigned long long sAcc;
+        long long lo = LVL_BINS, hi = 0x7fffffff;
+        while (lo < hi) {
+          const long long mid = (lo + hi) / 2;
+          unsigned long long part = 0;
+          for (int j = tid; j < w; j += blockDim.x) {
+            const int c = __ldcg(a.rho_p + j);
+            if (c == 0) continue;
+            const long long t = mid + 1 - __ldcg(a.rho + j);
+            part += t < 0 ? 0 : (t > c ? c : t);
+          }
+          if (tid == 0) sAcc = 0;
+          __syncthreads();
+          atomicAdd(&sAcc, part);
+          __syncthreads();
+          const long long T = (long long)sAcc;
+          __syncthreads();
+          if (T >= k_rem) hi = mid; else lo = mid + 1;
+        }
+        L = (int)lo;
+        unsigned long long part = 0;
+        for (int j = tid; j < w; j += blockDim.x) {
+          const int c = __ldcg(a.rho_p + j);
+          if (c == 0) continue;
+          const long long t = (long long)L - __ldcg(a.rho + j);
+          part += t < 0 ? 0 : (t > c ? c : t);
+        }
+        if (tid == 0) sAcc = 0;
+        __syncthreads();
+        atomicAdd(&sAcc, part);
+        __syncthreads();
+        before = (long long)sAcc;
+        __syncthreads();
+      }
+      const int need = (int)(k_rem - before);
+      level = L;
+      trace_mark(a.trace, 27);
+      // ---- P4: marked at L*, keep the first `need` in shuffled reference order
       grid_scan(
-          a.g, w, [&](int64_t j) { return __ldcg(a.rho_p + j); },
-          [&](int64_t j, int pre) { a.bstart[j] = pre; }, sh);
-      // ---- S7: F_l members left after the nearest pass, in shuffled population order
-      const int L_n = grid_scan(
-          a.g, R,
+          a.g, w,
           [&](int64_t p) {
-            const int i = a.perm_pop[p];
-            return (int)(a.ranks[i] == l && __ldcg(a.prom + i) == 0);
+            const int j = a.perm_ref[p];
+            const int c = __ldcg(a.rho_p + j);
+            const int r = __ldcg(a.rho + j);
+            return (int)(c > 0 && r <= L && (long long)L < (long long)r + c);
           },
           [&](int64_t p, int pre) {
-            const int i = a.perm_pop[p];
-            a.keyA[pre] = (uint32_t)__ldcg(a.pi + i);
-            a.valA[pre] = i;
+            if (pre < need) a.kept[a.perm_ref[p]] = 1;
           },
           sh);
       grid_sync(a.g.bar);
-      // ---- S8: stable radix sort by reference point -> the cache table Q as CSR
-      const int kbits = bitlen((uint32_t)(w > 1 ? w - 1 : 1));
-      uint32_t* kin = a.keyA;
-      int* vin = a.valA;
-      uint32_t* kout = a.keyB;
-      int* vout = a.valB;
-      for (int shift = 0; shift < kbits; shift += 8) {
-        grid_radix_pass(a.g, L_n, shift, kin, vin, kout, vout, wcnt, run, off, sh);
-        uint32_t* tk = kin;
-        kin = kout;
-        kout = tk;
-        int* tv = vin;
-        vin = vout;
-        vout = tv;
+      trace_mark(a.trace, 28);
+      // ---- P5: take_j; bucket storage for partially taken points
+      for (int j = gtid; j < w; j += gthreads) {
+        const int c = __ldcg(a.rho_p + j);
+        if (c == 0) continue;
+        const long long t0 = (long long)L - __ldcg(a.rho + j);
+        const int t = (int)(t0 < 0 ? 0 : (t0 > c ? c : t0)) + __ldcg(a.kept + j);
+        a.take[j] = t;
+        if (t > 0 && t < c) a.bstart[j] = atomicAdd(&a.sctl[SCTL_ALLOC], c);
       }
-      // ---- S9: promote the first take_j cache entries of every reference point
-      for (int s = gtid; s < L_n; s += gthreads) {
-        const int j = (int)__ldcg(kin + s);
-        const int i = __ldcg(vin + s);
-        if (s - __ldcg(a.bstart + j) < __ldcg(a.take + j)) a.prom[i] = 1;
+      grid_sync(a.g.bar);
+      trace_mark(a.trace, 29);
+      // ---- P6: cache members (F_l minus the nearest-promoted)
+      for (int i = gtid; i < R; i += gthreads) {
+        if (a.ranks[i] != l || __ldcg(a.prom + i)) continue;
+        const int j = __ldcg(a.pi + i);
+        const int t = __ldcg(a.take + j);
+        if (t == 0) continue;
+        if (t >= __ldcg(a.rho_p + j)) {
+          a.prom[i] = 1;
+        } else {
+          const int slot = __ldcg(a.bstart + j) + atomicAdd(&a.fill[j], 1);
+          a.bucket[slot] = a.pos_pop[i];
+        }
       }
+      grid_sync(a.g.bar);
+      trace_mark(a.trace, 30);
+      // ---- P7: the take_j smallest shuffled positions of every partial bucket (warp per point)
+      for (int j = gwarp; j < w; j += nwarps) {
+        const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
+        if (t == 0 || t >= c) continue;
+        const int* bk = a.bucket + __ldcg(a.bstart + j);
+        if (c <= 32) {
+          int v = lane < c ? __ldcg(bk + lane) : 0x7fffffff;
+          v = warp_bitonic_asc(v);
+          if (lane < t) a.prom[a.perm_pop[v]] = 1;
+        } else {
+          // smallest x with #{pos <= x} >= t (positions are distinct)
+          int lo = 0, hi = R - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            int cnt = 0;
+            for (int q = lane; q < c; q += 32) cnt += __ldcg(bk + q) <= mid;
+            cnt = warp_sum(cnt);
+            if (cnt >= t) hi = mid; else lo = mid + 1;
+          }
+          for (int q = lane; q < c; q += 32) {
+            const int v = __ldcg(bk + q);
+            if (v <= lo) a.prom[a.perm_pop[v]] = 1;
+          }
+        }
+      }
+      grid_sync(a.g.bar);
+      trace_mark(a.trace, 31);
     }
-    grid_sync(a.g.bar);
   }
-  // ---- S10: survivors = fronts < l + promoted (or fronts <= l when niching was skipped);
-  //           promoted rank = l - 1 (A-8); stable compaction in merged-row order (A-9)
+  // ---- P8: survivors = fronts < l + promoted (or fronts <= l when niching was skipped);
+  //          promoted rank = l - 1 (A-8); stable compaction in merged-row order (A-9)
   const int nsurv = grid_scan(
       a.g, R,
       [&](int64_t i) {
@@ -569,6 +637,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       },
       sh);
   grid_sync(a.g.bar);
+  trace_mark(a.trace, 35);
   for (int i = gtid; i < R; i += gthreads) {
     const int r = a.ranks[i];
     const bool pr = !skipped && __ldcg(a.prom + i) != 0;
@@ -582,6 +651,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
     a.info[MO_INFO_SURVIVORS] = nsurv;
     if (a.gen_ptr) *a.gen_ptr += 1u;
   }
+  trace_mark(a.trace, 36);
 }
 
 // ------------------------------------------------------------- launchers
@@ -685,7 +755,7 @@ int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
 int launch_select(const SelectArgs& a, cudaStream_t s) {
   if (cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   int blocks = select_grid_blocks();
-  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), SELECT_THREADS);
+  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), SELECT_THREADS * 2);
   if (blocks > need) blocks = need < 1 ? 1 : need;
   return launch_coop(k_select, blocks, SELECT_THREADS, a, s);
 }

@@ -29,7 +29,21 @@ struct PrepArgs {
   unsigned* bar;
   double* icpt_out;
   int mode;  // PREP_FULL | PREP_PERMS_CAND | PREP_PERMS
+  unsigned long long* trace;  // nullable phase trace (slots 16..19)
+  // niche-selection state cleared here for k_assoc_final / k_select
+  int* rho;
+  int* rho_p;
+  int* take;
+  int* kept;
+  int* fill;
+  unsigned long long* near_key;
+  uint8_t* prom;
+  int* lvl;   // 2 * LVL_BINS level histogram
+  int* sctl;  // 16 select counters
 };
+
+constexpr int LVL_BINS = 1024;
+enum { SCTL_M0 = 0, SCTL_ALLOC = 1 };
 
 enum { PREP_FULL = 0, PREP_PERMS_CAND = 1, PREP_PERMS = 2 };
 
@@ -61,6 +75,9 @@ struct AssocFinalArgs {
   float* d;
   float* Fn_out;  // nullable
   int fn_only;    // write Fn_out and stop (mo_normalize)
+  const int* ranks;  // niche counts (nullable: skip): rho over rank < l, rho' over rank == l
+  int* rho;
+  int* rho_p;
 };
 
 struct SelectArgs {
@@ -72,24 +89,26 @@ struct SelectArgs {
   const int* pos_pop;
   const int* perm_pop;
   const int* perm_ref;
-  int* rho;
-  int* rho_p;
-  int* take;
-  int* bstart;
+  int* rho;       // niche counts over rank < l (k_assoc_final), post-nearest in place
+  int* rho_p;     // candidates over rank == l, post-nearest in place
+  int* take;      // cache entries taken per reference point
+  int* kept;      // marked-and-kept at the last water-fill level
+  int* bstart;    // bucket start of partially taken reference points
+  int* fill;      // bucket fill cursors
+  int* bucket;    // shuffled positions of the bucketed candidates (R)
   unsigned long long* near_key;
   uint8_t* prom;
-  uint32_t* keyA;
-  int* valA;
-  uint32_t* keyB;
-  int* valB;
-  int* ctl;
+  int* lvl;       // 2 * LVL_BINS
+  int* sctl;
   uint8_t* selected;
   const float* XR;  // compaction sources (nullable)
   const float* FR;
   float* X_next;
   float* F_next;
   int dvars, m;
+  int count_inside;   // op-level: compute rho / rho' here (engine: fused in k_assoc_final)
   uint32_t* gen_ptr;  // nullable: incremented once the step is complete
+  unsigned long long* trace;  // nullable phase trace (slots 24..40)
   GridCtx g;
 };
 

@@ -44,66 +44,75 @@ __device__ __forceinline__ double pm_apply(double x, double u, double eta) {
 
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
-// Block = 128 threads; dynamic smem holds the MATING shuffle keys.
-__global__ void __launch_bounds__(128) k_vary_eval(int problem, const float* __restrict__ X, int n, int d, int m,
-                                                   uint64_t seed, uint32_t gen_val, const uint32_t* gen_ptr,
-                                                   mo_var_cfg cfg,
-                                                   float* __restrict__ Xo, float* __restrict__ Fo,
-                                                   float* __restrict__ ideal, int* __restrict__ domain_flag) {
+// One block = VARY_PAIRS mating pairs.  Phase 1: one thread per pair draws
+// the parents (keyed MATING permutation) into shared memory.  Phase 2: one
+// thread per (pair, variable) runs SBX + clamp + PM + clamp and writes both
+// children.  Phase 3: one thread per child evaluates DTLZ (FP64) and lowers
+// the block's column minima (ideal point).
+constexpr int VARY_PAIRS = 32;
+constexpr int VARY_THREADS = 2 * VARY_PAIRS;
+
+__global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const float* __restrict__ X, int n, int d,
+                                                            int m, uint64_t seed, uint32_t gen_val,
+                                                            const uint32_t* gen_ptr, mo_var_cfg cfg,
+                                                            float* __restrict__ Xo, float* __restrict__ Fo,
+                                                            float* __restrict__ ideal, int* __restrict__ domain_flag) {
   __shared__ uint32_t shK[MAX_SHUFFLE_ROUNDS], shS[MAX_SHUFFLE_ROUNDS];
   __shared__ int shR;
   __shared__ float shMin[16];
+  __shared__ int shA[VARY_PAIRS], shB[VARY_PAIRS];
+  __shared__ uint8_t shCross[VARY_PAIRS];
   const uint32_t gen = gen_ptr ? *gen_ptr : gen_val;
   load_shuffle_keys_smem(shK, shS, &shR, (uint32_t)n, seed, gen, STREAM_MATING);
   if (threadIdx.x < 16) shMin[threadIdx.x] = __int_as_float(0x7f800000);
   __syncthreads();
-  const int rounds = shR;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int npairs = n / 2;
+  const int q0 = blockIdx.x * VARY_PAIRS;
+  const int tid = threadIdx.x;
+  if (tid < VARY_PAIRS && q0 + tid < npairs) {
+    const int q = q0 + tid;
+    shA[tid] = (int)prp_inv(2u * q, shK, shS, shR, (uint32_t)n);
+    shB[tid] = (int)prp_inv(2u * q + 1u, shK, shS, shR, (uint32_t)n);
+    shCross[tid] = u01(philox4x32((uint32_t)q, PAIR_SLOT, gen, STREAM_SBX, seed).x) < cfg.p_c;
+  }
+  __syncthreads();
   const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
-  if (q < n / 2) {
-    const uint32_t a = prp_inv(2u * q, shK, shS, rounds, (uint32_t)n);
-    const uint32_t b = prp_inv(2u * q + 1u, shK, shS, rounds, (uint32_t)n);
-    const float* p1 = X + (int64_t)a * d;
-    const float* p2 = X + (int64_t)b * d;
-    float* c1 = Xo + (int64_t)(2 * q) * d;
-    float* c2 = Xo + (int64_t)(2 * q + 1) * d;
-    const bool cross = u01(philox4x32((uint32_t)q, PAIR_SLOT, gen, STREAM_SBX, seed).x) < cfg.p_c;
-    const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
-    for (int v = 0; v < d; ++v) {
-      double x1 = (double)p1[v], x2 = (double)p2[v];
-      float o1, o2;
-      if (cross) {
-        double u = (double)u01(philox4x32((uint32_t)q, (uint32_t)v, gen, STREAM_SBX, seed).x);
-        double be = sbx_beta(u, eta_c);
-        o1 = (float)clamp01(0.5 * ((1.0 + be) * x1 + (1.0 - be) * x2));
-        o2 = (float)clamp01(0.5 * ((1.0 - be) * x1 + (1.0 + be) * x2));
-      } else {
-        o1 = p1[v];
-        o2 = p2[v];
-      }
-      U4 r1 = philox4x32((uint32_t)(2 * q), (uint32_t)v, gen, STREAM_PM, seed);
-      U4 r2 = philox4x32((uint32_t)(2 * q + 1), (uint32_t)v, gen, STREAM_PM, seed);
-      if (u01(r1.x) < p_m) o1 = (float)clamp01(pm_apply((double)o1, (double)u01(r1.y), eta_m));
-      if (u01(r2.x) < p_m) o2 = (float)clamp01(pm_apply((double)o2, (double)u01(r2.y), eta_m));
-      c1[v] = o1;
-      c2[v] = o2;
+  const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
+  const int tasks = min(VARY_PAIRS, npairs - q0) * d;
+  for (int e = tid; e < tasks; e += VARY_THREADS) {
+    const int ql = e / d, v = e - ql * d;
+    const int q = q0 + ql;
+    const float y1 = X[(int64_t)shA[ql] * d + v], y2 = X[(int64_t)shB[ql] * d + v];
+    float o1 = y1, o2 = y2;
+    if (shCross[ql]) {
+      const double x1 = (double)y1, x2 = (double)y2;
+      const double u = (double)u01(philox4x32((uint32_t)q, (uint32_t)v, gen, STREAM_SBX, seed).x);
+      const double be = sbx_beta(u, eta_c);
+      o1 = (float)clamp01(0.5 * ((1.0 + be) * x1 + (1.0 - be) * x2));
+      o2 = (float)clamp01(0.5 * ((1.0 - be) * x1 + (1.0 + be) * x2));
     }
-    float* f1 = Fo + (int64_t)(2 * q) * m;
-    float* f2 = Fo + (int64_t)(2 * q + 1) * m;
-    bool ok = dtlz_eval_row(problem, c1, d, m, f1);
-    ok = dtlz_eval_row(problem, c2, d, m, f2) && ok;
+    const U4 r1 = philox4x32((uint32_t)(2 * q), (uint32_t)v, gen, STREAM_PM, seed);
+    const U4 r2 = philox4x32((uint32_t)(2 * q + 1), (uint32_t)v, gen, STREAM_PM, seed);
+    if (u01(r1.x) < p_m) o1 = (float)clamp01(pm_apply((double)o1, (double)u01(r1.y), eta_m));
+    if (u01(r2.x) < p_m) o2 = (float)clamp01(pm_apply((double)o2, (double)u01(r2.y), eta_m));
+    Xo[(int64_t)(2 * q) * d + v] = o1;
+    Xo[(int64_t)(2 * q + 1) * d + v] = o2;
+  }
+  __syncthreads();
+  const int child = 2 * q0 + tid;
+  if (child < n) {
+    float* f = Fo + (int64_t)child * m;
+    const bool ok = dtlz_eval_row(problem, Xo + (int64_t)child * d, d, m, f);
     if (!ok && domain_flag) atomicOr(domain_flag, 1);
-    if (ideal) {
-      for (int j = 0; j < m && j < 16; ++j) atomic_min_float(&shMin[j], fminf(f1[j], f2[j]));
-    }
+    if (ideal)
+      for (int j = 0; j < m; ++j) {
+        if (j < 16) atomic_min_float(&shMin[j], f[j]);
+        else atomic_min_float(&ideal[j], f[j]);
+      }
   }
   if (ideal) {
     __syncthreads();
-    if (threadIdx.x < m && threadIdx.x < 16) atomic_min_float(&ideal[threadIdx.x], shMin[threadIdx.x]);
-    // objectives beyond 16 columns: per-thread global atomics
-    if (m > 16 && q < n / 2)
-      for (int j = 16; j < m; ++j)
-        atomic_min_float(&ideal[j], fminf(Fo[(int64_t)(2 * q) * m + j], Fo[(int64_t)(2 * q + 1) * m + j]));
+    if (tid < m && tid < 16) atomic_min_float(&ideal[tid], shMin[tid]);
   }
 }
 
@@ -136,8 +145,9 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
   if (n <= 0 || (n & 1) || d < m || m < 2) return MO_ERR_PARAM;
   if (problem < MO_DTLZ1 || problem > MO_DTLZ7) return MO_ERR_PARAM;
   int pairs = (int)(n / 2);
-  k_vary_eval<<<(unsigned)ceil_div(pairs, 128), 128, 0, s>>>(problem, X, (int)n, d, m, seed, gen, gen_ptr, cfg,
-                                                               Xo, Fo, ideal, domain_flag);
+  k_vary_eval<<<(unsigned)ceil_div(pairs, VARY_PAIRS), VARY_THREADS, 0, s>>>(problem, X, (int)n, d, m, seed, gen,
+                                                                             gen_ptr, cfg, Xo, Fo, ideal,
+                                                                             domain_flag);
   MO_CHECK_LAUNCH();
   return MO_OK;
 }

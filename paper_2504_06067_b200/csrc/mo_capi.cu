@@ -17,14 +17,11 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
 int launch_init_population(float* X, int64_t n, int d, uint64_t seed, cudaStream_t s);
 int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float* F, int* domain_flag,
                      cudaStream_t s);
-// k_dominance.cu
-int64_t words_per_row(int64_t R);
-int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
-int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
-                      int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar, cudaStream_t s);
 }  // namespace mo
 
 #include "k_niche_args.cuh"
+
+#include "k_dominance_args.cuh"
 
 namespace mo {
 
@@ -33,7 +30,8 @@ constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/h
 struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
-      hist, sel, total;
+      hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
+      lvl, sctl, total;
 };
 
 static size_t bump(size_t& cur, size_t bytes) {
@@ -78,6 +76,22 @@ static Layout make_layout(int64_t R, int64_t w, int m) {
   L.part = bump(c, (size_t)2 * (MAX_GRID + 1) * 4);
   L.hist = bump(c, (size_t)256 * MAX_GRID * 4);
   L.sel = bump(c, (size_t)R);
+  L.FS = bump(c, (size_t)R * m * 4);
+  L.SS = bump(c, (size_t)R * 4);
+  L.perm_sort = bump(c, (size_t)R * 4);
+  L.wend = bump(c, (size_t)R * 4);
+  L.hasdom = bump(c, (size_t)R);
+  L.rank_pos = bump(c, (size_t)R * 4);
+  L.trace = bump(c, 64 * 8);
+  L.pcnt = bump(c, (size_t)(PRESORT_BUCKETS + 1) * 4);
+  L.pfill = bump(c, (size_t)(PRESORT_BUCKETS + 1) * 4);
+  L.blkmin = bump(c, (size_t)(R / 256 + 2) * 4);
+  L.blkmax = bump(c, (size_t)(R / 256 + 2) * 4);
+  L.pctl = bump(c, 16 * 4);
+  L.kept = bump(c, (size_t)(w + 1) * 4);
+  L.fill = bump(c, (size_t)(w + 1) * 4);
+  L.lvl = bump(c, (size_t)2 * LVL_BINS * 4);
+  L.sctl = bump(c, 16 * 4);
   L.total = (c + 255) & ~(size_t)255;
   return L;
 }
@@ -88,7 +102,7 @@ static T* at(void* ws, size_t off) {
 }
 
 // Barrier slots inside L.bar (each 2 x u32, 64-byte apart to avoid false sharing)
-enum { BAR_PEEL = 0, BAR_PREP = 16, BAR_SELECT = 32 };
+enum { BAR_PEEL = 0, BAR_PREP = 16, BAR_SELECT = 32, BAR_PRESORT = 48 };
 
 static int check_ws(const Layout& L, void* ws, size_t bytes) {
   if (ws == nullptr || bytes < L.total) return MO_ERR_PARAM;
@@ -126,6 +140,16 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.bar = at<unsigned>(ws, L.bar) + BAR_PREP;
   a.icpt_out = icpt_out;
   a.mode = mode;
+  a.trace = at<unsigned long long>(ws, L.trace);
+  a.rho = at<int>(ws, L.rho);
+  a.rho_p = at<int>(ws, L.rho_p);
+  a.take = at<int>(ws, L.take);
+  a.kept = at<int>(ws, L.kept);
+  a.fill = at<int>(ws, L.fill);
+  a.near_key = at<unsigned long long>(ws, L.near_key);
+  a.prom = at<uint8_t>(ws, L.prom);
+  a.lvl = at<int>(ws, L.lvl);
+  a.sctl = at<int>(ws, L.sctl);
   return a;
 }
 
@@ -145,14 +169,15 @@ static SelectArgs select_args(const Layout& L, void* ws, int64_t R, int64_t w, i
   a.rho = at<int>(ws, L.rho);
   a.rho_p = at<int>(ws, L.rho_p);
   a.take = at<int>(ws, L.take);
+  a.kept = at<int>(ws, L.kept);
   a.bstart = at<int>(ws, L.bstart);
+  a.fill = at<int>(ws, L.fill);
+  a.bucket = at<int>(ws, L.valA);
   a.near_key = at<unsigned long long>(ws, L.near_key);
   a.prom = at<uint8_t>(ws, L.prom);
-  a.keyA = at<uint32_t>(ws, L.keyA);
-  a.valA = at<int>(ws, L.valA);
-  a.keyB = at<uint32_t>(ws, L.keyB);
-  a.valB = at<int>(ws, L.valB);
-  a.ctl = at<int>(ws, L.ctl);
+  a.lvl = at<int>(ws, L.lvl);
+  a.sctl = at<int>(ws, L.sctl);
+  a.count_inside = 0;
   a.selected = selected;
   a.XR = nullptr;
   a.FR = nullptr;
@@ -161,6 +186,7 @@ static SelectArgs select_args(const Layout& L, void* ws, int64_t R, int64_t w, i
   a.dvars = 0;
   a.m = 0;
   a.gen_ptr = nullptr;
+  a.trace = at<unsigned long long>(ws, L.trace);
   a.g.bar = at<unsigned>(ws, L.bar) + BAR_SELECT;
   a.g.part = at<int>(ws, L.part);
   a.g.hist = at<int>(ws, L.hist);
@@ -183,9 +209,33 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   const int64_t n = a->n, R = 2 * n;
   void* ws = a->workspace;
   uint32_t* bits = at<uint32_t>(ws, L.bits);
-  MO_TRY(launch_dom_tile(a->FR, R, a->m, nullptr, bits, s));
+  PresortArgs ps;
+  ps.F = a->FR;
+  ps.R = (int)R;
+  ps.m = a->m;
+  ps.keyA = at<uint32_t>(ws, L.keyA);
+  ps.valA = at<int>(ws, L.valA);
+  ps.keyB = at<uint32_t>(ws, L.keyB);
+  ps.valB = at<int>(ws, L.pcnt);
+  ps.fill = at<int>(ws, L.pfill);
+  ps.blkmin = at<float>(ws, L.blkmin);
+  ps.blkmax = at<float>(ws, L.blkmax);
+  ps.ctl = at<unsigned>(ws, L.pctl);
+  ps.perm = at<int>(ws, L.perm_sort);
+  ps.FS = at<float>(ws, L.FS);
+  ps.SS = at<float>(ws, L.SS);
+  ps.wend = at<int>(ws, L.wend);
+  ps.g.bar = at<unsigned>(ws, L.bar) + BAR_PRESORT;
+  ps.g.part = at<int>(ws, L.part);
+  ps.g.hist = at<int>(ws, L.hist);
+  ps.g.parity = 0;
+  ps.trace = at<unsigned long long>(ws, L.trace);
+  MO_TRY(launch_presort(ps, s));
+  uint8_t* hasdom = at<uint8_t>(ws, L.hasdom);
+  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, R, a->m, bits, hasdom, s));
   return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
-                           at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, s);
+                           at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, ps.perm, hasdom, ps.wend,
+                           at<int>(ws, L.rank_pos), ps.trace, s);
 }
 
 static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
@@ -222,6 +272,9 @@ static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   fa.akey = pa.akey;
   fa.pi = at<int>(ws, L.pi);
   fa.d = at<float>(ws, L.d);
+  fa.ranks = a->ranks;
+  fa.rho = pa.rho;
+  fa.rho_p = pa.rho_p;
   MO_TRY(launch_assoc_final(fa, R, s));
   SelectArgs sa = select_args(L, ws, R, w, n, a->ranks, a->info, fa.pi, fa.d, at<uint8_t>(ws, L.sel));
   sa.XR = a->XR;
@@ -266,6 +319,8 @@ const char* mo_version(void) { return "manyobj_b200 0.1.0 (sm_100a)"; }
 
 int64_t mo_bits_words_per_row(int64_t R) { return words_per_row(R); }
 
+int64_t mo_trace_offset(int64_t n, int32_t m, int64_t w) { return (int64_t)make_layout(2 * n, w, m).trace; }
+
 int mo_workspace_bytes(int64_t n, int32_t m, int32_t d, int64_t w, size_t* bytes) {
   (void)d;
   if (!bytes || n < 1 || m < 1 || w < 1) return MO_ERR_PARAM;
@@ -309,13 +364,49 @@ int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid
   return launch_dom_tile(F, R, m, valid, bits, (cudaStream_t)stream_);
 }
 
+int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, float* SS, int32_t* wend,
+               float* blkmin, float* blkmax, void* workspace, size_t workspace_bytes, void* stream_) {
+  if (R < 1 || m < 1 || !F || !perm || !FS || !SS || !wend || !blkmin || !blkmax) return MO_ERR_PARAM;
+  Layout L = make_layout(R, 1, m);
+  MO_TRY(check_ws(L, workspace, workspace_bytes));
+  PresortArgs ps;
+  ps.F = F;
+  ps.R = (int)R;
+  ps.m = m;
+  ps.keyA = at<uint32_t>(workspace, L.keyA);
+  ps.valA = at<int>(workspace, L.valA);
+  ps.keyB = at<uint32_t>(workspace, L.keyB);
+  ps.valB = at<int>(workspace, L.pcnt);
+  ps.fill = at<int>(workspace, L.pfill);
+  ps.blkmin = blkmin;
+  ps.blkmax = blkmax;
+  ps.ctl = at<unsigned>(workspace, L.pctl);
+  ps.perm = perm;
+  ps.FS = FS;
+  ps.SS = SS;
+  ps.wend = wend;
+  ps.g.bar = at<unsigned>(workspace, L.bar) + BAR_PRESORT;
+  ps.g.part = at<int>(workspace, L.part);
+  ps.g.hist = at<int>(workspace, L.hist);
+  ps.g.parity = 0;
+  ps.trace = nullptr;
+  return launch_presort(ps, (cudaStream_t)stream_);
+}
+
+int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int32_t m,
+                             uint32_t* bits, uint8_t* hasdom, void* stream_) {
+  if (!FS || !blkmin || !blkmax || !bits || !hasdom) return MO_ERR_PARAM;
+  return launch_dom_tile_sorted(FS, blkmin, blkmax, R, m, bits, hasdom, (cudaStream_t)stream_);
+}
+
 int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int32_t* ranks,
                   int32_t* info, void* workspace, size_t workspace_bytes, void* stream_) {
   Layout L = make_layout(R, 1, 1);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   return launch_front_peel(bits, R, valid, stop_at, ranks, info, at<int>(workspace, L.resume),
                            at<uint32_t>(workspace, L.ranked), at<int>(workspace, L.fsizes),
-                           at<unsigned>(workspace, L.bar) + BAR_PEEL, (cudaStream_t)stream_);
+                           at<unsigned>(workspace, L.bar) + BAR_PEEL, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, (cudaStream_t)stream_);
 }
 
 int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, const int32_t* info, uint64_t seed,
@@ -396,6 +487,7 @@ int mo_niche_select(const int32_t* pi, const float* d, int64_t R, int64_t w, int
                           PREP_PERMS);
   MO_TRY(launch_prep(pa, s));
   SelectArgs sa = select_args(L, workspace, R, w, n, ranks, info, pi, d, selected);
+  sa.count_inside = 1;
   return launch_select(sa, s);
 }
 

@@ -120,6 +120,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int* total) {
 // cudaLaunchAttributeCooperative (all CTAs co-resident).  `bar` = {count, gen}.
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
+  if (gridDim.x == 1) return;
   if (threadIdx.x == 0) {
     volatile unsigned* vgen = bar + 1;
     unsigned gen = *vgen;
@@ -135,6 +136,17 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     __threadfence();
   }
   __syncthreads();
+}
+
+// Phase trace for the persistent kernels: block 0 / thread 0 stamps the
+// global nanosecond timer into tr[slot] (tr == nullptr: no-op).  Read back by
+// the host (engine.Engine.trace()) to time phases inside one launch.
+__device__ __forceinline__ void trace_mark(unsigned long long* tr, int slot) {
+  if (tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[slot] = t;
+  }
 }
 
 }  // namespace mo

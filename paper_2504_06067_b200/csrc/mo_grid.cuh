@@ -56,22 +56,41 @@ __device__ int grid_scan(GridCtx& g, int64_t N, ValueF value, EmitF emit, int* s
 }
 
 // One stable LSD radix pass (8-bit digit at `shift`) of N (key, val) pairs
-// from (kin, vin) to (kout, vout).  Shared memory: `wcnt` >= (blockDim/32)*256
-// ints, `run`/`off` >= 256 ints each.  Two internal grid barriers.
+// from (kin, vin) to (kout, vout).  Block b owns a contiguous chunk; warp w of
+// the block owns a contiguous sub-segment of that chunk and scatters it in
+// order, 32 keys at a time, ranking equal digits with __match_any_sync against
+// its own running counters -- no block barrier inside the scatter.  Shared
+// memory: `wcnt` >= (blockDim/32)*256 ints, `off` >= 256 ints.  Two grid
+// barriers per pass.
 __device__ inline void grid_radix_pass(GridCtx& g, int N, int shift, const uint32_t* kin, const int* vin,
                                        uint32_t* kout, int* vout, int* wcnt, int* run, int* off, int* sh) {
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nw = blockDim.x >> 5;
   const int chunk = (int)ceil_div(N, G);
   const int lo = min(b * chunk, N), hi = min(lo + chunk, N);
-  // 1. block digit histogram -> hist[d * G + b]
-  for (int d = tid; d < 256; d += blockDim.x) run[d] = 0;
+  const int seg = (int)ceil_div(hi - lo, nw);
+  const int wlo = min(lo + wid * seg, hi), whi = min(wlo + seg, hi);
+  int* my = wcnt + wid * 256;
+  // 1. per-warp digit histogram of its sub-segment
+  for (int q = lane; q < 256; q += 32) my[q] = 0;
+  __syncwarp();
+  for (int base = wlo; base < whi; base += 32) {
+    const int e = base + lane;
+    const bool act = e < whi;
+    const int dg = act ? (int)((__ldcg(kin + e) >> shift) & 255u) : 256 + lane;
+    const unsigned peers = __match_any_sync(MO_FULL, dg);
+    if (act && (peers & ((1u << lane) - 1u)) == 0) my[dg] += __popc(peers);
+    __syncwarp();
+  }
   __syncthreads();
-  for (int e = lo + tid; e < hi; e += blockDim.x) atomicAdd(&run[(__ldcg(kin + e) >> shift) & 255u], 1);
-  __syncthreads();
-  for (int d = tid; d < 256; d += blockDim.x) g.hist[d * G + b] = run[d];
+  // block histogram -> hist[d * G + b]
+  for (int d = tid; d < 256; d += blockDim.x) {
+    int t = 0;
+    for (int q = 0; q < nw; ++q) t += wcnt[q * 256 + d];
+    g.hist[d * G + b] = t;
+  }
   grid_sync(g.bar);
-  // 2. global offset of (digit d, this block): totals of smaller digits + earlier blocks of digit d
+  // 2. base of (digit d, this block) = totals of smaller digits + earlier blocks of digit d
   for (int d = tid; d < 256; d += blockDim.x) {
     int pre = 0, tot = 0;
     for (int q = 0; q < G; ++q) {
@@ -83,7 +102,7 @@ __device__ inline void grid_radix_pass(GridCtx& g, int N, int shift, const uint3
     run[d] = tot;
   }
   __syncthreads();
-  if (tid < 32) {  // exclusive scan of 256 digit totals by one warp (8 per lane)
+  if (tid < 32) {  // exclusive scan of the 256 digit totals by one warp (8 per lane)
     int v[8], s = 0;
     for (int q = 0; q < 8; ++q) {
       v[q] = run[lane * 8 + q];
@@ -101,38 +120,33 @@ __device__ inline void grid_radix_pass(GridCtx& g, int N, int shift, const uint3
     }
   }
   __syncthreads();
-  for (int d = tid; d < 256; d += blockDim.x) run[d] = 0;  // running count per digit in this block
-  for (int q = tid; q < nw * 256; q += blockDim.x) wcnt[q] = 0;
+  // per-warp running base: off[d] + counts of earlier warps of this block
+  for (int d = tid; d < 256; d += blockDim.x) {
+    int r = off[d];
+    for (int q = 0; q < nw; ++q) {
+      const int c = wcnt[q * 256 + d];
+      wcnt[q * 256 + d] = r;
+      r += c;
+    }
+  }
   __syncthreads();
-  // 3. stable scatter, one blockDim tile at a time
-  for (int base = lo; base < hi; base += blockDim.x) {
-    const int e = base + tid;
-    const bool act = e < hi;
-    uint32_t key = act ? __ldcg(kin + e) : 0u;
-    int val = act ? __ldcg(vin + e) : 0;
+  // 3. stable scatter of the warp's sub-segment
+  for (int base = wlo; base < whi; base += 32) {
+    const int e = base + lane;
+    const bool act = e < whi;
+    const uint32_t key = act ? __ldcg(kin + e) : 0u;
+    const int val = act ? __ldcg(vin + e) : 0;
     const int dg = act ? (int)((key >> shift) & 255u) : 256 + lane;
     const unsigned peers = __match_any_sync(MO_FULL, dg);
-    const int rank_w = __popc(peers & ((1u << lane) - 1u));
-    if (act && rank_w == 0) wcnt[wid * 256 + dg] = __popc(peers);
-    __syncthreads();
-    for (int d = tid; d < 256; d += blockDim.x) {
-      int r = run[d];
-      for (int q = 0; q < nw; ++q) {
-        int c = wcnt[q * 256 + d];
-        wcnt[q * 256 + d] = r;
-        r += c;
-      }
-      run[d] = r;
-    }
-    __syncthreads();
+    const unsigned below = peers & ((1u << lane) - 1u);
     if (act) {
-      const int pos = off[dg] + wcnt[wid * 256 + dg] + rank_w;
+      const int pos = my[dg] + __popc(below);
       kout[pos] = key;
       vout[pos] = val;
     }
-    __syncthreads();
-    for (int q = tid; q < nw * 256; q += blockDim.x) wcnt[q] = 0;
-    __syncthreads();
+    __syncwarp();
+    if (act && below == 0) my[dg] += __popc(peers);
+    __syncwarp();
   }
   grid_sync(g.bar);
   (void)sh;

@@ -36,6 +36,42 @@ def dominance_bits(F, valid=None):
     return bits
 
 
+def presort(F):
+    """The engine's sort-path prologue: rows bucketed by S = FP32 left-to-right objective sum.
+
+    Returns a dict of CUDA tensors: perm[p] = row at position p (buckets in
+    S order, arbitrary order inside a bucket), FS / SS = rows / sums in that
+    order, wend[p] = one past the last bit-matrix word that can hold a
+    dominator of p, blkmin / blkmax = S range of every 256-position block.
+    """
+    F = as_matrix(F)
+    R, m = F.shape
+    dev = F.device
+    nb = (R + 255) // 256
+    out = dict(perm=torch.empty(R, dtype=torch.int32, device=dev), FS=torch.empty_like(F),
+               SS=torch.empty(R, dtype=torch.float32, device=dev), wend=torch.empty(R, dtype=torch.int32, device=dev),
+               blkmin=torch.empty(nb, dtype=torch.float32, device=dev),
+               blkmax=torch.empty(nb, dtype=torch.float32, device=dev))
+    ws = _lib.workspace_rows(R, m, 1, dev)
+    _lib.check(_lib.lib().mo_presort(_lib.ptr(F), R, m, *(_lib.ptr(out[k]) for k in
+                                                          ("perm", "FS", "SS", "wend", "blkmin", "blkmax")),
+                                     _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "mo_presort")
+    return out
+
+
+def dominance_bits_sorted(ps):
+    """Bit-matrix of presorted rows (position space) + has-a-dominator flags, from :func:`presort`."""
+    FS = ps["FS"]
+    R, m = FS.shape
+    W = int(_lib.lib().mo_bits_words_per_row(R))
+    bits = torch.zeros((R, W), dtype=torch.int32, device=FS.device)
+    hasdom = torch.empty(R, dtype=torch.uint8, device=FS.device)
+    _lib.check(_lib.lib().mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), R,
+                                                   m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()),
+               "mo_dominance_bits_sorted")
+    return bits, hasdom
+
+
 def unpack_bits(bits, R):
     """(R x W) words -> dense bool M with M[i][j] = bit i of row j."""
     w = bits.view(torch.int32)
@@ -105,4 +141,4 @@ def split_from_info(info):
 
 
 __all__ = ["DROPPED", "dominates", "dominance_bits", "dominance_matrix", "non_dominated_sort", "FrontSplit",
-           "split_fronts", "split_from_info", "unpack_bits", "device"]
+           "split_fronts", "split_from_info", "unpack_bits", "presort", "dominance_bits_sorted", "device"]

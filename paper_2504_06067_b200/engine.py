@@ -189,6 +189,26 @@ class Engine:
     def F(self):
         return self.FR[self.cur][: self.cfg.n]
 
+    TRACE_SLOTS = {
+        "presort.sum": (0, 1), "presort.hist": (1, 2), "presort.scan": (2, 3), "presort.scatter": (3, 4),
+        "presort.bounds": (4, 5),
+        "peel.prologue": (8, 9), "peel.fronts": (9, 10),
+        "prep.phase0": (16, 17), "prep.extremes": (17, 18), "prep.solve": (18, 19),
+        "select.nearest_keys": (24, 25), "select.nearest": (25, 26), "select.level": (26, 27),
+        "select.marked": (27, 28), "select.take": (28, 29), "select.cache": (29, 30), "select.topk": (30, 31),
+        "select.compact": (31, 35), "select.ranks": (35, 36), "select.total": (24, 36),
+    }
+
+    def trace(self):
+        """Phase durations (us) inside the persistent kernels of the last step (globaltimer)."""
+        off = int(_lib.lib().mo_trace_offset(self.cfg.n, self.cfg.m, self.w))
+        t = self.ws[off: off + 64 * 8].view(torch.int64).cpu().tolist()
+        out = {}
+        for name, (a, b) in self.TRACE_SLOTS.items():
+            if t[a] and t[b] and t[b] >= t[a]:
+                out[name] = (t[b] - t[a]) / 1e3
+        return out
+
     def info_dict(self):
         h = self.info.cpu().tolist()
         return {k.lower(): h[v] for k, v in _lib.INFO.items()}

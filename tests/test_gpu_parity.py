@@ -118,6 +118,42 @@ def test_dominance_with_valid_mask(M):
     assert np.array_equal(r, Odom.non_dominated_sort(F, valid))
 
 
+def test_sorted_path_bits(M):
+    """Engine sort path: S-ordered buckets, bits of every row up to wend, hasdom flags."""
+    rs = np.random.default_rng(12)
+    cases = [rs.random((700, 3)), rs.integers(0, 3, size=(600, 4)), rs.random((1300, 5)),
+             np.repeat(rs.random((300, 2)), 3, axis=0), rs.random((257, 10))]
+    for F in cases:
+        F = F.astype(np.float32)
+        R, m = F.shape
+        ps = M.dominance.presort(F)
+        perm = np_(ps["perm"])
+        assert sorted(perm.tolist()) == list(range(R))
+        S = F[:, 0].copy()
+        for k in range(1, m):
+            S = (S + F[:, k]).astype(np.float32)
+        SS = np_(ps["SS"])
+        assert np.array_equal(SS, S[perm]) and np.array_equal(np_(ps["FS"]), F[perm])
+        # order inside a bucket is free ...
+        we = np_(ps["wend"])
+        # ... but no later position outside p's bucket may have S <= S[p]
+        for p in range(R):
+            later = np.arange((we[p]) * 32, R)
+            assert (SS[later] > SS[p]).all()
+        bmin, bmax = np_(ps["blkmin"]), np_(ps["blkmax"])
+        for b in range(len(bmin)):
+            blk = SS[b * 256:(b + 1) * 256]
+            assert bmin[b] == blk.min() and bmax[b] == blk.max()
+        bits, hasdom = M.dominance.dominance_bits_sorted(ps)
+        D = Odom.dominance_matrix(F[perm])                      # D[i][j]: i dominates j (position space)
+        dense = np_(M.dominance.unpack_bits(bits, R))
+        for j in range(R):
+            lim = min(R, we[j] * 32)
+            assert np.array_equal(dense[:lim, j], D[:lim, j]), (F.shape, j)
+            assert not D[lim:, j].any()
+        assert np.array_equal(np_(hasdom).astype(bool), D.any(axis=0))
+
+
 def test_nds_bit_exact(M):
     for F in _instances():
         assert np.array_equal(np_(M.dominance.non_dominated_sort(F)), Odom.non_dominated_sort(F)), F.shape
