@@ -215,7 +215,7 @@ def time_kernels(torch, eng, _lib):
     out.update({k: v * 1e3 for k, v in prof.items()})        # ms
     # the engine's dominance kernel alone (presorted rows of the last merged population)
     FR = eng.FR[eng.cur ^ 1]
-    perm, FS, SS, wend = dominance.presort(FR)
+    ps = dominance.presort(FR)
     W = int(L.mo_bits_words_per_row(R))
     bits = torch.empty((R, W), dtype=torch.int32, device="cuda")
     hasdom = torch.empty(R, dtype=torch.uint8, device="cuda")
@@ -223,8 +223,8 @@ def time_kernels(torch, eng, _lib):
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(SS), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
-                                              _lib.stream_ptr()), "dom")
+        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), R,
+                                              m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()), "dom")
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))

@@ -178,12 +178,14 @@ __global__ void __launch_bounds__(DOM_TILE) k_dom_tile_generic(const float* __re
 // never written (the peel is bounded by wend[p]).  hasdom[p] = 1 iff row p
 // has at least one dominator, so front 0 needs no scan at all.
 
+constexpr int DOMS_THREADS = DOM_TILE / 2;  // two j columns per thread
+
 template <int M>
-__global__ void __launch_bounds__(DOM_TILE) k_dom_tile_sorted(const float* __restrict__ FS,
-                                                              const float* __restrict__ blkmin,
-                                                              const float* __restrict__ blkmax, int R,
-                                                              uint32_t* __restrict__ bits, int64_t W,
-                                                              uint8_t* __restrict__ hasdom) {
+__global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* __restrict__ FS,
+                                                                  const float* __restrict__ blkmin,
+                                                                  const float* __restrict__ blkmax, int R,
+                                                                  uint32_t* __restrict__ bits, int64_t W,
+                                                                  uint8_t* __restrict__ hasdom) {
   constexpr int MP = (M + 3) & ~3;
   __shared__ __align__(16) float sFi[DOM_TILE * MP];
   __shared__ uint32_t sB2[DOM_TILE * 9];
@@ -192,54 +194,81 @@ __global__ void __launch_bounds__(DOM_TILE) k_dom_tile_sorted(const float* __res
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = bi * DOM_TILE, j0 = bj * DOM_TILE;
   // rows past R are padded with +FLT_MAX: they dominate nothing and are never stored
-  for (int e = tid; e < DOM_TILE * MP; e += DOM_TILE) {
+  for (int e = tid; e < DOM_TILE * MP; e += DOMS_THREADS) {
     int r = e / MP, k = e - r * MP;
     int i = i0 + r;
     sFi[e] = (k < M && i < R) ? FS[(int64_t)i * M + k] : 3.402823466e38f;
   }
-  const int j = j0 + tid;
-  float fj[M];
+  const int ja = j0 + tid, jb = j0 + tid + DOMS_THREADS;
+  float fa[M], fb[M];
 #pragma unroll
-  for (int k = 0; k < M; ++k) fj[k] = j < R ? FS[(int64_t)j * M + k] : 3.402823466e38f;
+  for (int k = 0; k < M; ++k) {
+    fa[k] = ja < R ? FS[(int64_t)ja * M + k] : 3.402823466e38f;
+    fb[k] = jb < R ? FS[(int64_t)jb * M + k] : 3.402823466e38f;
+  }
   const bool fast = (bi < bj) && (__ldg(blkmax + bi) < __ldg(blkmin + bj));
   __syncthreads();
-  uint32_t accw[8];
+  uint32_t wa[8], wb[8];
   if (fast) {
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
-      uint32_t acc = 0;
+      uint32_t acca = 0, accb = 0;
 #pragma unroll
-      for (int b = 0; b < 32; ++b) Chain<M>::le(sFi + (c * 32 + b) * MP, fj, acc, 1u << b);
-      accw[c] = acc;
+      for (int b = 0; b < 32; ++b) {
+        const float* fi = sFi + (c * 32 + b) * MP;
+        float v[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) v[k] = fi[k];
+        Chain<M>::le(v, fa, acca, 1u << b);
+        Chain<M>::le(v, fb, accb, 1u << b);
+      }
+      wa[c] = acca;
+      wb[c] = accb;
     }
   } else {
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
-      uint32_t acc = 0, mybal = 0;
+      uint32_t acca = 0, accb = 0, bala = 0, balb = 0;
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
-        const uint32_t bal = Chain<M>::sym(sFi + (c * 32 + b) * MP, fj, acc, 1u << b);
-        mybal = (lane == b) ? bal : mybal;
+        const float* fi = sFi + (c * 32 + b) * MP;
+        float v[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) v[k] = fi[k];
+        const uint32_t x = Chain<M>::sym(v, fa, acca, 1u << b);
+        const uint32_t y = Chain<M>::sym(v, fb, accb, 1u << b);
+        bala = (lane == b) ? x : bala;
+        balb = (lane == b) ? y : balb;
       }
-      accw[c] = acc;
-      sB2[(c * 32 + lane) * 9 + warp] = mybal;
+      wa[c] = acca;
+      wb[c] = accb;
+      sB2[(c * 32 + lane) * 9 + warp] = bala;
+      sB2[(c * 32 + lane) * 9 + warp + 4] = balb;
     }
   }
-  if (j < R) {
-    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)j * W + (int64_t)bi * 8);
-    dst[0] = make_uint4(accw[0], accw[1], accw[2], accw[3]);
-    dst[1] = make_uint4(accw[4], accw[5], accw[6], accw[7]);
-    if ((accw[0] | accw[1] | accw[2] | accw[3] | accw[4] | accw[5] | accw[6] | accw[7]) != 0u) hasdom[j] = 1;
+  if (ja < R) {
+    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)ja * W + (int64_t)bi * 8);
+    dst[0] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
+    dst[1] = make_uint4(wa[4], wa[5], wa[6], wa[7]);
+    if ((wa[0] | wa[1] | wa[2] | wa[3] | wa[4] | wa[5] | wa[6] | wa[7]) != 0u) hasdom[ja] = 1;
+  }
+  if (jb < R) {
+    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)jb * W + (int64_t)bi * 8);
+    dst[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
+    dst[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
+    if ((wb[0] | wb[1] | wb[2] | wb[3] | wb[4] | wb[5] | wb[6] | wb[7]) != 0u) hasdom[jb] = 1;
   }
   if (!fast && bi != bj) {
     __syncthreads();
-    const int i = i0 + tid;
-    if (i < R) {
-      const uint32_t* s = sB2 + tid * 9;
-      uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)i * W + (int64_t)bj * 8);
-      dst[0] = make_uint4(s[0], s[1], s[2], s[3]);
-      dst[1] = make_uint4(s[4], s[5], s[6], s[7]);
-      if ((s[0] | s[1] | s[2] | s[3] | s[4] | s[5] | s[6] | s[7]) != 0u) hasdom[i] = 1;
+    for (int r = tid; r < DOM_TILE; r += DOMS_THREADS) {
+      const int i = i0 + r;
+      if (i < R) {
+        const uint32_t* sw = sB2 + r * 9;
+        uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)i * W + (int64_t)bj * 8);
+        dst[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+        dst[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
+        if ((sw[0] | sw[1] | sw[2] | sw[3] | sw[4] | sw[5] | sw[6] | sw[7]) != 0u) hasdom[i] = 1;
+      }
     }
   }
 }
@@ -291,7 +320,7 @@ int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* bl
   dim3 grid((unsigned)tiles);
   switch (m) {
 #define MO_DOMS_CASE(MM) \
-  case MM: k_dom_tile_sorted<MM><<<grid, DOM_TILE, 0, s>>>(FS, blkmin, blkmax, (int)R, bits, W, hasdom); break;
+  case MM: k_dom_tile_sorted<MM><<<grid, DOMS_THREADS, 0, s>>>(FS, blkmin, blkmax, (int)R, bits, W, hasdom); break;
     MO_DOMS_CASE(2)
     MO_DOMS_CASE(3)
     MO_DOMS_CASE(4)

@@ -42,15 +42,10 @@ __device__ __forceinline__ void atomic_min_f(float* addr, float v) {
     atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
 }
 
-__device__ double solve_intercepts(const PrepArgs& a, const float* ideal, double* A, double* rhs, int* singular) {
-  // E b = 1 with partial pivoting, FP64, every operation separately rounded
-  // (library is built with -fmad=false).  Mirrors oracle niche.gauss_solve.
-  const int m = a.m;
-  for (int r = 0; r < m; ++r) {
-    const int row = __ldcg(a.perm_pop + (uint32_t)(__ldcg(a.ext_key + r) & 0xffffffffull));
-    for (int c = 0; c < m; ++c) A[r * m + c] = (double)__fsub_rn(a.F[(int64_t)row * m + c], ideal[c]);
-    rhs[r] = 1.0;
-  }
+// E b = 1 with partial pivoting, FP64, every operation separately rounded
+// (library built with -fmad=false).  Mirrors oracle niche.gauss_solve.
+// A (m x m, row-major) and rhs are overwritten; rhs returns b.
+__device__ void gauss_solve(double* A, double* rhs, int m, int* singular) {
   for (int c = 0; c < m; ++c) {
     int p = c;
     double best = fabs(A[c * m + c]);
@@ -61,7 +56,7 @@ __device__ double solve_intercepts(const PrepArgs& a, const float* ideal, double
       }
     if (best == 0.0) {
       *singular = 1;
-      return 0.0;
+      return;
     }
     if (p != c) {
       for (int q = 0; q < m; ++q) {
@@ -82,10 +77,9 @@ __device__ double solve_intercepts(const PrepArgs& a, const float* ideal, double
   for (int c = m - 1; c >= 0; --c) {
     double s = rhs[c];
     for (int q = c + 1; q < m; ++q) s = s - A[c * m + q] * rhs[q];
-    rhs[c] = s / A[c * m + c];  // rhs now holds b
+    rhs[c] = s / A[c * m + c];
   }
   *singular = 0;
-  return 0.0;
 }
 
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
@@ -110,7 +104,13 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   load_shuffle_keys_smem(sKr, sSr, &sRr, (uint32_t)w, a.seed, gen, STREAM_REF_SHUFFLE);
   __syncthreads();
   if (a.mode == PREP_FULL) {
-    for (int64_t e = gtid; e < (int64_t)R * m; e += gthreads) atomic_min_f(&sMin[e % m], a.F[e]);
+    // column minima: per column, strided rows, warp reduction, one smem atomic per warp
+    for (int k = 0; k < m; ++k) {
+      float v = __int_as_float(0x7f800000);
+      for (int i = gtid; i < R; i += gthreads) v = fminf(v, a.F[(int64_t)i * m + k]);
+      for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(MO_FULL, v, o));
+      if (lane == 0) atomic_min_f(&sMin[k], v);
+    }
     __syncthreads();
     for (int k = tid; k < m; k += blockDim.x) atomic_min_f(&a.ideal[k], sMin[k]);
   }
@@ -187,47 +187,53 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   grid_sync(a.bar);
   trace_mark(a.trace, 18);
 
-  // ---- phase 2: hyperplane solve (one thread), per-component fallbacks
-  if (blockIdx.x == 0 && tid == 0) {
-    int singular = 0;
-    float idl2[MAXM];
-    for (int k = 0; k < m; ++k) idl2[k] = __ldcg(a.ideal + k);
-    double fb[MAXM];
-    for (int k = 0; k < m; ++k) {
-      double mx = (double)ord2f(__ldcg(a.colmax + k));
-      fb[k] = mx > DEGENERATE ? mx : 1.0;
+  // ---- phase 2: hyperplane solve (one thread) on the extreme rows loaded by the block,
+  //      per-component fallbacks
+  if (blockIdx.x == 0) {
+    __shared__ double sFb[MAXM];
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int r = e / m, c = e - r * m;
+      const int row = __ldcg(a.perm_pop + (uint32_t)(__ldcg(a.ext_key + r) & 0xffffffffull));
+      sA[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
     }
-    if (ncand == 0) singular = 1;
-    else solve_intercepts(a, idl2, sA, sRhs, &singular);
-    bool bad = singular != 0;
-    if (!bad)
-      for (int k = 0; k < m; ++k)
-        if (!isfinite(sRhs[k])) bad = true;
-    for (int k = 0; k < m; ++k) {
-      double ak;
-      if (bad) {
-        ak = fb[k];
-      } else {
-        ak = 1.0 / sRhs[k];
-        if (!(isfinite(ak) && ak > DEGENERATE)) ak = fb[k];
+    for (int k = tid; k < m; k += blockDim.x) {
+      const double mx = (double)ord2f(__ldcg(a.colmax + k));
+      sFb[k] = mx > DEGENERATE ? mx : 1.0;
+      sRhs[k] = 1.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int singular = 0;
+      if (ncand == 0) singular = 1;
+      else gauss_solve(sA, sRhs, m, &singular);
+      bool bad = singular != 0;
+      if (!bad)
+        for (int k = 0; k < m; ++k)
+          if (!isfinite(sRhs[k])) bad = true;
+      for (int k = 0; k < m; ++k) {
+        double ak;
+        if (bad) {
+          ak = sFb[k];
+        } else {
+          ak = 1.0 / sRhs[k];
+          if (!(isfinite(ak) && ak > DEGENERATE)) ak = sFb[k];
+        }
+        a.icpt[k] = ak;
+        a.a32[k] = __double2float_rn(ak);
+        if (a.icpt_out) a.icpt_out[k] = ak;
       }
-      a.icpt[k] = ak;
-      a.a32[k] = __double2float_rn(ak);
-      if (a.icpt_out) a.icpt_out[k] = ak;
+      a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
     }
-    a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
   }
   trace_mark(a.trace, 19);
 }
 
 // ---------------------------------------------------------- association
 
-constexpr int ASSOC_THREADS = 128;
+constexpr int ASSOC_THREADS = 256;
 constexpr int ASSOC_RB = 4;                        // rows per thread
 constexpr int ASSOC_ROWS = ASSOC_THREADS * ASSOC_RB;
-constexpr int ASSOC_PTILE = 512;                   // reference points staged per smem tile
-
-
+constexpr int ASSOC_PTILE = 256;                   // reference points staged per smem tile
 
 template <int M>
 __device__ __forceinline__ float canon_dot(const float* f, const float* z) {
@@ -237,17 +243,13 @@ __device__ __forceinline__ float canon_dot(const float* f, const float* z) {
   return t;
 }
 
+// rows x reference-split grid.  Thread: ASSOC_RB candidate rows in registers;
+// the block streams its reference range through shared memory (shuffled
+// order) two points per step; strict '>' keeps the first maximum, and the
+// splits merge through a 64-bit atomicMax of (ord(t), ~position).
 template <int M>
-__global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
+__device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rbase, int p0, int p1, float* sz) {
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sz[ASSOC_PTILE * MP];
-  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
-  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
-  const int ncand = __ldcg(a.ctl);
-  const int rbase = blockIdx.x * ASSOC_ROWS;
-  if (rbase >= ncand) return;
-  const int p0 = blockIdx.y * a.psplit;
-  const int p1 = min(a.w, p0 + a.psplit);
   if (p0 >= p1) return;
   const int tid = threadIdx.x;
   float fn[ASSOC_RB][M];
@@ -275,22 +277,30 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
   for (int t0 = p0; t0 < p1; t0 += ASSOC_PTILE) {
     const int tn = min(ASSOC_PTILE, p1 - t0);
     __syncthreads();
-    for (int e = tid; e < tn * MP; e += ASSOC_THREADS) {
+    for (int e = tid; e < ASSOC_PTILE * MP; e += ASSOC_THREADS) {
       const int p = e / MP, k = e - p * MP;
-      sz[e] = k < M ? a.zs[(int64_t)(t0 + p) * M + k] : 0.0f;
+      sz[e] = (k < M && p < tn) ? a.zs[(int64_t)(t0 + p) * M + k] : -__int_as_float(0x7f800000);
     }
     __syncthreads();
-#pragma unroll 2
-    for (int p = 0; p < tn; ++p) {
-      float z[M];
+    // pairs of reference points; a padded point (-inf direction) never wins a strict '>'
+    for (int p = 0; p < tn; p += 2) {
+      float z0[M], z1[M];
 #pragma unroll
-      for (int k = 0; k < M; ++k) z[k] = sz[p * MP + k];
+      for (int k = 0; k < M; ++k) {
+        z0[k] = sz[p * MP + k];
+        z1[k] = sz[(p + 1) * MP + k];
+      }
 #pragma unroll
       for (int r = 0; r < ASSOC_RB; ++r) {
-        const float t = canon_dot<M>(fn[r], z);
-        if (t > best[r]) {
-          best[r] = t;
+        const float ta = canon_dot<M>(fn[r], z0);
+        const float tb = canon_dot<M>(fn[r], z1);
+        if (ta > best[r]) {
+          best[r] = ta;
           bp[r] = t0 + p;
+        }
+        if (tb > best[r]) {
+          best[r] = tb;
+          bp[r] = t0 + p + 1;
         }
       }
     }
@@ -304,6 +314,27 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
   }
 }
 
+template <int M>
+__global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sz[ASSOC_PTILE * MP];
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  // persistent schedule sized on the device from the real candidate count:
+  // (row block, reference split) items spread over exactly gridDim.x blocks
+  const int nrb = (ncand + ASSOC_ROWS - 1) / ASSOC_ROWS;
+  if (nrb == 0) return;
+  int splits = (int)gridDim.x / nrb;
+  const int maxsplit = (a.w + 63) / 64;
+  splits = splits < 1 ? 1 : (splits > maxsplit ? maxsplit : splits);
+  const int psplit = (a.w + splits - 1) / splits;
+  const int items = nrb * splits;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    assoc_item<M>(a, ncand, (item / splits) * ASSOC_ROWS, (item % splits) * psplit,
+                  min(a.w, (item % splits) * psplit + psplit), sz);
+  }
+}
 
 
 __global__ void k_assoc_final(AssocFinalArgs a) {
@@ -705,19 +736,16 @@ int launch_prep(const PrepArgs& a, cudaStream_t s) {
 
 int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   if (R <= 0) return MO_OK;
-  int rowblocks = (int)ceil_div(R, ASSOC_ROWS);
-  // split the reference points so the grid covers the GPU ~4x
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int want = 4 * sms;
-  int splits = (int)ceil_div(want, rowblocks);
-  int maxsplit = (int)ceil_div(a.w, 64);
-  if (splits > maxsplit) splits = maxsplit;
-  if (splits < 1) splits = 1;
+  static int capacity = 0;
+  if (!capacity) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assoc<5>, ASSOC_THREADS, 0);
+    capacity = sms * (per > 0 ? per : 1);
+  }
   AssocArgs b = a;
-  b.psplit = (int)ceil_div(a.w, splits);
-  dim3 grid(rowblocks, (unsigned)ceil_div(a.w, b.psplit));
+  dim3 grid(capacity);
   switch (m) {
 #define MO_AS_CASE(MM) \
   case MM: k_assoc<MM><<<grid, ASSOC_THREADS, 0, s>>>(b); break;

@@ -44,13 +44,13 @@ __device__ __forceinline__ double pm_apply(double x, double u, double eta) {
 
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
-// One block = VARY_PAIRS mating pairs.  Phase 1: one thread per pair draws
-// the parents (keyed MATING permutation) into shared memory.  Phase 2: one
-// thread per (pair, variable) runs SBX + clamp + PM + clamp and writes both
-// children.  Phase 3: one thread per child evaluates DTLZ (FP64) and lowers
-// the block's column minima (ideal point).
-constexpr int VARY_PAIRS = 32;
-constexpr int VARY_THREADS = 2 * VARY_PAIRS;
+// One block = VARY_PAIRS mating pairs, VARY_THREADS threads.  Phase 1: one
+// thread per pair draws the parents (keyed MATING permutation) into shared
+// memory.  Phase 2: one thread per (pair, variable) runs SBX + clamp + PM +
+// clamp and writes both children.  Phase 3: one thread per (child,
+// objective) evaluates DTLZ in FP64 and lowers the block's column minima.
+constexpr int VARY_PAIRS = 16;
+constexpr int VARY_THREADS = 256;
 
 __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const float* __restrict__ X, int n, int d,
                                                             int m, uint64_t seed, uint32_t gen_val,
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   __syncthreads();
   const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
   const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
-  const int tasks = min(VARY_PAIRS, npairs - q0) * d;
+  const int npb = min(VARY_PAIRS, npairs - q0);
+  const int tasks = npb * d;
   for (int e = tid; e < tasks; e += VARY_THREADS) {
     const int ql = e / d, v = e - ql * d;
     const int q = q0 + ql;
@@ -99,16 +100,22 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     Xo[(int64_t)(2 * q + 1) * d + v] = o2;
   }
   __syncthreads();
-  const int child = 2 * q0 + tid;
-  if (child < n) {
-    float* f = Fo + (int64_t)child * m;
-    const bool ok = dtlz_eval_row(problem, Xo + (int64_t)child * d, d, m, f);
-    if (!ok && domain_flag) atomicOr(domain_flag, 1);
-    if (ideal)
-      for (int j = 0; j < m; ++j) {
-        if (j < 16) atomic_min_float(&shMin[j], f[j]);
-        else atomic_min_float(&ideal[j], f[j]);
-      }
+  const int etasks = 2 * npb * m;
+  for (int e = tid; e < etasks; e += VARY_THREADS) {
+    const int cl = e / m, j = e - cl * m;
+    const int child = 2 * q0 + cl;
+    const float* x = Xo + (int64_t)child * d;
+    if (j == 0 && domain_flag) {
+      bool ok = true;
+      for (int v = 0; v < d; ++v) ok = ok && (x[v] >= 0.0f) && (x[v] <= 1.0f);
+      if (!ok) atomicOr(domain_flag, 1);
+    }
+    const float f = dtlz_eval_obj(problem, x, d, m, j);
+    Fo[(int64_t)child * m + j] = f;
+    if (ideal) {
+      if (j < 16) atomic_min_float(&shMin[j], f);
+      else atomic_min_float(&ideal[j], f);
+    }
   }
   if (ideal) {
     __syncthreads();

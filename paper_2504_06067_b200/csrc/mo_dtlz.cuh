@@ -96,4 +96,65 @@ __device__ inline bool dtlz_eval_row(int problem, const float* __restrict__ x, i
   return ok;
 }
 
+// Objective j of one individual -- the same operation order as dtlz_eval_row
+// (so the two agree bit for bit); used by the fused variation kernel, which
+// evaluates one (child, objective) per thread.
+__device__ inline float dtlz_eval_obj(int problem, const float* __restrict__ x, int d, int m, int j) {
+  const double PI = 3.141592653589793;
+  const int k = d - m + 1;
+  double g = 0.0;
+  if (problem == 1 || problem == 3) {
+    const double c20 = 20.0 * PI;
+    double s = 0.0;
+    for (int v = m - 1; v < d; ++v) {
+      double t = (double)x[v] - 0.5;
+      s = s + (t * t - cos(c20 * t));
+    }
+    g = 100.0 * ((double)k + s);
+  } else if (problem == 2 || problem == 4 || problem == 5) {
+    double s = 0.0;
+    for (int v = m - 1; v < d; ++v) {
+      double t = (double)x[v] - 0.5;
+      s = s + t * t;
+    }
+    g = s;
+  } else if (problem == 6) {
+    double s = 0.0;
+    for (int v = m - 1; v < d; ++v) s = s + pow((double)x[v], 0.1);
+    g = s;
+  } else {
+    double s = 0.0;
+    for (int v = m - 1; v < d; ++v) s = s + (double)x[v];
+    g = 1.0 + (9.0 / (double)k) * s;
+  }
+  if (problem == 1) {
+    double val = 0.5 * (1.0 + g);
+    for (int i = 0; i < m - 1 - j; ++i) val = val * (double)x[i];
+    if (j > 0) val = val * (1.0 - (double)x[m - 1 - j]);
+    return (float)val;
+  }
+  if (problem == 7) {
+    if (j < m - 1) return x[j];
+    double h = 0.0;
+    for (int q = 0; q < m - 1; ++q) {
+      double fj = (double)x[q];
+      h = h + fj / (1.0 + g) * (1.0 + sin(3.0 * PI * fj));
+    }
+    return (float)((1.0 + g) * ((double)m - h));
+  }
+  const double hp = PI / 2.0;
+  double val = 1.0 + g;
+  for (int i = 0; i <= m - 1 - j && i < m - 1; ++i) {
+    double xi = (double)x[i];
+    if (problem == 4) xi = pow(xi, 100.0);
+    const double th = ((problem == 5 || problem == 6) && i > 0) ? PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * xi)
+                                                                 : xi * hp;
+    if (i < m - 1 - j)
+      val = val * cos(th);
+    else if (j > 0)
+      val = val * sin(th);
+  }
+  return (float)val;
+}
+
 }  // namespace mo
