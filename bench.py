@@ -223,7 +223,7 @@ def time_kernels(torch, eng, _lib):
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), R,
+        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), _lib.ptr(ps["wend"]), R,
                                               m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()), "dom")
         e1.record()
         e1.synchronize()

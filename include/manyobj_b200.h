@@ -134,7 +134,8 @@ int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid
  * mo_dominance_bits. */
 int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, float* SS, int32_t* wend,
                float* blkmin, float* blkmax, void* workspace, size_t workspace_bytes, void* stream_);
-int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int32_t m,
+int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
+                             int64_t R, int32_t m,
                              uint32_t* bits, uint8_t* hasdom, void* stream_);
 
 /* dominance.non_dominated_sort + split_fronts, peeling the
@@ -204,7 +205,19 @@ typedef struct mo_step_args {
    * the generation from it (instead of `generation`) and the step increments
    * it, so one captured CUDA graph can be replayed generation after generation. */
   uint32_t* generation_dev;
+  /* Sort mode: MO_SORT_BITS (0, the default) stores the dominance bit-matrix
+   * and peels it inside mo_step; MO_SORT_STREAM (1) never stores it (O(R)
+   * memory, for R^2/8 bytes beyond HBM and for sharding) and is driven front
+   * by front by the host through mo_sort_stream_begin / _front / _end. */
+  int32_t sort_mode;
+  /* Shards of the streamed sort and of the association (one process per
+   * GPU): this process is shard `shard_rank` of `shard_count` (>= 1). */
+  int32_t shard_rank;
+  int32_t shard_count;
+  int32_t pad2;
 } mo_step_args;
+
+enum { MO_SORT_BITS = 0, MO_SORT_STREAM = 1 };
 
 int mo_step(const mo_step_args* args, void* stream_);
 
@@ -214,6 +227,51 @@ int mo_step(const mo_step_args* args, void* stream_);
  * survivor compaction.  mo_step == all three in order. */
 enum { MO_PHASE_VARY = 1, MO_PHASE_SORT = 2, MO_PHASE_NICHE = 4, MO_PHASE_ALL = 7 };
 int mo_step_phases(const mo_step_args* args, uint32_t phase_mask, void* stream_);
+
+/* MO_PHASE_NICHE split for the sharded association:
+ *   NICHE_PREP   running ideal, shuffles, candidate list, extremes, intercepts
+ *                (replicated on every shard);
+ *   NICHE_ASSOC  association keys of every candidate against this shard's
+ *                range of reference points (shuffled positions
+ *                [rank*w/count, (rank+1)*w/count)) into the akey array
+ *                (uint64 per merged row, mo_stream_offsets) -- the host then
+ *                max-reduces akey across shards (an exact integer max);
+ *   NICHE_FINISH pi, d, niche counts, niching, survivor compaction
+ *                (replicated).
+ * MO_PHASE_NICHE == the three in order with count == 1. */
+enum { MO_PHASE_NICHE_PREP = 8, MO_PHASE_NICHE_ASSOC = 16, MO_PHASE_NICHE_FINISH = 32 };
+int mo_niche_phases(const mo_step_args* args, uint32_t phase_mask, void* stream_);
+
+/* ------------------------------------------- streamed / sharded sort (L3) */
+
+/* dominance.non_dominated_sort + split_fronts without the
+ * bit-matrix: dominator counts of the shard's rows, then one call per front.
+ * Position blocks of 256 presorted rows are dealt round-robin to the shards;
+ * each shard writes its slice of the front mask (mask_local, T*8 words,
+ * T = ceil(ceil(R/256)/count)) and reads all slices concatenated in shard
+ * order (mask_full, count*T*8 words) -- the host all-gathers between the
+ * calls (with count == 1 they alias).
+ *   begin:      presort, dominator counts, front 0 -> mask_local
+ *   front(k):   front k from mask_full (ranks, front list, split decision);
+ *               if not done: decrement counts, front k+1 -> mask_local
+ *   end:        ranks in row order.
+ * After front(k) closed the split, info[MO_INFO_NFRONTS] = k + 1 (0 before)
+ * and later front calls are no-ops, so the host may poll lazily.  Needs a
+ * workspace sized with sort_mode = MO_SORT_STREAM. */
+int mo_sort_stream_begin(const mo_step_args* args, void* stream_);
+int mo_sort_stream_front(const mo_step_args* args, int32_t k, void* stream_);
+int mo_sort_stream_end(const mo_step_args* args, void* stream_);
+
+/* Workspace bytes for a sort mode and shard count (mo_workspace_bytes ==
+ * mode MO_SORT_BITS, 1 shard). */
+int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t sort_mode, int32_t shard_count,
+                          size_t* bytes);
+
+/* Byte offsets inside that workspace of mask_local / mask_full (uint32),
+ * their word counts, and of akey (uint64 per merged row). */
+int mo_stream_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count,
+                      int64_t* mask_local_off, int64_t* mask_local_words, int64_t* mask_full_off,
+                      int64_t* akey_off);
 
 /* Survivor selection only (NDS + split + niching + compaction) on merged
  * objectives already in FR -- the part of mo_step after variation. */

@@ -24,6 +24,8 @@ INFO = dict(L=0, SELECTED=1, K=2, NFRONTS=3, FL_SIZE=4, SKIPPED=5, NEAREST=6, LE
             SURVIVORS=9, ERROR=10)
 INFO_COUNT = 16
 PHASE_VARY, PHASE_SORT, PHASE_NICHE, PHASE_ALL = 1, 2, 4, 7
+NICHE_PREP, NICHE_ASSOC, NICHE_FINISH = 8, 16, 32
+SORT_BITS, SORT_STREAM = 0, 1
 PROBLEM_IDS = {f"DTLZ{i}": i for i in range(1, 8)}
 DROPPED = 2 ** 31 - 1
 
@@ -40,6 +42,7 @@ class StepArgs(ctypes.Structure):
         ("zhat", c_vp), ("XR", c_vp), ("FR", c_vp), ("X_next", c_vp), ("F_next", c_vp),
         ("ideal", c_vp), ("ranks", c_vp), ("info", c_vp), ("workspace", c_vp), ("workspace_bytes", c_sz),
         ("generation_dev", c_vp),
+        ("sort_mode", c_i32), ("shard_rank", c_i32), ("shard_count", c_i32), ("pad2", c_i32),
     ]
 
 
@@ -57,7 +60,7 @@ _PROTOS = {
     "mo_dominance_bits": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_front_peel": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_presort": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
-    "mo_dominance_bits_sorted": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "mo_dominance_bits_sorted": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_normalize": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_associate": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_sz,
                              c_vp]),
@@ -67,6 +70,13 @@ _PROTOS = {
     "mo_select": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
     "mo_step_phases": (c_i32, [ctypes.POINTER(StepArgs), c_u32, c_vp]),
     "mo_peak_issue": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
+    "mo_niche_phases": (c_i32, [ctypes.POINTER(StepArgs), c_u32, c_vp]),
+    "mo_sort_stream_begin": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
+    "mo_sort_stream_front": (c_i32, [ctypes.POINTER(StepArgs), c_i32, c_vp]),
+    "mo_sort_stream_end": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
+    "mo_workspace_bytes_ex": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_sz)]),
+    "mo_stream_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
+                                  ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
 }
 
 EXPORTED = tuple(_PROTOS)
@@ -121,6 +131,34 @@ def workspace_step(n, m, d, w, device=None):
     nbytes = c_sz(0)
     check(lib().mo_workspace_bytes(int(n), int(m), int(d), int(w), ctypes.byref(nbytes)), "mo_workspace_bytes")
     return torch.empty(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")
+
+
+def workspace_bytes_ex(n, m, d, w, sort_mode, shards):
+    nbytes = c_sz(0)
+    check(load_library_cached().mo_workspace_bytes_ex(int(n), int(m), int(d), int(w), int(sort_mode), int(shards),
+                                                      ctypes.byref(nbytes)), "mo_workspace_bytes_ex")
+    return int(nbytes.value)
+
+
+def stream_offsets(n, m, w, sort_mode, shards):
+    """(mask_local byte offset, mask_local words, mask_full byte offset, akey byte offset) in the workspace."""
+    out = [c_i64(0) for _ in range(4)]
+    check(load_library_cached().mo_stream_offsets(int(n), int(m), int(w), int(sort_mode), int(shards),
+                                                  *[ctypes.byref(o) for o in out]), "mo_stream_offsets")
+    return tuple(int(o.value) for o in out)
+
+
+_host_lib = None
+
+
+def load_library_cached():
+    """The library for sizing queries only (no device needed); compute calls go through lib()."""
+    global _host_lib
+    if _lib is not None:
+        return _lib
+    if _host_lib is None:
+        _host_lib = load_library()
+    return _host_lib
 
 
 def new_info(device=None, **fields):

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmanyobj_b200.so")
-SOURCES = ["mo_capi.cu", "k_vary.cu", "k_dominance.cu", "k_niche.cu", "k_peaks.cu"]
+SOURCES = ["mo_capi.cu", "k_vary.cu", "k_dominance.cu", "k_stream.cu", "k_niche.cu", "k_peaks.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -38,17 +38,31 @@ def needs_build():
 
 
 def build(verbose=False, force=False):
+    """Compile every source to an object in parallel (one nvcc per file), then link the .so."""
+    from concurrent.futures import ThreadPoolExecutor
     if not force and not needs_build():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS]
-    if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [_nvcc(), *cflags, "-c"] + (["-Xptxas", "-v"] if verbose else []) + \
+              ["-o", obj, os.path.join(CSRC, src)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for obj, res in results:
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {obj}:\n" + res.stdout + res.stderr)
+        if verbose:
+            sys.stderr.write(res.stderr)
+    cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp"] + [o for o, _ in results]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    if verbose:
-        sys.stderr.write(res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

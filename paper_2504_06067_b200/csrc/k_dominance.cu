@@ -183,7 +183,8 @@ constexpr int DOMS_THREADS = DOM_TILE / 2;  // two j columns per thread
 template <int M>
 __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* __restrict__ FS,
                                                                   const float* __restrict__ blkmin,
-                                                                  const float* __restrict__ blkmax, int R,
+                                                                  const float* __restrict__ blkmax,
+                                                                  const int* __restrict__ wend, int R,
                                                                   uint32_t* __restrict__ bits, int64_t W,
                                                                   uint8_t* __restrict__ hasdom) {
   constexpr int MP = (M + 3) & ~3;
@@ -258,6 +259,22 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
     dst[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
     if ((wb[0] | wb[1] | wb[2] | wb[3] | wb[4] | wb[5] | wb[6] | wb[7]) != 0u) hasdom[jb] = 1;
   }
+  if (fast) {
+    // rows i of the last S bucket of bi may share it with rows of bj: their
+    // words of block bj lie below wend and are read by the peel, so they must
+    // hold zeros (no j of a fast tile dominates an i) rather than stale bits
+    const int ilast = min(R, i0 + DOM_TILE) - 1;
+    if (__ldg(wend + ilast) > bj * 8) {
+      for (int r = tid; r < DOM_TILE; r += DOMS_THREADS) {
+        const int i = i0 + r;
+        if (i < R && __ldg(wend + i) > bj * 8) {
+          uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)i * W + (int64_t)bj * 8);
+          dst[0] = make_uint4(0u, 0u, 0u, 0u);
+          dst[1] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+    }
+  }
   if (!fast && bi != bj) {
     __syncthreads();
     for (int r = tid; r < DOM_TILE; r += DOMS_THREADS) {
@@ -309,8 +326,8 @@ int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint
 }
 
 
-int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int m,
-                           uint32_t* bits, uint8_t* hasdom, cudaStream_t s) {
+int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
+                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s) {
   if (R <= 0) return MO_OK;
   const int64_t W = words_per_row(R);
   const int64_t nb = W / 8;
@@ -320,7 +337,8 @@ int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* bl
   dim3 grid((unsigned)tiles);
   switch (m) {
 #define MO_DOMS_CASE(MM) \
-  case MM: k_dom_tile_sorted<MM><<<grid, DOMS_THREADS, 0, s>>>(FS, blkmin, blkmax, (int)R, bits, W, hasdom); break;
+  case MM: k_dom_tile_sorted<MM><<<grid, DOMS_THREADS, 0, s>>>(FS, blkmin, blkmax, wend, (int)R, bits, W, hasdom); \
+    break;
     MO_DOMS_CASE(2)
     MO_DOMS_CASE(3)
     MO_DOMS_CASE(4)
@@ -361,6 +379,7 @@ constexpr int PRESORT_THREADS = 512;
 __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   __shared__ int sh[40];
   __shared__ unsigned sMin, sMax;
+  __shared__ int sWcnt[(PRESORT_THREADS / 32) * 256], sRun[256], sOff[256];
   const int tid = threadIdx.x, lane = tid & 31;
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int R = a.R, m = a.m;
@@ -405,6 +424,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
     const uint32_t key = __ldcg(a.keyB + i);
     const uint32_t q = (uint32_t)(((uint64_t)(key - lo) * (uint64_t)PRESORT_BUCKETS) / span);
     a.keyA[i] = q;
+    if (a.stable) a.valA[i] = i;
     atomicAdd(&a.valB[q], 1);
   }
   grid_sync(a.g.bar);
@@ -416,19 +436,38 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   grid_sync(a.g.bar);
   trace_mark(a.trace, 3);
   // P3: scatter rows into their buckets
-  for (int i = gtid; i < R; i += gthreads) {
-    const uint32_t q = __ldcg(a.keyA + i);
-    const int pos = atomicAdd(&a.fill[q], 1);
-    a.perm[pos] = i;
-    a.SS[pos] = ord2f(__ldcg(a.keyB + i));
-    for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+  if (a.stable) {
+    // (bucket, row) pairs sorted by bucket, rows ascending inside a bucket
+    grid_radix_pass(a.g, R, 0, a.keyA, a.valA, a.tkey, a.tval, sWcnt, sRun, sOff, sh);
+    grid_radix_pass(a.g, R, 8, a.tkey, a.tval, a.keyA, a.valA, sWcnt, sRun, sOff, sh);
+    for (int pos = gtid; pos < R; pos += gthreads) {
+      const int i = __ldcg(a.valA + pos);
+      a.perm[pos] = i;
+      a.SS[pos] = ord2f(__ldcg(a.keyB + i));
+      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+    }
+    // bucket ends for P4 (the atomic path leaves fill[q] at the end of bucket q)
+    for (int q = gtid; q < PRESORT_BUCKETS; q += gthreads) a.fill[q] += __ldcg(a.valB + q);
+    grid_sync(a.g.bar);
+    // keyA was overwritten by the sorted keys: restore row -> bucket for P4
+    for (int pos = gtid; pos < R; pos += gthreads) a.tkey[__ldcg(a.valA + pos)] = __ldcg(a.keyA + pos);
+    grid_sync(a.g.bar);
+  } else {
+    for (int i = gtid; i < R; i += gthreads) {
+      const uint32_t q = __ldcg(a.keyA + i);
+      const int pos = atomicAdd(&a.fill[q], 1);
+      a.perm[pos] = i;
+      a.SS[pos] = ord2f(__ldcg(a.keyB + i));
+      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+    }
   }
   grid_sync(a.g.bar);
+  const uint32_t* rowq = a.stable ? a.tkey : a.keyA;
   trace_mark(a.trace, 4);
   // P4: wend (after P3 fill[q] = end of bucket q) and per-256-row S range
   for (int p = gtid; p < R; p += gthreads) {
     const int i = __ldcg(a.perm + p);
-    const uint32_t q = __ldcg(a.keyA + i);
+    const uint32_t q = __ldcg(rowq + i);
     const int last = __ldcg(a.fill + q) - 1;
     a.wend[p] = last / 32 + 1;
   }

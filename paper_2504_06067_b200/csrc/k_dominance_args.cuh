@@ -23,13 +23,19 @@ struct PresortArgs {
   int* fill;        // PRESORT_BUCKETS
   GridCtx g;
   unsigned long long* trace;
+  // stable = 1: rows inside a bucket keep ascending row order (two stable
+  // 8-bit radix passes of the bucket key instead of the atomic scatter), so
+  // every shard of a sharded sort derives the same position space
+  int stable;
+  uint32_t* tkey;   // R (stable only)
+  int* tval;        // R (stable only)
 };
 
 int64_t words_per_row(int64_t R);
 int launch_presort(const PresortArgs& args, cudaStream_t s);
 int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
-int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int m,
-                           uint32_t* bits, uint8_t* hasdom, cudaStream_t s);
+int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
+                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s);
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,

@@ -325,14 +325,16 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
   // (row block, reference split) items spread over exactly gridDim.x blocks
   const int nrb = (ncand + ASSOC_ROWS - 1) / ASSOC_ROWS;
   if (nrb == 0) return;
+  const int wr = a.zend - a.zbeg;
+  if (wr <= 0) return;
   int splits = (int)gridDim.x / nrb;
-  const int maxsplit = (a.w + 63) / 64;
+  const int maxsplit = (wr + 63) / 64;
   splits = splits < 1 ? 1 : (splits > maxsplit ? maxsplit : splits);
-  const int psplit = (a.w + splits - 1) / splits;
+  const int psplit = (wr + splits - 1) / splits;
   const int items = nrb * splits;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    assoc_item<M>(a, ncand, (item / splits) * ASSOC_ROWS, (item % splits) * psplit,
-                  min(a.w, (item % splits) * psplit + psplit), sz);
+    const int p0 = a.zbeg + (item % splits) * psplit;
+    assoc_item<M>(a, ncand, (item / splits) * ASSOC_ROWS, p0, min(a.zend, p0 + psplit), sz);
   }
 }
 

@@ -58,6 +58,7 @@ struct AssocArgs {
   int w;
   int psplit;            // reference points per blockIdx.y
   unsigned long long* akey;
+  int zbeg, zend;        // shuffled reference positions handled by this launch (shard range)
 };
 
 struct AssocFinalArgs {

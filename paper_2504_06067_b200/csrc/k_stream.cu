@@ -1,0 +1,387 @@
+// Streamed / row-sharded non-dominated sort (no bit-matrix in memory).
+//
+// Reference: dominance.non_dominated_sort + split_fronts,
+// dominance_matrix.  Same ranks as the bit-matrix path
+// (k_dominance.cu); this one is for populations whose R^2/8-byte bit-matrix
+// does not fit (C4: R = 2M -> 500 GB) and for sharding across GPUs
+// (north_star: rows of the dominance relation split across the GPUs of a
+// box, per-front masks all-gathered over NVLink).
+//
+// Rows live in presort position space (k_presort: S-ordered buckets, so the
+// dominators of position p sit at positions < wend[p] * 32).  Position blocks
+// of 256 rows are dealt round-robin to the G shards (block b -> shard b % G,
+// local index b / G), which balances the triangular work.  A shard owns the
+// dominated rows j of its blocks:
+//
+//   begin     cnt[j] = #dominators of j       (k_stream_tiles, COUNT)
+//             front 0 = owned rows with cnt 0 (k_stream_mark -> mask_local)
+//   front k   host all-gathers mask_local -> mask_full (NCCL; G = 1: alias)
+//             k_stream_apply: rank_pos = k for the front, ordered front list
+//             fl (position order), |F_k|, cumulative size, split decision
+//             cnt[j] -= #dominators of j in F_k  (k_stream_tiles, DEC)
+//             front k+1 = owned unranked rows with cnt 0
+//   end       ranks in row order
+//
+// Count-decrement is bounded: sum_k |F_k| x R pairs <= the R^2/2 triangle
+// (only F_k rows before j in position order are compared), so a generation
+// costs at most two triangle sweeps of m-compare chains and O(R) memory.
+// Every kernel checks ctl[SC_DONE] first, so the host may run ahead of the
+// split decision (it polls info[MO_INFO_NFRONTS] every few fronts).
+// Work is a device-planned queue: k_stream_plan counts the (row block, i
+// chunk) items of every owned block from wend / the front list, and the
+// persistent k_stream_tiles CTAs pull items with one atomic each.
+#include "mo_chains.cuh"
+#include "mo_common.cuh"
+#include "mo_grid.cuh"
+#include "k_stream_args.cuh"
+
+namespace mo {
+
+constexpr int ST_THREADS = STREAM_BLK / 2;   // two j columns per thread
+constexpr int PLAN_THREADS = 1024;
+constexpr int APPLY_THREADS = 512;
+enum { MODE_COUNT = 0, MODE_DEC = 1 };
+
+__device__ __forceinline__ int owned_block(const StreamArgs& a, int t) { return t * a.G + a.g; }
+__device__ __forceinline__ int nblocks(int R) { return (R + STREAM_BLK - 1) / STREAM_BLK; }
+// first position after every possible dominator of the rows of block b
+__device__ __forceinline__ int block_bend(const StreamArgs& a, int b) {
+  const int last = min(a.R, (b + 1) * STREAM_BLK) - 1;
+  return min(a.R, __ldg(a.wend + last) * 32);
+}
+
+__global__ void k_stream_reset(StreamArgs a) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int p = gt; p < a.R; p += gs) {
+    a.rank_pos[p] = MO_RANK_UNRANKED;
+    a.cnt[p] = 0;
+  }
+  for (int t = gt; t < a.T; t += gs) {
+    const int b = owned_block(a, t);
+    a.ucnt[t] = max(0, min(a.R, (b + 1) * STREAM_BLK) - b * STREAM_BLK);
+  }
+  if (gt < SC_COUNT) a.ctl[gt] = 0;
+  if (gt < MO_INFO_COUNT) a.info[gt] = 0;
+}
+
+// One CTA: items per owned block, exclusive prefix into plan[0..T].
+template <int MODE>
+__global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
+  __shared__ int sh[40];
+  const int tid = threadIdx.x;
+  const bool done = __ldcg(a.ctl + SC_DONE) != 0;
+  const int nb = nblocks(a.R);
+  const int fln = __ldcg(a.ctl + SC_FLN);
+  const int per = (a.T + PLAN_THREADS - 1) / PLAN_THREADS;
+  const int t0 = min(a.T, tid * per), t1 = min(a.T, t0 + per);
+  int mine = 0;
+  for (int t = t0; t < t1; ++t) {
+    const int b = owned_block(a, t);
+    int items = 0;
+    if (!done && b < nb) {
+      const int bend = block_bend(a, b);
+      if (MODE == MODE_COUNT) {
+        const int nib = (bend + STREAM_BLK - 1) / STREAM_BLK;
+        items = (nib + STREAM_CHUNK - 1) / STREAM_CHUNK;
+      } else if (__ldcg(a.ucnt + t) > 0) {
+        int lo = 0, hi = fln;  // fl entries with position < bend
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (__ldcg(a.fl + mid) < bend) lo = mid + 1; else hi = mid;
+        }
+        items = (lo + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
+      }
+    }
+    a.plan[t] = items;  // temporarily the count
+    mine += items;
+  }
+  int total;
+  int pre = block_excl_scan(mine, sh, &total);
+  for (int t = t0; t < t1; ++t) {
+    const int c = a.plan[t];
+    a.plan[t] = pre;
+    pre += c;
+  }
+  if (tid == 0) {
+    a.plan[a.T] = total;
+    a.ctl[SC_ITEMS] = total;
+    a.ctl[SC_WORK] = 0;
+  }
+}
+
+// Persistent tiles: item = (owned block t, chunk c).  COUNT: i over the
+// position blocks [c*CHUNK, ...) below the block's bound; DEC: i over the
+// front list entries [c*CHUNK*256, ...) below the bound.  Thread = 2 rows j;
+// i rows staged in shared memory.  Fast tiles (every S_i < every S_j) need
+// only the m-long <= chain; others the full dominance chain (also rejects
+// i == j).  Counts accumulate with a predicated FADD (FMA pipe, exact below
+// 2^24) and land with one atomic per row per item.
+template <int M, int MODE>
+__global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
+  __shared__ int sItem;
+  const int tid = threadIdx.x;
+  const int items = __ldcg(a.ctl + SC_ITEMS);
+  const int fln = MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0;
+  const float PINF = __int_as_float(0x7f800000);
+  for (;;) {
+    if (tid == 0) sItem = atomicAdd(a.ctl + SC_WORK, 1);
+    __syncthreads();
+    const int item = sItem;
+    __syncthreads();
+    if (item >= items) break;
+    int lo = 0, hi = a.T;  // largest t with plan[t] <= item
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(a.plan + mid) <= item) lo = mid; else hi = mid;
+    }
+    const int t = lo, c = item - __ldg(a.plan + t);
+    const int bj = owned_block(a, t);
+    const int j0 = bj * STREAM_BLK;
+    const int ja = j0 + tid, jb = ja + ST_THREADS;
+    float fa[M], fb[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      fa[k] = ja < a.R ? __ldg(a.FS + (int64_t)ja * M + k) : PINF;
+      fb[k] = jb < a.R ? __ldg(a.FS + (int64_t)jb * M + k) : PINF;
+    }
+    const float jmin = __ldg(a.blkmin + bj);
+    const int bend = block_bend(a, bj);
+    int e0, e1;  // i range: positions (COUNT) or front-list entries (DEC)
+    if (MODE == MODE_COUNT) {
+      e0 = c * STREAM_CHUNK * STREAM_BLK;
+      e1 = min(bend, e0 + STREAM_CHUNK * STREAM_BLK);
+      e1 = (e1 + STREAM_BLK - 1) / STREAM_BLK * STREAM_BLK;  // whole blocks (rows >= bend cannot dominate)
+      e1 = min(e1, a.R);
+    } else {
+      e0 = c * STREAM_CHUNK * STREAM_BLK;
+      e1 = min(fln, e0 + STREAM_CHUNK * STREAM_BLK);
+    }
+    float ca = 0.0f, cb = 0.0f;
+    for (int s0 = e0; s0 < e1; s0 += STREAM_BLK) {
+      const int nv = min(STREAM_BLK, e1 - s0);
+      for (int e = tid; e < STREAM_BLK; e += ST_THREADS) {
+        int src = -1;
+        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : __ldg(a.fl + s0 + e);
+        float* dst = sFi + e * MP;
+#pragma unroll
+        for (int k = 0; k < MP; ++k) dst[k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
+      }
+      const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : __ldg(a.flmax + s0 / STREAM_BLK);
+      const bool fast = (MODE == MODE_COUNT ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
+      __syncthreads();
+      const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
+      if (fast) {
+        for (int i = 0; i < nv8; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float v[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+            Chain<M>::le_cnt(v, fa, ca);
+            Chain<M>::le_cnt(v, fb, cb);
+          }
+        }
+      } else {
+        for (int i = 0; i < nv8; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float v[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+            Chain<M>::dom_cnt(v, fa, ca);
+            Chain<M>::dom_cnt(v, fb, cb);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int ia = (int)ca, ib = (int)cb;
+    if (ja < a.R && ia) atomicAdd(a.cnt + ja, MODE == MODE_COUNT ? ia : -ia);
+    if (jb < a.R && ib) atomicAdd(a.cnt + jb, MODE == MODE_COUNT ? ib : -ib);
+  }
+}
+
+// Owned unranked rows with no unranked dominator left -> local mask slice.
+__global__ void k_stream_mark(StreamArgs a) {
+  if (__ldcg(a.ctl + SC_DONE) != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t)a.T * (STREAM_BLK / 32);
+  if (gw >= nw) return;
+  const int t = (int)(gw / (STREAM_BLK / 32)), w8 = (int)(gw % (STREAM_BLK / 32));
+  const int p = owned_block(a, t) * STREAM_BLK + w8 * 32 + lane;
+  const bool in = p < a.R && __ldcg(a.rank_pos + p) == MO_RANK_UNRANKED && __ldcg(a.cnt + p) == 0;
+  const uint32_t word = __ballot_sync(MO_FULL, in);
+  if (lane == 0) a.mask_local[gw] = word;
+}
+
+// Front k from the gathered mask: ranks, ordered front list, split decision.
+__global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, int k) {
+  __shared__ int sh[40];
+  __shared__ float sMax[APPLY_THREADS / 32];
+  if (__ldcg(a.ctl + SC_DONE) != 0) return;  // set only after the last barrier below
+  const int nb = nblocks(a.R);
+  const int64_t N = (int64_t)nb * (STREAM_BLK / 32);
+  auto word = [&](int64_t e) -> uint32_t {
+    const int b = (int)(e / (STREAM_BLK / 32)), w8 = (int)(e % (STREAM_BLK / 32));
+    return __ldcg(a.mask_full + ((int64_t)(b % a.G) * a.T + b / a.G) * (STREAM_BLK / 32) + w8);
+  };
+  const int fk = grid_scan(
+      a.gc, N, [&](int64_t e) { return __popc(word(e)); },
+      [&](int64_t e, int pre) {
+        uint32_t wv = word(e);
+        const int b = (int)(e / (STREAM_BLK / 32));
+        const int base = (int)(e * 32);
+        if (b % a.G == a.g) atomicSub(a.ucnt + b / a.G, __popc(wv));
+        int r = pre;
+        while (wv) {
+          const int bit = __ffs(wv) - 1;
+          wv &= wv - 1;
+          a.fl[r++] = base + bit;
+          a.rank_pos[base + bit] = k;
+        }
+      },
+      sh);
+  grid_sync(a.gc.bar);
+  // max S per 256-entry block of the front list (fast-tile test of DEC)
+  const int nq = (fk + STREAM_BLK - 1) / STREAM_BLK;
+  for (int q = blockIdx.x; q < nq; q += gridDim.x) {
+    const int e = q * STREAM_BLK + (int)threadIdx.x;
+    float v = -__int_as_float(0x7f800000);
+    if (threadIdx.x < STREAM_BLK && e < fk) v = __ldg(a.SS + __ldcg(a.fl + e));
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(MO_FULL, v, o));
+    if ((threadIdx.x & 31) == 0) sMax[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float mx = sMax[0];
+      for (int w = 1; w < APPLY_THREADS / 32; ++w) mx = fmaxf(mx, sMax[w]);
+      a.flmax[q] = mx;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t sel = __ldcg(a.ctl + SC_CUM);
+    const int64_t cum = sel + fk;
+    a.ctl[SC_CUM] = (int)cum;
+    a.ctl[SC_FLN] = fk;
+    if (cum >= a.stop_at || fk == 0) {
+      a.info[MO_INFO_L] = k;
+      a.info[MO_INFO_SELECTED] = (int)sel;
+      a.info[MO_INFO_K] = (int)(a.stop_at - sel);
+      a.info[MO_INFO_FL_SIZE] = fk;
+      a.info[MO_INFO_SKIPPED] = (sel + fk == a.stop_at) ? 1 : 0;
+      a.info[MO_INFO_ERROR] = (cum < a.stop_at) ? MO_ERR_INFEASIBLE : 0;
+      __threadfence();
+      a.info[MO_INFO_NFRONTS] = k + 1;
+      a.ctl[SC_DONE] = k + 1;
+    }
+  }
+}
+
+__global__ void k_stream_end(StreamArgs a) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int p = gt; p < a.R; p += gs) {
+    const int r = __ldcg(a.rank_pos + p);
+    a.ranks[__ldg(a.perm + p)] = r == MO_RANK_UNRANKED ? MO_RANK_DROPPED : r;
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+template <int MODE>
+static int launch_tiles(const StreamArgs& a, cudaStream_t s) {
+  static int per[17][2];
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  switch (a.m) {
+#define MO_ST_CASE(MM)                                                                          \
+  case MM: {                                                                                    \
+    if (!per[MM][MODE]) {                                                                       \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[MM][MODE], k_stream_tiles<MM, MODE>,   \
+                                                    ST_THREADS, 0);                             \
+      if (per[MM][MODE] < 1) per[MM][MODE] = 1;                                                 \
+    }                                                                                           \
+    k_stream_tiles<MM, MODE><<<sms * per[MM][MODE], ST_THREADS, 0, s>>>(a);                     \
+    break;                                                                                      \
+  }
+    MO_ST_CASE(2)
+    MO_ST_CASE(3)
+    MO_ST_CASE(4)
+    MO_ST_CASE(5)
+    MO_ST_CASE(6)
+    MO_ST_CASE(7)
+    MO_ST_CASE(8)
+    MO_ST_CASE(9)
+    MO_ST_CASE(10)
+    MO_ST_CASE(11)
+    MO_ST_CASE(12)
+    MO_ST_CASE(13)
+    MO_ST_CASE(14)
+    MO_ST_CASE(15)
+    MO_ST_CASE(16)
+#undef MO_ST_CASE
+    default:
+      return MO_ERR_PARAM;
+  }
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+static int mark_launch(const StreamArgs& a, cudaStream_t s) {
+  const int64_t threads = (int64_t)a.T * STREAM_BLK;
+  k_stream_mark<<<(unsigned)ceil_div(threads, 256), 256, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+int launch_stream_begin(StreamArgs a, cudaStream_t s) {
+  if (a.R < 1 || a.G < 1 || a.g < 0 || a.g >= a.G || a.m < 2 || a.m > 16) return MO_ERR_PARAM;
+  int64_t rb = ceil_div(a.R > a.T ? a.R : a.T, 256);
+  k_stream_reset<<<(unsigned)(rb > 4096 ? 4096 : rb), 256, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  k_stream_plan<MODE_COUNT><<<1, PLAN_THREADS, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  MO_TRY(launch_tiles<MODE_COUNT>(a, s));
+  return mark_launch(a, s);
+}
+
+int launch_stream_front(StreamArgs a, int k, cudaStream_t s) {
+  static int blocks = 0;
+  if (!blocks) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_apply, APPLY_THREADS, 0);
+    blocks = sms * (per > 1 ? 1 : (per > 0 ? per : 1));
+  }
+  if (cudaMemsetAsync(a.gc.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  a.gc.parity = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(APPLY_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k_stream_apply, a, k) != cudaSuccess) return MO_ERR_CUDA;
+  MO_CHECK_LAUNCH();
+  k_stream_plan<MODE_DEC><<<1, PLAN_THREADS, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  MO_TRY(launch_tiles<MODE_DEC>(a, s));
+  return mark_launch(a, s);
+}
+
+int launch_stream_end(StreamArgs a, cudaStream_t s) {
+  unsigned blocks = (unsigned)ceil_div(a.R, 256);
+  if (blocks > 4096) blocks = 4096;
+  k_stream_end<<<blocks, 256, 0, s>>>(a);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+}  // namespace mo

@@ -23,6 +23,8 @@ int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float
 
 #include "k_dominance_args.cuh"
 
+#include "k_stream_args.cuh"
+
 namespace mo {
 
 constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/hist sizing)
@@ -31,7 +33,8 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, total;
+      lvl, sctl, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+  int64_t T, mask_local_words, mask_full_words;
 };
 
 static size_t bump(size_t& cur, size_t bytes) {
@@ -40,15 +43,17 @@ static size_t bump(size_t& cur, size_t bytes) {
   return at;
 }
 
-static Layout make_layout(int64_t R, int64_t w, int m) {
+static int shards_of(int32_t count) { return count < 1 ? 1 : count; }
+
+static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_BITS, int G = 1) {
   Layout L;
   size_t c = 0;
   const int64_t W = words_per_row(R);
-  L.bits = bump(c, (size_t)R * W * 4);
+  L.bits = bump(c, sort_mode == MO_SORT_BITS ? (size_t)R * W * 4 : 0);
   L.resume = bump(c, (size_t)R * 4);
   L.ranked = bump(c, (size_t)W * 4);
   L.fsizes = bump(c, (size_t)(R + 4) * 4);
-  L.bar = bump(c, 64 * 4);
+  L.bar = bump(c, 128 * 4);
   L.pos_pop = bump(c, (size_t)R * 4);
   L.perm_pop = bump(c, (size_t)R * 4);
   L.pos_ref = bump(c, (size_t)w * 4);
@@ -92,6 +97,22 @@ static Layout make_layout(int64_t R, int64_t w, int m) {
   L.fill = bump(c, (size_t)(w + 1) * 4);
   L.lvl = bump(c, (size_t)2 * LVL_BINS * 4);
   L.sctl = bump(c, 16 * 4);
+  // streamed / sharded sort (sort_mode == MO_SORT_STREAM)
+  const bool st = sort_mode == MO_SORT_STREAM;
+  const int64_t nb = ceil_div(R, STREAM_BLK);
+  L.T = ceil_div(nb, (int64_t)G);
+  L.mask_local_words = L.T * (STREAM_BLK / 32);
+  L.mask_full_words = L.mask_local_words * G;
+  L.tkey = bump(c, st ? (size_t)R * 4 : 0);
+  L.tval = bump(c, st ? (size_t)R * 4 : 0);
+  L.cnt = bump(c, st ? (size_t)R * 4 : 0);
+  L.mask_local = bump(c, st ? (size_t)L.mask_local_words * 4 : 0);
+  L.mask_full = G > 1 ? bump(c, st ? (size_t)L.mask_full_words * 4 : 0) : L.mask_local;
+  L.fl = bump(c, st ? (size_t)R * 4 : 0);
+  L.flmax = bump(c, st ? (size_t)(nb + 2) * 4 : 0);
+  L.plan = bump(c, st ? (size_t)(L.T + 1) * 4 : 0);
+  L.ucnt = bump(c, st ? (size_t)(L.T + 1) * 4 : 0);
+  L.stctl = bump(c, SC_COUNT * 4);
   L.total = (c + 255) & ~(size_t)255;
   return L;
 }
@@ -102,7 +123,7 @@ static T* at(void* ws, size_t off) {
 }
 
 // Barrier slots inside L.bar (each 2 x u32, 64-byte apart to avoid false sharing)
-enum { BAR_PEEL = 0, BAR_PREP = 16, BAR_SELECT = 32, BAR_PRESORT = 48 };
+enum { BAR_PEEL = 0, BAR_PREP = 16, BAR_SELECT = 32, BAR_PRESORT = 48, BAR_STREAM = 64 };
 
 static int check_ws(const Layout& L, void* ws, size_t bytes) {
   if (ws == nullptr || bytes < L.total) return MO_ERR_PARAM;
@@ -205,10 +226,9 @@ __global__ void k_permutation(int n, uint64_t seed, uint32_t gen, uint32_t strea
   if (perm) perm[i] = (int)prp_inv((uint32_t)i, sK, sS, sR, (uint32_t)n);
 }
 
-static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
-  const int64_t n = a->n, R = 2 * n;
+static PresortArgs presort_args(const mo_step_args* a, const Layout& L) {
+  const int64_t R = 2 * a->n;
   void* ws = a->workspace;
-  uint32_t* bits = at<uint32_t>(ws, L.bits);
   PresortArgs ps;
   ps.F = a->FR;
   ps.R = (int)R;
@@ -230,22 +250,35 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   ps.g.hist = at<int>(ws, L.hist);
   ps.g.parity = 0;
   ps.trace = at<unsigned long long>(ws, L.trace);
+  ps.stable = a->sort_mode == MO_SORT_STREAM;
+  ps.tkey = ps.stable ? at<uint32_t>(ws, L.tkey) : nullptr;
+  ps.tval = ps.stable ? at<int>(ws, L.tval) : nullptr;
+  return ps;
+}
+
+static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
+  const int64_t n = a->n, R = 2 * n;
+  void* ws = a->workspace;
+  uint32_t* bits = at<uint32_t>(ws, L.bits);
+  PresortArgs ps = presort_args(a, L);
   MO_TRY(launch_presort(ps, s));
   uint8_t* hasdom = at<uint8_t>(ws, L.hasdom);
-  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, R, a->m, bits, hasdom, s));
+  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s));
   return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
                            at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, ps.perm, hasdom, ps.wend,
                            at<int>(ws, L.rank_pos), ps.trace, s);
 }
 
-static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
+static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cudaStream_t s) {
   const int64_t n = a->n, R = 2 * n, w = a->w;
   const int m = a->m;
   void* ws = a->workspace;
   PrepArgs pa = prep_args(L, ws, a->FR, R, m, w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
                           nullptr, PREP_FULL);
   pa.gen_ptr = a->generation_dev;
-  MO_TRY(launch_prep(pa, s));
+  if (mask & MO_PHASE_NICHE_PREP) MO_TRY(launch_prep(pa, s));
+  if (mask & MO_PHASE_NICHE_ASSOC) {
+  const int G = shards_of(a->shard_count);
   AssocArgs aa;
   aa.F = a->FR;
   aa.ideal = a->ideal;
@@ -257,7 +290,11 @@ static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   aa.w = (int)w;
   aa.psplit = (int)w;
   aa.akey = pa.akey;
+  aa.zbeg = (int)(w * a->shard_rank / G);
+  aa.zend = (int)(w * (a->shard_rank + 1) / G);
   MO_TRY(launch_assoc(aa, m, R, s));
+  }
+  if (!(mask & MO_PHASE_NICHE_FINISH)) return MO_OK;
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));
   fa.F = a->FR;
@@ -287,16 +324,66 @@ static int niche_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   return launch_select(sa, s);
 }
 
+static Layout step_layout(const mo_step_args* a) {
+  return make_layout(2 * a->n, a->w, a->m, a->sort_mode, shards_of(a->shard_count));
+}
+
 static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
-  const int64_t n = a->n, R = 2 * n;
-  Layout L = make_layout(R, a->w, a->m);
+  const int64_t n = a->n;
+  Layout L = step_layout(a);
   MO_TRY(check_ws(L, a->workspace, a->workspace_bytes));
+  if (mask & MO_PHASE_NICHE) mask |= MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH;
+  if ((mask & MO_PHASE_SORT) && a->sort_mode != MO_SORT_BITS) return MO_ERR_PARAM;  // host-driven fronts
+  if ((mask & (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH)) == (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH) &&
+      shards_of(a->shard_count) > 1)
+    return MO_ERR_PARAM;  // the akey max-reduction across shards sits between the two
   if (mask & MO_PHASE_VARY)
     MO_TRY(launch_vary_eval(a->problem, a->XR, n, a->d, a->m, a->seed, a->generation, a->generation_dev, a->var,
                             a->XR + n * a->d, a->FR + n * a->m, nullptr, nullptr, s));
   if (mask & MO_PHASE_SORT) MO_TRY(sort_phase(a, L, s));
-  if (mask & MO_PHASE_NICHE) MO_TRY(niche_phase(a, L, s));
+  if (mask & (MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH))
+    MO_TRY(niche_phase(a, L, mask, s));
   return MO_OK;
+}
+
+static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
+  void* ws = a->workspace;
+  StreamArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  sa.FS = at<float>(ws, L.FS);
+  sa.SS = at<float>(ws, L.SS);
+  sa.wend = at<int>(ws, L.wend);
+  sa.blkmin = at<float>(ws, L.blkmin);
+  sa.blkmax = at<float>(ws, L.blkmax);
+  sa.perm = at<int>(ws, L.perm_sort);
+  sa.R = (int)(2 * a->n);
+  sa.m = a->m;
+  sa.G = shards_of(a->shard_count);
+  sa.g = a->shard_rank;
+  sa.T = (int)L.T;
+  sa.stop_at = a->n;
+  sa.cnt = at<int>(ws, L.cnt);
+  sa.rank_pos = at<int>(ws, L.rank_pos);
+  sa.mask_local = at<uint32_t>(ws, L.mask_local);
+  sa.mask_full = at<uint32_t>(ws, L.mask_full);
+  sa.fl = at<int>(ws, L.fl);
+  sa.flmax = at<float>(ws, L.flmax);
+  sa.plan = at<int>(ws, L.plan);
+  sa.ucnt = at<int>(ws, L.ucnt);
+  sa.ctl = at<int>(ws, L.stctl);
+  sa.info = a->info;
+  sa.ranks = a->ranks;
+  sa.gc.bar = at<unsigned>(ws, L.bar) + BAR_STREAM;
+  sa.gc.part = at<int>(ws, L.part);
+  sa.gc.hist = at<int>(ws, L.hist);
+  sa.gc.parity = 0;
+  return sa;
+}
+
+static int check_stream(const mo_step_args* a, Layout& L) {
+  if (a->sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
+  L = step_layout(a);
+  return check_ws(L, a->workspace, a->workspace_bytes);
 }
 
 static int check_step_args(const mo_step_args* a) {
@@ -306,6 +393,8 @@ static int check_step_args(const mo_step_args* a) {
   if (!a->zhat || !a->XR || !a->FR || !a->X_next || !a->F_next || !a->ideal || !a->ranks || !a->info)
     return MO_ERR_PARAM;
   if (a->problem < MO_DTLZ1 || a->problem > MO_DTLZ7) return MO_ERR_PARAM;
+  if (a->sort_mode != MO_SORT_BITS && a->sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
+  if (a->shard_count < 0 || a->shard_rank < 0 || a->shard_rank >= shards_of(a->shard_count)) return MO_ERR_PARAM;
   return MO_OK;
 }
 
@@ -390,13 +479,16 @@ int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, f
   ps.g.hist = at<int>(workspace, L.hist);
   ps.g.parity = 0;
   ps.trace = nullptr;
+  ps.stable = 0;
+  ps.tkey = nullptr;
+  ps.tval = nullptr;
   return launch_presort(ps, (cudaStream_t)stream_);
 }
 
-int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, int64_t R, int32_t m,
-                             uint32_t* bits, uint8_t* hasdom, void* stream_) {
-  if (!FS || !blkmin || !blkmax || !bits || !hasdom) return MO_ERR_PARAM;
-  return launch_dom_tile_sorted(FS, blkmin, blkmax, R, m, bits, hasdom, (cudaStream_t)stream_);
+int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
+                             int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* stream_) {
+  if (!FS || !blkmin || !blkmax || !wend || !bits || !hasdom) return MO_ERR_PARAM;
+  return launch_dom_tile_sorted(FS, blkmin, blkmax, wend, R, m, bits, hasdom, (cudaStream_t)stream_);
 }
 
 int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int32_t* ranks,
@@ -459,6 +551,8 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
   aa.w = (int)w;
   aa.psplit = (int)w;
   aa.akey = pa.akey;
+  aa.zbeg = 0;
+  aa.zend = (int)w;
   MO_TRY(launch_assoc(aa, m, R, s));
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));
@@ -505,6 +599,57 @@ int mo_step_phases(const mo_step_args* a, uint32_t phase_mask, void* stream_) {
   MO_TRY(check_step_args(a));
   if (phase_mask == 0 || (phase_mask & ~(uint32_t)MO_PHASE_ALL)) return MO_ERR_PARAM;
   return run_phases(a, phase_mask, (cudaStream_t)stream_);
+}
+
+int mo_niche_phases(const mo_step_args* a, uint32_t phase_mask, void* stream_) {
+  MO_TRY(check_step_args(a));
+  const uint32_t all = MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH;
+  if (phase_mask == 0 || (phase_mask & ~all)) return MO_ERR_PARAM;
+  return run_phases(a, phase_mask, (cudaStream_t)stream_);
+}
+
+int mo_sort_stream_begin(const mo_step_args* a, void* stream_) {
+  MO_TRY(check_step_args(a));
+  Layout L;
+  MO_TRY(check_stream(a, L));
+  cudaStream_t s = (cudaStream_t)stream_;
+  MO_TRY(launch_presort(presort_args(a, L), s));
+  return launch_stream_begin(stream_args(a, L), s);
+}
+
+int mo_sort_stream_front(const mo_step_args* a, int32_t k, void* stream_) {
+  MO_TRY(check_step_args(a));
+  Layout L;
+  MO_TRY(check_stream(a, L));
+  if (k < 0) return MO_ERR_PARAM;
+  return launch_stream_front(stream_args(a, L), k, (cudaStream_t)stream_);
+}
+
+int mo_sort_stream_end(const mo_step_args* a, void* stream_) {
+  MO_TRY(check_step_args(a));
+  Layout L;
+  MO_TRY(check_stream(a, L));
+  return launch_stream_end(stream_args(a, L), (cudaStream_t)stream_);
+}
+
+int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t sort_mode, int32_t shard_count,
+                          size_t* bytes) {
+  (void)d;
+  if (!bytes || n < 1 || m < 1 || w < 1 || shard_count < 0) return MO_ERR_PARAM;
+  if (sort_mode != MO_SORT_BITS && sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
+  *bytes = make_layout(2 * n, w, m, sort_mode, shards_of(shard_count)).total;
+  return MO_OK;
+}
+
+int mo_stream_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count,
+                      int64_t* mask_local_off, int64_t* mask_local_words, int64_t* mask_full_off, int64_t* akey_off) {
+  if (n < 1 || m < 1 || w < 1 || shard_count < 0) return MO_ERR_PARAM;
+  Layout L = make_layout(2 * n, w, m, sort_mode, shards_of(shard_count));
+  if (mask_local_off) *mask_local_off = (int64_t)L.mask_local;
+  if (mask_local_words) *mask_local_words = L.mask_local_words;
+  if (mask_full_off) *mask_full_off = (int64_t)L.mask_full;
+  if (akey_off) *akey_off = (int64_t)L.akey;
+  return MO_OK;
 }
 
 }  // extern "C"

@@ -59,14 +59,16 @@ def presort(F):
     return out
 
 
-def dominance_bits_sorted(ps):
-    """Bit-matrix of presorted rows (position space) + has-a-dominator flags, from :func:`presort`."""
+def dominance_bits_sorted(ps, poison=False):
+    """Bit-matrix of presorted rows (position space) + has-a-dominator flags, from :func:`presort`.
+    ``poison`` pre-fills the matrix with ones (tests: words below wend must all be written)."""
     FS = ps["FS"]
     R, m = FS.shape
     W = int(_lib.lib().mo_bits_words_per_row(R))
-    bits = torch.zeros((R, W), dtype=torch.int32, device=FS.device)
+    bits = torch.full((R, W), -1 if poison else 0, dtype=torch.int32, device=FS.device)
     hasdom = torch.empty(R, dtype=torch.uint8, device=FS.device)
-    _lib.check(_lib.lib().mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), R,
+    _lib.check(_lib.lib().mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
+                                                   _lib.ptr(ps["wend"]), R,
                                                    m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()),
                "mo_dominance_bits_sorted")
     return bits, hasdom
@@ -110,6 +112,56 @@ def non_dominated_sort(F, valid=None, stop_at=None, return_info=False):
     return ranks
 
 
+def stream_sort(F, n, shards=1, poll=1):
+    """non_dominated_sort + split_fronts of R = 2n rows through the streamed
+    (no bit-matrix) sort the engine uses when the bit-matrix exceeds HBM and
+    when it shards (mo_sort_stream_*).  ``shards`` > 1 runs every shard in
+    this process on its own workspace and exchanges the front masks by
+    concatenation -- the same bytes NCCL's all-gather moves between GPUs.
+    Returns (ranks, info) of shard 0 (all shards agree; checked)."""
+    F = as_matrix(F)
+    R, m = F.shape
+    if R != 2 * n or n < 1:
+        raise ShapeError("stream_sort needs R = 2n rows")
+    L = _lib.lib()
+    s = _lib.stream_ptr()
+    nb = _lib.workspace_bytes_ex(n, m, m, 1, _lib.SORT_STREAM, shards)
+    lo, words, fo, _ = _lib.stream_offsets(n, m, 1, _lib.SORT_STREAM, shards)
+    shard = []
+    for g in range(shards):
+        ws = torch.empty(nb, dtype=torch.uint8, device=F.device)
+        ranks = torch.empty(R, dtype=torch.int32, device=F.device)
+        info = _lib.new_info(F.device)
+        a = _lib.StepArgs()
+        a.problem, a.m, a.d, a.n, a.w = 1, m, m, n, 1
+        for f in ("zhat", "XR", "FR", "X_next", "F_next", "ideal"):
+            setattr(a, f, F.data_ptr())
+        a.ranks, a.info = ranks.data_ptr(), info.data_ptr()
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+        a.sort_mode, a.shard_rank, a.shard_count = _lib.SORT_STREAM, g, shards
+        loc = ws[lo: lo + 4 * words].view(torch.int32)
+        full = ws[fo: fo + 4 * words * shards].view(torch.int32)
+        shard.append((a, ranks, info, loc, full))
+        _lib.check(L.mo_sort_stream_begin(a, s), "mo_sort_stream_begin")
+    k = 0
+    while True:
+        if shards > 1:
+            cat = torch.cat([x[3] for x in shard])
+            for x in shard:
+                x[4].copy_(cat)
+        for x in shard:
+            _lib.check(L.mo_sort_stream_front(x[0], k, s), "mo_sort_stream_front")
+        k += 1
+        if k % poll == 0 and int(shard[0][2][_lib.INFO["NFRONTS"]].item()) > 0:
+            break
+    for x in shard:
+        _lib.check(L.mo_sort_stream_end(x[0], s), "mo_sort_stream_end")
+    for x in shard[1:]:
+        if not (torch.equal(x[1], shard[0][1]) and torch.equal(x[2], shard[0][2])):
+            raise RuntimeError("shards disagree on the ranks")
+    return shard[0][1], shard[0][2]
+
+
 @dataclass(frozen=True)
 class FrontSplit:
     """SPEC.md:172-175."""
@@ -141,4 +193,4 @@ def split_from_info(info):
 
 
 __all__ = ["DROPPED", "dominates", "dominance_bits", "dominance_matrix", "non_dominated_sort", "FrontSplit",
-           "split_fronts", "split_from_info", "unpack_bits", "presort", "dominance_bits_sorted", "device"]
+           "split_fronts", "split_from_info", "unpack_bits", "presort", "dominance_bits_sorted", "device", "stream_sort"]

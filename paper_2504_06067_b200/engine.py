@@ -13,6 +13,22 @@ CUDA-graph replay (one graph per buffer parity); the generation counter lives
 in device memory so the same two graphs are replayed generation after
 generation.
 
+Sort modes (``sort=``): "bits" keeps the R x R dominance bit-matrix in HBM
+and runs a generation as one ``mo_step`` (graph-capturable); "stream" never
+stores it (O(R) memory) and peels front by front from the host through
+``mo_sort_stream_*`` -- the path for populations whose bit-matrix exceeds
+HBM (C4: R = 2M) and for sharding.  "auto" picks bits when it fits.
+
+Sharding (``group=`` a torch.distributed process group, one process per
+GPU): the streamed sort's dominated rows are dealt to the shards in
+256-row position blocks and the per-front masks all-gathered; the
+association splits the reference points and max-reduces the packed
+(key, position) words; everything else is replicated, so every shard holds
+the same survivors, bit-identical to one GPU.  A
+generation is written as a generator that yields its collectives, so the
+same code runs under NCCL, gloo, or an in-process emulation of G shards on
+one device (``LocalShards``, used by the tests).
+
 Only the ``batched`` back-end exists here: the Alg. 1 one-at-a-time oracle
  is CPU test infrastructure (oracle/manyobj_ref) and asking
 for it raises ConfigError rather than falling back to the CPU.
@@ -73,7 +89,7 @@ def build_reference_set(cfg):
 class Engine:
     """Device-resident NSGA-III run: buffers, workspace and (optionally) a CUDA graph."""
 
-    def __init__(self, cfg, graph=False, device=None):
+    def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4):
         validate(cfg)
         self.cfg = cfg
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -81,6 +97,19 @@ class Engine:
         self.problem = problems.ContinuousProblem(cfg.problem, m, d)
         self.Z, zh = build_reference_set(cfg)
         self.w = zh.shape[0]
+        self.group = group
+        if shard is None:
+            shard = (0, 1)
+            if group is not None:
+                import torch.distributed as dist
+                shard = (dist.get_rank(group), dist.get_world_size(group))
+        self.shard_rank, self.shard_count = int(shard[0]), int(shard[1])
+        if not (0 <= self.shard_rank < self.shard_count):
+            raise ConfigError("shard", f"bad shard {shard}")
+        self.sort_mode = self._choose_sort(sort)
+        self.poll = max(1, int(poll))
+        if graph and (self.sort_mode != _lib.SORT_BITS or self.shard_count > 1):
+            raise ConfigError("graph", "CUDA-graph replay needs the single-shard bit-matrix sort")
         with torch.cuda.device(self.dev):
             L = _lib.lib()
             self.zhat = torch.from_numpy(zh).to(self.dev)
@@ -89,7 +118,13 @@ class Engine:
             self.ranks = torch.empty(2 * n, dtype=torch.int32, device=self.dev)
             self.info = torch.zeros(_lib.INFO_COUNT, dtype=torch.int32, device=self.dev)
             self.gen_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
-            self.ws = _lib.workspace_step(n, m, d, self.w, self.dev)
+            nbytes = _lib.workspace_bytes_ex(n, m, d, self.w, self.sort_mode, self.shard_count)
+            self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+            if self.sort_mode == _lib.SORT_STREAM:
+                lo, words, fo, ao = _lib.stream_offsets(n, m, self.w, self.sort_mode, self.shard_count)
+                self.mask_local = self.ws[lo: lo + 4 * words].view(torch.int32)
+                self.mask_full = self.ws[fo: fo + 4 * words * self.shard_count].view(torch.int32)
+                self.akey = self.ws[ao: ao + 8 * 2 * n].view(torch.int64)
             X0 = init_population(n, d, cfg.seed)
             self.XR[0][:n].copy_(X0)
             self.FR[0][:n].copy_(problems.dtlz_eval(self.problem, X0))
@@ -101,6 +136,18 @@ class Engine:
         self._graph = None
         if graph:
             self.capture()
+
+    def _choose_sort(self, sort):
+        if sort not in ("auto", "bits", "stream"):
+            raise ConfigError("sort", f"unknown sort mode {sort!r}")
+        if sort == "bits" and self.shard_count > 1:
+            raise ConfigError("sort", "the sharded sort is the streamed one")
+        if sort == "auto":
+            R = 2 * self.cfg.n
+            bits = R * ((R + 255) // 256 * 8) * 4
+            budget = 0.5 * torch.cuda.get_device_properties(self.dev).total_memory
+            sort = "bits" if self.shard_count == 1 and bits <= budget else "stream"
+        return _lib.SORT_BITS if sort == "bits" else _lib.SORT_STREAM
 
     # ------------------------------------------------------------ C-ABI args
     def _make_args(self, cur, use_dev_gen=False):
@@ -123,6 +170,8 @@ class Engine:
         a.workspace = self.ws.data_ptr()
         a.workspace_bytes = self.ws.numel()
         a.generation_dev = self.gen_dev.data_ptr() if use_dev_gen else None
+        a.sort_mode = self.sort_mode
+        a.shard_rank, a.shard_count = self.shard_rank, self.shard_count
         return a
 
     def _launch(self, cur, generation, phases=_lib.PHASE_ALL, use_dev_gen=False):
@@ -132,7 +181,11 @@ class Engine:
 
     # ------------------------------------------------------------- stepping
     def step(self, profile=None):
-        """Advance one generation (eager launch).  ``profile``: dict receiving per-phase ms."""
+        """Advance one generation (eager launch).  ``profile``: dict receiving per-phase seconds."""
+        if self.sort_mode == _lib.SORT_STREAM:
+            for req in self.step_gen(profile):
+                run_collective(req, self.group)
+            return
         if profile is None:
             self._launch(self.cur, self.generation)
         else:
@@ -148,6 +201,47 @@ class Engine:
             for name, a, b in (("t_variation", 0, 1), ("t_sort", 1, 2), ("t_niche", 2, 3)):
                 profile[name] = profile.get(name, 0.0) + ev[a].elapsed_time(ev[b]) / 1e3
             profile["t_eval"] = profile.get("t_eval", 0.0)   # fused into t_variation (k_vary_eval)
+        self.cur ^= 1
+        self.generation += 1
+
+    def step_gen(self, profile=None):
+        """One streamed/sharded generation; yields its collectives (see run_collective)."""
+        L, s = _lib.lib(), _lib.stream_ptr()
+        a = self._args[self.cur]
+        a.generation = int(self.generation) & 0xFFFFFFFF
+        sharded = self.shard_count > 1
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if profile is not None else None
+        if ev:
+            ev[0].record()
+        _lib.check(L.mo_step_phases(a, _lib.PHASE_VARY, s), "mo_step_phases(VARY)")
+        if ev:
+            ev[1].record()
+        _lib.check(L.mo_sort_stream_begin(a, s), "mo_sort_stream_begin")
+        k = 0
+        while True:
+            if sharded:
+                yield ("all_gather", self.mask_local, self.mask_full)
+            _lib.check(L.mo_sort_stream_front(a, k, s), "mo_sort_stream_front")
+            k += 1
+            if k % self.poll == 0 or k == 1:
+                if int(self.info[_lib.INFO["NFRONTS"]].item()) > 0:   # identical on every shard
+                    break
+        _lib.check(L.mo_sort_stream_end(a, s), "mo_sort_stream_end")
+        if ev:
+            ev[2].record()
+        if sharded:
+            _lib.check(L.mo_niche_phases(a, _lib.NICHE_PREP | _lib.NICHE_ASSOC, s), "mo_niche_phases")
+            yield ("all_max_u64", self.akey)
+            _lib.check(L.mo_niche_phases(a, _lib.NICHE_FINISH, s), "mo_niche_phases")
+        else:
+            _lib.check(L.mo_step_phases(a, _lib.PHASE_NICHE, s), "mo_step_phases(NICHE)")
+        if ev:
+            ev[3].record()
+            ev[3].synchronize()
+            for name, i, j in (("t_variation", 0, 1), ("t_sort", 1, 2), ("t_niche", 2, 3)):
+                profile[name] = profile.get(name, 0.0) + ev[i].elapsed_time(ev[j]) / 1e3
+            profile["t_eval"] = profile.get("t_eval", 0.0)
+            profile["fronts_issued"] = k
         self.cur ^= 1
         self.generation += 1
 
@@ -214,6 +308,62 @@ class Engine:
         return {k.lower(): h[v] for k, v in _lib.INFO.items()}
 
 
+_SIGN64 = -(1 << 63)
+
+
+def run_collective(req, group):
+    """Execute one collective request of Engine.step_gen over torch.distributed."""
+    import torch.distributed as dist
+    kind = req[0]
+    if kind == "all_gather":
+        dist.all_gather_into_tensor(req[2], req[1], group=group)
+    elif kind == "all_max_u64":
+        # packed (ord(t), ~position) keys are unsigned: flip the sign bit so the signed max agrees
+        t = req[1]
+        t.bitwise_xor_(_SIGN64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        t.bitwise_xor_(_SIGN64)
+    else:
+        raise ValueError(kind)
+
+
+class LocalShards:
+    """G shards of one run emulated in one process on one device: every shard
+    is a full Engine; collectives are performed by concatenation / elementwise
+    max across the shards' buffers.  Results must be bit-identical to G
+    processes over NCCL (the kernels only see their shard index)."""
+
+    def __init__(self, cfg, shards, device=None, poll=4):
+        self.engines = [Engine(cfg, device=device, sort="stream", shard=(g, shards), poll=poll)
+                        for g in range(shards)]
+
+    def step(self):
+        gens = [e.step_gen() for e in self.engines]
+        while True:
+            reqs = []
+            for g in gens:
+                try:
+                    reqs.append(next(g))
+                except StopIteration:
+                    reqs.append(None)
+            if all(r is None for r in reqs):
+                return
+            if any(r is None for r in reqs) or len({r[0] for r in reqs}) != 1:
+                raise RuntimeError("shards diverged: " + repr([r and r[0] for r in reqs]))
+            if reqs[0][0] == "all_gather":
+                full = torch.cat([r[1] for r in reqs])
+                for r in reqs:
+                    r[2].copy_(full)
+            else:
+                ts = [r[1] ^ _SIGN64 for r in reqs]
+                mx = ts[0]
+                for t in ts[1:]:
+                    mx = torch.maximum(mx, t)
+                mx ^= _SIGN64
+                for r in reqs:
+                    r[1].copy_(mx)
+
+
 @dataclass
 class RunState:
     """SPEC.md:444-447.  X/F are views into the engine's ping-pong buffers
@@ -234,9 +384,10 @@ def _state(engine, timings):
     return RunState(engine.generation, engine.X, engine.F, engine.ideal, engine, timings)
 
 
-def initialize(cfg, graph=False):
-    """uniform population in bounds, evaluated; generation 0."""
-    eng = Engine(cfg, graph=graph)
+def initialize(cfg, graph=False, **engine_kw):
+    """uniform population in bounds, evaluated; generation 0.
+    ``engine_kw``: Engine options (sort=, group=, device=)."""
+    eng = Engine(cfg, graph=graph, **engine_kw)
     return _state(eng, {})
 
 
@@ -250,9 +401,9 @@ def step(state, cfg=None, profile=False):
     return _state(eng, timings)
 
 
-def run(cfg, record=True, profile=False, graph=False):
+def run(cfg, record=True, profile=False, graph=False, **engine_kw):
     """history of per-generation records + final state."""
-    state = initialize(cfg, graph=graph and not record and not profile)
+    state = initialize(cfg, graph=graph and not record and not profile, **engine_kw)
     eng = state.engine
     history = []
     g = cfg.generations
@@ -269,4 +420,5 @@ def run(cfg, record=True, profile=False, graph=False):
     return history, state
 
 
-__all__ = ["RunConfig", "RunState", "Engine", "initialize", "step", "run", "validate", "build_reference_set"]
+__all__ = ["RunConfig", "RunState", "Engine", "LocalShards", "initialize", "step", "run", "validate",
+           "build_reference_set", "run_collective"]

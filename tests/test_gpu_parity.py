@@ -144,7 +144,7 @@ def test_sorted_path_bits(M):
         for b in range(len(bmin)):
             blk = SS[b * 256:(b + 1) * 256]
             assert bmin[b] == blk.min() and bmax[b] == blk.max()
-        bits, hasdom = M.dominance.dominance_bits_sorted(ps)
+        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True)
         D = Odom.dominance_matrix(F[perm])                      # D[i][j]: i dominates j (position space)
         dense = np_(M.dominance.unpack_bits(bits, R))
         for j in range(R):
@@ -152,6 +152,36 @@ def test_sorted_path_bits(M):
             assert np.array_equal(dense[:lim, j], D[:lim, j]), (F.shape, j)
             assert not D[lim:, j].any()
         assert np.array_equal(np_(hasdom).astype(bool), D.any(axis=0))
+
+
+def test_sorted_bits_bucket_straddling_fast_tile(M):
+    """A S-bucket straddling a block boundary whose tile is fast: the i rows' words of the later block
+    lie below wend and must be written (zeros), not left stale (regression: stale bits from the previous
+    generation made the peel see phantom dominators)."""
+    rs = np.random.default_rng(44)
+    hit = 0
+    for trial in range(40):
+        low = rs.random((255, 3)).astype(np.float32) * 3.0               # S < 9
+        high = 11.0 + rs.random((255, 3)).astype(np.float32) * 1000.0    # S > 33
+        pair = np.array([[10.2, 0.0, 0.0], [0.0, 10.2 + 1e-5 * (1 + trial % 5), 0.0]], np.float32)
+        ext = np.array([[0.0, 0.0, 0.0]], np.float32)
+        F = np.concatenate([low[:254], ext, pair, high, [[65536.0, 0.0, 0.0]]]).astype(np.float32)
+        F = F[rs.permutation(len(F))]
+        R = F.shape[0]
+        ps = M.dominance.presort(F)
+        perm = np_(ps["perm"])
+        we = np_(ps["wend"])
+        bmin, bmax = np_(ps["blkmin"]), np_(ps["blkmax"])
+        hit += int(we[255] > 8 and bmax[0] < bmin[1])
+        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True)
+        D = Odom.dominance_matrix(F[perm])
+        dense = np_(M.dominance.unpack_bits(bits, R))
+        for j in range(R):
+            lim = min(R, we[j] * 32)
+            assert np.array_equal(dense[:lim, j], D[:lim, j]), (trial, j)
+        r = np_(M.dominance.non_dominated_sort(F, stop_at=R // 2))
+        assert np.array_equal(r, Odom.non_dominated_sort(F, stop_at=R // 2))
+    assert hit > 0, "construction never produced a straddling fast tile"
 
 
 def test_nds_bit_exact(M):

@@ -1,0 +1,123 @@
+"""Streamed / sharded non-dominated sort and sharded association (GPU).
+
+The streamed sort (mo_sort_stream_*: dominator counts + per-front
+count-decrement, no bit-matrix) must give the oracle's ranks and split on
+the same objectives, for 1..8 shards exchanging their front masks; an engine
+in streamed mode must produce bit-identical generations to the bit-matrix
+engine; and G shards (emulated in one process on one GPU: every shard has its
+own workspace and only sees its shard index; the collectives are the same
+bytes NCCL moves) must produce bit-identical generations to one GPU.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.manyobj_ref import dominance as Odom
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2504_06067_b200 as pkg
+    from paper_2504_06067_b200 import _lib
+    _lib.lib()
+    return pkg
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def _cases():
+    rs = np.random.default_rng(31)
+    for R, m in [(4, 2), (64, 3), (184, 3), (512, 2), (772, 5), (1000, 10), (2048, 3), (3000, 4)]:
+        yield rs.random((R, m)).astype(np.float32)
+        yield rs.integers(0, 4, size=(R, m)).astype(np.float32)           # ties + duplicates
+    x = np.sort(rs.random(600)).astype(np.float32)
+    yield np.stack([x, x, x], 1)                                          # one chain: 600 fronts
+    yield np.repeat(rs.random((100, 3)).astype(np.float32), 4, axis=0)    # every row 4 times
+    yield np.zeros((256, 5), np.float32)                                  # all identical
+    x = rs.random(2000).astype(np.float32)
+    yield np.stack([x, 1 - x], 1).astype(np.float32)                       # all mutually non-dominated
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3, 8])
+def test_stream_sort_matches_oracle(M, shards):
+    for F in _cases():
+        R = F.shape[0]
+        n = R // 2
+        ranks, info = M.dominance.stream_sort(F, n, shards=shards, poll=1 + (R % 3))
+        want = Odom.non_dominated_sort(F, stop_at=n)
+        assert np.array_equal(np_(ranks), want), (F.shape, shards)
+        sp = M.dominance.split_from_info(info)
+        wsp = Odom.split_fronts(want, n)
+        assert (sp.l, sp.selected_count, sp.k) == (wsp.l, wsp.selected_count, wsp.k), (F.shape, shards)
+        h = np_(info)
+        assert h[M._lib.INFO["NFRONTS"]] == wsp.l + 1
+
+
+def test_stream_sort_equals_bits_path_large(M):
+    """R = 40,000 (m = 3, random + ties): streamed ranks == the bit-matrix peel's ranks."""
+    rs = np.random.default_rng(5)
+    for F in (rs.random((40000, 3)).astype(np.float32),
+              (rs.integers(0, 50, size=(40000, 3)) / 50).astype(np.float32)):
+        n = 20000
+        r1, i1 = M.dominance.stream_sort(F, n, shards=1, poll=4)
+        r2, i2 = M.dominance.non_dominated_sort(F, stop_at=n, return_info=True)
+        assert torch.equal(r1, r2)
+        for key in ("L", "SELECTED", "K", "NFRONTS", "FL_SIZE", "SKIPPED"):
+            assert int(i1[M._lib.INFO[key]]) == int(i2[M._lib.INFO[key]]), key
+        r3, _ = M.dominance.stream_sort(F, n, shards=4, poll=4)
+        assert torch.equal(r1, r3)
+
+
+@pytest.mark.parametrize("kind,n,m,d,gens", [("DTLZ2", 1000, 5, 14, 5), ("DTLZ7", 2000, 3, 22, 5),
+                                             ("DTLZ3", 600, 10, 19, 4), ("DTLZ1", 92, 3, 7, 20)])
+def test_stream_engine_equals_bits_engine(M, kind, n, m, d, gens):
+    cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=3)
+    a = M.engine.Engine(cfg, sort="bits")
+    b = M.engine.Engine(cfg, sort="stream")
+    for g in range(gens):
+        a.step()
+        b.step()
+        assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F), f"generation {g}"
+        assert torch.equal(a.ideal, b.ideal)
+        assert a.info_dict() == b.info_dict()
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+def test_local_shards_equal_one_gpu(M, shards):
+    cfg = M.engine.RunConfig(problem="DTLZ7", n=1500, m=3, d=22, generations=4, seed=11)
+    one = M.engine.Engine(cfg, sort="stream")
+    grp = M.engine.LocalShards(cfg, shards)
+    for g in range(4):
+        one.step()
+        grp.step()
+        for e in grp.engines:
+            assert torch.equal(e.X, one.X) and torch.equal(e.F, one.F), (shards, g)
+            assert torch.equal(e.ideal, one.ideal)
+            assert e.info_dict() == one.info_dict()
+
+
+def test_local_shards_m10(M):
+    cfg = M.engine.RunConfig(problem="DTLZ3", n=800, m=10, d=19, generations=3, seed=2)
+    one = M.engine.Engine(cfg, sort="bits")
+    grp = M.engine.LocalShards(cfg, 3)
+    for _ in range(3):
+        one.step()
+        grp.step()
+        for e in grp.engines:
+            assert torch.equal(e.X, one.X) and torch.equal(e.F, one.F)
+
+
+def test_stream_engine_profile_and_poll(M):
+    cfg = M.engine.RunConfig(problem="DTLZ7", n=3000, m=3, d=22, generations=3, seed=1)
+    a = M.engine.Engine(cfg, sort="stream", poll=1)
+    b = M.engine.Engine(cfg, sort="stream", poll=16)
+    prof = {}
+    for _ in range(3):
+        a.step(profile=prof)
+        b.step()
+    assert torch.equal(a.X, b.X)
+    assert prof["t_sort"] > 0 and prof["fronts_issued"] >= 1
