@@ -19,8 +19,12 @@ merged rows, w = 8,855 Das-Dennis points), synthetic seed-0 population.
 * cpu_baseline / --impl reference: the numpy restatement of the reference
   (oracle/manyobj_ref) on this host's cores; a bounded sample of the
   generation (see cpu_generation_estimate) extrapolated to one generation.
-N > 1 (torchrun): independent replicas, one per GPU, seeds 0..N-1 (the
-sharded bit-matrix path is for N >= 1M populations).
+N > 1 (torchrun): C1-C3 run independent replicas, one per GPU, seeds
+0..N-1 (scaling "weak"); C4 (--workload c4) runs ONE population sharded
+over the N GPUs -- dominated rows of the streamed sort dealt to the ranks,
+front masks all-gathered and association keys max-reduced over NCCL --
+(scaling "strong").  C4 generations are eager (the front loop is host
+driven); C1-C3 are CUDA-graph replays.
 """
 import argparse
 import json
@@ -35,9 +39,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    "c1": dict(problem="DTLZ1", m=3, d=7, n=92, label="C1 DTLZ1 m=3 d=7 N=92 (w=91, H=12)"),
-    "c2": dict(problem="DTLZ2", m=5, d=14, n=10000, label="C2 DTLZ2 m=5 d=14 N=10k (w=8855, H=19)"),
-    "c3": dict(problem="DTLZ3", m=10, d=19, n=100000, label="C3 DTLZ3 m=10 d=19 N=100k (w=97383)"),
+    "c1": dict(problem="DTLZ1", m=3, d=7, n=92, sort="bits", label="C1 DTLZ1 m=3 d=7 N=92 (w=91, H=12)"),
+    "c2": dict(problem="DTLZ2", m=5, d=14, n=10000, sort="bits", label="C2 DTLZ2 m=5 d=14 N=10k (w=8855, H=19)"),
+    "c3": dict(problem="DTLZ3", m=10, d=19, n=100000, sort="bits", label="C3 DTLZ3 m=10 d=19 N=100k (w=97383)"),
+    # C4: the R^2/8 = 500 GB bit-matrix does not fit -> streamed sort; under torchrun it is sharded
+    "c4": dict(problem="DTLZ7", m=3, d=22, n=1000000, sort="stream",
+               label="C4 DTLZ7 m=3 d=22 N=1M (w=998991, H=1412)"),
 }
 METRIC = "NSGA-III generations/sec on DTLZ (m=3–10, N to 1M+) at 1/2/4/8 B200 vs CPU ref"
 
@@ -200,20 +207,33 @@ def measure_peaks(torch, L, _lib):
 
 
 def time_kernels(torch, eng, _lib):
-    """Per-phase and per-kernel device times on the engine's current state (outside the timed run)."""
+    """Per-phase and dominant-kernel device times on the engine's current state (outside the timed run)."""
     from paper_2504_06067_b200 import dominance
     L = _lib.lib()
     cfg = eng.cfg
     n, m = cfg.n, cfg.m
     R = 2 * n
     out = {}
-    # phases (eager, events)
     prof = {}
-    for _ in range(3):
+    for _ in range(1 if eng.sort_mode == _lib.SORT_STREAM else 3):
         prof = {}
         eng.step(profile=prof)
-    out.update({k: v * 1e3 for k, v in prof.items()})        # ms
-    # the engine's dominance kernel alone (presorted rows of the last merged population)
+    out.update({k: v * 1e3 for k, v in prof.items() if k.startswith("t_")})        # ms
+    if eng.sort_mode == _lib.SORT_STREAM:
+        # dominant kernel: the dominator-count sweep (k_stream_tiles<COUNT>) inside mo_sort_stream_begin
+        # (presort + count + front-0 mark; presort is < 0.1 % of it at C4)
+        a = eng._args[eng.cur ^ 1]        # the buffer pair the last step consumed (FR still holds its rows)
+        ts = []
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _lib.check(L.mo_sort_stream_begin(a, _lib.stream_ptr()), "begin")
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out["dom_tile_ms"] = float(min(ts))
+        out["fronts_issued"] = prof.get("fronts_issued")
+        return out
     FR = eng.FR[eng.cur ^ 1]
     ps = dominance.presort(FR)
     W = int(L.mo_bits_words_per_row(R))
@@ -223,8 +243,9 @@ def time_kernels(torch, eng, _lib):
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), _lib.ptr(ps["wend"]), R,
-                                              m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()), "dom")
+        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
+                                              _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
+                                              _lib.stream_ptr()), "dom")
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
@@ -240,12 +261,22 @@ def run_ours(args, rank, world):
 
     wl = WORKLOADS[args.workload]
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
+    sharded = wl["sort"] == "stream" and world > 1
+    group = None
+    if sharded:
+        import torch.distributed as dist
+        group = dist.group.WORLD
     cfg = engine.RunConfig(problem=wl["problem"], n=wl["n"], m=wl["m"], d=wl["d"],
-                           generations=args.steps + args.warmup, seed=rank)
-    eng = engine.Engine(cfg, graph=True)
+                           generations=args.steps + args.warmup, seed=0 if sharded else rank)
+    graph = wl["sort"] == "bits"
+    eng = engine.Engine(cfg, graph=graph, sort=wl["sort"], group=group)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     # warm-up
-    eng.replay(max(3, args.warmup))
+    if graph:
+        eng.replay(max(3, args.warmup))
+    else:
+        for _ in range(max(3, args.warmup)):
+            eng.step()
     torch.cuda.synchronize()
     dist = None
     if world > 1:
@@ -259,7 +290,10 @@ def run_ours(args, rank, world):
         for i in range(args.steps):
             flush.fill_(i & 255)
             starts[i].record()
-            eng.replay_one()
+            if graph:
+                eng.replay_one()
+            else:
+                eng.step()
             ends[i].record()
         torch.cuda.synchronize()
     if dist:
@@ -281,9 +315,11 @@ def run_ours(args, rank, world):
     hX.copy_(eng.X)
     hF.copy_(eng.F)
     hI.copy_(eng.ideal)
-    e_steps = max(5, args.steps // 2)
+    e_steps = max(5, args.steps // 2) if graph else max(2, args.steps // 2)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     e0.record()
     for _ in range(e_steps):
         eng.XR[eng.cur][:n].copy_(hX, non_blocking=True)
@@ -297,13 +333,18 @@ def run_ours(args, rank, world):
     e1.record()
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
     h2d = n * d * 4 + n * m * 4 + m * 4
     d2h = n * d * 4 + n * m * 4 + m * 4 + _lib.INFO_COUNT * 4
 
     result = {"ms": ms, "clk": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "info": info,
-              "w": eng.w}
+              "w": eng.w, "sharded": sharded, "sort": wl["sort"]}
+    kern = time_kernels(torch, eng, _lib) if (rank == 0 or sharded) else None
     if rank == 0:
-        result["kernels"] = time_kernels(torch, eng, _lib)
+        result["kernels"] = kern
         result["peaks"] = measure_peaks(torch, _lib.lib(), _lib)
     return result
 
@@ -351,27 +392,39 @@ def main():
         return
     K = args.steps
     ms_per = r["ms"] / K
-    value = world * K / (r["ms"] / 1e3)
+    sharded = r["sharded"]
+    reps = 1 if sharded else world             # sharded: one population over all GPUs (strong scaling)
+    value = reps * K / (r["ms"] / 1e3)
     kern = r["kernels"]
     peaks = r["peaks"]
     n, m, R = wl["n"], wl["m"], 2 * wl["n"]
     step_ms = kern["t_variation"] + kern["t_sort"] + kern["t_niche"]
-    cmp_work = R * (R - 1) // 2 * m     # unordered pairs x m FP32 compares (one direction after the S-sort)
+    # unordered pairs x m FP32 compares (one direction after the S-sort); a shard sweeps 1/world of them
+    cmp_work = R * (R - 1) // 2 * m // (world if sharded else 1)
     dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
-    roof = {"kernel": "k_dom_tile_sorted (dominance bit-matrix)", "bound": "fp32-compare-issue",
+    kname = ("k_stream_tiles<COUNT> (dominator-count sweep, streamed sort)" if r["sort"] == "stream"
+             else "k_dom_tile_sorted (dominance bit-matrix)")
+    launches = K * 8 if r["sort"] == "bits" else K * (14 + 4 * int(kern.get("fronts_issued") or 0))
+    roof = {"kernel": kname, "bound": "fp32-compare-issue",
             "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12, "unit": "Tcmp/s",
             "frac": dom_achieved / peaks["compare"], "traffic": None,
             "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
             "share_of_step": kern["dom_tile_ms"] / step_ms if step_ms else None,
-            "algorithmic": f"R(R-1)/2 * m = {cmp_work:.3e} compares per launch"}
+            "algorithmic": f"R(R-1)/2 * m{' / world' if sharded else ''} = {cmp_work:.3e} compares per launch"}
+    par = f"sharded{world}" if sharded else ("replicas" if world > 1 else "single")
+    cfg_out = dict(cfgd, parallelism=par, w=r["w"], sort=r["sort"])
+    if r["sort"] == "stream":
+        cfg_out["graph"] = "eager generations (host-driven front loop)"
+        cfg_out["l2"] = "inputs larger than L2 (merged X is 176 MB) + 512 MiB flush between generations"
     line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded uniform population, random-init)",
-            "config": dict(cfgd, parallelism="replicas" if world > 1 else "single", w=r["w"]),
+            "config": cfg_out,
             "clocks": r["clk"],
-            "e2e": {"value": world * 1e3 / r["e2e_ms"], "unit": "generations/s", "h2d_bytes_per_step": r["h2d"],
+            "e2e": {"value": reps * 1e3 / r["e2e_ms"], "unit": "generations/s", "h2d_bytes_per_step": r["h2d"],
                     "d2h_bytes_per_step": r["d2h"]},
-            "gpu_launches": K * 8,
+            "gpu_launches": launches,
             "roofline": roof,
             "phases_ms": {k: round(v, 4) for k, v in kern.items()},
             "peaks": {"compare_per_s": peaks["compare"], "fp32_flop_per_s": peaks["fp32"]},

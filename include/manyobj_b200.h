@@ -56,6 +56,8 @@ enum {
   MO_INFO_SINGULAR = 8,   /* 1 if the intercept solve fell back entirely   */
   MO_INFO_SURVIVORS = 9,  /* survivors written (must equal n)              */
   MO_INFO_ERROR = 10,     /* non-zero status raised on the device          */
+  MO_INFO_ASSOC_FALLBACK = 11, /* candidates the lattice-pruned association
+                                  could not certify (full scan instead)     */
   MO_INFO_COUNT = 16
 };
 
@@ -215,6 +217,14 @@ typedef struct mo_step_args {
   int32_t shard_rank;
   int32_t shard_count;
   int32_t pad2;
+  /* Optional lattice pruning of the association (exact; see k_assoc_lattice):
+   * for a single-layer Das-Dennis set of H divisions and m <= 4, `lattice`
+   * maps (k_0, ..., k_{m-2}) (mixed radix H+1, k_0 most significant) to the
+   * reference-point index of k/H; -1 marks k outside the simplex.  NULL =
+   * full scan.  lattice_r: box radius in lattice steps (0 = default 6). */
+  const int32_t* lattice;
+  int32_t lattice_H;
+  int32_t lattice_r;
 } mo_step_args;
 
 enum { MO_SORT_BITS = 0, MO_SORT_STREAM = 1 };

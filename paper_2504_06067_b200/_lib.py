@@ -21,7 +21,7 @@ c_i32, c_i64, c_u32, c_u64, c_f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uin
 c_vp, c_sz = ctypes.c_void_p, ctypes.c_size_t
 
 INFO = dict(L=0, SELECTED=1, K=2, NFRONTS=3, FL_SIZE=4, SKIPPED=5, NEAREST=6, LEVEL=7, SINGULAR=8,
-            SURVIVORS=9, ERROR=10)
+            SURVIVORS=9, ERROR=10, ASSOC_FALLBACK=11)
 INFO_COUNT = 16
 PHASE_VARY, PHASE_SORT, PHASE_NICHE, PHASE_ALL = 1, 2, 4, 7
 NICHE_PREP, NICHE_ASSOC, NICHE_FINISH = 8, 16, 32
@@ -43,6 +43,7 @@ class StepArgs(ctypes.Structure):
         ("ideal", c_vp), ("ranks", c_vp), ("info", c_vp), ("workspace", c_vp), ("workspace_bytes", c_sz),
         ("generation_dev", c_vp),
         ("sort_mode", c_i32), ("shard_rank", c_i32), ("shard_count", c_i32), ("pad2", c_i32),
+        ("lattice", c_vp), ("lattice_H", c_i32), ("lattice_r", c_i32),
     ]
 
 

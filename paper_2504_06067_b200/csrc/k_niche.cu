@@ -339,6 +339,95 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
 }
 
 
+// ------------------------------------------------- lattice-pruned association
+//
+// Single-layer Das-Dennis sets (z = k/H, k integer, sum k = H) at m <= 4: the
+// direction with the largest key t = f.zhat lies near the simplex projection
+// u = f / sum(f).  A thread evaluates the canonical key (same arithmetic and
+// tie-break as assoc_item) on the lattice points with |k_i - u_i H| < r for
+// i < m-1, found through a dense (k_0..k_{m-2}) -> index table, then
+// certifies the winner: every point outside that box has ||z - u|| >= r/H,
+// hence sin(angle) >= ||z - u|| / sqrt(m) (z, u on the simplex, ||z|| <= 1),
+// hence an FP32 key <= ||f|| sqrt(1 - (r/H)^2 / m) (1 + (m + 2) 2^-24): all
+// terms are nonnegative, so the m roundings of the products / sums and the
+// FP32 rounding of zhat perturb the key by at most (m + 1) 2^-24 relative.  A winner above that bound is the
+// global argmax, ties included; rows that fail (or f = 0) go to a fallback
+// list that the full-scan k_assoc processes.  Exact: the result equals the
+// full scan bit for bit; the certificate only decides where it is computed.
+template <int M>
+__global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncand) return;
+  const int row = __ldcg(a.cand + c);
+  const int H = a.lat_H, r = a.lat_r;
+  float fn[M];
+  double s = 0.0, nn = 0.0;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    float v = a.F[(int64_t)row * M + k];
+    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+    fn[k] = v;
+    s += (double)v;
+    nn += (double)v * (double)v;
+  }
+  bool ok = s > 0.0 && isfinite(s);
+#pragma unroll
+  for (int k = 0; k < M; ++k) ok = ok && fn[k] >= 0.0f;
+  float best = -__int_as_float(0x7f800000);
+  int bp = 0x7fffffff;
+  if (ok) {
+    int lo[M], hi[M];
+#pragma unroll
+    for (int k = 0; k < M - 1; ++k) {
+      const double x = (double)fn[k] / s * (double)H;
+      lo[k] = max(0, (int)floor(x - (double)r) + 1);
+      hi[k] = min(H, (int)ceil(x + (double)r) - 1);
+    }
+    // odometer over the first m-1 lattice coordinates
+    int k_[M];
+#pragma unroll
+    for (int k = 0; k < M - 1; ++k) k_[k] = lo[k];
+    bool more = true;
+    for (int k = 0; k < M - 1; ++k) more = more && lo[k] <= hi[k];
+    while (more) {
+      int rest = H, idx = 0;
+#pragma unroll
+      for (int k = 0; k < M - 1; ++k) {
+        rest -= k_[k];
+        idx = idx * (H + 1) + k_[k];
+      }
+      if (rest >= 0) {
+        const int j = __ldg(a.lat_table + idx);
+        const int p = __ldg(a.pos_ref + j);
+        const float t = canon_dot<M>(fn, a.zs + (int64_t)p * M);
+        if (t > best || (t == best && p < bp)) {
+          best = t;
+          bp = p;
+        }
+      }
+      int k = M - 2;
+      for (; k >= 0; --k) {
+        if (++k_[k] <= hi[k]) break;
+        k_[k] = lo[k];
+      }
+      more = k >= 0;
+    }
+    const double rho = ((double)r - 1e-6) / (double)H;
+    const double bound = sqrt(nn) * sqrt(1.0 - rho * rho / (double)M) * (1.0 + (M + 2) * 5.9604644775390625e-8);
+    ok = bp != 0x7fffffff && (double)best > bound;
+  }
+  if (ok) {
+    a.akey[row] = ((unsigned long long)f2ord(best) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp);
+  } else {
+    a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row;
+    atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
+  }
+}
+
 __global__ void k_assoc_final(AssocFinalArgs a) {
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
@@ -773,6 +862,26 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   }
   MO_CHECK_LAUNCH();
   return MO_OK;
+}
+
+int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  if (cudaMemsetAsync(a.fb_ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
+    return MO_ERR_CUDA;
+  const unsigned blocks = (unsigned)ceil_div(R, 256);
+  switch (m) {
+    case 2: k_assoc_lattice<2><<<blocks, 256, 0, s>>>(a); break;
+    case 3: k_assoc_lattice<3><<<blocks, 256, 0, s>>>(a); break;
+    case 4: k_assoc_lattice<4><<<blocks, 256, 0, s>>>(a); break;
+    default: return MO_ERR_PARAM;
+  }
+  MO_CHECK_LAUNCH();
+  // fallback rows: the full scan over this launch's reference range
+  AssocArgs b = a;
+  b.cand = a.fb_cand;
+  b.ctl = a.fb_ctl;
+  return launch_assoc(b, m, R, s);
 }
 
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {

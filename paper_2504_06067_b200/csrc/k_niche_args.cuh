@@ -59,6 +59,13 @@ struct AssocArgs {
   int psplit;            // reference points per blockIdx.y
   unsigned long long* akey;
   int zbeg, zend;        // shuffled reference positions handled by this launch (shard range)
+  // lattice pruning (k_assoc_lattice): dense (k_0..k_{m-2}) -> reference index table, H, box radius;
+  // rows it cannot certify are appended to fb_cand (count fb_ctl[0]) for the full scan
+  const int* lat_table;
+  int lat_H, lat_r;
+  const int* pos_ref;
+  int* fb_cand;
+  int* fb_ctl;
 };
 
 struct AssocFinalArgs {
@@ -115,6 +122,7 @@ struct SelectArgs {
 
 int launch_prep(const PrepArgs& a, cudaStream_t s);
 int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
+int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s);
 int launch_select(const SelectArgs& a, cudaStream_t s);
 

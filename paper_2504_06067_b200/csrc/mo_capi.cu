@@ -33,7 +33,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, fcand, fctl, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -103,6 +103,8 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.T = ceil_div(nb, (int64_t)G);
   L.mask_local_words = L.T * (STREAM_BLK / 32);
   L.mask_full_words = L.mask_local_words * G;
+  L.fcand = bump(c, (size_t)R * 4);
+  L.fctl = bump(c, 64);
   L.tkey = bump(c, st ? (size_t)R * 4 : 0);
   L.tval = bump(c, st ? (size_t)R * 4 : 0);
   L.cnt = bump(c, st ? (size_t)R * 4 : 0);
@@ -292,7 +294,16 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.akey = pa.akey;
   aa.zbeg = (int)(w * a->shard_rank / G);
   aa.zend = (int)(w * (a->shard_rank + 1) / G);
-  MO_TRY(launch_assoc(aa, m, R, s));
+  aa.lat_table = a->lattice;
+  aa.lat_H = a->lattice_H;
+  aa.lat_r = a->lattice_r > 0 ? a->lattice_r : 6;
+  aa.pos_ref = pa.pos_ref;
+  aa.fb_cand = at<int>(ws, L.fcand);
+  aa.fb_ctl = at<int>(ws, L.fctl);
+  if (a->lattice && m >= 2 && m <= 4)
+    MO_TRY(launch_assoc_lattice(aa, m, R, s));
+  else
+    MO_TRY(launch_assoc(aa, m, R, s));
   }
   if (!(mask & MO_PHASE_NICHE_FINISH)) return MO_OK;
   AssocFinalArgs fa;
@@ -395,6 +406,7 @@ static int check_step_args(const mo_step_args* a) {
   if (a->problem < MO_DTLZ1 || a->problem > MO_DTLZ7) return MO_ERR_PARAM;
   if (a->sort_mode != MO_SORT_BITS && a->sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
   if (a->shard_count < 0 || a->shard_rank < 0 || a->shard_rank >= shards_of(a->shard_count)) return MO_ERR_PARAM;
+  if (a->lattice && (a->lattice_H < 1 || a->lattice_r < 0)) return MO_ERR_PARAM;
   return MO_OK;
 }
 
@@ -553,6 +565,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
   aa.akey = pa.akey;
   aa.zbeg = 0;
   aa.zend = (int)w;
+  aa.lat_table = nullptr;
   MO_TRY(launch_assoc(aa, m, R, s));
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));

@@ -89,7 +89,7 @@ def build_reference_set(cfg):
 class Engine:
     """Device-resident NSGA-III run: buffers, workspace and (optionally) a CUDA graph."""
 
-    def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4):
+    def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4, prune="auto"):
         validate(cfg)
         self.cfg = cfg
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -113,6 +113,7 @@ class Engine:
         with torch.cuda.device(self.dev):
             L = _lib.lib()
             self.zhat = torch.from_numpy(zh).to(self.dev)
+            self.lattice, self.lattice_H = self._lattice_table(prune)
             self.XR = [torch.empty((2 * n, d), dtype=torch.float32, device=self.dev) for _ in range(2)]
             self.FR = [torch.empty((2 * n, m), dtype=torch.float32, device=self.dev) for _ in range(2)]
             self.ranks = torch.empty(2 * n, dtype=torch.int32, device=self.dev)
@@ -136,6 +137,26 @@ class Engine:
         self._graph = None
         if graph:
             self.capture()
+
+    def _lattice_table(self, prune):
+        """Dense (k_0..k_{m-2}) -> reference index table for the exact lattice-pruned association
+        (single-layer Das-Dennis, m <= 4).  prune: "auto" (when it pays), True (whenever legal), False."""
+        cfg, m, w = self.cfg, self.cfg.m, self.w
+        Ho, Hi = cfg.reference_points if cfg.reference_points is not None else refpoints.choose_divisions(m, cfg.n)
+        legal = Hi == 0 and 2 <= m <= 4 and (Ho + 1) ** (m - 1) <= (1 << 26)
+        if prune is False or not legal:
+            if prune is True and not legal:
+                raise ConfigError("prune", "lattice pruning needs a single-layer Das-Dennis set and m <= 4")
+            return None, 0
+        if prune == "auto" and 4 * 11 ** (m - 1) >= w:    # box of (2r-1)^(m-1) points, r = 6
+            return None, 0
+        k = np.rint(np.asarray(self.Z, np.float64) * Ho).astype(np.int64)
+        idx = np.zeros(w, np.int64)
+        for i in range(m - 1):
+            idx = idx * (Ho + 1) + k[:, i]
+        table = np.full((Ho + 1) ** (m - 1), -1, np.int32)
+        table[idx] = np.arange(w, dtype=np.int32)
+        return torch.from_numpy(table).to(self.dev), Ho
 
     def _choose_sort(self, sort):
         if sort not in ("auto", "bits", "stream"):
@@ -172,6 +193,9 @@ class Engine:
         a.generation_dev = self.gen_dev.data_ptr() if use_dev_gen else None
         a.sort_mode = self.sort_mode
         a.shard_rank, a.shard_count = self.shard_rank, self.shard_count
+        a.lattice = self.lattice.data_ptr() if self.lattice is not None else None
+        a.lattice_H = self.lattice_H
+        a.lattice_r = 0
         return a
 
     def _launch(self, cur, generation, phases=_lib.PHASE_ALL, use_dev_gen=False):
@@ -333,8 +357,8 @@ class LocalShards:
     max across the shards' buffers.  Results must be bit-identical to G
     processes over NCCL (the kernels only see their shard index)."""
 
-    def __init__(self, cfg, shards, device=None, poll=4):
-        self.engines = [Engine(cfg, device=device, sort="stream", shard=(g, shards), poll=poll)
+    def __init__(self, cfg, shards, device=None, poll=4, prune="auto"):
+        self.engines = [Engine(cfg, device=device, sort="stream", shard=(g, shards), poll=poll, prune=prune)
                         for g in range(shards)]
 
     def step(self):

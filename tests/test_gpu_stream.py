@@ -121,3 +121,72 @@ def test_stream_engine_profile_and_poll(M):
         b.step()
     assert torch.equal(a.X, b.X)
     assert prof["t_sort"] > 0 and prof["fronts_issued"] >= 1
+
+
+# ------------------------------------------------------- lattice-pruned association
+
+@pytest.mark.parametrize("kind,n,m,d,gens", [("DTLZ7", 3000, 3, 22, 6), ("DTLZ1", 2000, 3, 7, 6),
+                                             ("DTLZ2", 4000, 4, 13, 5), ("DTLZ5", 1000, 2, 11, 5),
+                                             ("DTLZ4", 5000, 3, 12, 5)])
+def test_lattice_pruned_association_equals_full_scan(M, kind, n, m, d, gens):
+    cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=6)
+    a = M.engine.Engine(cfg, prune=False)
+    b = M.engine.Engine(cfg, prune=True)
+    assert a.lattice is None and b.lattice is not None
+    for g in range(gens):
+        a.step()
+        b.step()
+        assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F), (kind, g)
+        ia, ib = a.info_dict(), b.info_dict()
+        fb = ib.pop("assoc_fallback")
+        ia.pop("assoc_fallback")
+        assert ia == ib
+        if not ib["skipped"]:
+            assert fb < 0.02 * n, fb          # the certificate holds for almost every candidate
+
+
+def test_lattice_pruned_association_adversarial(M):
+    """Candidates on lattice directions, on cell boundaries, on the simplex edges and at the ideal point."""
+    from paper_2504_06067_b200 import _lib
+    cfg = M.engine.RunConfig(problem="DTLZ1", n=2000, m=3, d=7, generations=1, seed=2)
+    rs = np.random.default_rng(3)
+    n = 2000
+    Z = M.refpoints.reference_points(3, n)
+    H = M.refpoints.choose_divisions(3, n)[0]
+    F = np.concatenate([
+        Z[rs.integers(0, len(Z), 800)] * rs.uniform(0.5, 2.0, (800, 1)),           # exactly on directions
+        (np.floor(rs.random((800, 3)) * H) + 0.5) / H,                            # cell midpoints
+        np.eye(3)[rs.integers(0, 3, 600)] * rs.random((600, 1)),                  # simplex vertices
+        np.concatenate([rs.random((600, 2)), np.zeros((600, 1))], 1),             # an edge
+        np.zeros((200, 3)),                                                        # the ideal point
+        rs.random((1000, 3)),
+    ]).astype(np.float32)
+    F = np.concatenate([np.zeros((1, 3), np.float32), F])[:2 * n]
+    outs = []
+    for prune in (False, True):
+        eng = M.engine.Engine(cfg, prune=prune)
+        eng.FR[eng.cur].copy_(torch.from_numpy(F))
+        a = eng._args[eng.cur]
+        L = _lib.lib()
+        _lib.check(L.mo_step_phases(a, _lib.PHASE_SORT | _lib.PHASE_NICHE, _lib.stream_ptr()), "select")
+        torch.cuda.synchronize()
+        ao = _lib.stream_offsets(n, 3, eng.w, eng.sort_mode, 1)[3]
+        akey = np_(eng.ws[ao: ao + 8 * 2 * n].view(torch.int64)).copy()
+        info = eng.info_dict()
+        info.pop("assoc_fallback")
+        outs.append((np_(eng.FR[eng.cur ^ 1][:n]).copy(), np_(eng.ranks).copy(), info, akey))
+    assert (outs[0][3] != 0).sum() > n                       # the association keys of every candidate row
+    assert np.array_equal(outs[0][3], outs[1][3])
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
+def test_local_shards_with_lattice(M):
+    cfg = M.engine.RunConfig(problem="DTLZ7", n=3000, m=3, d=22, generations=3, seed=8)
+    one = M.engine.Engine(cfg, sort="bits", prune=False)
+    grp = M.engine.LocalShards(cfg, 4, prune=True)
+    for _ in range(3):
+        one.step()
+        grp.step()
+        for e in grp.engines:
+            assert torch.equal(e.X, one.X) and torch.equal(e.F, one.F)
