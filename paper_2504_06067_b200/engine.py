@@ -228,9 +228,17 @@ class Engine:
         self.cur ^= 1
         self.generation += 1
 
+    def _lib(self):
+        return _lib.lib()
+
+    def _stream(self):
+        return _lib.stream_ptr()
+
     def step_gen(self, profile=None):
-        """One streamed/sharded generation; yields its collectives (see run_collective)."""
-        L, s = _lib.lib(), _lib.stream_ptr()
+        """One streamed/sharded generation; yields its collectives (see run_collective).
+        The host logic here (order of the collectives, lazy split polling, lockstep exit) is shared by
+        NCCL runs, the in-process LocalShards emulation and the gloo CPU tests."""
+        L, s = self._lib(), self._stream()
         a = self._args[self.cur]
         a.generation = int(self.generation) & 0xFFFFFFFF
         sharded = self.shard_count > 1
