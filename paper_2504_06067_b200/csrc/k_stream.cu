@@ -30,6 +30,17 @@
 // Work is a device-planned queue: k_stream_plan counts the (row block, i
 // chunk) items of every owned block from wend / the front list, and the
 // persistent k_stream_tiles CTAs pull items with one atomic each.
+//
+// Two position spaces.  "Slab" (m > 4): k_presort's S-ordered buckets --
+// dominators precede (triangle), S-separated tiles need only the <= chain.
+// "Boxed" (m <= 4): k_presort_morton's Morton order of the quantised
+// objectives makes every 256-row block compact in objective space, so an
+// ordered block pair (i block, j block) is usually decided by the two
+// bounding boxes alone: some min_i[k] > max_j[k] -> no i dominates any j;
+// max_i <= min_j everywhere and < somewhere -> every i dominates every j
+// (count += |block|); only "mixed" pairs are computed row by row.  Every
+// ordered pair is visited (no triangle) but at C4 (m = 3, R = 2M) only a few
+// per cent are mixed.  The front-list chunks of DEC carry boxes too.
 #include "mo_chains.cuh"
 #include "mo_common.cuh"
 #include "mo_grid.cuh"
@@ -78,7 +89,12 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
   for (int t = t0; t < t1; ++t) {
     const int b = owned_block(a, t);
     int items = 0;
-    if (!done && b < nb) {
+    if (!done && b < nb && a.boxed) {
+      if (MODE == MODE_COUNT)
+        items = (nb + STREAM_CHUNK - 1) / STREAM_CHUNK;
+      else if (__ldcg(a.ucnt + t) > 0)
+        items = (fln + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
+    } else if (!done && b < nb) {
       const int bend = block_bend(a, b);
       if (MODE == MODE_COUNT) {
         const int nib = (bend + STREAM_BLK - 1) / STREAM_BLK;
@@ -147,7 +163,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       fb[k] = jb < a.R ? __ldg(a.FS + (int64_t)jb * M + k) : PINF;
     }
     const float jmin = __ldg(a.blkmin + bj);
-    const int bend = block_bend(a, bj);
+    const int bend = a.boxed ? a.R : block_bend(a, bj);
     int e0, e1;  // i range: positions (COUNT) or front-list entries (DEC)
     if (MODE == MODE_COUNT) {
       e0 = c * STREAM_CHUNK * STREAM_BLK;
@@ -161,6 +177,25 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
     float ca = 0.0f, cb = 0.0f;
     for (int s0 = e0; s0 < e1; s0 += STREAM_BLK) {
       const int nv = min(STREAM_BLK, e1 - s0);
+      if (a.boxed) {  // block-pair classification from the bounding boxes (uniform over the CTA)
+        const float* ib = (MODE == MODE_COUNT ? a.blkbox : a.flbox) + (int64_t)(s0 / STREAM_BLK) * 2 * M;
+        const float* jb2 = a.blkbox + (int64_t)bj * 2 * M;
+        bool none = false, all = true, strict = false;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const float imn = __ldg(ib + k), imx = __ldg(ib + M + k);
+          const float jmn = __ldg(jb2 + k), jmx = __ldg(jb2 + M + k);
+          none |= imn > jmx;
+          all &= imx <= jmn;
+          strict |= imx < jmn;
+        }
+        if (none) continue;
+        if (all && strict) {
+          ca += (float)nv;
+          cb += (float)nv;
+          continue;
+        }
+      }
       for (int e = tid; e < STREAM_BLK; e += ST_THREADS) {
         int src = -1;
         if (e < nv) src = MODE == MODE_COUNT ? s0 + e : __ldg(a.fl + s0 + e);
@@ -169,7 +204,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
         for (int k = 0; k < MP; ++k) dst[k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
       }
       const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : __ldg(a.flmax + s0 / STREAM_BLK);
-      const bool fast = (MODE == MODE_COUNT ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
+      const bool fast = (MODE == MODE_COUNT && !a.boxed ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
       __syncthreads();
       const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
       if (fast) {
@@ -220,7 +255,7 @@ __global__ void k_stream_mark(StreamArgs a) {
 // Front k from the gathered mask: ranks, ordered front list, split decision.
 __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, int k) {
   __shared__ int sh[40];
-  __shared__ float sMax[APPLY_THREADS / 32];
+  __shared__ float sMax[APPLY_THREADS / 32], sMin[APPLY_THREADS / 32];
   if (__ldcg(a.ctl + SC_DONE) != 0) return;  // set only after the last barrier below
   const int nb = nblocks(a.R);
   const int64_t N = (int64_t)nb * (STREAM_BLK / 32);
@@ -249,8 +284,9 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
   const int nq = (fk + STREAM_BLK - 1) / STREAM_BLK;
   for (int q = blockIdx.x; q < nq; q += gridDim.x) {
     const int e = q * STREAM_BLK + (int)threadIdx.x;
-    float v = -__int_as_float(0x7f800000);
-    if (threadIdx.x < STREAM_BLK && e < fk) v = __ldg(a.SS + __ldcg(a.fl + e));
+    const bool act = threadIdx.x < STREAM_BLK && e < fk;
+    const int p = act ? __ldcg(a.fl + e) : 0;
+    float v = act ? __ldg(a.SS + p) : -__int_as_float(0x7f800000);
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(MO_FULL, v, o));
     if ((threadIdx.x & 31) == 0) sMax[threadIdx.x >> 5] = v;
     __syncthreads();
@@ -260,6 +296,31 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
       a.flmax[q] = mx;
     }
     __syncthreads();
+    if (a.boxed) {
+      for (int k = 0; k < a.m; ++k) {
+        const float f = act ? __ldg(a.FS + (int64_t)p * a.m + k) : 0.0f;
+        float mn = act ? f : __int_as_float(0x7f800000), mx = act ? f : -__int_as_float(0x7f800000);
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+          sMax[threadIdx.x >> 5] = mx;
+          sMin[threadIdx.x >> 5] = mn;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          float a0 = sMin[0], a1 = sMax[0];
+          for (int w = 1; w < APPLY_THREADS / 32; ++w) {
+            a0 = fminf(a0, sMin[w]);
+            a1 = fmaxf(a1, sMax[w]);
+          }
+          a.flbox[(int64_t)q * 2 * a.m + k] = a0;
+          a.flbox[(int64_t)q * 2 * a.m + a.m + k] = a1;
+        }
+        __syncthreads();
+      }
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t sel = __ldcg(a.ctl + SC_CUM);
@@ -286,6 +347,157 @@ __global__ void k_stream_end(StreamArgs a) {
     const int r = __ldcg(a.rank_pos + p);
     a.ranks[__ldg(a.perm + p)] = r == MO_RANK_UNRANKED ? MO_RANK_DROPPED : r;
   }
+}
+
+// ------------------------------------------------------------ Morton presort
+//
+// Boxed mode position space.  P0 per-coordinate min / max (ordered-uint
+// atomics) and row sums S; P1 Morton key of the quantised objectives
+// (b = 30 / m bits per coordinate, interleaved most significant first) and
+// row ids; P2 four stable 8-bit radix passes (ties keep row order, so every
+// shard derives the same positions); P3 gather FS / SS / perm; P4 per-block
+// S range and bounding box.
+constexpr int MORTON_THREADS = 512;
+
+__global__ void __launch_bounds__(MORTON_THREADS) k_presort_morton(MortonArgs a) {
+  __shared__ int sh[40];
+  __shared__ int sWcnt[(MORTON_THREADS / 32) * 256], sRun[256], sOff[256];
+  __shared__ unsigned sMn[16], sMx[16];
+  __shared__ float sRed[2][MORTON_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
+  const int R = a.R, m = a.m;
+  if (tid < 16) {
+    sMn[tid] = 0xffffffffu;
+    sMx[tid] = 0u;
+  }
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    unsigned mn = 0xffffffffu, mx = 0u;
+    for (int i = gtid; i < R; i += gthreads) {
+      const unsigned o = f2ord(a.F[(int64_t)i * m + k]);
+      mn = min(mn, o);
+      mx = max(mx, o);
+    }
+    mn = warp_min_u32(mn);
+    mx = warp_max_u32(mx);
+    if (lane == 0) {
+      atomicMin(&sMn[k], mn);
+      atomicMax(&sMx[k], mx);
+    }
+  }
+  __syncthreads();
+  if (tid < m) {
+    atomicMin(&a.cbox[tid], sMn[tid]);
+    atomicMax(&a.cbox[16 + tid], sMx[tid]);
+  }
+  grid_sync(a.g.bar);
+  // P1: Morton keys
+  const int bits = 30 / m;
+  const float levels = (float)((1u << bits) - 1u);
+  float lo[16], sc[16];
+  for (int k = 0; k < m; ++k) {
+    lo[k] = ord2f(__ldcg(a.cbox + k));
+    const float hi = ord2f(__ldcg(a.cbox + 16 + k));
+    sc[k] = hi > lo[k] ? levels / (hi - lo[k]) : 0.0f;
+  }
+  for (int i = gtid; i < R; i += gthreads) {
+    uint32_t q[16];
+    for (int k = 0; k < m; ++k) {
+      float v = (a.F[(int64_t)i * m + k] - lo[k]) * sc[k];
+      v = fminf(fmaxf(v, 0.0f), levels);
+      q[k] = (uint32_t)v;
+    }
+    uint32_t key = 0;
+    for (int b = bits - 1; b >= 0; --b)
+      for (int k = 0; k < m; ++k) key = (key << 1) | ((q[k] >> b) & 1u);
+    a.keyA[i] = key;
+    a.valA[i] = i;
+  }
+  grid_sync(a.g.bar);
+  // P2: stable radix sort by key (4 x 8 bits), result back in keyA / valA
+  grid_radix_pass(a.g, R, 0, a.keyA, a.valA, a.tkey, a.tval, sWcnt, sRun, sOff, sh);
+  grid_radix_pass(a.g, R, 8, a.tkey, a.tval, a.keyA, a.valA, sWcnt, sRun, sOff, sh);
+  grid_radix_pass(a.g, R, 16, a.keyA, a.valA, a.tkey, a.tval, sWcnt, sRun, sOff, sh);
+  grid_radix_pass(a.g, R, 24, a.tkey, a.tval, a.keyA, a.valA, sWcnt, sRun, sOff, sh);
+  // P3: gather
+  for (int p = gtid; p < R; p += gthreads) {
+    const int i = __ldcg(a.valA + p);
+    a.perm[p] = i;
+    const float* f = a.F + (int64_t)i * m;
+    float s = f[0];
+    a.FS[(int64_t)p * m] = f[0];
+    for (int k = 1; k < m; ++k) {
+      s = __fadd_rn(s, f[k]);
+      a.FS[(int64_t)p * m + k] = f[k];
+    }
+    a.SS[p] = s;
+  }
+  grid_sync(a.g.bar);
+  // P4: per-block S range and bounding box
+  const int nblk = (R + STREAM_BLK - 1) / STREAM_BLK;
+  for (int b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const int p = b * STREAM_BLK + tid;
+    const bool act = tid < STREAM_BLK && p < R;
+    for (int k = -1; k < m; ++k) {
+      float v = 0.0f;
+      if (act) v = k < 0 ? __ldcg(a.SS + p) : __ldcg(a.FS + (int64_t)p * m + k);
+      float mn = act ? v : __int_as_float(0x7f800000), mx = act ? v : -__int_as_float(0x7f800000);
+      for (int o = 16; o > 0; o >>= 1) {
+        mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+      }
+      if (lane == 0) {
+        sRed[0][tid >> 5] = mn;
+        sRed[1][tid >> 5] = mx;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < MORTON_THREADS / 32; ++w) {
+          mn = fminf(mn, sRed[0][w]);
+          mx = fmaxf(mx, sRed[1][w]);
+        }
+        if (k < 0) {
+          a.blkmin[b] = mn;
+          a.blkmax[b] = mx;
+        } else {
+          a.blkbox[(int64_t)b * 2 * m + k] = mn;
+          a.blkbox[(int64_t)b * 2 * m + m + k] = mx;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+int launch_presort_morton(const MortonArgs& a, cudaStream_t s) {
+  static int maxb = 0;
+  if (!maxb) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_presort_morton, MORTON_THREADS, 0);
+    maxb = sms * (per > 0 ? 1 : 1);
+  }
+  if (a.R < 1 || a.m < 1 || a.m > 16) return MO_ERR_PARAM;
+  int blocks = (int)ceil_div(a.R, MORTON_THREADS * 4);
+  if (blocks > maxb) blocks = maxb;
+  if (blocks < 1) blocks = 1;
+  if (cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(a.cbox, 0xff, 16 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaMemsetAsync(a.cbox + 16, 0, 16 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(MORTON_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k_presort_morton, a) != cudaSuccess) return MO_ERR_CUDA;
+  MO_CHECK_LAUNCH();
+  return MO_OK;
 }
 
 // ------------------------------------------------------------- launchers

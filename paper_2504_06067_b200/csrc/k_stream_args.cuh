@@ -42,8 +42,32 @@ struct StreamArgs {
   int* info;             // MO_INFO_COUNT
   int* ranks;            // R   output ranks (row order)
   GridCtx gc;
+  // boxed mode (m <= 4): Morton-ordered positions, per-block bounding boxes,
+  // all ordered block pairs classified none / all / mixed (k_presort_morton)
+  int boxed;
+  float* blkbox;         // nb x 2 x m: per 256-row block min[m], max[m]
+  float* flbox;          // nb x 2 x m: per 256-entry front-list chunk
 };
 
+// Morton presort of the boxed mode (F -> perm, FS, SS, S block range, boxes)
+struct MortonArgs {
+  const float* F;
+  int R, m;
+  uint32_t* keyA;
+  int* valA;
+  uint32_t* tkey;
+  int* tval;
+  unsigned* cbox;        // 2 x 16 ordered-uint per-coordinate min / max
+  int* perm;
+  float* FS;
+  float* SS;
+  float* blkmin;
+  float* blkmax;
+  float* blkbox;
+  GridCtx g;
+};
+
+int launch_presort_morton(const MortonArgs& a, cudaStream_t s);
 int launch_stream_begin(StreamArgs a, cudaStream_t s);
 int launch_stream_front(StreamArgs a, int k, cudaStream_t s);
 int launch_stream_end(StreamArgs a, cudaStream_t s);

@@ -33,7 +33,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, fcand, fctl, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, fcand, fctl, blkbox, flbox, cbox, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -105,6 +105,9 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.mask_full_words = L.mask_local_words * G;
   L.fcand = bump(c, (size_t)R * 4);
   L.fctl = bump(c, 64);
+  L.blkbox = bump(c, st ? (size_t)(nb + 1) * 2 * m * 4 : 0);
+  L.flbox = bump(c, st ? (size_t)(nb + 1) * 2 * m * 4 : 0);
+  L.cbox = bump(c, 32 * 4);
   L.tkey = bump(c, st ? (size_t)R * 4 : 0);
   L.tval = bump(c, st ? (size_t)R * 4 : 0);
   L.cnt = bump(c, st ? (size_t)R * 4 : 0);
@@ -357,6 +360,9 @@ static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
   return MO_OK;
 }
 
+// Boxed (Morton) position space for the streamed sort at m <= 4, S slabs above
+static int stream_boxed(int m) { return m <= 4 ? 1 : 0; }
+
 static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   void* ws = a->workspace;
   StreamArgs sa;
@@ -388,6 +394,9 @@ static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   sa.gc.part = at<int>(ws, L.part);
   sa.gc.hist = at<int>(ws, L.hist);
   sa.gc.parity = 0;
+  sa.boxed = stream_boxed(a->m);
+  sa.blkbox = at<float>(ws, L.blkbox);
+  sa.flbox = at<float>(ws, L.flbox);
   return sa;
 }
 
@@ -626,8 +635,33 @@ int mo_sort_stream_begin(const mo_step_args* a, void* stream_) {
   Layout L;
   MO_TRY(check_stream(a, L));
   cudaStream_t s = (cudaStream_t)stream_;
-  MO_TRY(launch_presort(presort_args(a, L), s));
-  return launch_stream_begin(stream_args(a, L), s);
+  StreamArgs sa = stream_args(a, L);
+  if (sa.boxed) {
+    void* ws = a->workspace;
+    MortonArgs ma;
+    ma.F = a->FR;
+    ma.R = (int)(2 * a->n);
+    ma.m = a->m;
+    ma.keyA = at<uint32_t>(ws, L.keyA);
+    ma.valA = at<int>(ws, L.valA);
+    ma.tkey = at<uint32_t>(ws, L.tkey);
+    ma.tval = at<int>(ws, L.tval);
+    ma.cbox = at<unsigned>(ws, L.cbox);
+    ma.perm = at<int>(ws, L.perm_sort);
+    ma.FS = at<float>(ws, L.FS);
+    ma.SS = at<float>(ws, L.SS);
+    ma.blkmin = at<float>(ws, L.blkmin);
+    ma.blkmax = at<float>(ws, L.blkmax);
+    ma.blkbox = at<float>(ws, L.blkbox);
+    ma.g.bar = at<unsigned>(ws, L.bar) + BAR_PRESORT;
+    ma.g.part = at<int>(ws, L.part);
+    ma.g.hist = at<int>(ws, L.hist);
+    ma.g.parity = 0;
+    MO_TRY(launch_presort_morton(ma, s));
+  } else {
+    MO_TRY(launch_presort(presort_args(a, L), s));
+  }
+  return launch_stream_begin(sa, s);
 }
 
 int mo_sort_stream_front(const mo_step_args* a, int32_t k, void* stream_) {
