@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
     const int t = lo, c = item - __ldg(a.plan + t);
     const int bj = owned_block(a, t);
     const int j0 = bj * STREAM_BLK;
-    const int ja = j0 + tid, jb = ja + ST_THREADS;
+    // two adjacent rows per thread: a warp owns 64 consecutive positions (one j box per warp)
+    const int ja = j0 + 2 * tid, jb = ja + 1;
     float fa[M], fb[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) {
@@ -163,6 +164,17 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       fb[k] = jb < a.R ? __ldg(a.FS + (int64_t)jb * M + k) : PINF;
     }
     const float jmin = __ldg(a.blkmin + bj);
+    float wjmn[M], wjmx[M];  // bounding box of this warp's 64 j rows (boxed mode)
+    if (a.boxed) {
+      const int q = (j0 + 64 * (tid >> 5)) / 32;
+      const int q2 = min(q + 1, (a.R - 1) / 32);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        wjmn[k] = fminf(__ldg(a.blkbox32 + (int64_t)q * 2 * M + k), __ldg(a.blkbox32 + (int64_t)q2 * 2 * M + k));
+        wjmx[k] = fmaxf(__ldg(a.blkbox32 + (int64_t)q * 2 * M + M + k),
+                        __ldg(a.blkbox32 + (int64_t)q2 * 2 * M + M + k));
+      }
+    }
     const int bend = a.boxed ? a.R : block_bend(a, bj);
     int e0, e1;  // i range: positions (COUNT) or front-list entries (DEC)
     if (MODE == MODE_COUNT) {
@@ -207,26 +219,47 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       const bool fast = (MODE == MODE_COUNT && !a.boxed ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
       __syncthreads();
       const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
-      if (fast) {
-        for (int i = 0; i < nv8; i += 8) {
+      for (int g0 = 0; g0 < nv8; g0 += 32) {
+        const int g1 = min(nv8, g0 + 32);
+        if (a.boxed) {  // warp-uniform: 32 i rows (their box) against this warp's 64 j rows
+          const float* ib = (MODE == MODE_COUNT ? a.blkbox32 : a.flbox32) + (int64_t)((s0 + g0) / 32) * 2 * M;
+          bool none = false, all = true, strict = false;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float v[M];
-#pragma unroll
-            for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
-            Chain<M>::le_cnt(v, fa, ca);
-            Chain<M>::le_cnt(v, fb, cb);
+          for (int k = 0; k < M; ++k) {
+            const float imn = __ldg(ib + k), imx = __ldg(ib + M + k);
+            none |= imn > wjmx[k];
+            all &= imx <= wjmn[k];
+            strict |= imx < wjmn[k];
+          }
+          if (none) continue;
+          if (all && strict) {
+            const float cnt = (float)min(32, nv - g0);
+            ca += cnt;
+            cb += cnt;
+            continue;
           }
         }
-      } else {
-        for (int i = 0; i < nv8; i += 8) {
+        if (fast) {
+          for (int i = g0; i < g1; i += 8) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float v[M];
+            for (int u = 0; u < 8; ++u) {
+              float v[M];
 #pragma unroll
-            for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
-            Chain<M>::dom_cnt(v, fa, ca);
-            Chain<M>::dom_cnt(v, fb, cb);
+              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+              Chain<M>::le_cnt(v, fa, ca);
+              Chain<M>::le_cnt(v, fb, cb);
+            }
+          }
+        } else {
+          for (int i = g0; i < g1; i += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              float v[M];
+#pragma unroll
+              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+              Chain<M>::dom_cnt(v, fa, ca);
+              Chain<M>::dom_cnt(v, fb, cb);
+            }
           }
         }
       }
@@ -303,6 +336,11 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
         for (int o = 16; o > 0; o >>= 1) {
           mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
           mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+        }
+        if ((threadIdx.x & 31) == 0 && threadIdx.x < STREAM_BLK) {
+          const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + (threadIdx.x >> 5);
+          a.flbox32[q32 * 2 * a.m + k] = mn;
+          a.flbox32[q32 * 2 * a.m + a.m + k] = mx;
         }
         if ((threadIdx.x & 31) == 0) {
           sMax[threadIdx.x >> 5] = mx;
@@ -446,6 +484,11 @@ __global__ void __launch_bounds__(MORTON_THREADS) k_presort_morton(MortonArgs a)
       for (int o = 16; o > 0; o >>= 1) {
         mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
         mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+      }
+      if (lane == 0 && k >= 0 && tid < STREAM_BLK) {
+        const int64_t q32 = (int64_t)b * (STREAM_BLK / 32) + (tid >> 5);
+        a.blkbox32[q32 * 2 * m + k] = mn;
+        a.blkbox32[q32 * 2 * m + m + k] = mx;
       }
       if (lane == 0) {
         sRed[0][tid >> 5] = mn;

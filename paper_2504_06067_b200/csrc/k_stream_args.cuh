@@ -47,6 +47,8 @@ struct StreamArgs {
   int boxed;
   float* blkbox;         // nb x 2 x m: per 256-row block min[m], max[m]
   float* flbox;          // nb x 2 x m: per 256-entry front-list chunk
+  float* blkbox32;       // ceil(R/32) x 2 x m: per 32-row group
+  float* flbox32;        // ceil(R/32) x 2 x m: per 32-entry front-list group
 };
 
 // Morton presort of the boxed mode (F -> perm, FS, SS, S block range, boxes)
@@ -64,6 +66,7 @@ struct MortonArgs {
   float* blkmin;
   float* blkmax;
   float* blkbox;
+  float* blkbox32;
   GridCtx g;
 };
 
