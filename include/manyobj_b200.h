@@ -217,12 +217,19 @@ typedef struct mo_step_args {
   int32_t shard_rank;
   int32_t shard_count;
   int32_t pad2;
-  /* Optional lattice pruning of the association (exact; see k_assoc_lattice):
-   * for a single-layer Das-Dennis set of H divisions and m <= 4, `lattice`
-   * maps (k_0, ..., k_{m-2}) (mixed radix H+1, k_0 most significant) to the
-   * reference-point index of k/H; -1 marks k outside the simplex.  NULL =
-   * full scan.  lattice_r: box radius in lattice steps (0 = default 6). */
-  const int32_t* lattice;
+  /* Optional lattice pruning of the association (exact; see k_assoc_lattice),
+   * for a single-layer Das-Dennis set of H divisions and m <= 5.  Lattice
+   * index of k = (k_0, ..., k_{m-2}) in mixed radix H+1, k_0 most significant.
+   *   lattice_z:     (H+1)^(m-1) x m FP32: zhat of the point k/H at its
+   *                  lattice index (entries outside the simplex unused);
+   *   lattice_index: w: lattice index of every reference point;
+   *   lattice_pos:   (H+1)^(m-1) int32 scratch (the step writes the shuffled
+   *                  position of every point there).
+   * NULL lattice_z = full scan.  lattice_r: box radius in lattice steps
+   * (0 = default: 6 at m <= 3, 4 at m = 4, 3 at m = 5). */
+  const float* lattice_z;
+  const int32_t* lattice_index;
+  int32_t* lattice_pos;
   int32_t lattice_H;
   int32_t lattice_r;
 } mo_step_args;

@@ -43,7 +43,8 @@ class StepArgs(ctypes.Structure):
         ("ideal", c_vp), ("ranks", c_vp), ("info", c_vp), ("workspace", c_vp), ("workspace_bytes", c_sz),
         ("generation_dev", c_vp),
         ("sort_mode", c_i32), ("shard_rank", c_i32), ("shard_count", c_i32), ("pad2", c_i32),
-        ("lattice", c_vp), ("lattice_H", c_i32), ("lattice_r", c_i32),
+        ("lattice_z", c_vp), ("lattice_index", c_vp), ("lattice_pos", c_vp), ("lattice_H", c_i32),
+        ("lattice_r", c_i32),
     ]
 
 

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   for (int j = gtid; j < w; j += gthreads) {
     const int p = (int)prp((uint32_t)j, sKr, sSr, sRr, (uint32_t)w);
     a.pos_ref[j] = p;
+    if (a.lat_pos) a.lat_pos[__ldg(a.lat_index + j)] = p;
     a.perm_ref[p] = j;
     if (a.rho) {
       a.rho[j] = 0;
@@ -341,27 +342,33 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
 
 // ------------------------------------------------- lattice-pruned association
 //
-// Single-layer Das-Dennis sets (z = k/H, k integer, sum k = H) at m <= 4: the
+// Single-layer Das-Dennis sets (z = k/H, k integer, sum k = H) at m <= 5: the
 // direction with the largest key t = f.zhat lies near the simplex projection
-// u = f / sum(f).  A thread evaluates the canonical key (same arithmetic and
-// tie-break as assoc_item) on the lattice points with |k_i - u_i H| < r for
-// i < m-1, found through a dense (k_0..k_{m-2}) -> index table, then
-// certifies the winner: every point outside that box has ||z - u|| >= r/H,
-// hence sin(angle) >= ||z - u|| / sqrt(m) (z, u on the simplex, ||z|| <= 1),
-// hence an FP32 key <= ||f|| sqrt(1 - (r/H)^2 / m) (1 + (m + 2) 2^-24): all
-// terms are nonnegative, so the m roundings of the products / sums and the
-// FP32 rounding of zhat perturb the key by at most (m + 1) 2^-24 relative.  A winner above that bound is the
+// u = f / sum(f).  A group of LPR lanes evaluates the canonical key (same
+// arithmetic and tie-break as assoc_item) on the lattice points with
+// |k_i - u_i H| < r for i < m-1, reading the directions from a static copy
+// in lattice order (zl) and their shuffled positions from lat_pos (scattered
+// by k_prep every generation), so no load depends on another.  The winner is
+// then certified: every point outside the box has ||z - u|| >= r/H, and the
+// distance from u to the line through z is >= ||z - u|| / (sqrt(m) ||z||)
+// (the line crosses the simplex plane at angle acos(1 / (sqrt(m) ||z||))),
+// so sin(angle) >= (r/H) / (sqrt(m) ||u||) with ||z|| <= 1; its FP32 key is
+// then <= ||f|| cos(angle) (1 + (m + 2) 2^-24) -- every term is nonnegative,
+// so the m roundings of products / sums and the FP32 rounding of zhat move a
+// key by at most (m + 1) 2^-24 relative.  A winner above that bound is the
 // global argmax, ties included; rows that fail (or f = 0) go to a fallback
-// list that the full-scan k_assoc processes.  Exact: the result equals the
-// full scan bit for bit; the certificate only decides where it is computed.
-template <int M>
+// list for the full-scan k_assoc.  Exact: the result equals the full scan
+// bit for bit; the certificate only decides where it is computed.
+template <int M, int LPR>
 __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
   const int ncand = __ldcg(a.ctl);
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncand) return;
-  const int row = __ldcg(a.cand + c);
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = gt / LPR, sub = gt % LPR;
+  if ((gt & ~31) / LPR >= ncand) return;       // whole warp idle (no lane of it has a row)
+  const bool live = c < ncand;                   // idle groups still join the warp shuffles
+  const int row = live ? __ldcg(a.cand + c) : __ldcg(a.cand);
   const int H = a.lat_H, r = a.lat_r;
   float fn[M];
   double s = 0.0, nn = 0.0;
@@ -374,50 +381,61 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
     s += (double)v;
     nn += (double)v * (double)v;
   }
-  bool ok = s > 0.0 && isfinite(s);
+  bool ok = live && s > 0.0 && isfinite(s);
 #pragma unroll
   for (int k = 0; k < M; ++k) ok = ok && fn[k] >= 0.0f;
   float best = -__int_as_float(0x7f800000);
   int bp = 0x7fffffff;
   if (ok) {
-    int lo[M], hi[M];
+    int lo[M], ext[M];
+    int total = 1;
 #pragma unroll
     for (int k = 0; k < M - 1; ++k) {
       const double x = (double)fn[k] / s * (double)H;
       lo[k] = max(0, (int)floor(x - (double)r) + 1);
-      hi[k] = min(H, (int)ceil(x + (double)r) - 1);
+      const int hi = min(H, (int)ceil(x + (double)r) - 1);
+      ext[k] = max(0, hi - lo[k] + 1);
+      total *= ext[k];
     }
-    // odometer over the first m-1 lattice coordinates
-    int k_[M];
+    for (int q = sub; q < total; q += LPR) {
+      int rem = q, rest, idx = 0;
+      int kv[M];                           // mixed-radix decode of the box index, k_{m-2} fastest
 #pragma unroll
-    for (int k = 0; k < M - 1; ++k) k_[k] = lo[k];
-    bool more = true;
-    for (int k = 0; k < M - 1; ++k) more = more && lo[k] <= hi[k];
-    while (more) {
-      int rest = H, idx = 0;
+      for (int k = M - 2; k >= 0; --k) {
+        kv[k] = lo[k] + rem % ext[k];
+        rem /= ext[k];
+      }
+      rest = H;
 #pragma unroll
       for (int k = 0; k < M - 1; ++k) {
-        rest -= k_[k];
-        idx = idx * (H + 1) + k_[k];
+        rest -= kv[k];
+        idx = idx * (H + 1) + kv[k];
       }
-      if (rest >= 0) {
-        const int j = __ldg(a.lat_table + idx);
-        const int p = __ldg(a.pos_ref + j);
-        const float t = canon_dot<M>(fn, a.zs + (int64_t)p * M);
-        if (t > best || (t == best && p < bp)) {
-          best = t;
-          bp = p;
-        }
+      if (rest < 0) continue;
+      const int p = __ldg(a.lat_pos + idx);
+      const float t = canon_dot<M>(fn, a.lat_z + (int64_t)idx * M);
+      if (t > best || (t == best && p < bp)) {
+        best = t;
+        bp = p;
       }
-      int k = M - 2;
-      for (; k >= 0; --k) {
-        if (++k_[k] <= hi[k]) break;
-        k_[k] = lo[k];
-      }
-      more = k >= 0;
     }
-    const double rho = ((double)r - 1e-6) / (double)H;
-    const double bound = sqrt(nn) * sqrt(1.0 - rho * rho / (double)M) * (1.0 + (M + 2) * 5.9604644775390625e-8);
+  }
+  // group reduction: max key, lowest position on ties
+#pragma unroll
+  for (int o = LPR / 2; o > 0; o >>= 1) {
+    const float tb = __shfl_xor_sync(MO_FULL, best, o);
+    const int pb = __shfl_xor_sync(MO_FULL, bp, o);
+    if (tb > best || (tb == best && pb < bp)) {
+      best = tb;
+      bp = pb;
+    }
+  }
+  if (sub != 0 || !live) return;
+  if (ok) {
+    const double un = sqrt(nn) / s;                       // ||u||, u = f / sum(f)
+    double se = ((double)r - 1e-6) / (double)H / (sqrt((double)M) * un);
+    se = se < 1.0 ? se : 1.0;
+    const double bound = sqrt(nn) * sqrt(1.0 - se * se) * (1.0 + (M + 2) * 5.9604644775390625e-8);
     ok = bp != 0x7fffffff && (double)best > bound;
   }
   if (ok) {
@@ -869,11 +887,12 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   if (cudaMemsetAsync(a.fb_ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
   if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
     return MO_ERR_CUDA;
-  const unsigned blocks = (unsigned)ceil_div(R, 256);
+  // lanes per candidate row: enough to cover the box with few points each
   switch (m) {
-    case 2: k_assoc_lattice<2><<<blocks, 256, 0, s>>>(a); break;
-    case 3: k_assoc_lattice<3><<<blocks, 256, 0, s>>>(a); break;
-    case 4: k_assoc_lattice<4><<<blocks, 256, 0, s>>>(a); break;
+    case 2: k_assoc_lattice<2, 1><<<(unsigned)ceil_div(R, 256), 256, 0, s>>>(a); break;
+    case 3: k_assoc_lattice<3, 8><<<(unsigned)ceil_div(R * 8, 256), 256, 0, s>>>(a); break;
+    case 4: k_assoc_lattice<4, 32><<<(unsigned)ceil_div(R * 32, 256), 256, 0, s>>>(a); break;
+    case 5: k_assoc_lattice<5, 32><<<(unsigned)ceil_div(R * 32, 256), 256, 0, s>>>(a); break;
     default: return MO_ERR_PARAM;
   }
   MO_CHECK_LAUNCH();

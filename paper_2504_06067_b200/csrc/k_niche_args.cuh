@@ -40,6 +40,8 @@ struct PrepArgs {
   uint8_t* prom;
   int* lvl;   // 2 * LVL_BINS level histogram
   int* sctl;  // 16 select counters
+  const int* lat_index;  // nullable: lattice index of every reference point (lattice-pruned association)
+  int* lat_pos;          // lat_pos[lat_index[j]] = shuffled position of j
 };
 
 constexpr int LVL_BINS = 1024;
@@ -61,7 +63,8 @@ struct AssocArgs {
   int zbeg, zend;        // shuffled reference positions handled by this launch (shard range)
   // lattice pruning (k_assoc_lattice): dense (k_0..k_{m-2}) -> reference index table, H, box radius;
   // rows it cannot certify are appended to fb_cand (count fb_ctl[0]) for the full scan
-  const int* lat_table;
+  const float* lat_z;    // (H+1)^(m-1) x m: unit directions in lattice order (static)
+  const int* lat_pos;    // (H+1)^(m-1): shuffled position of each lattice point (k_prep, per generation)
   int lat_H, lat_r;
   const int* pos_ref;
   int* fb_cand;

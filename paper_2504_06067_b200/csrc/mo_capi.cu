@@ -178,6 +178,8 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.prom = at<uint8_t>(ws, L.prom);
   a.lvl = at<int>(ws, L.lvl);
   a.sctl = at<int>(ws, L.sctl);
+  a.lat_index = nullptr;
+  a.lat_pos = nullptr;
   return a;
 }
 
@@ -276,6 +278,9 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
                            at<int>(ws, L.rank_pos), ps.trace, s);
 }
 
+// box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
+static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 4 : 3); }
+
 static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cudaStream_t s) {
   const int64_t n = a->n, R = 2 * n, w = a->w;
   const int m = a->m;
@@ -283,6 +288,10 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   PrepArgs pa = prep_args(L, ws, a->FR, R, m, w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
                           nullptr, PREP_FULL);
   pa.gen_ptr = a->generation_dev;
+  if (a->lattice_z && m >= 2 && m <= 5) {
+    pa.lat_index = a->lattice_index;
+    pa.lat_pos = a->lattice_pos;
+  }
   if (mask & MO_PHASE_NICHE_PREP) MO_TRY(launch_prep(pa, s));
   if (mask & MO_PHASE_NICHE_ASSOC) {
   const int G = shards_of(a->shard_count);
@@ -299,13 +308,14 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.akey = pa.akey;
   aa.zbeg = (int)(w * a->shard_rank / G);
   aa.zend = (int)(w * (a->shard_rank + 1) / G);
-  aa.lat_table = a->lattice;
+  aa.lat_z = a->lattice_z;
+  aa.lat_pos = a->lattice_pos;
   aa.lat_H = a->lattice_H;
-  aa.lat_r = a->lattice_r > 0 ? a->lattice_r : 6;
+  aa.lat_r = a->lattice_r > 0 ? a->lattice_r : default_lattice_r(m);
   aa.pos_ref = pa.pos_ref;
   aa.fb_cand = at<int>(ws, L.fcand);
   aa.fb_ctl = at<int>(ws, L.fctl);
-  if (a->lattice && m >= 2 && m <= 4)
+  if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
   else
     MO_TRY(launch_assoc(aa, m, R, s));
@@ -419,7 +429,8 @@ static int check_step_args(const mo_step_args* a) {
   if (a->problem < MO_DTLZ1 || a->problem > MO_DTLZ7) return MO_ERR_PARAM;
   if (a->sort_mode != MO_SORT_BITS && a->sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
   if (a->shard_count < 0 || a->shard_rank < 0 || a->shard_rank >= shards_of(a->shard_count)) return MO_ERR_PARAM;
-  if (a->lattice && (a->lattice_H < 1 || a->lattice_r < 0)) return MO_ERR_PARAM;
+  if (a->lattice_z && (a->lattice_H < 1 || a->lattice_r < 0 || !a->lattice_index || !a->lattice_pos))
+    return MO_ERR_PARAM;
   return MO_OK;
 }
 
@@ -578,7 +589,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
   aa.akey = pa.akey;
   aa.zbeg = 0;
   aa.zend = (int)w;
-  aa.lat_table = nullptr;
+  aa.lat_z = nullptr;
   MO_TRY(launch_assoc(aa, m, R, s));
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));

@@ -113,7 +113,7 @@ class Engine:
         with torch.cuda.device(self.dev):
             L = _lib.lib()
             self.zhat = torch.from_numpy(zh).to(self.dev)
-            self.lattice, self.lattice_H = self._lattice_table(prune)
+            self.lattice, self.lattice_H = self._lattice_table(prune)   # (z, index, pos) or None
             self.XR = [torch.empty((2 * n, d), dtype=torch.float32, device=self.dev) for _ in range(2)]
             self.FR = [torch.empty((2 * n, m), dtype=torch.float32, device=self.dev) for _ in range(2)]
             self.ranks = torch.empty(2 * n, dtype=torch.int32, device=self.dev)
@@ -143,20 +143,24 @@ class Engine:
         (single-layer Das-Dennis, m <= 4).  prune: "auto" (when it pays), True (whenever legal), False."""
         cfg, m, w = self.cfg, self.cfg.m, self.w
         Ho, Hi = cfg.reference_points if cfg.reference_points is not None else refpoints.choose_divisions(m, cfg.n)
-        legal = Hi == 0 and 2 <= m <= 4 and (Ho + 1) ** (m - 1) <= (1 << 26)
+        legal = Hi == 0 and 2 <= m <= 5 and (Ho + 1) ** (m - 1) <= (1 << 26)
         if prune is False or not legal:
             if prune is True and not legal:
-                raise ConfigError("prune", "lattice pruning needs a single-layer Das-Dennis set and m <= 4")
+                raise ConfigError("prune", "lattice pruning needs a single-layer Das-Dennis set and m <= 5")
             return None, 0
-        if prune == "auto" and 4 * 11 ** (m - 1) >= w:    # box of (2r-1)^(m-1) points, r = 6
+        r = 6 if m <= 3 else (4 if m == 4 else 3)        # default_lattice_r (mo_capi.cu)
+        # a box point costs ~30x a full-scan point (decode + gathered loads): measured break-even
+        if prune == "auto" and 32 * (2 * r - 1) ** (m - 1) >= w:    # box of (2r-1)^(m-1) points
             return None, 0
         k = np.rint(np.asarray(self.Z, np.float64) * Ho).astype(np.int64)
         idx = np.zeros(w, np.int64)
         for i in range(m - 1):
             idx = idx * (Ho + 1) + k[:, i]
-        table = np.full((Ho + 1) ** (m - 1), -1, np.int32)
-        table[idx] = np.arange(w, dtype=np.int32)
-        return torch.from_numpy(table).to(self.dev), Ho
+        size = (Ho + 1) ** (m - 1)
+        zl = np.zeros((size, m), np.float32)
+        zl[idx] = self.zhat.cpu().numpy()              # the same FP32 directions the full scan reads
+        dev = lambda x: torch.from_numpy(x).to(self.dev)
+        return (dev(zl), dev(idx.astype(np.int32)), torch.zeros(size, dtype=torch.int32, device=self.dev)), Ho
 
     def _choose_sort(self, sort):
         if sort not in ("auto", "bits", "stream"):
@@ -193,7 +197,8 @@ class Engine:
         a.generation_dev = self.gen_dev.data_ptr() if use_dev_gen else None
         a.sort_mode = self.sort_mode
         a.shard_rank, a.shard_count = self.shard_rank, self.shard_count
-        a.lattice = self.lattice.data_ptr() if self.lattice is not None else None
+        if self.lattice is not None:
+            a.lattice_z, a.lattice_index, a.lattice_pos = (t.data_ptr() for t in self.lattice)
         a.lattice_H = self.lattice_H
         a.lattice_r = 0
         return a

@@ -127,7 +127,8 @@ def test_stream_engine_profile_and_poll(M):
 
 @pytest.mark.parametrize("kind,n,m,d,gens", [("DTLZ7", 3000, 3, 22, 6), ("DTLZ1", 2000, 3, 7, 6),
                                              ("DTLZ2", 4000, 4, 13, 5), ("DTLZ5", 1000, 2, 11, 5),
-                                             ("DTLZ4", 5000, 3, 12, 5)])
+                                             ("DTLZ4", 5000, 3, 12, 5), ("DTLZ2", 10000, 5, 14, 4),
+                                             ("DTLZ1", 6000, 5, 9, 4)])
 def test_lattice_pruned_association_equals_full_scan(M, kind, n, m, d, gens):
     cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=6)
     a = M.engine.Engine(cfg, prune=False)
