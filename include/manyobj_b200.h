@@ -294,6 +294,26 @@ int mo_stream_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_
  * objectives already in FR -- the part of mo_step after variation. */
 int mo_select(const mo_step_args* args, void* stream_);
 
+/* -------------------------------------------------------- metrics (L5) */
+
+/* metrics.igd: mean over the nr reference points (nr x m)
+ * of the Euclidean distance to the nearest of the nf front rows (nf x m),
+ * FP64 arithmetic; *out (device double) receives the value.  Deterministic.
+ * Workspace: mo_igd_workspace_bytes(nr).  Empty input -> MO_ERR_EMPTY. */
+size_t mo_igd_workspace_bytes(int64_t nr);
+int mo_igd(const float* front, int64_t nf, const float* ref, int64_t nr, int32_t m, double* out, void* workspace,
+           size_t workspace_bytes, void* stream_);
+
+/* metrics.hv Monte-Carlo branch (m > 3): `samples`
+ * Philox-seeded points uniform in the box [lower, upper] (device double[m]);
+ * *hits_out (device uint64) = how many are weakly dominated by some front
+ * row.  hv = volume(box) * hits / samples (the caller discards front rows
+ * that do not dominate the reference point first).  Workspace:
+ * mo_hv_mc_workspace_bytes(samples). */
+size_t mo_hv_mc_workspace_bytes(int64_t samples);
+int mo_hv_mc(const float* front, int64_t nf, int32_t m, const double* lower, const double* upper, int64_t samples,
+             uint64_t seed, unsigned long long* hits_out, void* workspace, size_t workspace_bytes, void* stream_);
+
 /* ---------------------------------------------------- measurement helper */
 
 /* Issue-rate microbenchmark for the roofline of the CUDA-core kernels (not a

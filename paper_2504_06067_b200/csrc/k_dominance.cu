@@ -211,20 +211,22 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
   __syncthreads();
   uint32_t wa[8], wb[8];
   if (fast) {
+    // sign-of-difference chains (FMA pipe); the 32 sign bits of a chunk are funnel-shifted into
+    // a word, i = 31 first so that i lands on bit i, then inverted (set = dominated)
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
       uint32_t acca = 0, accb = 0;
 #pragma unroll
-      for (int b = 0; b < 32; ++b) {
+      for (int b = 31; b >= 0; --b) {
         const float* fi = sFi + (c * 32 + b) * MP;
         float v[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) v[k] = fi[k];
-        Chain<M>::le(v, fa, acca, 1u << b);
-        Chain<M>::le(v, fb, accb, 1u << b);
+        acca = __funnelshift_l(le_sign<M>(v, fa), acca, 1);
+        accb = __funnelshift_l(le_sign<M>(v, fb), accb, 1);
       }
-      wa[c] = acca;
-      wb[c] = accb;
+      wa[c] = ~acca;
+      wb[c] = ~accb;
     }
   } else {
 #pragma unroll 1
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
       const int i = __ldcg(a.valA + pos);
       a.perm[pos] = i;
       a.SS[pos] = ord2f(__ldcg(a.keyB + i));
-      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = __fadd_rn(a.F[(int64_t)i * m + k], 0.0f);  // -0 -> +0
     }
     // bucket ends for P4 (the atomic path leaves fill[q] at the end of bucket q)
     for (int q = gtid; q < PRESORT_BUCKETS; q += gthreads) a.fill[q] += __ldcg(a.valB + q);
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
       const int pos = atomicAdd(&a.fill[q], 1);
       a.perm[pos] = i;
       a.SS[pos] = ord2f(__ldcg(a.keyB + i));
-      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = a.F[(int64_t)i * m + k];
+      for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = __fadd_rn(a.F[(int64_t)i * m + k], 0.0f);  // -0 -> +0
     }
   }
   grid_sync(a.g.bar);

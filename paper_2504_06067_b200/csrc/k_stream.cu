@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       e0 = c * STREAM_CHUNK * STREAM_BLK;
       e1 = min(fln, e0 + STREAM_CHUNK * STREAM_BLK);
     }
-    float ca = 0.0f, cb = 0.0f;
+    float ca = 0.0f, cb = 0.0f;   // predicated-FADD counts (full dominance chains)
+    int na = 0, nb2 = 0;          // popcount counts (sign-of-difference chains, box "all")
     for (int s0 = e0; s0 < e1; s0 += STREAM_BLK) {
       const int nv = min(STREAM_BLK, e1 - s0);
       if (a.boxed) {  // block-pair classification from the bounding boxes (uniform over the CTA)
@@ -233,23 +234,25 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
           }
           if (none) continue;
           if (all && strict) {
-            const float cnt = (float)min(32, nv - g0);
-            ca += cnt;
-            cb += cnt;
+            const int cnt = min(32, nv - g0);
+            na += cnt;
+            nb2 += cnt;
             continue;
           }
         }
         if (fast) {
-          for (int i = g0; i < g1; i += 8) {
+          // all 32 entries of the group (staging pads are +inf rows: never <= a finite row)
+          uint32_t acca = 0, accb = 0;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              float v[M];
+          for (int u = 0; u < 32; ++u) {
+            float v[M];
 #pragma unroll
-              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
-              Chain<M>::le_cnt(v, fa, ca);
-              Chain<M>::le_cnt(v, fb, cb);
-            }
+            for (int k = 0; k < M; ++k) v[k] = sFi[(g0 + u) * MP + k];
+            acca = __funnelshift_l(le_sign<M>(v, fa), acca, 1);
+            accb = __funnelshift_l(le_sign<M>(v, fb), accb, 1);
           }
+          na += __popc(~acca);
+          nb2 += __popc(~accb);
         } else {
           for (int i = g0; i < g1; i += 8) {
 #pragma unroll
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       }
       __syncthreads();
     }
-    const int ia = (int)ca, ib = (int)cb;
+    const int ia = (int)ca + na, ib = (int)cb + nb2;
     if (ja < a.R && ia) atomicAdd(a.cnt + ja, MODE == MODE_COUNT ? ia : -ia);
     if (jb < a.R && ib) atomicAdd(a.cnt + jb, MODE == MODE_COUNT ? ib : -ib);
   }
@@ -464,10 +467,10 @@ __global__ void __launch_bounds__(MORTON_THREADS) k_presort_morton(MortonArgs a)
     a.perm[p] = i;
     const float* f = a.F + (int64_t)i * m;
     float s = f[0];
-    a.FS[(int64_t)p * m] = f[0];
+    a.FS[(int64_t)p * m] = __fadd_rn(f[0], 0.0f);  // -0 -> +0 (the sign-of-difference chains rely on it)
     for (int k = 1; k < m; ++k) {
       s = __fadd_rn(s, f[k]);
-      a.FS[(int64_t)p * m + k] = f[k];
+      a.FS[(int64_t)p * m + k] = __fadd_rn(f[k], 0.0f);
     }
     a.SS[p] = s;
   }

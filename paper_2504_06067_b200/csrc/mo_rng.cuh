@@ -18,6 +18,7 @@ enum Stream : uint32_t {
   STREAM_PM = 4,
   STREAM_POP_SHUFFLE = 5,
   STREAM_REF_SHUFFLE = 6,
+  STREAM_HV = 7,   // Monte-Carlo hypervolume samples (metrics, not the generation)
 };
 constexpr uint32_t PAIR_SLOT = 0xffffffffu;
 constexpr int MAX_SHUFFLE_ROUNDS = 32 + 2 * 32;
