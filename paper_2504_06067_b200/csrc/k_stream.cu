@@ -75,39 +75,43 @@ __global__ void k_stream_reset(StreamArgs a) {
   if (gt < MO_INFO_COUNT) a.info[gt] = 0;
 }
 
+// Work items of owned block t: (j block, chunk of CHUNK i blocks / front-list entries).
+template <int MODE>
+__device__ __forceinline__ int block_items(const StreamArgs& a, int t, int fln) {
+  const int nb = nblocks(a.R);
+  const int b = owned_block(a, t);
+  if (b >= nb) return 0;
+  if (a.boxed) {
+    if (MODE == MODE_COUNT) return (nb + STREAM_CHUNK - 1) / STREAM_CHUNK;
+    if (__ldcg(a.ucnt + t) == 0) return 0;
+    return (fln + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
+  }
+  const int bend = block_bend(a, b);
+  if (MODE == MODE_COUNT) {
+    const int nib = (bend + STREAM_BLK - 1) / STREAM_BLK;
+    return (nib + STREAM_CHUNK - 1) / STREAM_CHUNK;
+  }
+  if (__ldcg(a.ucnt + t) == 0) return 0;
+  int lo = 0, hi = fln;  // fl entries with position < bend
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldcg(a.fl + mid) < bend) lo = mid + 1; else hi = mid;
+  }
+  return (lo + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
+}
+
 // One CTA: items per owned block, exclusive prefix into plan[0..T].
 template <int MODE>
 __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
   __shared__ int sh[40];
   const int tid = threadIdx.x;
   const bool done = __ldcg(a.ctl + SC_DONE) != 0;
-  const int nb = nblocks(a.R);
   const int fln = __ldcg(a.ctl + SC_FLN);
   const int per = (a.T + PLAN_THREADS - 1) / PLAN_THREADS;
   const int t0 = min(a.T, tid * per), t1 = min(a.T, t0 + per);
   int mine = 0;
   for (int t = t0; t < t1; ++t) {
-    const int b = owned_block(a, t);
-    int items = 0;
-    if (!done && b < nb && a.boxed) {
-      if (MODE == MODE_COUNT)
-        items = (nb + STREAM_CHUNK - 1) / STREAM_CHUNK;
-      else if (__ldcg(a.ucnt + t) > 0)
-        items = (fln + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
-    } else if (!done && b < nb) {
-      const int bend = block_bend(a, b);
-      if (MODE == MODE_COUNT) {
-        const int nib = (bend + STREAM_BLK - 1) / STREAM_BLK;
-        items = (nib + STREAM_CHUNK - 1) / STREAM_CHUNK;
-      } else if (__ldcg(a.ucnt + t) > 0) {
-        int lo = 0, hi = fln;  // fl entries with position < bend
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (__ldcg(a.fl + mid) < bend) lo = mid + 1; else hi = mid;
-        }
-        items = (lo + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
-      }
-    }
+    const int items = done ? 0 : block_items<MODE>(a, t, fln);
     a.plan[t] = items;  // temporarily the count
     mine += items;
   }
@@ -132,27 +136,29 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
 // only the m-long <= chain; others the full dominance chain (also rejects
 // i == j).  Counts accumulate with a predicated FADD (FMA pipe, exact below
 // 2^24) and land with one atomic per row per item.
+// The work loop of the tile sweep, shared by k_stream_tiles (one launch per
+// sweep) and k_stream_fused (all sweeps of a generation in one launch).
+// Items are pulled from `counter`; the item index is the counter value minus
+// `base`.  Arrays written earlier in the same fused launch (plan, fl, flmax,
+// flbox) are read through L2 (__ldcg).
 template <int M, int MODE>
-__global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
+__device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* sItem, int items, int fln,
+                                          int* counter, int base) {
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
-  __shared__ int sItem;
   const int tid = threadIdx.x;
-  const int items = __ldcg(a.ctl + SC_ITEMS);
-  const int fln = MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0;
   const float PINF = __int_as_float(0x7f800000);
   for (;;) {
-    if (tid == 0) sItem = atomicAdd(a.ctl + SC_WORK, 1);
+    if (tid == 0) *sItem = atomicAdd(counter, 1) - base;
     __syncthreads();
-    const int item = sItem;
+    const int item = *sItem;
     __syncthreads();
     if (item >= items) break;
     int lo = 0, hi = a.T;  // largest t with plan[t] <= item
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (__ldg(a.plan + mid) <= item) lo = mid; else hi = mid;
+      if (__ldcg(a.plan + mid) <= item) lo = mid; else hi = mid;
     }
-    const int t = lo, c = item - __ldg(a.plan + t);
+    const int t = lo, c = item - __ldcg(a.plan + t);
     const int bj = owned_block(a, t);
     const int j0 = bj * STREAM_BLK;
     // two adjacent rows per thread: a warp owns 64 consecutive positions (one j box per warp)
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
         bool none = false, all = true, strict = false;
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const float imn = __ldg(ib + k), imx = __ldg(ib + M + k);
+          const float imn = __ldcg(ib + k), imx = __ldcg(ib + M + k);
           const float jmn = __ldg(jb2 + k), jmx = __ldg(jb2 + M + k);
           none |= imn > jmx;
           all &= imx <= jmn;
@@ -211,12 +217,12 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
       }
       for (int e = tid; e < STREAM_BLK; e += ST_THREADS) {
         int src = -1;
-        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : __ldg(a.fl + s0 + e);
+        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : __ldcg(a.fl + s0 + e);
         float* dst = sFi + e * MP;
 #pragma unroll
         for (int k = 0; k < MP; ++k) dst[k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
       }
-      const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : __ldg(a.flmax + s0 / STREAM_BLK);
+      const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : __ldcg(a.flmax + s0 / STREAM_BLK);
       const bool fast = (MODE == MODE_COUNT && !a.boxed ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
       __syncthreads();
       const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
           bool none = false, all = true, strict = false;
 #pragma unroll
           for (int k = 0; k < M; ++k) {
-            const float imn = __ldg(ib + k), imx = __ldg(ib + M + k);
+            const float imn = __ldcg(ib + k), imx = __ldcg(ib + M + k);
             none |= imn > wjmx[k];
             all &= imx <= wjmn[k];
             strict |= imx < wjmn[k];
@@ -272,6 +278,15 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
     if (ja < a.R && ia) atomicAdd(a.cnt + ja, MODE == MODE_COUNT ? ia : -ia);
     if (jb < a.R && ib) atomicAdd(a.cnt + jb, MODE == MODE_COUNT ? ib : -ib);
   }
+}
+
+template <int M, int MODE>
+__global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
+  __shared__ int sItem;
+  tiles_run<M, MODE>(a, sFi, &sItem, __ldcg(a.ctl + SC_ITEMS), MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0,
+                     a.ctl + SC_WORK, 0);
 }
 
 // Owned unranked rows with no unranked dominator left -> local mask slice.
@@ -385,6 +400,219 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
 __global__ void k_stream_end(StreamArgs a) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   for (int p = gt; p < a.R; p += gs) {
+    const int r = __ldcg(a.rank_pos + p);
+    a.ranks[__ldg(a.perm + p)] = r == MO_RANK_UNRANKED ? MO_RANK_DROPPED : r;
+  }
+}
+
+// ------------------------------------------------- single-GPU fused sweep loop
+//
+// k_stream_fused: the whole streamed sort of one generation (G = 1) in one
+// cooperative launch -- reset, dominator counts, front 0, then per front:
+// ordered front list from the mask (grid scan), chunk ranges / boxes, the
+// DEC plan (per-block item counts + grid scan), the DEC sweep, the next mask
+// -- with grid barriers instead of host round trips, so a generation is one
+// graph-capturable mo_step.  Work items are pulled from one counter that
+// keeps counting across sweeps: every CTA overshoots each sweep exactly once,
+// so sweep s starts at base_s = sum_{r<s} (items_r + gridDim.x).
+
+// grid_scan that calls emit(e, prefix) for EVERY e (zero values included).
+template <class ValueF, class EmitF>
+__device__ int grid_scan_all(GridCtx& g, int64_t N, ValueF value, EmitF emit, int* sh) {
+  const int G = gridDim.x, b = blockIdx.x;
+  int* part = g.part + g.parity * (G + 1);
+  g.parity ^= 1;
+  const int64_t chunk = ceil_div(N, (int64_t)G);
+  const int64_t lo = min((int64_t)b * chunk, N), hi = min(lo + chunk, N);
+  int cnt = 0;
+  for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) cnt += value(e);
+  int tot;
+  block_excl_scan(cnt, sh, &tot);
+  if (threadIdx.x == 0) part[b] = tot;
+  grid_sync(g.bar);
+  int pre = 0, all = 0;
+  for (int q = threadIdx.x; q < G; q += blockDim.x) {
+    const int v = __ldcg(part + q);
+    all += v;
+    if (q < b) pre += v;
+  }
+  int offset, total;
+  block_excl_scan(pre, sh, &offset);
+  block_excl_scan(all, sh, &total);
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t e = base + threadIdx.x;
+    const int v = (e < hi) ? value(e) : 0;
+    int t;
+    const int p = block_excl_scan(v, sh, &t);
+    if (e < hi) emit(e, offset + p);
+    offset += t;
+  }
+  return total;
+}
+
+// plan[t] = exclusive prefix of the items of owned block t; returns the total (all CTAs).
+__device__ __noinline__ int plan_all(const StreamArgs& a, GridCtx& g, int mode, int fln, int* sh) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  for (int t = gt; t < a.T; t += gs)
+    a.plan[t] = mode == MODE_COUNT ? block_items<MODE_COUNT>(a, t, fln) : block_items<MODE_DEC>(a, t, fln);
+  grid_sync(g.bar);
+  const int total = grid_scan_all(
+      g, a.T, [&](int64_t t) { return __ldcg(a.plan + t); }, [&](int64_t t, int pre) { a.plan[t] = pre; }, sh);
+  grid_sync(g.bar);   // every prefix written before any CTA searches the plan
+  return total;
+}
+
+__device__ void mark_all(const StreamArgs& a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)a.T * (STREAM_BLK / 32);
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t gw = w0; gw < nw; gw += ws) {
+    const int t = (int)(gw / (STREAM_BLK / 32)), w8 = (int)(gw % (STREAM_BLK / 32));
+    const int p = owned_block(a, t) * STREAM_BLK + w8 * 32 + lane;
+    const bool in = p < a.R && __ldcg(a.rank_pos + p) == MO_RANK_UNRANKED && __ldcg(a.cnt + p) == 0;
+    const uint32_t word = __ballot_sync(MO_FULL, in);
+    if (lane == 0) a.mask_local[gw] = word;
+  }
+}
+
+// max S and (boxed) bounding boxes of every 256- and 32-entry chunk of fl[0, fk)
+template <int M>
+__device__ void chunk_boxes(const StreamArgs& a, int fk, float* sRedMin, float* sRedMax) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nq = (fk + STREAM_BLK - 1) / STREAM_BLK;
+  for (int q = blockIdx.x; q < nq; q += gridDim.x) {
+    int p[2];
+    bool act[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {   // entry q*256 + tid + 128u: warp w covers 32-groups w and w+4
+      const int e = q * STREAM_BLK + tid + ST_THREADS * u;
+      act[u] = e < fk;
+      p[u] = act[u] ? __ldcg(a.fl + e) : 0;
+    }
+    for (int k = -1; k < (a.boxed ? M : 0); ++k) {
+      float mn = __int_as_float(0x7f800000), mx = -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        float gmn = __int_as_float(0x7f800000), gmx = -__int_as_float(0x7f800000);
+        if (act[u]) {
+          const float v = k < 0 ? __ldg(a.SS + p[u]) : __ldg(a.FS + (int64_t)p[u] * M + k);
+          gmn = v;
+          gmx = v;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          gmn = fminf(gmn, __shfl_xor_sync(MO_FULL, gmn, o));
+          gmx = fmaxf(gmx, __shfl_xor_sync(MO_FULL, gmx, o));
+        }
+        if (k >= 0 && lane == 0) {
+          const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + wid + 4 * u;
+          a.flbox32[q32 * 2 * M + k] = gmn;
+          a.flbox32[q32 * 2 * M + M + k] = gmx;
+        }
+        mn = fminf(mn, gmn);
+        mx = fmaxf(mx, gmx);
+      }
+      if (lane == 0) {
+        sRedMin[wid] = mn;
+        sRedMax[wid] = mx;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < ST_THREADS / 32; ++w) {
+          mn = fminf(mn, sRedMin[w]);
+          mx = fmaxf(mx, sRedMax[w]);
+        }
+        if (k < 0) {
+          a.flmax[q] = mx;
+        } else {
+          a.flbox[(int64_t)q * 2 * M + k] = mn;
+          a.flbox[(int64_t)q * 2 * M + M + k] = mx;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __noinline__ int apply_front_local(const StreamArgs& a, GridCtx& g, int64_t N, int k, int* sh) {
+  return grid_scan(
+      g, N, [&](int64_t e) { return __popc(__ldcg(a.mask_local + e)); },
+      [&](int64_t e, int pre) {
+        uint32_t wv = __ldcg(a.mask_local + e);
+        const int base_p = (int)(e * 32);
+        atomicSub(a.ucnt + (int)(e / (STREAM_BLK / 32)), __popc(wv));
+        int r = pre;
+        while (wv) {
+          const int bit = __ffs(wv) - 1;
+          wv &= wv - 1;
+          a.fl[r++] = base_p + bit;
+          a.rank_pos[base_p + bit] = k;
+        }
+      },
+      sh);
+}
+
+template <int M>
+__global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
+  constexpr int MP = (M + 3) & ~3;
+  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
+  __shared__ int sItem;
+  __shared__ int sh[40];
+  __shared__ float sRedMin[ST_THREADS / 32], sRedMax[ST_THREADS / 32];
+  GridCtx g = a.gc;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int R = a.R;
+  // reset
+  for (int p = gt; p < R; p += gs) {
+    a.rank_pos[p] = MO_RANK_UNRANKED;
+    a.cnt[p] = 0;
+  }
+  for (int t = gt; t < a.T; t += gs) {
+    const int b = owned_block(a, t);
+    a.ucnt[t] = max(0, min(R, (b + 1) * STREAM_BLK) - b * STREAM_BLK);
+  }
+  if (gt < MO_INFO_COUNT && gt != MO_INFO_ASSOC_FALLBACK) a.info[gt] = 0;
+  if (gt == 0) a.ctl[SC_WORK] = 0;
+  grid_sync(g.bar);
+  // dominator counts, front 0
+  int base = 0;
+  int items = plan_all(a, g, MODE_COUNT, 0, sh);
+  tiles_run<M, MODE_COUNT>(a, sFi, &sItem, items, 0, a.ctl + SC_WORK, base);
+  base += items + (int)gridDim.x;
+  grid_sync(g.bar);
+  mark_all(a);
+  grid_sync(g.bar);
+  const int nb = nblocks(R);
+  const int64_t N = (int64_t)nb * (STREAM_BLK / 32);
+  int64_t cum = 0;
+  for (int k = 0;; ++k) {
+    // front k: ordered list, ranks, unranked counts per block (mask_full aliases mask_local, G = 1)
+    const int fk = apply_front_local(a, g, N, k, sh);
+    const int64_t sel = cum;
+    cum += fk;
+    if (cum >= a.stop_at || fk == 0) {
+      if (gt == 0) {
+        a.info[MO_INFO_L] = k;
+        a.info[MO_INFO_SELECTED] = (int)sel;
+        a.info[MO_INFO_K] = (int)(a.stop_at - sel);
+        a.info[MO_INFO_FL_SIZE] = fk;
+        a.info[MO_INFO_SKIPPED] = (sel + fk == a.stop_at) ? 1 : 0;
+        a.info[MO_INFO_ERROR] = (cum < a.stop_at) ? MO_ERR_INFEASIBLE : 0;
+        a.info[MO_INFO_NFRONTS] = k + 1;
+      }
+      break;
+    }
+    grid_sync(g.bar);            // fl / rank_pos / ucnt of front k visible
+    chunk_boxes<M>(a, fk, sRedMin, sRedMax);
+    items = plan_all(a, g, MODE_DEC, fk, sh);  // (its first barrier also publishes the chunk boxes)
+    tiles_run<M, MODE_DEC>(a, sFi, &sItem, items, fk, a.ctl + SC_WORK, base);
+    base += items + (int)gridDim.x;
+    grid_sync(g.bar);
+    mark_all(a);
+    grid_sync(g.bar);
+  }
+  grid_sync(g.bar);              // every rank_pos write of the last front done
+  for (int p = gt; p < R; p += gs) {
     const int r = __ldcg(a.rank_pos + p);
     a.ranks[__ldg(a.perm + p)] = r == MO_RANK_UNRANKED ? MO_RANK_DROPPED : r;
   }
@@ -632,6 +860,60 @@ int launch_stream_front(StreamArgs a, int k, cudaStream_t s) {
   MO_CHECK_LAUNCH();
   MO_TRY(launch_tiles<MODE_DEC>(a, s));
   return mark_launch(a, s);
+}
+
+int launch_stream_fused(StreamArgs a, cudaStream_t s) {
+  if (a.G != 1) return MO_ERR_PARAM;
+  static int blocks[17];
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaMemsetAsync(a.gc.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  a.gc.parity = 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(ST_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaSuccess;
+  switch (a.m) {
+#define MO_SF_CASE(MM)                                                                            \
+  case MM: {                                                                                      \
+    if (!blocks[MM]) {                                                                            \
+      int per = 0;                                                                                \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fused<MM>, ST_THREADS, 0);     \
+      per = per > 6 ? 6 : (per < 1 ? 1 : per);   /* grid <= MAX_GRID (GridCtx part) */        \
+      blocks[MM] = sms * per;                                                                     \
+    }                                                                                             \
+    cfg.gridDim = dim3(blocks[MM]);                                                               \
+    e = cudaLaunchKernelEx(&cfg, k_stream_fused<MM>, a);                                          \
+    break;                                                                                        \
+  }
+    MO_SF_CASE(2)
+    MO_SF_CASE(3)
+    MO_SF_CASE(4)
+    MO_SF_CASE(5)
+    MO_SF_CASE(6)
+    MO_SF_CASE(7)
+    MO_SF_CASE(8)
+    MO_SF_CASE(9)
+    MO_SF_CASE(10)
+    MO_SF_CASE(11)
+    MO_SF_CASE(12)
+    MO_SF_CASE(13)
+    MO_SF_CASE(14)
+    MO_SF_CASE(15)
+    MO_SF_CASE(16)
+#undef MO_SF_CASE
+    default:
+      return MO_ERR_PARAM;
+  }
+  if (e != cudaSuccess) return MO_ERR_CUDA;
+  MO_CHECK_LAUNCH();
+  return MO_OK;
 }
 
 int launch_stream_end(StreamArgs a, cudaStream_t s) {

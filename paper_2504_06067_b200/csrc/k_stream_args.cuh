@@ -74,5 +74,6 @@ int launch_presort_morton(const MortonArgs& a, cudaStream_t s);
 int launch_stream_begin(StreamArgs a, cudaStream_t s);
 int launch_stream_front(StreamArgs a, int k, cudaStream_t s);
 int launch_stream_end(StreamArgs a, cudaStream_t s);
+int launch_stream_fused(StreamArgs a, cudaStream_t s);
 
 }  // namespace mo

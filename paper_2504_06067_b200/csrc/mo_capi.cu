@@ -350,6 +350,9 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   return launch_select(sa, s);
 }
 
+static int stream_presort(const mo_step_args* a, const Layout& L, cudaStream_t s);
+static StreamArgs stream_args(const mo_step_args* a, const Layout& L);
+
 static Layout step_layout(const mo_step_args* a) {
   return make_layout(2 * a->n, a->w, a->m, a->sort_mode, shards_of(a->shard_count));
 }
@@ -359,14 +362,22 @@ static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
   Layout L = step_layout(a);
   MO_TRY(check_ws(L, a->workspace, a->workspace_bytes));
   if (mask & MO_PHASE_NICHE) mask |= MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH;
-  if ((mask & MO_PHASE_SORT) && a->sort_mode != MO_SORT_BITS) return MO_ERR_PARAM;  // host-driven fronts
+  // the streamed sort runs device-side in one launch on one shard; sharded fronts are host-driven
+  if ((mask & MO_PHASE_SORT) && a->sort_mode != MO_SORT_BITS && shards_of(a->shard_count) > 1) return MO_ERR_PARAM;
   if ((mask & (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH)) == (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH) &&
       shards_of(a->shard_count) > 1)
     return MO_ERR_PARAM;  // the akey max-reduction across shards sits between the two
   if (mask & MO_PHASE_VARY)
     MO_TRY(launch_vary_eval(a->problem, a->XR, n, a->d, a->m, a->seed, a->generation, a->generation_dev, a->var,
                             a->XR + n * a->d, a->FR + n * a->m, nullptr, nullptr, s));
-  if (mask & MO_PHASE_SORT) MO_TRY(sort_phase(a, L, s));
+  if (mask & MO_PHASE_SORT) {
+    if (a->sort_mode == MO_SORT_BITS) {
+      MO_TRY(sort_phase(a, L, s));
+    } else {
+      MO_TRY(stream_presort(a, L, s));
+      MO_TRY(launch_stream_fused(stream_args(a, L), s));
+    }
+  }
   if (mask & (MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH))
     MO_TRY(niche_phase(a, L, mask, s));
   return MO_OK;
@@ -412,6 +423,33 @@ static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   sa.blkbox32 = at<float>(ws, L.blkbox32);
   sa.flbox32 = at<float>(ws, L.flbox32);
   return sa;
+}
+
+// Position space of the streamed sort: Morton order + boxes (m <= 4) or S slabs.
+static int stream_presort(const mo_step_args* a, const Layout& L, cudaStream_t s) {
+  if (!stream_boxed(a->m)) return launch_presort(presort_args(a, L), s);
+  void* ws = a->workspace;
+  MortonArgs ma;
+  ma.F = a->FR;
+  ma.R = (int)(2 * a->n);
+  ma.m = a->m;
+  ma.keyA = at<uint32_t>(ws, L.keyA);
+  ma.valA = at<int>(ws, L.valA);
+  ma.tkey = at<uint32_t>(ws, L.tkey);
+  ma.tval = at<int>(ws, L.tval);
+  ma.cbox = at<unsigned>(ws, L.cbox);
+  ma.perm = at<int>(ws, L.perm_sort);
+  ma.FS = at<float>(ws, L.FS);
+  ma.SS = at<float>(ws, L.SS);
+  ma.blkmin = at<float>(ws, L.blkmin);
+  ma.blkmax = at<float>(ws, L.blkmax);
+  ma.blkbox = at<float>(ws, L.blkbox);
+  ma.blkbox32 = at<float>(ws, L.blkbox32);
+  ma.g.bar = at<unsigned>(ws, L.bar) + BAR_PRESORT;
+  ma.g.part = at<int>(ws, L.part);
+  ma.g.hist = at<int>(ws, L.hist);
+  ma.g.parity = 0;
+  return launch_presort_morton(ma, s);
 }
 
 static int check_stream(const mo_step_args* a, Layout& L) {
@@ -650,34 +688,8 @@ int mo_sort_stream_begin(const mo_step_args* a, void* stream_) {
   Layout L;
   MO_TRY(check_stream(a, L));
   cudaStream_t s = (cudaStream_t)stream_;
-  StreamArgs sa = stream_args(a, L);
-  if (sa.boxed) {
-    void* ws = a->workspace;
-    MortonArgs ma;
-    ma.F = a->FR;
-    ma.R = (int)(2 * a->n);
-    ma.m = a->m;
-    ma.keyA = at<uint32_t>(ws, L.keyA);
-    ma.valA = at<int>(ws, L.valA);
-    ma.tkey = at<uint32_t>(ws, L.tkey);
-    ma.tval = at<int>(ws, L.tval);
-    ma.cbox = at<unsigned>(ws, L.cbox);
-    ma.perm = at<int>(ws, L.perm_sort);
-    ma.FS = at<float>(ws, L.FS);
-    ma.SS = at<float>(ws, L.SS);
-    ma.blkmin = at<float>(ws, L.blkmin);
-    ma.blkmax = at<float>(ws, L.blkmax);
-    ma.blkbox = at<float>(ws, L.blkbox);
-    ma.blkbox32 = at<float>(ws, L.blkbox32);
-    ma.g.bar = at<unsigned>(ws, L.bar) + BAR_PRESORT;
-    ma.g.part = at<int>(ws, L.part);
-    ma.g.hist = at<int>(ws, L.hist);
-    ma.g.parity = 0;
-    MO_TRY(launch_presort_morton(ma, s));
-  } else {
-    MO_TRY(launch_presort(presort_args(a, L), s));
-  }
-  return launch_stream_begin(sa, s);
+  MO_TRY(stream_presort(a, L, s));
+  return launch_stream_begin(stream_args(a, L), s);
 }
 
 int mo_sort_stream_front(const mo_step_args* a, int32_t k, void* stream_) {

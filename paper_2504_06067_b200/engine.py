@@ -89,7 +89,8 @@ def build_reference_set(cfg):
 class Engine:
     """Device-resident NSGA-III run: buffers, workspace and (optionally) a CUDA graph."""
 
-    def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4, prune="auto"):
+    def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4, prune="auto",
+                 host_fronts=None):
         validate(cfg)
         self.cfg = cfg
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -108,8 +109,15 @@ class Engine:
             raise ConfigError("shard", f"bad shard {shard}")
         self.sort_mode = self._choose_sort(sort)
         self.poll = max(1, int(poll))
-        if graph and (self.sort_mode != _lib.SORT_BITS or self.shard_count > 1):
-            raise ConfigError("graph", "CUDA-graph replay needs the single-shard bit-matrix sort")
+        # streamed sort, one shard: the front loop either runs on the device inside mo_step (one
+        # cooperative launch, graph-capturable) or front by front from the host (full-occupancy sweep
+        # launches; faster today at C4 scale, so the default unless a graph is captured).  Sharded runs
+        # are always host-driven: the collectives sit between the fronts.
+        if host_fronts is None:
+            host_fronts = not graph
+        self.host_fronts = self.sort_mode == _lib.SORT_STREAM and (self.shard_count > 1 or bool(host_fronts))
+        if graph and self.host_fronts:
+            raise ConfigError("graph", "CUDA-graph replay needs the device-side front loop (one shard)")
         with torch.cuda.device(self.dev):
             L = _lib.lib()
             self.zhat = torch.from_numpy(zh).to(self.dev)
@@ -171,7 +179,11 @@ class Engine:
             R = 2 * self.cfg.n
             bits = R * ((R + 255) // 256 * 8) * 4
             budget = 0.5 * torch.cuda.get_device_properties(self.dev).total_memory
-            sort = "bits" if self.shard_count == 1 and bits <= budget else "stream"
+            # measured crossovers (profiles/r01_sort_modes.jsonl): the boxed streamed sort overtakes
+            # the bit-matrix at n ~ 100k (m = 3) and n ~ 48k (m = 4); above m = 4 bits wins while it fits
+            n, m = self.cfg.n, self.cfg.m
+            boxed_wins = (m <= 3 and n >= 100_000) or (m == 4 and n >= 48_000)
+            sort = "bits" if self.shard_count == 1 and bits <= budget and not boxed_wins else "stream"
         return _lib.SORT_BITS if sort == "bits" else _lib.SORT_STREAM
 
     # ------------------------------------------------------------ C-ABI args
@@ -211,7 +223,7 @@ class Engine:
     # ------------------------------------------------------------- stepping
     def step(self, profile=None):
         """Advance one generation (eager launch).  ``profile``: dict receiving per-phase seconds."""
-        if self.sort_mode == _lib.SORT_STREAM:
+        if self.host_fronts:
             for req in self.step_gen(profile):
                 run_collective(req, self.group)
             return
@@ -371,8 +383,8 @@ class LocalShards:
     processes over NCCL (the kernels only see their shard index)."""
 
     def __init__(self, cfg, shards, device=None, poll=4, prune="auto"):
-        self.engines = [Engine(cfg, device=device, sort="stream", shard=(g, shards), poll=poll, prune=prune)
-                        for g in range(shards)]
+        self.engines = [Engine(cfg, device=device, sort="stream", shard=(g, shards), poll=poll, prune=prune,
+                               host_fronts=True) for g in range(shards)]
 
     def step(self):
         gens = [e.step_gen() for e in self.engines]

@@ -77,13 +77,17 @@ def test_stream_sort_equals_bits_path_large(M):
 def test_stream_engine_equals_bits_engine(M, kind, n, m, d, gens):
     cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=3)
     a = M.engine.Engine(cfg, sort="bits")
-    b = M.engine.Engine(cfg, sort="stream")
+    b = M.engine.Engine(cfg, sort="stream", host_fronts=False)   # device-side front loop (k_stream_fused)
+    c = M.engine.Engine(cfg, sort="stream", host_fronts=True)    # host-driven fronts (the sharded protocol)
+    assert not b.host_fronts and c.host_fronts
     for g in range(gens):
         a.step()
         b.step()
-        assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F), f"generation {g}"
-        assert torch.equal(a.ideal, b.ideal)
-        assert a.info_dict() == b.info_dict()
+        c.step()
+        for e in (b, c):
+            assert torch.equal(a.X, e.X) and torch.equal(a.F, e.F), f"generation {g}"
+            assert torch.equal(a.ideal, e.ideal)
+            assert a.info_dict() == e.info_dict()
 
 
 @pytest.mark.parametrize("shards", [2, 4, 8])
@@ -113,8 +117,8 @@ def test_local_shards_m10(M):
 
 def test_stream_engine_profile_and_poll(M):
     cfg = M.engine.RunConfig(problem="DTLZ7", n=3000, m=3, d=22, generations=3, seed=1)
-    a = M.engine.Engine(cfg, sort="stream", poll=1)
-    b = M.engine.Engine(cfg, sort="stream", poll=16)
+    a = M.engine.Engine(cfg, sort="stream", poll=1, host_fronts=True)
+    b = M.engine.Engine(cfg, sort="stream", poll=16, host_fronts=True)
     prof = {}
     for _ in range(3):
         a.step(profile=prof)
@@ -191,3 +195,33 @@ def test_local_shards_with_lattice(M):
         grp.step()
         for e in grp.engines:
             assert torch.equal(e.X, one.X) and torch.equal(e.F, one.F)
+
+
+@pytest.mark.parametrize("kind,m,n", [("DTLZ7", 3, 3000), ("DTLZ4", 3, 2000), ("DTLZ2", 6, 1500)])
+def test_stream_graph_replay_equals_eager(M, kind, m, n):
+    """One shard: the whole streamed generation is one mo_step, so it captures into a CUDA graph."""
+    cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=m + 9, generations=6, seed=12)
+    a = M.engine.Engine(cfg, sort="stream", host_fronts=False)
+    for _ in range(6):
+        a.step()
+    b = M.engine.Engine(cfg, sort="stream", graph=True)
+    b.replay(6)
+    torch.cuda.synchronize()
+    assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F) and a.info_dict() == b.info_dict()
+
+
+def test_stream_many_fronts(M):
+    """A chain-like population (hundreds of fronts) through the device-side front loop."""
+    x = np.sort(np.random.default_rng(3).random(1024)).astype(np.float32)
+    F = np.stack([x, x + 1, x + 2], 1)
+    for stream in (True, False):
+        cfg = M.engine.RunConfig(problem="DTLZ7", n=512, m=3, d=22, generations=1, seed=0)
+        eng = M.engine.Engine(cfg, sort="stream" if stream else "bits")
+        eng.FR[eng.cur].copy_(torch.from_numpy(F))
+        from paper_2504_06067_b200 import _lib
+        _lib.check(_lib.lib().mo_step_phases(eng._args[eng.cur], _lib.PHASE_SORT, _lib.stream_ptr()), "sort")
+        torch.cuda.synchronize()
+        r = np_(eng.ranks)
+        want = Odom.non_dominated_sort(F, stop_at=512)
+        assert np.array_equal(r, want), stream
+        assert eng.info_dict()["nfronts"] == 512
