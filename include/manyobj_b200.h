@@ -226,7 +226,7 @@ typedef struct mo_step_args {
    *   lattice_pos:   (H+1)^(m-1) int32 scratch (the step writes the shuffled
    *                  position of every point there).
    * NULL lattice_z = full scan.  lattice_r: box radius in lattice steps
-   * (0 = default: 6 at m <= 3, 4 at m = 4, 3 at m = 5). */
+   * (0 = default: 6 at m <= 3, 3 at m = 4, 2 at m = 5). */
   const float* lattice_z;
   const int32_t* lattice_index;
   int32_t* lattice_pos;

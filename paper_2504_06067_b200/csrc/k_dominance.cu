@@ -211,22 +211,22 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
   __syncthreads();
   uint32_t wa[8], wb[8];
   if (fast) {
-    // sign-of-difference chains (FMA pipe); the 32 sign bits of a chunk are funnel-shifted into
-    // a word, i = 31 first so that i lands on bit i, then inverted (set = dominated)
+    // m-long setp.le.and chains + predicated OR.  (A sign-of-difference variant -- m FADD on the FMA
+    // pipe + LOP3 + funnel shift -- measured no faster: the tile is issue-bound, not ALU-bound.)
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
       uint32_t acca = 0, accb = 0;
 #pragma unroll
-      for (int b = 31; b >= 0; --b) {
+      for (int b = 0; b < 32; ++b) {
         const float* fi = sFi + (c * 32 + b) * MP;
         float v[M];
 #pragma unroll
         for (int k = 0; k < M; ++k) v[k] = fi[k];
-        acca = __funnelshift_l(le_sign<M>(v, fa), acca, 1);
-        accb = __funnelshift_l(le_sign<M>(v, fb), accb, 1);
+        Chain<M>::le(v, fa, acca, 1u << b);
+        Chain<M>::le(v, fb, accb, 1u << b);
       }
-      wa[c] = ~acca;
-      wb[c] = ~accb;
+      wa[c] = acca;
+      wb[c] = accb;
     }
   } else {
 #pragma unroll 1

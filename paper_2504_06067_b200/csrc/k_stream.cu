@@ -141,7 +141,15 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
 // Items are pulled from `counter`; the item index is the counter value minus
 // `base`.  Arrays written earlier in the same fused launch (plan, fl, flmax,
 // flbox) are read through L2 (__ldcg).
-template <int M, int MODE>
+// Read-only-during-the-launch data through L1 (__ldg); data written earlier in the same fused launch
+// through L2 (__ldcg).
+template <bool FUSED, class T>
+__device__ __forceinline__ T ldx(const T* p) {
+  if (FUSED) return __ldcg(p);
+  return __ldg(p);
+}
+
+template <int M, int MODE, bool FUSED>
 __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* sItem, int items, int fln,
                                           int* counter, int base) {
   constexpr int MP = (M + 3) & ~3;
@@ -156,9 +164,9 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
     int lo = 0, hi = a.T;  // largest t with plan[t] <= item
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (__ldcg(a.plan + mid) <= item) lo = mid; else hi = mid;
+      if (ldx<FUSED>(a.plan + mid) <= item) lo = mid; else hi = mid;
     }
-    const int t = lo, c = item - __ldcg(a.plan + t);
+    const int t = lo, c = item - ldx<FUSED>(a.plan + t);
     const int bj = owned_block(a, t);
     const int j0 = bj * STREAM_BLK;
     // two adjacent rows per thread: a warp owns 64 consecutive positions (one j box per warp)
@@ -202,7 +210,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
         bool none = false, all = true, strict = false;
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const float imn = __ldcg(ib + k), imx = __ldcg(ib + M + k);
+          const float imn = ldx<FUSED>(ib + k), imx = ldx<FUSED>(ib + M + k);
           const float jmn = __ldg(jb2 + k), jmx = __ldg(jb2 + M + k);
           none |= imn > jmx;
           all &= imx <= jmn;
@@ -217,12 +225,12 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
       }
       for (int e = tid; e < STREAM_BLK; e += ST_THREADS) {
         int src = -1;
-        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : __ldcg(a.fl + s0 + e);
+        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : ldx<FUSED>(a.fl + s0 + e);
         float* dst = sFi + e * MP;
 #pragma unroll
         for (int k = 0; k < MP; ++k) dst[k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
       }
-      const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : __ldcg(a.flmax + s0 / STREAM_BLK);
+      const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : ldx<FUSED>(a.flmax + s0 / STREAM_BLK);
       const bool fast = (MODE == MODE_COUNT && !a.boxed ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
       __syncthreads();
       const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
@@ -233,7 +241,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
           bool none = false, all = true, strict = false;
 #pragma unroll
           for (int k = 0; k < M; ++k) {
-            const float imn = __ldcg(ib + k), imx = __ldcg(ib + M + k);
+            const float imn = ldx<FUSED>(ib + k), imx = ldx<FUSED>(ib + M + k);
             none |= imn > wjmx[k];
             all &= imx <= wjmn[k];
             strict |= imx < wjmn[k];
@@ -247,18 +255,16 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
           }
         }
         if (fast) {
-          // all 32 entries of the group (staging pads are +inf rows: never <= a finite row)
-          uint32_t acca = 0, accb = 0;
+          for (int i = g0; i < g1; i += 8) {
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            float v[M];
+            for (int u = 0; u < 8; ++u) {
+              float v[M];
 #pragma unroll
-            for (int k = 0; k < M; ++k) v[k] = sFi[(g0 + u) * MP + k];
-            acca = __funnelshift_l(le_sign<M>(v, fa), acca, 1);
-            accb = __funnelshift_l(le_sign<M>(v, fb), accb, 1);
+              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+              Chain<M>::le_cnt(v, fa, ca);
+              Chain<M>::le_cnt(v, fb, cb);
+            }
           }
-          na += __popc(~acca);
-          nb2 += __popc(~accb);
         } else {
           for (int i = g0; i < g1; i += 8) {
 #pragma unroll
@@ -285,8 +291,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
   constexpr int MP = (M + 3) & ~3;
   __shared__ __align__(16) float sFi[STREAM_BLK * MP];
   __shared__ int sItem;
-  tiles_run<M, MODE>(a, sFi, &sItem, __ldcg(a.ctl + SC_ITEMS), MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0,
-                     a.ctl + SC_WORK, 0);
+  tiles_run<M, MODE, false>(a, sFi, &sItem, __ldcg(a.ctl + SC_ITEMS),
+                            MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0, a.ctl + SC_WORK, 0);
 }
 
 // Owned unranked rows with no unranked dominator left -> local mask slice.
@@ -577,7 +583,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
   // dominator counts, front 0
   int base = 0;
   int items = plan_all(a, g, MODE_COUNT, 0, sh);
-  tiles_run<M, MODE_COUNT>(a, sFi, &sItem, items, 0, a.ctl + SC_WORK, base);
+  tiles_run<M, MODE_COUNT, true>(a, sFi, &sItem, items, 0, a.ctl + SC_WORK, base);
   base += items + (int)gridDim.x;
   grid_sync(g.bar);
   mark_all(a);
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
     grid_sync(g.bar);            // fl / rank_pos / ucnt of front k visible
     chunk_boxes<M>(a, fk, sRedMin, sRedMax);
     items = plan_all(a, g, MODE_DEC, fk, sh);  // (its first barrier also publishes the chunk boxes)
-    tiles_run<M, MODE_DEC>(a, sFi, &sItem, items, fk, a.ctl + SC_WORK, base);
+    tiles_run<M, MODE_DEC, true>(a, sFi, &sItem, items, fk, a.ctl + SC_WORK, base);
     base += items + (int)gridDim.x;
     grid_sync(g.bar);
     mark_all(a);
@@ -695,7 +701,7 @@ __global__ void __launch_bounds__(MORTON_THREADS) k_presort_morton(MortonArgs a)
     a.perm[p] = i;
     const float* f = a.F + (int64_t)i * m;
     float s = f[0];
-    a.FS[(int64_t)p * m] = __fadd_rn(f[0], 0.0f);  // -0 -> +0 (the sign-of-difference chains rely on it)
+    a.FS[(int64_t)p * m] = __fadd_rn(f[0], 0.0f);  // -0 -> +0 (canonical zero in the sorted rows)
     for (int k = 1; k < m; ++k) {
       s = __fadd_rn(s, f[k]);
       a.FS[(int64_t)p * m + k] = __fadd_rn(f[k], 0.0f);

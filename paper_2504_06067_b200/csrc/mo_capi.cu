@@ -279,7 +279,7 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
 }
 
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
-static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 4 : 3); }
+static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 2); }
 
 static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cudaStream_t s) {
   const int64_t n = a->n, R = 2 * n, w = a->w;

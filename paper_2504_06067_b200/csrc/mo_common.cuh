@@ -77,20 +77,6 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
   return v;
 }
 
-// "a[k] <= b[k] for every k" on the FMA pipe: OR of the bit patterns of the
-// differences b[k] - a[k]; its sign bit is clear iff no difference is
-// negative.  Exact for finite values when neither side holds -0 (b - a is
-// then +0 iff a == b, and never underflows to 0 for a != b without FTZ):
-// the presorts canonicalise -0 to +0 (x + 0).  Costs m FADD (FMA pipe)
-// + m-1 LOP3 folded to ~m/2 instead of m FSETP on the half-rate ALU pipe.
-template <int M>
-__device__ __forceinline__ uint32_t le_sign(const float* a, const float* b) {
-  uint32_t o = __float_as_uint(__fsub_rn(b[0], a[0]));
-#pragma unroll
-  for (int k = 1; k < M; ++k) o |= __float_as_uint(__fsub_rn(b[k], a[k]));
-  return o;  // bit 31 clear  <=>  a <= b componentwise
-}
-
 // Warp-aggregated histogram increment: lanes with equal `bin` elect one leader
 // (__match_any_sync) that adds the group's population with a single atomic.
 __device__ __forceinline__ void warp_agg_add(int* hist, int bin, bool active) {

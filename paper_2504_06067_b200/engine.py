@@ -90,7 +90,7 @@ class Engine:
     """Device-resident NSGA-III run: buffers, workspace and (optionally) a CUDA graph."""
 
     def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4, prune="auto",
-                 host_fronts=None):
+                 host_fronts=None, prune_r=0):
         validate(cfg)
         self.cfg = cfg
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -109,6 +109,7 @@ class Engine:
             raise ConfigError("shard", f"bad shard {shard}")
         self.sort_mode = self._choose_sort(sort)
         self.poll = max(1, int(poll))
+        self.prune_r = int(prune_r)          # lattice box radius (0 = the library default for m)
         # streamed sort, one shard: the front loop either runs on the device inside mo_step (one
         # cooperative launch, graph-capturable) or front by front from the host (full-occupancy sweep
         # launches; faster today at C4 scale, so the default unless a graph is captured).  Sharded runs
@@ -156,9 +157,10 @@ class Engine:
             if prune is True and not legal:
                 raise ConfigError("prune", "lattice pruning needs a single-layer Das-Dennis set and m <= 5")
             return None, 0
-        r = 6 if m <= 3 else (4 if m == 4 else 3)        # default_lattice_r (mo_capi.cu)
-        # a box point costs ~30x a full-scan point (decode + gathered loads): measured break-even
-        if prune == "auto" and 32 * (2 * r - 1) ** (m - 1) >= w:    # box of (2r-1)^(m-1) points
+        r = self.prune_r or (6 if m <= 3 else (3 if m == 4 else 2))   # default_lattice_r (mo_capi.cu)
+        # a box point costs several full-scan points (decode + gathered loads); measured: C2 (m=5, w=8855,
+        # r=2) 185 -> 167 us niche phase, m=5 N=100k 6.2 -> 0.54 ms (scripts/assoc_probe.py)
+        if prune == "auto" and 8 * (2 * r - 1) ** (m - 1) >= w:     # box of (2r-1)^(m-1) points
             return None, 0
         k = np.rint(np.asarray(self.Z, np.float64) * Ho).astype(np.int64)
         idx = np.zeros(w, np.int64)
@@ -212,7 +214,7 @@ class Engine:
         if self.lattice is not None:
             a.lattice_z, a.lattice_index, a.lattice_pos = (t.data_ptr() for t in self.lattice)
         a.lattice_H = self.lattice_H
-        a.lattice_r = 0
+        a.lattice_r = self.prune_r
         return a
 
     def _launch(self, cur, generation, phases=_lib.PHASE_ALL, use_dev_gen=False):
