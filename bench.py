@@ -41,6 +41,7 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     "c1": dict(problem="DTLZ1", m=3, d=7, n=92, sort="bits", label="C1 DTLZ1 m=3 d=7 N=92 (w=91, H=12)"),
     "c2": dict(problem="DTLZ2", m=5, d=14, n=10000, sort="bits", label="C2 DTLZ2 m=5 d=14 N=10k (w=8855, H=19)"),
+    # C3 (DTLZ3, several fronts): bits and boxed-stream tie at 40 gen/s; bits keeps the graph replay
     "c3": dict(problem="DTLZ3", m=10, d=19, n=100000, sort="bits", label="C3 DTLZ3 m=10 d=19 N=100k (w=97383)"),
     # C4: the R^2/8 = 500 GB bit-matrix does not fit -> streamed sort; under torchrun it is sharded
     "c4": dict(problem="DTLZ7", m=3, d=22, n=1000000, sort="stream",

@@ -31,9 +31,9 @@
 // chunk) items of every owned block from wend / the front list, and the
 // persistent k_stream_tiles CTAs pull items with one atomic each.
 //
-// Two position spaces.  "Slab" (m > 4): k_presort's S-ordered buckets --
+// Two position spaces.  "Slab" (m > 10): k_presort's S-ordered buckets --
 // dominators precede (triangle), S-separated tiles need only the <= chain.
-// "Boxed" (m <= 4): k_presort_morton's Morton order of the quantised
+// "Boxed" (m <= 10): k_presort_morton's Morton order of the quantised
 // objectives makes every 256-row block compact in objective space, so an
 // ordered block pair (i block, j block) is usually decided by the two
 // bounding boxes alone: some min_i[k] > max_j[k] -> no i dominates any j;

@@ -42,7 +42,7 @@ struct StreamArgs {
   int* info;             // MO_INFO_COUNT
   int* ranks;            // R   output ranks (row order)
   GridCtx gc;
-  // boxed mode (m <= 4): Morton-ordered positions, per-block bounding boxes,
+  // boxed mode (m <= 10): Morton-ordered positions, per-block bounding boxes,
   // all ordered block pairs classified none / all / mixed (k_presort_morton)
   int boxed;
   float* blkbox;         // nb x 2 x m: per 256-row block min[m], max[m]

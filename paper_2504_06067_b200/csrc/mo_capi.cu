@@ -383,8 +383,10 @@ static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
   return MO_OK;
 }
 
-// Boxed (Morton) position space for the streamed sort at m <= 4, S slabs above
-static int stream_boxed(int m) { return m <= 4 ? 1 : 0; }
+// Boxed (Morton) position space for the streamed sort at m <= 10, S slabs above
+// (boxes from a 30-bit Morton key: 3+ bits per coordinate up to m = 10; measured faster than the S slabs
+// at every m <= 10 tried, profiles/r01_sort_modes.jsonl)
+static int stream_boxed(int m) { return m <= 10 ? 1 : 0; }
 
 static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   void* ws = a->workspace;

@@ -182,9 +182,9 @@ class Engine:
             bits = R * ((R + 255) // 256 * 8) * 4
             budget = 0.5 * torch.cuda.get_device_properties(self.dev).total_memory
             # measured crossovers (profiles/r01_sort_modes.jsonl): the boxed streamed sort overtakes
-            # the bit-matrix at n ~ 100k (m = 3) and n ~ 48k (m = 4); above m = 4 bits wins while it fits
+            # the bit-matrix at n ~ 100k (m = 3) and n ~ 48k (m >= 4, e.g. C3: 20.0 vs 26.1 ms)
             n, m = self.cfg.n, self.cfg.m
-            boxed_wins = (m <= 3 and n >= 100_000) or (m == 4 and n >= 48_000)
+            boxed_wins = (m <= 3 and n >= 100_000) or (4 <= m <= 10 and n >= 48_000)
             sort = "bits" if self.shard_count == 1 and bits <= budget and not boxed_wins else "stream"
         return _lib.SORT_BITS if sort == "bits" else _lib.SORT_STREAM
 

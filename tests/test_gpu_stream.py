@@ -31,7 +31,7 @@ def np_(t):
 
 def _cases():
     rs = np.random.default_rng(31)
-    for R, m in [(4, 2), (64, 3), (184, 3), (512, 2), (772, 5), (1000, 10), (2048, 3), (3000, 4)]:
+    for R, m in [(4, 2), (64, 3), (184, 3), (512, 2), (772, 5), (1000, 10), (2048, 3), (3000, 4), (600, 12), (900, 16)]:
         yield rs.random((R, m)).astype(np.float32)
         yield rs.integers(0, 4, size=(R, m)).astype(np.float32)           # ties + duplicates
     x = np.sort(rs.random(600)).astype(np.float32)
