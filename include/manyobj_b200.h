@@ -279,6 +279,11 @@ int mo_sort_stream_begin(const mo_step_args* args, void* stream_);
 int mo_sort_stream_front(const mo_step_args* args, int32_t k, void* stream_);
 int mo_sort_stream_end(const mo_step_args* args, void* stream_);
 
+/* Zero a workspace (once, before its first mo_step / mo_step_phases / mo_niche_phases): inside a step
+ * the kernels keep their own counters and grid barriers consistent instead of re-initialising them with
+ * memset nodes, so a captured generation has no memset nodes. */
+int mo_workspace_init(void* workspace, size_t workspace_bytes, void* stream_);
+
 /* Workspace bytes for a sort mode and shard count (mo_workspace_bytes ==
  * mode MO_SORT_BITS, 1 shard). */
 int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t sort_mode, int32_t shard_count,

@@ -80,6 +80,7 @@ _PROTOS = {
     "mo_sort_stream_begin": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
     "mo_sort_stream_front": (c_i32, [ctypes.POINTER(StepArgs), c_i32, c_vp]),
     "mo_sort_stream_end": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
+    "mo_workspace_init": (c_i32, [c_vp, c_sz, c_vp]),
     "mo_workspace_bytes_ex": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_sz)]),
     "mo_stream_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
@@ -136,7 +137,7 @@ def workspace_rows(R, m, w, device=None):
 def workspace_step(n, m, d, w, device=None):
     nbytes = c_sz(0)
     check(lib().mo_workspace_bytes(int(n), int(m), int(d), int(w), ctypes.byref(nbytes)), "mo_workspace_bytes")
-    return torch.empty(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")
+    return torch.zeros(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")   # mo_workspace_init
 
 
 def workspace_bytes_ex(n, m, d, w, sort_mode, shards):

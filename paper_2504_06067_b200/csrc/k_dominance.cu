@@ -329,13 +329,13 @@ int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint
 
 
 int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
-                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s) {
+                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s, bool clear_hasdom) {
   if (R <= 0) return MO_OK;
   const int64_t W = words_per_row(R);
   const int64_t nb = W / 8;
   const int64_t tiles = nb * (nb + 1) / 2;
   if (tiles > 0x7fffffffll) return MO_ERR_PARAM;
-  if (cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
+  if (clear_hasdom && cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
   dim3 grid((unsigned)tiles);
   switch (m) {
 #define MO_DOMS_CASE(MM) \
@@ -414,13 +414,13 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    atomicMin(&a.ctl[0], sMin);
+    atomicMax(&a.ctl[0], ~sMin);   // ~min: 0 is the neutral value (no reset node needed)
     atomicMax(&a.ctl[1], sMax);
   }
   grid_sync(a.g.bar);
   trace_mark(a.trace, 1);
   // P1: bucket of every row + histogram
-  const uint32_t lo = __ldcg(a.ctl), hi = __ldcg(a.ctl + 1);
+  const uint32_t lo = ~__ldcg(a.ctl), hi = __ldcg(a.ctl + 1);
   const uint64_t span = (uint64_t)(hi - lo) + 1ull;
   for (int i = gtid; i < R; i += gthreads) {
     const uint32_t key = __ldcg(a.keyB + i);
@@ -437,6 +437,13 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
       [&](int64_t q, int pre) { a.fill[q] = pre; }, sh);
   grid_sync(a.g.bar);
   trace_mark(a.trace, 3);
+  // every block has read the key range (P1): restore its neutral values for the next launch
+  if (gtid == 0) {
+    a.ctl[0] = 0u;
+    a.ctl[1] = 0u;
+  }
+  if (a.hasdom)
+    for (int p = gtid; p < R; p += gthreads) a.hasdom[p] = 0;
   // P3: scatter rows into their buckets
   if (a.stable) {
     // (bucket, row) pairs sorted by bucket, rows ascending inside a bucket
@@ -516,11 +523,10 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
   int blocks = (int)ceil_div(args.R > PRESORT_BUCKETS ? args.R : PRESORT_BUCKETS, PRESORT_THREADS * 2);
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
-  const unsigned init[2] = {0xffffffffu, 0u};
-  if (cudaMemsetAsync(args.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
-  if (cudaMemsetAsync(args.ctl, 0xff, sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
-  if (cudaMemsetAsync(args.ctl + 1, 0, sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
-  (void)init;
+  if (!args.in_step) {
+    if (cudaMemsetAsync(args.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(args.ctl, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(PRESORT_THREADS);
@@ -601,9 +607,11 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   const int nvalid = __ldcg(a.front_sizes);
   const int64_t target = a.stop_at > 0 ? a.stop_at : (int64_t)nvalid;
   if (a.stop_at > 0 && nvalid < a.stop_at) {
+    grid_sync(a.bar);            // everyone has read front_sizes[0]
     if (gtid == 0) {
       a.info[MO_INFO_ERROR] = MO_ERR_INFEASIBLE;
       a.info[MO_INFO_L] = -1;
+      a.front_sizes[0] = 0;      // neutral for the next launch (no memset node)
     }
     return;
   }
@@ -697,6 +705,7 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
         a.info[MO_INFO_FL_SIZE] = fk;
         a.info[MO_INFO_SKIPPED] = (a.stop_at > 0 && sel + fk == a.stop_at) ? 1 : 0;
         a.info[MO_INFO_ERROR] = 0;
+        a.front_sizes[0] = 0;    // read by every block after the prologue barrier, long passed
       }
       trace_mark(a.trace, 10);
       return;
@@ -728,12 +737,14 @@ int peel_grid_blocks() {
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
-                      unsigned long long* trace, cudaStream_t s) {
+                      unsigned long long* trace, cudaStream_t s, bool in_step) {
   if (R <= 0) return MO_ERR_PARAM;
   PeelArgs a{bits, (int)R, words_per_row(R), valid, stop_at, ranks, info, resume, ranked, front_sizes, bar,
              perm, hasdom, wend, rank_pos, trace};
-  if (cudaMemsetAsync(front_sizes, 0, 2 * sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
-  if (cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (!in_step) {
+    if (cudaMemsetAsync(front_sizes, 0, 2 * sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  }
   int blocks = peel_grid_blocks();
   // two grid barriers per front: ~32 rows per warp keeps the barriers cheap
   int needed = (int)ceil_div(R, (PEEL_THREADS / 32) * 32);

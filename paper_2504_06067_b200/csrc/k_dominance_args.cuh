@@ -29,16 +29,20 @@ struct PresortArgs {
   int stable;
   uint32_t* tkey;   // R (stable only)
   int* tval;        // R (stable only)
+  // in_step = 1 (mo_step): no memset nodes -- the grid barrier is self-resetting, the key range is
+  // reset by the kernel after its last use, and hasdom (nullable) is cleared here for the tile kernel
+  int in_step;
+  uint8_t* hasdom;
 };
 
 int64_t words_per_row(int64_t R);
 int launch_presort(const PresortArgs& args, cudaStream_t s);
 int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
 int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
-                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s);
+                           int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s, bool clear_hasdom = true);
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
-                      unsigned long long* trace, cudaStream_t s);
+                      unsigned long long* trace, cudaStream_t s, bool in_step = false);
 
 }  // namespace mo

@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   if (a.lvl)
     for (int q = gtid; q < 2 * LVL_BINS; q += gthreads) a.lvl[q] = 0;
   if (a.sctl && gtid < 16) a.sctl[gtid] = 0;
+  if (gtid == 0 && a.fb_ctl) {
+    a.fb_ctl[0] = 0;
+    a.info[MO_INFO_ASSOC_FALLBACK] = 0;
+  }
   if (a.mode != PREP_FULL) return;
   if (gtid < m) {
     a.ext_key[gtid] = ~0ull;
@@ -531,6 +535,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const int R = a.R, w = a.w;
+  if (a.reset_ctl && gtid == 0) *a.reset_ctl = 0;   // k_assoc_final (the last reader) has completed
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   const int l = __ldcg(a.info + MO_INFO_L);
   const int k = __ldcg(a.info + MO_INFO_K);
@@ -835,8 +840,10 @@ int select_grid_blocks() {
 
 int launch_prep(const PrepArgs& a, cudaStream_t s) {
   if (a.m < 1 || a.m > MAXM) return MO_ERR_PARAM;
-  if (cudaMemsetAsync(a.ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
-  if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (!a.in_step) {
+    if (cudaMemsetAsync(a.ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  }
   int blocks = prep_grid_blocks();
   int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), 256);
   if (blocks > need) blocks = need < 1 ? 1 : need;
@@ -884,9 +891,11 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
 
 int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   if (R <= 0) return MO_OK;
-  if (cudaMemsetAsync(a.fb_ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
-  if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
-    return MO_ERR_CUDA;
+  if (!a.in_step) {
+    if (cudaMemsetAsync(a.fb_ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
+      return MO_ERR_CUDA;
+  }
   // lanes per candidate row: enough to cover the box with few points each
   switch (m) {
     case 2: k_assoc_lattice<2, 1><<<(unsigned)ceil_div(R, 256), 256, 0, s>>>(a); break;
@@ -911,7 +920,7 @@ int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
 }
 
 int launch_select(const SelectArgs& a, cudaStream_t s) {
-  if (cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
+  if (!a.in_step && cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   int blocks = select_grid_blocks();
   int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), SELECT_THREADS * 2);
   if (blocks > need) blocks = need < 1 ? 1 : need;

@@ -42,6 +42,10 @@ struct PrepArgs {
   int* sctl;  // 16 select counters
   const int* lat_index;  // nullable: lattice index of every reference point (lattice-pruned association)
   int* lat_pos;          // lat_pos[lat_index[j]] = shuffled position of j
+  // in_step = 1 (mo_step): no memset nodes -- ctl[0] is zeroed by the previous step's k_select, the
+  // barrier is self-resetting, and the lattice fallback counters (nullable) are cleared here
+  int in_step;
+  int* fb_ctl;
 };
 
 constexpr int LVL_BINS = 1024;
@@ -69,6 +73,7 @@ struct AssocArgs {
   const int* pos_ref;
   int* fb_cand;
   int* fb_ctl;
+  int in_step;           // fb_ctl / info[MO_INFO_ASSOC_FALLBACK] already cleared by k_prep
 };
 
 struct AssocFinalArgs {
@@ -121,6 +126,8 @@ struct SelectArgs {
   uint32_t* gen_ptr;  // nullable: incremented once the step is complete
   unsigned long long* trace;  // nullable phase trace (slots 24..40)
   GridCtx g;
+  int in_step;        // no barrier memset node (self-resetting barrier)
+  int* reset_ctl;     // nullable: k_prep's candidate counter, zeroed here after its last reader
 };
 
 int launch_prep(const PrepArgs& a, cudaStream_t s);

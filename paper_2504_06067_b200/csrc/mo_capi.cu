@@ -180,6 +180,8 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.sctl = at<int>(ws, L.sctl);
   a.lat_index = nullptr;
   a.lat_pos = nullptr;
+  a.in_step = 0;
+  a.fb_ctl = nullptr;
   return a;
 }
 
@@ -221,6 +223,8 @@ static SelectArgs select_args(const Layout& L, void* ws, int64_t R, int64_t w, i
   a.g.part = at<int>(ws, L.part);
   a.g.hist = at<int>(ws, L.hist);
   a.g.parity = 0;
+  a.in_step = 0;
+  a.reset_ctl = nullptr;
   return a;
 }
 
@@ -262,6 +266,8 @@ static PresortArgs presort_args(const mo_step_args* a, const Layout& L) {
   ps.stable = a->sort_mode == MO_SORT_STREAM;
   ps.tkey = ps.stable ? at<uint32_t>(ws, L.tkey) : nullptr;
   ps.tval = ps.stable ? at<int>(ws, L.tval) : nullptr;
+  ps.in_step = 0;
+  ps.hasdom = nullptr;
   return ps;
 }
 
@@ -270,12 +276,15 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   void* ws = a->workspace;
   uint32_t* bits = at<uint32_t>(ws, L.bits);
   PresortArgs ps = presort_args(a, L);
-  MO_TRY(launch_presort(ps, s));
   uint8_t* hasdom = at<uint8_t>(ws, L.hasdom);
-  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s));
+  // no memset nodes inside a step (workspace zero-initialised once, mo_workspace_init)
+  ps.in_step = 1;
+  ps.hasdom = hasdom;
+  MO_TRY(launch_presort(ps, s));
+  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s, false));
   return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
                            at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, ps.perm, hasdom, ps.wend,
-                           at<int>(ws, L.rank_pos), ps.trace, s);
+                           at<int>(ws, L.rank_pos), ps.trace, s, true);
 }
 
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
@@ -288,6 +297,8 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   PrepArgs pa = prep_args(L, ws, a->FR, R, m, w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
                           nullptr, PREP_FULL);
   pa.gen_ptr = a->generation_dev;
+  pa.in_step = 1;
+  pa.fb_ctl = at<int>(ws, L.fctl);
   if (a->lattice_z && m >= 2 && m <= 5) {
     pa.lat_index = a->lattice_index;
     pa.lat_pos = a->lattice_pos;
@@ -315,6 +326,7 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.pos_ref = pa.pos_ref;
   aa.fb_cand = at<int>(ws, L.fcand);
   aa.fb_ctl = at<int>(ws, L.fctl);
+  aa.in_step = 1;
   if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
   else
@@ -347,6 +359,8 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   sa.dvars = a->d;
   sa.m = m;
   sa.gen_ptr = a->generation_dev;
+  sa.in_step = 1;
+  sa.reset_ctl = pa.ctl;
   return launch_select(sa, s);
 }
 
@@ -558,6 +572,8 @@ int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, f
   ps.stable = 0;
   ps.tkey = nullptr;
   ps.tval = nullptr;
+  ps.in_step = 0;
+  ps.hasdom = nullptr;
   return launch_presort(ps, (cudaStream_t)stream_);
 }
 
@@ -630,6 +646,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
   aa.zbeg = 0;
   aa.zend = (int)w;
   aa.lat_z = nullptr;
+  aa.in_step = 0;
   MO_TRY(launch_assoc(aa, m, R, s));
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));
@@ -707,6 +724,11 @@ int mo_sort_stream_end(const mo_step_args* a, void* stream_) {
   Layout L;
   MO_TRY(check_stream(a, L));
   return launch_stream_end(stream_args(a, L), (cudaStream_t)stream_);
+}
+
+int mo_workspace_init(void* workspace, size_t workspace_bytes, void* stream_) {
+  if (!workspace) return MO_ERR_PARAM;
+  return cudaMemsetAsync(workspace, 0, workspace_bytes, (cudaStream_t)stream_) == cudaSuccess ? MO_OK : MO_ERR_CUDA;
 }
 
 int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t sort_mode, int32_t shard_count,

@@ -130,6 +130,7 @@ class Engine:
             self.gen_dev = torch.zeros(1, dtype=torch.int32, device=self.dev)
             nbytes = _lib.workspace_bytes_ex(n, m, d, self.w, self.sort_mode, self.shard_count)
             self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+            _lib.check(L.mo_workspace_init(self.ws.data_ptr(), nbytes, _lib.stream_ptr()), "mo_workspace_init")
             if self.sort_mode == _lib.SORT_STREAM:
                 lo, words, fo, ao = _lib.stream_offsets(n, m, self.w, self.sort_mode, self.shard_count)
                 self.mask_local = self.ws[lo: lo + 4 * words].view(torch.int32)
