@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
                                                                   const int* __restrict__ wend, int R,
                                                                   uint32_t* __restrict__ bits, int64_t W,
                                                                   uint8_t* __restrict__ hasdom) {
+  pdl_wait();
   constexpr int MP = (M + 3) & ~3;
   __shared__ __align__(16) float sFi[DOM_TILE * MP];
   __shared__ uint32_t sB2[DOM_TILE * 9];
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
       }
     }
   }
+  pdl_trigger();   // multi-wave grid: let the peel's CTAs in only as this CTA retires
 }
 
 int64_t words_per_row(int64_t R) { return round_up(R, DOM_TILE) / 32; }
@@ -339,7 +341,9 @@ int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* bl
   dim3 grid((unsigned)tiles);
   switch (m) {
 #define MO_DOMS_CASE(MM) \
-  case MM: k_dom_tile_sorted<MM><<<grid, DOMS_THREADS, 0, s>>>(FS, blkmin, blkmax, wend, (int)R, bits, W, hasdom); \
+  case MM:                                                                                                  \
+    MO_TRY(launch_ex(k_dom_tile_sorted<MM>, grid, dim3(DOMS_THREADS), 0, s, false, g_mo_pdl, FS, blkmin, blkmax, \
+                     wend, (int)R, bits, W, hasdom));                                                        \
     break;
     MO_DOMS_CASE(2)
     MO_DOMS_CASE(3)
@@ -379,6 +383,7 @@ int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* bl
 constexpr int PRESORT_THREADS = 512;
 
 __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
+  pdl_wait();
   __shared__ int sh[40];
   __shared__ unsigned sMin, sMax;
   __shared__ int sWcnt[(PRESORT_THREADS / 32) * 256], sRun[256], sOff[256];
@@ -527,18 +532,7 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     if (cudaMemsetAsync(args.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
     if (cudaMemsetAsync(args.ctl, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(PRESORT_THREADS);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, k_presort, args) != cudaSuccess) return MO_ERR_CUDA;
-  MO_CHECK_LAUNCH();
-  return MO_OK;
+  return launch_ex(k_presort, dim3(blocks), dim3(PRESORT_THREADS), 0, s, true, g_mo_pdl && args.in_step, args);
 }
 
 // ------------------------------------------------------------------ peeling
@@ -568,6 +562,7 @@ struct PeelArgs {
 constexpr int PEEL_THREADS = 256;
 
 __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
+  pdl_wait();
   __shared__ int sCount[PEEL_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int gthreads = gridDim.x * blockDim.x;
@@ -749,19 +744,7 @@ int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int
   // two grid barriers per front: ~32 rows per warp keeps the barriers cheap
   int needed = (int)ceil_div(R, (PEEL_THREADS / 32) * 32);
   if (blocks > needed) blocks = needed < 1 ? 1 : needed;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(PEEL_THREADS);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, k_front_peel, a) != cudaSuccess) return MO_ERR_CUDA;
-  MO_CHECK_LAUNCH();
-  return MO_OK;
+  return launch_ex(k_front_peel, dim3(blocks), dim3(PEEL_THREADS), 0, s, true, g_mo_pdl && in_step, a);
 }
 
 }  // namespace mo

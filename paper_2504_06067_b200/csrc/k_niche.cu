@@ -83,6 +83,7 @@ __device__ void gauss_solve(double* A, double* rhs, int m, int* singular) {
 }
 
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
+  pdl_wait();
   __shared__ uint32_t sKp[MAX_SHUFFLE_ROUNDS], sSp[MAX_SHUFFLE_ROUNDS], sKr[MAX_SHUFFLE_ROUNDS],
       sSr[MAX_SHUFFLE_ROUNDS];
   __shared__ int sRp, sRr;
@@ -321,6 +322,7 @@ __device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rb
 
 template <int M>
 __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
+  pdl_wait();
   constexpr int MP = (M + 3) & ~3;
   __shared__ __align__(16) float sz[ASSOC_PTILE * MP];
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
 // bit for bit; the certificate only decides where it is computed.
 template <int M, int LPR>
 __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
+  pdl_wait();
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
   const int ncand = __ldcg(a.ctl);
@@ -451,6 +454,7 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
 }
 
 __global__ void k_assoc_final(AssocFinalArgs a) {
+  pdl_wait();
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
   const int ncand = __ldcg(a.ctl);
@@ -528,6 +532,7 @@ __device__ __forceinline__ int warp_bitonic_asc(int v) {
 //      threshold search) -- equal to the cursor order of the cache table
 //   P8 survivors: stable compaction in merged-row order
 __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
+  pdl_wait();
   __shared__ int sh[40];
   __shared__ int sHist[2][LVL_BINS];
   __shared__ int sRes[4];
@@ -812,19 +817,7 @@ static int coop_blocks(const void* fn, int threads, int cap_per_sm) {
 
 template <class Args>
 static int launch_coop(void (*fn)(Args), int blocks, int threads, Args args, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, fn, args) != cudaSuccess) return MO_ERR_CUDA;
-  MO_CHECK_LAUNCH();
-  return MO_OK;
+  return launch_ex(fn, dim3(blocks), dim3(threads), 0, s, true, g_mo_pdl, args);
 }
 
 int prep_grid_blocks() {
@@ -864,7 +857,7 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   dim3 grid(capacity);
   switch (m) {
 #define MO_AS_CASE(MM) \
-  case MM: k_assoc<MM><<<grid, ASSOC_THREADS, 0, s>>>(b); break;
+  case MM: MO_TRY(launch_ex(k_assoc<MM>, grid, dim3(ASSOC_THREADS), 0, s, false, g_mo_pdl, b)); break;
     MO_AS_CASE(1)
     MO_AS_CASE(2)
     MO_AS_CASE(3)
@@ -898,10 +891,10 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   }
   // lanes per candidate row: enough to cover the box with few points each
   switch (m) {
-    case 2: k_assoc_lattice<2, 1><<<(unsigned)ceil_div(R, 256), 256, 0, s>>>(a); break;
-    case 3: k_assoc_lattice<3, 8><<<(unsigned)ceil_div(R * 8, 256), 256, 0, s>>>(a); break;
-    case 4: k_assoc_lattice<4, 32><<<(unsigned)ceil_div(R * 32, 256), 256, 0, s>>>(a); break;
-    case 5: k_assoc_lattice<5, 32><<<(unsigned)ceil_div(R * 32, 256), 256, 0, s>>>(a); break;
+    case 2: MO_TRY(launch_ex(k_assoc_lattice<2, 1>, dim3((unsigned)ceil_div(R, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
+    case 3: MO_TRY(launch_ex(k_assoc_lattice<3, 8>, dim3((unsigned)ceil_div(R * 8, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
+    case 4: MO_TRY(launch_ex(k_assoc_lattice<4, 32>, dim3((unsigned)ceil_div(R * 32, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
+    case 5: MO_TRY(launch_ex(k_assoc_lattice<5, 32>, dim3((unsigned)ceil_div(R * 32, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
     default: return MO_ERR_PARAM;
   }
   MO_CHECK_LAUNCH();
@@ -914,9 +907,7 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
 
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
   if (R <= 0) return MO_OK;
-  k_assoc_final<<<(unsigned)ceil_div(R, 128), 128, 0, s>>>(a);
-  MO_CHECK_LAUNCH();
-  return MO_OK;
+  return launch_ex(k_assoc_final, dim3((unsigned)ceil_div(R, 128)), dim3(128), 0, s, false, g_mo_pdl, a);
 }
 
 int launch_select(const SelectArgs& a, cudaStream_t s) {

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
                                                             const uint32_t* gen_ptr, mo_var_cfg cfg,
                                                             float* __restrict__ Xo, float* __restrict__ Fo,
                                                             float* __restrict__ ideal, int* __restrict__ domain_flag) {
+  pdl_wait();
   __shared__ uint32_t shK[MAX_SHUFFLE_ROUNDS], shS[MAX_SHUFFLE_ROUNDS];
   __shared__ int shR;
   __shared__ float shMin[16];

@@ -3,6 +3,7 @@
 // Every entry point validates its scalar arguments, carves the caller's
 // workspace, and enqueues kernels on the caller's stream.  No allocation, no
 // synchronisation, no host round trip: device-side outcomes land in `info`.
+#include <stdlib.h>
 #include <string.h>
 
 #include "mo_common.cuh"
@@ -26,6 +27,13 @@ int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float
 #include "k_stream_args.cuh"
 
 namespace mo {
+
+thread_local bool g_mo_pdl = false;
+
+struct PdlScope {  // PDL on for the kernels of one generation enqueued by this host thread
+  PdlScope() { g_mo_pdl = getenv("MO_NO_PDL") == nullptr; }
+  ~PdlScope() { g_mo_pdl = false; }
+};
 
 constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/hist sizing)
 
@@ -373,6 +381,7 @@ static Layout step_layout(const mo_step_args* a) {
 
 static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
   const int64_t n = a->n;
+  PdlScope pdl;
   Layout L = step_layout(a);
   MO_TRY(check_ws(L, a->workspace, a->workspace_bytes));
   if (mask & MO_PHASE_NICHE) mask |= MO_PHASE_NICHE_PREP | MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH;

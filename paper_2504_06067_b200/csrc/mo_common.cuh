@@ -138,6 +138,48 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// Programmatic dependent launch (PDL): kernels of a generation are launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization, so the next
+// kernel's CTAs are scheduled while the previous one drains.  pdl_wait()
+// (griddepcontrol.wait) blocks until the previous grid has completed and its
+// writes are visible -- every such kernel calls it before touching inputs;
+// it is a no-op when the kernel was launched without the attribute.
+// pdl_trigger() lets the dependent grid launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Set by mo_step / mo_step_phases / mo_niche_phases while they enqueue a
+// generation (per host thread): the launchers then add the PDL attribute.
+extern thread_local bool g_mo_pdl;
+
+// Launch with optional cooperative / PDL attributes (cudaLaunchKernelEx).
+template <typename... KArgs, typename... Args>
+inline int launch_ex(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool coop, bool pdl,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...) != cudaSuccess) return MO_ERR_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return MO_ERR_CUDA;
+  return MO_OK;
+}
+
 // Phase trace for the persistent kernels: block 0 / thread 0 stamps the
 // global nanosecond timer into tr[slot] (tr == nullptr: no-op).  Read back by
 // the host (engine.Engine.trace()) to time phases inside one launch.
