@@ -24,6 +24,7 @@
 #include "mo_grid.cuh"
 #include "mo_rng.cuh"
 #include "k_niche_args.cuh"
+#include "mo_prologue.cuh"
 
 namespace mo {
 
@@ -101,10 +102,8 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   // ---- phase 0: running ideal over all R rows (A-4), shuffles, candidate list
   for (int k = tid; k < m; k += blockDim.x) sMin[k] = __int_as_float(0x7f800000);
   const uint32_t gen = a.gen_ptr ? __ldcg(a.gen_ptr) : a.gen;
-  load_shuffle_keys_smem(sKp, sSp, &sRp, (uint32_t)R, a.seed, gen, STREAM_POP_SHUFFLE);
-  load_shuffle_keys_smem(sKr, sSr, &sRr, (uint32_t)w, a.seed, gen, STREAM_REF_SHUFFLE);
   __syncthreads();
-  if (a.mode == PREP_FULL) {
+  if (a.mode == PREP_FULL && !a.ideal_done) {
     // column minima: per column, strided rows, warp reduction, one smem atomic per warp
     for (int k = 0; k < m; ++k) {
       float v = __int_as_float(0x7f800000);
@@ -116,38 +115,17 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     for (int k = tid; k < m; k += blockDim.x) atomic_min_f(&a.ideal[k], sMin[k]);
   }
   if (skipped) return;
-  for (int i = gtid; i < R; i += gthreads) {
-    const int p = (int)prp((uint32_t)i, sKp, sSp, sRp, (uint32_t)R);
-    a.pos_pop[i] = p;
-    a.perm_pop[p] = i;
-    if (a.prom) a.prom[i] = 0;
-    if (a.mode == PREP_PERMS) continue;
-    a.akey[i] = 0ull;
-    if (a.ranks[i] >= 0 && a.ranks[i] <= l) a.cand[atomicAdd(a.ctl, 1)] = i;
-  }
-  for (int j = gtid; j < w; j += gthreads) {
-    const int p = (int)prp((uint32_t)j, sKr, sSr, sRr, (uint32_t)w);
-    a.pos_ref[j] = p;
-    if (a.lat_pos) a.lat_pos[__ldg(a.lat_index + j)] = p;
-    a.perm_ref[p] = j;
-    if (a.rho) {
-      a.rho[j] = 0;
-      a.rho_p[j] = 0;
-      a.take[j] = 0;
-      a.kept[j] = 0;
-      a.fill[j] = 0;
-      a.near_key[j] = ~0ull;
+  if (!a.pro_done) {
+    if (a.mode == PREP_PERMS) {   // op-level niche_select: shuffles + niche state only
+      PrepArgs b = a;
+      b.akey = nullptr;
+      gen_prologue(b, gen, gtid, gthreads, sKp, sSp, &sRp, sKr, sSr, &sRr);
+      return;
     }
-    if (a.zhat)
-      for (int k = 0; k < m; ++k) a.zs[(int64_t)p * m + k] = a.zhat[(int64_t)j * m + k];
+    gen_prologue(a, gen, gtid, gthreads, sKp, sSp, &sRp, sKr, sSr, &sRr);
   }
-  if (a.lvl)
-    for (int q = gtid; q < 2 * LVL_BINS; q += gthreads) a.lvl[q] = 0;
-  if (a.sctl && gtid < 16) a.sctl[gtid] = 0;
-  if (gtid == 0 && a.fb_ctl) {
-    a.fb_ctl[0] = 0;
-    a.info[MO_INFO_ASSOC_FALLBACK] = 0;
-  }
+  for (int i = gtid; i < R; i += gthreads)
+    if (a.ranks[i] >= 0 && a.ranks[i] <= l) a.cand[atomicAdd(a.ctl, 1)] = i;
   if (a.mode != PREP_FULL) return;
   if (gtid < m) {
     a.ext_key[gtid] = ~0ull;

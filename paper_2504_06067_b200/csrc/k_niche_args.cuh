@@ -46,6 +46,8 @@ struct PrepArgs {
   // barrier is self-resetting, and the lattice fallback counters (nullable) are cleared here
   int in_step;
   int* fb_ctl;
+  int pro_done;    // gen_prologue already ran (in k_vary_eval): only the candidate list in phase 0
+  int ideal_done;  // the running ideal was already lowered by the offspring (k_vary_eval)
 };
 
 constexpr int LVL_BINS = 1024;

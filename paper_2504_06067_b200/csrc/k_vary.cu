@@ -8,9 +8,12 @@
 // Philox(q, v, g, SBX).x, PM flag/draw = Philox(i, v, g, PM).x/.y.  The
 // arithmetic is FP64 (oracle order), children are rounded to FP32 once after
 // SBX+clamp and once after PM+clamp.
+#include <string.h>
+
 #include "mo_common.cuh"
 #include "mo_dtlz.cuh"
 #include "mo_rng.cuh"
+#include "mo_prologue.cuh"
 
 namespace mo {
 
@@ -56,10 +59,20 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
                                                             int m, uint64_t seed, uint32_t gen_val,
                                                             const uint32_t* gen_ptr, mo_var_cfg cfg,
                                                             float* __restrict__ Xo, float* __restrict__ Fo,
-                                                            float* __restrict__ ideal, int* __restrict__ domain_flag) {
+                                                            float* __restrict__ ideal, int* __restrict__ domain_flag,
+                                                            PrepArgs pro, int pro_blocks) {
   pdl_wait();
   __shared__ uint32_t shK[MAX_SHUFFLE_ROUNDS], shS[MAX_SHUFFLE_ROUNDS];
   __shared__ int shR;
+  if ((int)blockIdx.x < pro_blocks) {   // first CTAs (scheduled first): the generation prologue
+    __shared__ uint32_t shK2[MAX_SHUFFLE_ROUNDS], shS2[MAX_SHUFFLE_ROUNDS];
+    __shared__ int shR2;
+    const uint32_t g = gen_ptr ? *gen_ptr : gen_val;
+    gen_prologue(pro, g, (int)blockIdx.x * VARY_THREADS + (int)threadIdx.x, pro_blocks * VARY_THREADS, shK, shS,
+                 &shR, shK2, shS2, &shR2);
+    return;
+  }
+  const int vblock = (int)blockIdx.x - pro_blocks;
   __shared__ float shMin[16];
   __shared__ int shA[VARY_PAIRS], shB[VARY_PAIRS];
   __shared__ uint8_t shCross[VARY_PAIRS];
@@ -68,7 +81,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   if (threadIdx.x < 16) shMin[threadIdx.x] = __int_as_float(0x7f800000);
   __syncthreads();
   const int npairs = n / 2;
-  const int q0 = blockIdx.x * VARY_PAIRS;
+  const int q0 = vblock * VARY_PAIRS;
   const int tid = threadIdx.x;
   if (tid < VARY_PAIRS && q0 + tid < npairs) {
     const int q = q0 + tid;
@@ -149,13 +162,22 @@ __global__ void k_min_rows(const float* __restrict__ F, int64_t R, int m, float*
 
 int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint64_t seed, uint32_t gen,
                      const uint32_t* gen_ptr, const mo_var_cfg& cfg, float* Xo, float* Fo, float* ideal,
-                     int* domain_flag, cudaStream_t s) {
+                     int* domain_flag, cudaStream_t s, const PrepArgs* pro) {
   if (n <= 0 || (n & 1) || d < m || m < 2) return MO_ERR_PARAM;
   if (problem < MO_DTLZ1 || problem > MO_DTLZ7) return MO_ERR_PARAM;
-  int pairs = (int)(n / 2);
-  k_vary_eval<<<(unsigned)ceil_div(pairs, VARY_PAIRS), VARY_THREADS, 0, s>>>(problem, X, (int)n, d, m, seed, gen,
-                                                                             gen_ptr, cfg, Xo, Fo, ideal,
-                                                                             domain_flag);
+  const int pairs = (int)(n / 2);
+  const int vblocks = (int)ceil_div(pairs, VARY_PAIRS);
+  int pblocks = 0;
+  PrepArgs p;
+  memset(&p, 0, sizeof(p));
+  if (pro) {
+    p = *pro;
+    const int64_t items = pro->R > pro->w ? pro->R : pro->w;
+    pblocks = (int)ceil_div(items, (int64_t)VARY_THREADS * 4);
+    pblocks = pblocks < 1 ? 1 : (pblocks > 296 ? 296 : pblocks);
+  }
+  k_vary_eval<<<(unsigned)(vblocks + pblocks), VARY_THREADS, 0, s>>>(problem, X, (int)n, d, m, seed, gen, gen_ptr,
+                                                                     cfg, Xo, Fo, ideal, domain_flag, p, pblocks);
   MO_CHECK_LAUNCH();
   return MO_OK;
 }

@@ -12,9 +12,10 @@
 
 namespace mo {
 // k_vary.cu
+struct PrepArgs;
 int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint64_t seed, uint32_t gen,
                      const uint32_t* gen_ptr, const mo_var_cfg& cfg, float* Xo, float* Fo, float* ideal,
-                     int* domain_flag, cudaStream_t s);
+                     int* domain_flag, cudaStream_t s, const PrepArgs* pro = nullptr);
 int launch_init_population(float* X, int64_t n, int d, uint64_t seed, cudaStream_t s);
 int launch_dtlz_eval(int problem, const float* X, int64_t n, int d, int m, float* F, int* domain_flag,
                      cudaStream_t s);
@@ -190,6 +191,8 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.lat_pos = nullptr;
   a.in_step = 0;
   a.fb_ctl = nullptr;
+  a.pro_done = 0;
+  a.ideal_done = 0;
   return a;
 }
 
@@ -298,19 +301,28 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
 static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 2); }
 
-static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cudaStream_t s) {
-  const int64_t n = a->n, R = 2 * n, w = a->w;
-  const int m = a->m;
+static PrepArgs niche_prep_args(const mo_step_args* a, const Layout& L) {
+  const int64_t R = 2 * a->n;
   void* ws = a->workspace;
-  PrepArgs pa = prep_args(L, ws, a->FR, R, m, w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
+  PrepArgs pa = prep_args(L, ws, a->FR, R, a->m, a->w, a->ranks, a->info, a->ideal, a->seed, a->generation, a->zhat,
                           nullptr, PREP_FULL);
   pa.gen_ptr = a->generation_dev;
   pa.in_step = 1;
   pa.fb_ctl = at<int>(ws, L.fctl);
-  if (a->lattice_z && m >= 2 && m <= 5) {
+  if (a->lattice_z && a->m >= 2 && a->m <= 5) {
     pa.lat_index = a->lattice_index;
     pa.lat_pos = a->lattice_pos;
   }
+  return pa;
+}
+
+static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cudaStream_t s) {
+  const int64_t n = a->n, R = 2 * n, w = a->w;
+  const int m = a->m;
+  void* ws = a->workspace;
+  PrepArgs pa = niche_prep_args(a, L);
+  pa.pro_done = (mask & MO_PHASE_VARY) ? 1 : 0;
+  pa.ideal_done = pa.pro_done;
   if (mask & MO_PHASE_NICHE_PREP) MO_TRY(launch_prep(pa, s));
   if (mask & MO_PHASE_NICHE_ASSOC) {
   const int G = shards_of(a->shard_count);
@@ -390,9 +402,14 @@ static int run_phases(const mo_step_args* a, uint32_t mask, cudaStream_t s) {
   if ((mask & (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH)) == (MO_PHASE_NICHE_ASSOC | MO_PHASE_NICHE_FINISH) &&
       shards_of(a->shard_count) > 1)
     return MO_ERR_PARAM;  // the akey max-reduction across shards sits between the two
-  if (mask & MO_PHASE_VARY)
+  if (mask & MO_PHASE_VARY) {
+    // the generation prologue (shuffles, niche-state reset) runs in extra CTAs of the variation kernel,
+    // and the running ideal is lowered by the offspring there (min is idempotent: a later NICHE call
+    // without VARY recomputes both, to the same values)
+    PrepArgs pa = niche_prep_args(a, L);
     MO_TRY(launch_vary_eval(a->problem, a->XR, n, a->d, a->m, a->seed, a->generation, a->generation_dev, a->var,
-                            a->XR + n * a->d, a->FR + n * a->m, nullptr, nullptr, s));
+                            a->XR + n * a->d, a->FR + n * a->m, a->ideal, nullptr, s, &pa));
+  }
   if (mask & MO_PHASE_SORT) {
     if (a->sort_mode == MO_SORT_BITS) {
       MO_TRY(sort_phase(a, L, s));
