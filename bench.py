@@ -46,6 +46,8 @@ WORKLOADS = {
     # C4: the R^2/8 = 500 GB bit-matrix does not fit -> streamed sort; under torchrun it is sharded
     "c4": dict(problem="DTLZ7", m=3, d=22, n=1000000, sort="stream",
                label="C4 DTLZ7 m=3 d=22 N=1M (w=998991, H=1412)"),
+    # C4's shape at N=100k (quick checks of the sharded path)
+    "c4s": dict(problem="DTLZ7", m=3, d=22, n=100000, sort="stream", label="C4-small DTLZ7 m=3 d=22 N=100k"),
 }
 METRIC = "NSGA-III generations/sec on DTLZ (m=3–10, N to 1M+) at 1/2/4/8 B200 vs CPU ref"
 
@@ -384,7 +386,8 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # MO_DIST_BACKEND=gloo: functional multi-process runs with several ranks on one GPU
+        dist.init_process_group(os.environ.get("MO_DIST_BACKEND", "nccl"))
     r = run_ours(args, rank, world)
     if rank != 0:
         if world > 1:

@@ -364,16 +364,32 @@ _SIGN64 = -(1 << 63)
 
 
 def run_collective(req, group):
-    """Execute one collective request of Engine.step_gen over torch.distributed."""
+    """Execute one collective request of Engine.step_gen over torch.distributed.
+
+    NCCL moves the device buffers directly (NVLink).  Under gloo with device
+    buffers (several processes sharing one GPU in the tests) the bytes are
+    staged through host memory; the collective itself is the same."""
     import torch.distributed as dist
     kind = req[0]
+    staged = req[1].is_cuda and dist.get_backend(group) == "gloo"
     if kind == "all_gather":
-        dist.all_gather_into_tensor(req[2], req[1], group=group)
+        src, dst = req[1], req[2]
+        if staged:
+            host = dst.cpu()
+            dist.all_gather_into_tensor(host, src.cpu(), group=group)
+            dst.copy_(host)
+        else:
+            dist.all_gather_into_tensor(dst, src, group=group)
     elif kind == "all_max_u64":
         # packed (ord(t), ~position) keys are unsigned: flip the sign bit so the signed max agrees
         t = req[1]
         t.bitwise_xor_(_SIGN64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        if staged:
+            host = t.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.MAX, group=group)
+            t.copy_(host)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         t.bitwise_xor_(_SIGN64)
     else:
         raise ValueError(kind)
