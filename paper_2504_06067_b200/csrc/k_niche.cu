@@ -371,9 +371,12 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
   for (int k = 0; k < M; ++k) ok = ok && fn[k] >= 0.0f;
   float best = -__int_as_float(0x7f800000);
   int bp = 0x7fffffff;
-  if (ok) {
-    int lo[M], ext[M];
-    int total = 1;
+  // the box (lo, extent per coordinate) is computed once per group, by its leader, in FP64, and broadcast
+  int lo[M], ext[M];
+  float inv[M];
+  int total = 0;
+  if (sub == 0 && ok) {
+    total = 1;
 #pragma unroll
     for (int k = 0; k < M - 1; ++k) {
       const double x = (double)fn[k] / s * (double)H;
@@ -382,13 +385,24 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
       ext[k] = max(0, hi - lo[k] + 1);
       total *= ext[k];
     }
+  }
+  total = __shfl_sync(MO_FULL, total, 0, LPR);
+#pragma unroll
+  for (int k = 0; k < M - 1; ++k) {
+    lo[k] = __shfl_sync(MO_FULL, lo[k], 0, LPR);
+    ext[k] = __shfl_sync(MO_FULL, ext[k], 0, LPR);
+    inv[k] = ext[k] > 0 ? 1.0f / (float)ext[k] : 0.0f;
+  }
+  if (ok) {
     for (int q = sub; q < total; q += LPR) {
       int rem = q, rest, idx = 0;
-      int kv[M];                           // mixed-radix decode of the box index, k_{m-2} fastest
+      int kv[M];  // mixed-radix decode of the box index, k_{m-2} fastest; (rem + .5) / ext is exact in
+                  // FP32 for these small operands, so no integer division
 #pragma unroll
       for (int k = M - 2; k >= 0; --k) {
-        kv[k] = lo[k] + rem % ext[k];
-        rem /= ext[k];
+        const int qk = (int)(((float)rem + 0.5f) * inv[k]);
+        kv[k] = lo[k] + (rem - qk * ext[k]);
+        rem = qk;
       }
       rest = H;
 #pragma unroll
@@ -428,6 +442,57 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
   } else {
     a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row;
     atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
+  }
+}
+
+// Full scan for the few rows the lattice certificate rejected: items = (row, slice of the shard's
+// reference range, 512 points); a warp per item, lanes stride the slice in shuffled order with the
+// canonical key and a strict '>' (first maximum per lane), a warp reduction (max key, lowest position),
+// and an atomicMax merge of the slices into akey -- many short independent scans instead of a few long
+// latency-bound ones.
+template <int M>
+__global__ void __launch_bounds__(256) k_assoc_fallback(AssocArgs a) {
+  pdl_wait();
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int nfb = __ldcg(a.fb_ctl);
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  constexpr int SLICE = 512;
+  const int nslice = (a.zend - a.zbeg + SLICE - 1) / SLICE;
+  for (int it = warp; it < nfb * nslice; it += nwarps) {
+    const int c = it / nslice, sl = it - c * nslice;
+    const int row = __ldcg(a.fb_cand + c);
+    const int p0 = a.zbeg + sl * SLICE, p1 = min(a.zend, p0 + SLICE);
+    float fn[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      float v = a.F[(int64_t)row * M + k];
+      if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+      if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+      fn[k] = v;
+    }
+    float best = -__int_as_float(0x7f800000);
+    int bp = 0x7fffffff;
+#pragma unroll 4
+    for (int p = p0 + lane; p < p1; p += 32) {
+      const float t = canon_dot<M>(fn, a.zs + (int64_t)p * M);
+      if (t > best) {
+        best = t;
+        bp = p;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float tb = __shfl_xor_sync(MO_FULL, best, o);
+      const int pb = __shfl_xor_sync(MO_FULL, bp, o);
+      if (tb > best || (tb == best && pb < bp)) {
+        best = tb;
+        bp = pb;
+      }
+    }
+    if (lane == 0 && bp != 0x7fffffff)
+      atomicMax(&a.akey[row], ((unsigned long long)f2ord(best) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp));
   }
 }
 
@@ -875,12 +940,18 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     case 5: MO_TRY(launch_ex(k_assoc_lattice<5, 32>, dim3((unsigned)ceil_div(R * 32, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
     default: return MO_ERR_PARAM;
   }
-  MO_CHECK_LAUNCH();
-  // fallback rows: the full scan over this launch's reference range
-  AssocArgs b = a;
-  b.cand = a.fb_cand;
-  b.ctl = a.fb_ctl;
-  return launch_assoc(b, m, R, s);
+  // fallback rows: a warp-per-row full scan over this launch's reference range
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const dim3 fg((unsigned)sms), fb(256);
+  switch (m) {
+    case 2: return launch_ex(k_assoc_fallback<2>, fg, fb, 0, s, false, g_mo_pdl, a);
+    case 3: return launch_ex(k_assoc_fallback<3>, fg, fb, 0, s, false, g_mo_pdl, a);
+    case 4: return launch_ex(k_assoc_fallback<4>, fg, fb, 0, s, false, g_mo_pdl, a);
+    case 5: return launch_ex(k_assoc_fallback<5>, fg, fb, 0, s, false, g_mo_pdl, a);
+    default: return MO_ERR_PARAM;
+  }
 }
 
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {

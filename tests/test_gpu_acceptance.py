@@ -1,0 +1,87 @@
+"""SPEC.md acceptance criteria that need the engine and the metrics together (GPU).
+
+* Criterion 5 (population-size trend, Fig. 3 analogue): DTLZ2
+  m=3 d=12, 100 generations, n in {50, 200, 800}, 10 seeds -- the median final
+  IGD strictly decreases with n and n=800 vs n=50 differ (Mann-Whitney
+  p < 0.05).
+* Criterion 7 (comparative speed, Table I analogue): the batched
+  niche selection at n=3200 (DTLZ2 m=3) is >= 5x faster than the scalar
+  Alg. 1 oracle back-end, and the per-generation time grows sub-quadratically
+  from n=200 to n=3200 (ratio < 256 for the 16x size increase).
+* DTLZ2 m=3 d=12 n=92, 200 generations -> IGD < 0.08.
+"""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2504_06067_b200 as pkg
+    from paper_2504_06067_b200 import _lib
+    _lib.lib()
+    return pkg
+
+
+def _final_igd(M, n, seed, gens, ref):
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=n, m=3, d=12, generations=gens, seed=seed)
+    _, st = M.engine.run(cfg, record=False, graph=True)
+    torch.cuda.synchronize()
+    return M.metrics.igd(st.F, ref)
+
+
+def test_spec_engine_igd_example(M):
+    ref = M.metrics.dtlz_pf_sample("DTLZ2", 3, 10_000).astype(np.float32)
+    assert _final_igd(M, 92, 0, 200, ref) < 0.08
+
+
+def test_criterion5_population_size_trend(M):
+    from scipy.stats import mannwhitneyu
+    ref = M.metrics.dtlz_pf_sample("DTLZ2", 3, 10_000).astype(np.float32)
+    igd = {n: [_final_igd(M, n, s, 100, ref) for s in range(10)] for n in (50, 200, 800)}
+    med = [np.median(igd[n]) for n in (50, 200, 800)]
+    assert med[0] > med[1] > med[2], med
+    assert mannwhitneyu(igd[800], igd[50], alternative="less").pvalue < 0.05
+
+
+def _gen_ms(M, n, gens=20):
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=n, m=3, d=12, generations=gens + 3, seed=1)
+    eng = M.engine.Engine(cfg, graph=True)
+    eng.replay(3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    eng.replay(gens)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / gens
+
+
+def test_criterion7_comparative_speed(M):
+    from oracle.manyobj_ref import dominance as Odom
+    from oracle.manyobj_ref import niche as On
+    n = 3200
+    # GPU: the niche phase of one generation (normalise .. compaction), eager, event-timed
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=n, m=3, d=12, generations=10, seed=2)
+    eng = M.engine.Engine(cfg)
+    prof = {}
+    for _ in range(5):
+        eng.step()
+    for _ in range(5):
+        eng.step(profile=prof)
+    gpu_niche = prof["t_niche"] / 5
+    # CPU: the scalar Alg. 1 oracle back-end on the same kind of generation
+    FR = eng.FR[eng.cur ^ 1].cpu().numpy().copy()
+    ranks = Odom.non_dominated_sort(FR, stop_at=n)
+    split = Odom.split_fronts(ranks, n)
+    zhat = torch.as_tensor(eng.zhat).cpu().numpy()
+    ideal = FR.min(axis=0)
+    t0 = time.perf_counter()
+    On.select(FR, ranks, split, ideal, zhat, 2, 9, backend="oracle", gen=np.random.default_rng(0))
+    cpu_niche = time.perf_counter() - t0
+    assert cpu_niche / gpu_niche >= 5.0, (cpu_niche, gpu_niche)
+    assert _gen_ms(M, 3200) / _gen_ms(M, 200) < 256.0
