@@ -819,17 +819,23 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         return (int)s;
       },
       [&](int64_t i, int pre) {
-        if (a.X_next) {
-          const float* src = a.XR + i * a.dvars;
-          float* dst = a.X_next + (int64_t)pre * a.dvars;
-          for (int v = 0; v < a.dvars; ++v) dst[v] = src[v];
-          const float* fs = a.FR + i * a.m;
-          float* fd = a.F_next + (int64_t)pre * a.m;
-          for (int v = 0; v < a.m; ++v) fd[v] = fs[v];
-        }
+        if (a.X_next) a.bucket[pre] = (int)i;   // source row of survivor `pre` (bucket storage is free now)
       },
       sh);
   grid_sync(a.g.bar);
+  if (a.X_next) {
+    // coalesced gather: consecutive threads write consecutive output floats
+    const int d = a.dvars, mm = a.m;
+    const int64_t nx = (int64_t)nsurv * d, nf = (int64_t)nsurv * mm;
+    for (int64_t e = gtid; e < nx; e += gthreads) {
+      const int r = (int)(e / d);
+      a.X_next[e] = a.XR[(int64_t)__ldcg(a.bucket + r) * d + (e - (int64_t)r * d)];
+    }
+    for (int64_t e = gtid; e < nf; e += gthreads) {
+      const int r = (int)(e / mm);
+      a.F_next[e] = a.FR[(int64_t)__ldcg(a.bucket + r) * mm + (e - (int64_t)r * mm)];
+    }
+  }
   trace_mark(a.trace, 35);
   for (int i = gtid; i < R; i += gthreads) {
     const int r = a.ranks[i];
@@ -962,7 +968,9 @@ int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
 int launch_select(const SelectArgs& a, cudaStream_t s) {
   if (!a.in_step && cudaMemsetAsync(a.g.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   int blocks = select_grid_blocks();
-  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), SELECT_THREADS * 2);
+  // ~128 rows per CTA (one CTA per SM at C2): the phases are latency-bound, and more CTAs in flight beat
+  // the extra barrier arrivals (C2: 64 -> 44 us, rows/CTA 1024 -> 128)
+  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), 128);
   if (blocks > need) blocks = need < 1 ? 1 : need;
   return launch_coop(k_select, blocks, SELECT_THREADS, a, s);
 }
