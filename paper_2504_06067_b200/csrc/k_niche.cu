@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
       }
       if (rest < 0) continue;
       const int p = __ldg(a.lat_pos + idx);
-      const float t = canon_dot<M>(fn, a.lat_z + (int64_t)idx * M);
+      const float t = canon_dot<M>(fn, a.lat_z + (int64_t)idx * M);   // (lat_pos -> zs measured slower)
       if (t > best || (t == best && p < bp)) {
         best = t;
         bp = p;
