@@ -180,7 +180,21 @@ __global__ void __launch_bounds__(DOM_TILE) k_dom_tile_generic(const float* __re
 
 constexpr int DOMS_THREADS = DOM_TILE / 2;  // two j columns per thread
 
-template <int M>
+template <int NW>
+__device__ __forceinline__ void store_words(uint32_t* dst, const uint32_t* w) {
+  if (NW % 4 == 0) {
+#pragma unroll
+    for (int c = 0; c < NW; c += 4) reinterpret_cast<uint4*>(dst)[c / 4] = make_uint4(w[c], w[c + 1], w[c + 2], w[c + 3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < NW; c += 2) reinterpret_cast<uint2*>(dst)[c / 2] = make_uint2(w[c], w[c + 1]);
+  }
+}
+
+// TI = i rows per tile (256 or 128): a (256-row i block, 256-row j block) pair is split into 256/TI
+// tiles of TI i rows each -- the same work in more, shorter CTAs, which shrinks the last partial wave
+// (C2: 3,160 tiles of 256 = 2.1 waves -> 6,320 of 128).
+template <int M, int TI>
 __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* __restrict__ FS,
                                                                   const float* __restrict__ blkmin,
                                                                   const float* __restrict__ blkmax,
@@ -189,14 +203,17 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
                                                                   uint8_t* __restrict__ hasdom) {
   pdl_wait();
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sFi[DOM_TILE * MP];
-  __shared__ uint32_t sB2[DOM_TILE * 9];
+  constexpr int HALVES = DOM_TILE / TI;   // tiles per block pair
+  constexpr int NW = TI / 32;             // words of a j row written by this tile
+  __shared__ __align__(16) float sFi[TI * MP];
+  __shared__ uint32_t sB2[TI * 9];
   int bi, bj;
-  tri_decode(blockIdx.x, bi, bj);
+  tri_decode(blockIdx.x / HALVES, bi, bj);
+  const int h = blockIdx.x % HALVES;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int i0 = bi * DOM_TILE, j0 = bj * DOM_TILE;
+  const int i0 = bi * DOM_TILE + h * TI, j0 = bj * DOM_TILE;
   // rows past R are padded with +FLT_MAX: they dominate nothing and are never stored
-  for (int e = tid; e < DOM_TILE * MP; e += DOMS_THREADS) {
+  for (int e = tid; e < TI * MP; e += DOMS_THREADS) {
     int r = e / MP, k = e - r * MP;
     int i = i0 + r;
     sFi[e] = (k < M && i < R) ? FS[(int64_t)i * M + k] : 3.402823466e38f;
@@ -210,12 +227,12 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
   }
   const bool fast = (bi < bj) && (__ldg(blkmax + bi) < __ldg(blkmin + bj));
   __syncthreads();
-  uint32_t wa[8], wb[8];
+  uint32_t wa[NW], wb[NW];
   if (fast) {
     // m-long setp.le.and chains + predicated OR.  (A sign-of-difference variant -- m FADD on the FMA
     // pipe + LOP3 + funnel shift -- measured no faster: the tile is issue-bound, not ALU-bound.)
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < NW; ++c) {
       uint32_t acca = 0, accb = 0;
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
@@ -231,7 +248,7 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
     }
   } else {
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < NW; ++c) {
       uint32_t acca = 0, accb = 0, bala = 0, balb = 0;
 #pragma unroll
       for (int b = 0; b < 32; ++b) {
@@ -250,25 +267,27 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
       sB2[(c * 32 + lane) * 9 + warp + 4] = balb;
     }
   }
+  uint32_t anya = 0, anyb = 0;
+#pragma unroll
+  for (int c = 0; c < NW; ++c) {
+    anya |= wa[c];
+    anyb |= wb[c];
+  }
   if (ja < R) {
-    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)ja * W + (int64_t)bi * 8);
-    dst[0] = make_uint4(wa[0], wa[1], wa[2], wa[3]);
-    dst[1] = make_uint4(wa[4], wa[5], wa[6], wa[7]);
-    if ((wa[0] | wa[1] | wa[2] | wa[3] | wa[4] | wa[5] | wa[6] | wa[7]) != 0u) hasdom[ja] = 1;
+    store_words<NW>(bits + (int64_t)ja * W + (int64_t)(i0 / 32), wa);
+    if (anya) hasdom[ja] = 1;
   }
   if (jb < R) {
-    uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)jb * W + (int64_t)bi * 8);
-    dst[0] = make_uint4(wb[0], wb[1], wb[2], wb[3]);
-    dst[1] = make_uint4(wb[4], wb[5], wb[6], wb[7]);
-    if ((wb[0] | wb[1] | wb[2] | wb[3] | wb[4] | wb[5] | wb[6] | wb[7]) != 0u) hasdom[jb] = 1;
+    store_words<NW>(bits + (int64_t)jb * W + (int64_t)(i0 / 32), wb);
+    if (anyb) hasdom[jb] = 1;
   }
   if (fast) {
     // rows i of the last S bucket of bi may share it with rows of bj: their
     // words of block bj lie below wend and are read by the peel, so they must
     // hold zeros (no j of a fast tile dominates an i) rather than stale bits
-    const int ilast = min(R, i0 + DOM_TILE) - 1;
-    if (__ldg(wend + ilast) > bj * 8) {
-      for (int r = tid; r < DOM_TILE; r += DOMS_THREADS) {
+    const int ilast = min(R, i0 + TI) - 1;
+    if (ilast >= i0 && __ldg(wend + ilast) > bj * 8) {
+      for (int r = tid; r < TI; r += DOMS_THREADS) {
         const int i = i0 + r;
         if (i < R && __ldg(wend + i) > bj * 8) {
           uint4* dst = reinterpret_cast<uint4*>(bits + (int64_t)i * W + (int64_t)bj * 8);
@@ -280,7 +299,7 @@ __global__ void __launch_bounds__(DOMS_THREADS) k_dom_tile_sorted(const float* _
   }
   if (!fast && bi != bj) {
     __syncthreads();
-    for (int r = tid; r < DOM_TILE; r += DOMS_THREADS) {
+    for (int r = tid; r < TI; r += DOMS_THREADS) {
       const int i = i0 + r;
       if (i < R) {
         const uint32_t* sw = sB2 + r * 9;
@@ -335,15 +354,19 @@ int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* bl
   if (R <= 0) return MO_OK;
   const int64_t W = words_per_row(R);
   const int64_t nb = W / 8;
-  const int64_t tiles = nb * (nb + 1) / 2;
+  const int64_t pairs = nb * (nb + 1) / 2;
+  // 128-row i tiles: 256-row tiles leave a ragged last wave on small grids (C2: 0.105 -> 0.095 ms;
+  // 64-row tiles measured the same as 128)
+  constexpr int TI = 128;
+  const int64_t tiles = pairs * (DOM_TILE / TI);
   if (tiles > 0x7fffffffll) return MO_ERR_PARAM;
   if (clear_hasdom && cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
   dim3 grid((unsigned)tiles);
   switch (m) {
 #define MO_DOMS_CASE(MM) \
   case MM:                                                                                                  \
-    MO_TRY(launch_ex(k_dom_tile_sorted<MM>, grid, dim3(DOMS_THREADS), 0, s, false, g_mo_pdl, FS, blkmin, blkmax, \
-                     wend, (int)R, bits, W, hasdom));                                                        \
+    MO_TRY(launch_ex(k_dom_tile_sorted<MM, TI>, grid, dim3(DOMS_THREADS), 0, s, false, g_mo_pdl, FS, blkmin,    \
+                     blkmax, wend, (int)R, bits, W, hasdom));                                                 \
     break;
     MO_DOMS_CASE(2)
     MO_DOMS_CASE(3)
