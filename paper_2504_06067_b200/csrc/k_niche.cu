@@ -215,8 +215,12 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 // ---------------------------------------------------------- association
 
 constexpr int ASSOC_THREADS = 256;
-constexpr int ASSOC_RB = 4;                        // rows per thread
-constexpr int ASSOC_ROWS = ASSOC_THREADS * ASSOC_RB;
+// candidate rows per thread (registers) and rows per item
+template <int M>
+struct AssocShape {
+  static constexpr int RB = 4;   // (2 rows at m = 10: fewer registers but slower, C3 10.0 -> 10.6 ms)
+  static constexpr int ROWS = ASSOC_THREADS * RB;
+};
 constexpr int ASSOC_PTILE = 256;                   // reference points staged per smem tile
 
 template <int M>
@@ -227,7 +231,7 @@ __device__ __forceinline__ float canon_dot(const float* f, const float* z) {
   return t;
 }
 
-// rows x reference-split grid.  Thread: ASSOC_RB candidate rows in registers;
+// rows x reference-split grid.  Thread: AssocShape<M>::RB candidate rows in registers;
 // the block streams its reference range through shared memory (shuffled
 // order) two points per step; strict '>' keeps the first maximum, and the
 // splits merge through a 64-bit atomicMax of (ord(t), ~position).
@@ -236,10 +240,10 @@ __device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rb
   constexpr int MP = (M + 3) & ~3;
   if (p0 >= p1) return;
   const int tid = threadIdx.x;
-  float fn[ASSOC_RB][M];
-  int rows[ASSOC_RB];
+  float fn[AssocShape<M>::RB][M];
+  int rows[AssocShape<M>::RB];
 #pragma unroll
-  for (int r = 0; r < ASSOC_RB; ++r) {
+  for (int r = 0; r < AssocShape<M>::RB; ++r) {
     const int c = rbase + r * ASSOC_THREADS + tid;
     rows[r] = c < ncand ? __ldcg(a.cand + c) : -1;
     const int row = rows[r] < 0 ? 0 : rows[r];
@@ -251,10 +255,10 @@ __device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rb
       fn[r][k] = v;
     }
   }
-  float best[ASSOC_RB];
-  int bp[ASSOC_RB];
+  float best[AssocShape<M>::RB];
+  int bp[AssocShape<M>::RB];
 #pragma unroll
-  for (int r = 0; r < ASSOC_RB; ++r) {
+  for (int r = 0; r < AssocShape<M>::RB; ++r) {
     best[r] = -__int_as_float(0x7f800000);
     bp[r] = p0;
   }
@@ -275,7 +279,7 @@ __device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rb
         z1[k] = sz[(p + 1) * MP + k];
       }
 #pragma unroll
-      for (int r = 0; r < ASSOC_RB; ++r) {
+      for (int r = 0; r < AssocShape<M>::RB; ++r) {
         const float ta = canon_dot<M>(fn[r], z0);
         const float tb = canon_dot<M>(fn[r], z1);
         if (ta > best[r]) {
@@ -290,7 +294,7 @@ __device__ __forceinline__ void assoc_item(const AssocArgs& a, int ncand, int rb
     }
   }
 #pragma unroll
-  for (int r = 0; r < ASSOC_RB; ++r) {
+  for (int r = 0; r < AssocShape<M>::RB; ++r) {
     if (rows[r] >= 0) {
       const unsigned long long key = ((unsigned long long)f2ord(best[r]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp[r]);
       atomicMax(&a.akey[rows[r]], key);
@@ -308,18 +312,20 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
   const int ncand = __ldcg(a.ctl);
   // persistent schedule sized on the device from the real candidate count:
   // (row block, reference split) items spread over exactly gridDim.x blocks
-  const int nrb = (ncand + ASSOC_ROWS - 1) / ASSOC_ROWS;
+  constexpr int ROWS = AssocShape<M>::ROWS;
+  const int nrb = (ncand + ROWS - 1) / ROWS;
   if (nrb == 0) return;
   const int wr = a.zend - a.zbeg;
   if (wr <= 0) return;
-  int splits = (int)gridDim.x / nrb;
+  // ~4 items per CTA so the last wave is short (items are long: 1024 rows x a slice of the points)
+  int splits = (4 * (int)gridDim.x + nrb - 1) / nrb;
   const int maxsplit = (wr + 63) / 64;
   splits = splits < 1 ? 1 : (splits > maxsplit ? maxsplit : splits);
   const int psplit = (wr + splits - 1) / splits;
   const int items = nrb * splits;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int p0 = a.zbeg + (item % splits) * psplit;
-    assoc_item<M>(a, ncand, (item / splits) * ASSOC_ROWS, p0, min(a.zend, p0 + psplit), sz);
+    assoc_item<M>(a, ncand, (item / splits) * ROWS, p0, min(a.zend, p0 + psplit), sz);
   }
 }
 
