@@ -35,15 +35,29 @@ def _seqsum(terms):
     return s
 
 
+G_LANES = 8
+
+
+def _gsum(terms):
+    """The g sum over the distance variables in the GPU's order: G_LANES partial sums (terms l, l+8,
+    l+16, ... left to right), then the fixed pairwise tree ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7)) that the
+    xor-shuffle butterfly of an 8-lane group computes.  (Pinned with the kernels.)"""
+    n, k = terms.shape
+    p = [_seqsum(terms[:, l::G_LANES]) if l < k else np.zeros(n) for l in range(G_LANES)]
+    a = [p[l] + p[l + 4] for l in range(4)]
+    b = [a[0] + a[2], a[1] + a[3]]
+    return b[0] + b[1]
+
+
 def _g_rastrigin(xm):
     k = xm.shape[1]
     t = xm - 0.5
-    return 100.0 * (k + _seqsum(t * t - np.cos(20.0 * np.pi * t)))
+    return 100.0 * (k + _gsum(t * t - np.cos(20.0 * np.pi * t)))
 
 
 def _g_sphere(xm):
     t = xm - 0.5
-    return _seqsum(t * t)
+    return _gsum(t * t)
 
 
 def _spherical(theta, g):
@@ -90,7 +104,7 @@ def dtlz_eval(problem, X):
         pos = xp ** 100.0 if kind == "DTLZ4" else xp
         return _spherical(pos * (np.pi / 2.0), g)
     if kind in ("DTLZ5", "DTLZ6"):
-        g = _g_sphere(xm) if kind == "DTLZ5" else _seqsum(xm ** 0.1)
+        g = _g_sphere(xm) if kind == "DTLZ5" else _gsum(xm ** 0.1)
         theta = np.empty_like(xp)
         if m > 1:
             theta[:, 0] = xp[:, 0] * (np.pi / 2.0)
@@ -99,7 +113,7 @@ def dtlz_eval(problem, X):
         return _spherical(theta, g)
     # DTLZ7
     k = xm.shape[1]
-    g = 1.0 + 9.0 / k * _seqsum(xm)
+    g = 1.0 + 9.0 / k * _gsum(xm)
     f = np.empty((n, m))
     f[:, : m - 1] = xp
     h = m - _seqsum(xp / (1.0 + g)[:, None] * (1.0 + np.sin(3.0 * np.pi * xp)))

@@ -830,16 +830,15 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       sh);
   grid_sync(a.g.bar);
   if (a.X_next) {
-    // coalesced gather: consecutive threads write consecutive output floats
+    // coalesced gather, one warp per survivor row: lanes stride the d + m columns
     const int d = a.dvars, mm = a.m;
-    const int64_t nx = (int64_t)nsurv * d, nf = (int64_t)nsurv * mm;
-    for (int64_t e = gtid; e < nx; e += gthreads) {
-      const int r = (int)(e / d);
-      a.X_next[e] = a.XR[(int64_t)__ldcg(a.bucket + r) * d + (e - (int64_t)r * d)];
-    }
-    for (int64_t e = gtid; e < nf; e += gthreads) {
-      const int r = (int)(e / mm);
-      a.F_next[e] = a.FR[(int64_t)__ldcg(a.bucket + r) * mm + (e - (int64_t)r * mm)];
+    for (int r = gwarp; r < nsurv; r += nwarps) {
+      const int64_t src = __ldcg(a.bucket + r);
+      const float* xs = a.XR + src * d;
+      float* xd = a.X_next + (int64_t)r * d;
+#pragma unroll 4
+      for (int v = lane; v < d; v += 32) xd[v] = xs[v];
+      if (lane < mm) a.F_next[(int64_t)r * mm + lane] = a.FR[src * mm + lane];
     }
   }
   trace_mark(a.trace, 35);

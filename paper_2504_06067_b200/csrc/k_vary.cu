@@ -114,17 +114,35 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     Xo[(int64_t)(2 * q + 1) * d + v] = o2;
   }
   __syncthreads();
-  const int etasks = 2 * npb * m;
+  // Phase 3a: g of every child by a group of 8 lanes (strided partial sums + the pinned xor
+  // butterfly, = dtlz_g), and the domain check; 256 threads = 32 children x 8 lanes
+  static_assert(VARY_THREADS == 2 * VARY_PAIRS * G_LANES, "one 8-lane group per child");
+  __shared__ double shG[2 * VARY_PAIRS];
+  const int nch = 2 * npb;
+  {
+    const int cl = tid / G_LANES, l = tid % G_LANES;
+    double p = 0.0;
+    bool ok = true;
+    if (cl < nch) {
+      const float* x = Xo + (int64_t)(2 * q0 + cl) * d;
+      p = dtlz_g_partial(problem, x, d, m, l);
+      if (domain_flag)
+        for (int v = l; v < d; v += G_LANES) ok = ok && (x[v] >= 0.0f) && (x[v] <= 1.0f);
+    }
+    p = p + __shfl_xor_sync(MO_FULL, p, 4, G_LANES);
+    p = p + __shfl_xor_sync(MO_FULL, p, 2, G_LANES);
+    p = p + __shfl_xor_sync(MO_FULL, p, 1, G_LANES);
+    if (cl < nch && l == 0) shG[cl] = dtlz_g_finish(problem, p, d - m + 1);
+    if (!ok) atomicOr(domain_flag, 1);
+  }
+  __syncthreads();
+  // Phase 3b: one thread per (child, objective)
+  const int etasks = nch * m;
   for (int e = tid; e < etasks; e += VARY_THREADS) {
     const int cl = e / m, j = e - cl * m;
     const int child = 2 * q0 + cl;
     const float* x = Xo + (int64_t)child * d;
-    if (j == 0 && domain_flag) {
-      bool ok = true;
-      for (int v = 0; v < d; ++v) ok = ok && (x[v] >= 0.0f) && (x[v] <= 1.0f);
-      if (!ok) atomicOr(domain_flag, 1);
-    }
-    const float f = dtlz_eval_obj(problem, x, d, m, j);
+    const float f = dtlz_eval_obj(problem, x, m, j, shG[cl]);
     Fo[(int64_t)child * m + j] = f;
     if (ideal) {
       if (j < 16) atomic_min_float(&shMin[j], f);

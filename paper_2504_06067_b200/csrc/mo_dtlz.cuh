@@ -11,43 +11,57 @@
 
 namespace mo {
 
+// One term of the g sum (distance variable t = v - (m-1)), FP64.
+__device__ __forceinline__ double dtlz_g_term(int problem, float xv) {
+  const double PI = 3.141592653589793;
+  if (problem == 1 || problem == 3) {
+    const double t = (double)xv - 0.5;
+    return t * t - cos(20.0 * PI * t);
+  }
+  if (problem == 2 || problem == 4 || problem == 5) {
+    const double t = (double)xv - 0.5;
+    return t * t;
+  }
+  if (problem == 6) return pow((double)xv, 0.1);
+  return (double)xv;  // DTLZ7
+}
+
+// g from the summed terms.
+__device__ __forceinline__ double dtlz_g_finish(int problem, double s, int k) {
+  if (problem == 1 || problem == 3) return 100.0 * ((double)k + s);
+  if (problem == 7) return 1.0 + (9.0 / (double)k) * s;
+  return s;
+}
+
+// Partial sum of lane l (of G_LANES) of the g terms: terms l, l + 8, ... left to right.
+constexpr int G_LANES = 8;
+__device__ __forceinline__ double dtlz_g_partial(int problem, const float* __restrict__ x, int d, int m, int l) {
+  double s = 0.0;
+  for (int v = m - 1 + l; v < d; v += G_LANES) s = s + dtlz_g_term(problem, x[v]);
+  return s;
+}
+
+// The whole g sum in the pinned order (8 strided partials, then ((p0+p4)+(p2+p6)) + ((p1+p5)+(p3+p7)),
+// = the xor butterfly of an 8-lane group), sequentially.
+__device__ inline double dtlz_g(int problem, const float* __restrict__ x, int d, int m) {
+  double p[G_LANES];
+  for (int l = 0; l < G_LANES; ++l) p[l] = dtlz_g_partial(problem, x, d, m, l);
+  const double a0 = p[0] + p[4], a1 = p[1] + p[5], a2 = p[2] + p[6], a3 = p[3] + p[7];
+  return dtlz_g_finish(problem, (a0 + a2) + (a1 + a3), d - m + 1);
+}
+
 // x: FP32 row (d entries, stride 1); f: FP32 output (m entries).  Returns
 // true iff every x lies in [0,1] (DomainError otherwise).
 __device__ inline bool dtlz_eval_row(int problem, const float* __restrict__ x, int d, int m,
                                      float* __restrict__ f) {
   const double PI = 3.141592653589793;
-  const int k = d - m + 1;
   bool ok = true;
   for (int v = 0; v < d; ++v) {
     float xv = x[v];
     ok = ok && (xv >= 0.0f) && (xv <= 1.0f);
   }
-  // g over the distance variables x[m-1 .. d-1], summed left to right
-  double g = 0.0;
-  if (problem == 1 || problem == 3) {
-    const double c20 = 20.0 * PI;
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) {
-      double t = (double)x[v] - 0.5;
-      s = s + (t * t - cos(c20 * t));
-    }
-    g = 100.0 * ((double)k + s);
-  } else if (problem == 2 || problem == 4 || problem == 5) {
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) {
-      double t = (double)x[v] - 0.5;
-      s = s + t * t;
-    }
-    g = s;
-  } else if (problem == 6) {
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) s = s + pow((double)x[v], 0.1);
-    g = s;
-  } else {  // DTLZ7
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) s = s + (double)x[v];
-    g = 1.0 + (9.0 / (double)k) * s;
-  }
+  // g over the distance variables x[m-1 .. d-1] (pinned grouped order, dtlz_g)
+  const double g = dtlz_g(problem, x, d, m);
 
   if (problem == 1) {
     for (int j = 0; j < m; ++j) {
@@ -96,37 +110,12 @@ __device__ inline bool dtlz_eval_row(int problem, const float* __restrict__ x, i
   return ok;
 }
 
-// Objective j of one individual -- the same operation order as dtlz_eval_row
-// (so the two agree bit for bit); used by the fused variation kernel, which
-// evaluates one (child, objective) per thread.
-__device__ inline float dtlz_eval_obj(int problem, const float* __restrict__ x, int d, int m, int j) {
+// Objective j of one individual given its g -- the same operation order as
+// dtlz_eval_row (so the two agree bit for bit); used by the fused variation
+// kernel, which sums g with 8 lanes per child and then evaluates one (child,
+// objective) per thread.
+__device__ inline float dtlz_eval_obj(int problem, const float* __restrict__ x, int m, int j, double g) {
   const double PI = 3.141592653589793;
-  const int k = d - m + 1;
-  double g = 0.0;
-  if (problem == 1 || problem == 3) {
-    const double c20 = 20.0 * PI;
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) {
-      double t = (double)x[v] - 0.5;
-      s = s + (t * t - cos(c20 * t));
-    }
-    g = 100.0 * ((double)k + s);
-  } else if (problem == 2 || problem == 4 || problem == 5) {
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) {
-      double t = (double)x[v] - 0.5;
-      s = s + t * t;
-    }
-    g = s;
-  } else if (problem == 6) {
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) s = s + pow((double)x[v], 0.1);
-    g = s;
-  } else {
-    double s = 0.0;
-    for (int v = m - 1; v < d; ++v) s = s + (double)x[v];
-    g = 1.0 + (9.0 / (double)k) * s;
-  }
   if (problem == 1) {
     double val = 0.5 * (1.0 + g);
     for (int i = 0; i < m - 1 - j; ++i) val = val * (double)x[i];
