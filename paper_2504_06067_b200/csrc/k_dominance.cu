@@ -413,13 +413,14 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   const int tid = threadIdx.x, lane = tid & 31;
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int R = a.R, m = a.m;
+  const int NB = presort_buckets(R);
   trace_mark(a.trace, 0);
   // P0: sums, keys, key range; clear bucket counts and fill cursors
   if (tid == 0) {
     sMin = 0xffffffffu;
     sMax = 0u;
   }
-  for (int q = gtid; q < PRESORT_BUCKETS; q += gthreads) {
+  for (int q = gtid; q < NB; q += gthreads) {
     a.valB[q] = 0;
     a.fill[q] = 0;
   }
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   const uint64_t span = (uint64_t)(hi - lo) + 1ull;
   for (int i = gtid; i < R; i += gthreads) {
     const uint32_t key = __ldcg(a.keyB + i);
-    const uint32_t q = (uint32_t)(((uint64_t)(key - lo) * (uint64_t)PRESORT_BUCKETS) / span);
+    const uint32_t q = (uint32_t)(((uint64_t)(key - lo) * (uint64_t)NB) / span);
     a.keyA[i] = q;
     if (a.stable) a.valA[i] = i;
     atomicAdd(&a.valB[q], 1);
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   trace_mark(a.trace, 2);
   // P2: exclusive scan of the bucket counts -> bucket starts (in fill[] to keep counts)
   grid_scan(
-      a.g, PRESORT_BUCKETS, [&](int64_t q) { return __ldcg(a.valB + q); },
+      a.g, NB, [&](int64_t q) { return __ldcg(a.valB + q); },
       [&](int64_t q, int pre) { a.fill[q] = pre; }, sh);
   grid_sync(a.g.bar);
   trace_mark(a.trace, 3);
@@ -484,7 +485,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
       for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = __fadd_rn(a.F[(int64_t)i * m + k], 0.0f);  // -0 -> +0
     }
     // bucket ends for P4 (the atomic path leaves fill[q] at the end of bucket q)
-    for (int q = gtid; q < PRESORT_BUCKETS; q += gthreads) a.fill[q] += __ldcg(a.valB + q);
+    for (int q = gtid; q < NB; q += gthreads) a.fill[q] += __ldcg(a.valB + q);
     grid_sync(a.g.bar);
     // keyA was overwritten by the sorted keys: restore row -> bucket for P4
     for (int pos = gtid; pos < R; pos += gthreads) a.tkey[__ldcg(a.valA + pos)] = __ldcg(a.keyA + pos);
@@ -548,7 +549,8 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_presort, PRESORT_THREADS, 0);
     maxb = sms * (per > 0 ? (per > 1 ? 1 : per) : 1);
   }
-  int blocks = (int)ceil_div(args.R > PRESORT_BUCKETS ? args.R : PRESORT_BUCKETS, PRESORT_THREADS * 2);
+  const int NB = presort_buckets(args.R);
+  int blocks = (int)ceil_div(args.R > NB ? args.R : NB, PRESORT_THREADS * 2);
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
   if (!args.in_step) {

@@ -4,7 +4,14 @@
 
 namespace mo {
 
-constexpr int PRESORT_BUCKETS = 65536;
+constexpr int PRESORT_BUCKETS = 65536;   // maximum (workspace sizing)
+
+// Buckets used for R rows: ~one per row, 1024 .. 65536 (the bucket scan is a fixed cost per step).
+__host__ __device__ inline int presort_buckets(int R) {
+  int nb = 1024;
+  while (nb < R && nb < PRESORT_BUCKETS) nb <<= 1;
+  return nb;
+}
 
 struct PresortArgs {
   const float* F;

@@ -83,6 +83,59 @@ __device__ void gauss_solve(double* A, double* rhs, int m, int* singular) {
   *singular = 0;
 }
 
+// gauss_solve with one warp (m <= 32): lane r owns row r.  Same operations on the same elements as
+// the one-thread version (pivot = first row with the strictly largest |A[r][c]|; each lane updates its
+// own row from the unchanged pivot row), so the solution is bit-identical; only the schedule differs.
+// Called by all 32 lanes of one warp; result in rhs, *singular set by lane 0.
+__device__ void gauss_solve_warp(double* A, double* rhs, int m, int* singular) {
+  const int lane = threadIdx.x & 31;
+  for (int c = 0; c < m; ++c) {
+    double v = (lane >= c && lane < m) ? fabs(A[lane * m + c]) : -1.0;
+    int p = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double vo = __shfl_xor_sync(MO_FULL, v, o);
+      const int po = __shfl_xor_sync(MO_FULL, p, o);
+      if (vo > v || (vo == v && po < p)) {
+        v = vo;
+        p = po;
+      }
+    }
+    if (v == 0.0) {
+      if (lane == 0) *singular = 1;
+      return;
+    }
+    if (p != c) {
+      if (lane < m) {
+        const double t = A[c * m + lane];
+        A[c * m + lane] = A[p * m + lane];
+        A[p * m + lane] = t;
+      }
+      if (lane == 0) {
+        const double t = rhs[c];
+        rhs[c] = rhs[p];
+        rhs[p] = t;
+      }
+    }
+    __syncwarp();
+    if (lane > c && lane < m) {
+      const double f = A[lane * m + c] / A[c * m + c];
+      for (int q = c; q < m; ++q) A[lane * m + q] = A[lane * m + q] - f * A[c * m + q];
+      rhs[lane] = rhs[lane] - f * rhs[c];
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    for (int c = m - 1; c >= 0; --c) {
+      double s = rhs[c];
+      for (int q = c + 1; q < m; ++q) s = s - A[c * m + q] * rhs[q];
+      rhs[c] = s / A[c * m + c];
+    }
+    *singular = 0;
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   pdl_wait();
   __shared__ uint32_t sKp[MAX_SHUFFLE_ROUNDS], sSp[MAX_SHUFFLE_ROUNDS], sKr[MAX_SHUFFLE_ROUNDS],
@@ -186,10 +239,21 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       sRhs[k] = 1.0;
     }
     __syncthreads();
+    __shared__ int sSing;
+    if (tid < 32) {
+      if (tid == 0) sSing = 0;
+      __syncwarp();
+      if (ncand == 0) {
+        if (tid == 0) sSing = 1;
+      } else if (m <= 32) {
+        gauss_solve_warp(sA, sRhs, m, &sSing);
+      } else if (tid == 0) {
+        gauss_solve(sA, sRhs, m, &sSing);
+      }
+    }
+    __syncthreads();
     if (tid == 0) {
-      int singular = 0;
-      if (ncand == 0) singular = 1;
-      else gauss_solve(sA, sRhs, m, &singular);
+      const int singular = sSing;
       bool bad = singular != 0;
       if (!bad)
         for (int k = 0; k < m; ++k)

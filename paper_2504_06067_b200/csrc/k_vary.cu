@@ -47,7 +47,7 @@ __device__ __forceinline__ double pm_apply(double x, double u, double eta) {
 
 __device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
-// One block = VARY_PAIRS mating pairs, VARY_THREADS threads.  Phase 1: one
+// One block = ppb <= VARY_PAIRS mating pairs, VARY_THREADS threads.  Phase 1: one
 // thread per pair draws the parents (keyed MATING permutation) into shared
 // memory.  Phase 2: one thread per (pair, variable) runs SBX + clamp + PM +
 // clamp and writes both children.  Phase 3: one thread per (child,
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
                                                             const uint32_t* gen_ptr, mo_var_cfg cfg,
                                                             float* __restrict__ Xo, float* __restrict__ Fo,
                                                             float* __restrict__ ideal, int* __restrict__ domain_flag,
-                                                            PrepArgs pro, int pro_blocks) {
+                                                            PrepArgs pro, int pro_blocks, int ppb) {
   pdl_wait();
   __shared__ uint32_t shK[MAX_SHUFFLE_ROUNDS], shS[MAX_SHUFFLE_ROUNDS];
   __shared__ int shR;
@@ -81,9 +81,9 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   if (threadIdx.x < 16) shMin[threadIdx.x] = __int_as_float(0x7f800000);
   __syncthreads();
   const int npairs = n / 2;
-  const int q0 = vblock * VARY_PAIRS;
+  const int q0 = vblock * ppb;
   const int tid = threadIdx.x;
-  if (tid < VARY_PAIRS && q0 + tid < npairs) {
+  if (tid < ppb && q0 + tid < npairs) {
     const int q = q0 + tid;
     shA[tid] = (int)prp_inv(2u * q, shK, shS, shR, (uint32_t)n);
     shB[tid] = (int)prp_inv(2u * q + 1u, shK, shS, shR, (uint32_t)n);
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   __syncthreads();
   const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
   const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
-  const int npb = min(VARY_PAIRS, npairs - q0);
+  const int npb = min(ppb, npairs - q0);
   const int tasks = npb * d;
   for (int e = tid; e < tasks; e += VARY_THREADS) {
     const int ql = e / d, v = e - ql * d;
@@ -184,7 +184,17 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
   if (n <= 0 || (n & 1) || d < m || m < 2) return MO_ERR_PARAM;
   if (problem < MO_DTLZ1 || problem > MO_DTLZ7) return MO_ERR_PARAM;
   const int pairs = (int)(n / 2);
-  const int vblocks = (int)ceil_div(pairs, VARY_PAIRS);
+  // pairs per block: 16, fewer when that would leave SMs idle (small n: spread the (pair, variable)
+  // work; every block also pays the mating-shuffle keys, so no fewer than needed)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int ppb = (int)ceil_div(pairs, 2 * (int64_t)sms);
+  ppb = ppb < 1 ? 1 : (ppb > VARY_PAIRS ? VARY_PAIRS : ppb);
+  const int vblocks = (int)ceil_div(pairs, ppb);
   int pblocks = 0;
   PrepArgs p;
   memset(&p, 0, sizeof(p));
@@ -195,7 +205,7 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
     pblocks = pblocks < 1 ? 1 : (pblocks > 296 ? 296 : pblocks);
   }
   k_vary_eval<<<(unsigned)(vblocks + pblocks), VARY_THREADS, 0, s>>>(problem, X, (int)n, d, m, seed, gen, gen_ptr,
-                                                                     cfg, Xo, Fo, ideal, domain_flag, p, pblocks);
+                                                                     cfg, Xo, Fo, ideal, domain_flag, p, pblocks, ppb);
   MO_CHECK_LAUNCH();
   return MO_OK;
 }
