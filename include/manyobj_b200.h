@@ -289,6 +289,12 @@ int mo_workspace_init(void* workspace, size_t workspace_bytes, void* stream_);
 int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t sort_mode, int32_t shard_count,
                           size_t* bytes);
 
+/* Byte offset of the streamed sort's uint64[4] pair counters (measurement: (i, j) pairs evaluated by
+ * the COUNT sweep with the <= chain / the full dominance chain, then the same for the DEC sweeps of
+ * the generation); reset by every mo_sort_stream_begin / streamed mo_step. */
+int mo_stream_stats_offset(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count,
+                           int64_t* stats_off);
+
 /* Byte offsets inside that workspace of mask_local / mask_full (uint32),
  * their word counts, and of akey (uint64 per merged row). */
 int mo_stream_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count,

@@ -81,6 +81,7 @@ _PROTOS = {
     "mo_sort_stream_front": (c_i32, [ctypes.POINTER(StepArgs), c_i32, c_vp]),
     "mo_sort_stream_end": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
     "mo_workspace_init": (c_i32, [c_vp, c_sz, c_vp]),
+    "mo_stream_stats_offset": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64)]),
     "mo_workspace_bytes_ex": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_sz)]),
     "mo_stream_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),

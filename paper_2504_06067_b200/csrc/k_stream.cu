@@ -73,6 +73,7 @@ __global__ void k_stream_reset(StreamArgs a) {
   }
   if (gt < SC_COUNT) a.ctl[gt] = 0;
   if (gt < MO_INFO_COUNT) a.info[gt] = 0;
+  if (a.stats && gt < 4) a.stats[gt] = 0;
 }
 
 // Work items of owned block t: (j block, chunk of CHUNK i blocks / front-list entries).
@@ -201,6 +202,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
       e1 = min(fln, e0 + STREAM_CHUNK * STREAM_BLK);
     }
     float ca = 0.0f, cb = 0.0f;   // predicated-FADD counts (full dominance chains)
+    unsigned long long nfast = 0, nfull = 0;   // (i, j) pairs evaluated by this thread (measurement)
     int na = 0, nb2 = 0;          // popcount counts (sign-of-difference chains, box "all")
     for (int s0 = e0; s0 < e1; s0 += STREAM_BLK) {
       const int nv = min(STREAM_BLK, e1 - s0);
@@ -255,6 +257,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
           }
         }
         if (fast) {
+          nfast += 2 * (g1 - g0);
           for (int i = g0; i < g1; i += 8) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -266,6 +269,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
             }
           }
         } else {
+          nfull += 2 * (g1 - g0);
           for (int i = g0; i < g1; i += 8) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -279,6 +283,14 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
         }
       }
       __syncthreads();
+    }
+    if (a.stats) {   // executed pairs, for the roofline (one atomic per warp and item)
+      nfast = warp_sum(nfast);
+      nfull = warp_sum(nfull);
+      if ((tid & 31) == 0) {
+        if (nfast) atomicAdd(a.stats + (MODE == MODE_COUNT ? 0 : 2), nfast);
+        if (nfull) atomicAdd(a.stats + (MODE == MODE_COUNT ? 1 : 3), nfull);
+      }
     }
     const int ia = (int)ca + na, ib = (int)cb + nb2;
     if (ja < a.R && ia) atomicAdd(a.cnt + ja, MODE == MODE_COUNT ? ia : -ia);
@@ -579,6 +591,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
   }
   if (gt < MO_INFO_COUNT && gt != MO_INFO_ASSOC_FALLBACK) a.info[gt] = 0;
   if (gt == 0) a.ctl[SC_WORK] = 0;
+  if (a.stats && gt < 4) a.stats[gt] = 0;
   grid_sync(g.bar);
   // dominator counts, front 0
   int base = 0;

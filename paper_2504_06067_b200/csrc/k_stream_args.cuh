@@ -49,6 +49,7 @@ struct StreamArgs {
   float* flbox;          // nb x 2 x m: per 256-entry front-list chunk
   float* blkbox32;       // ceil(R/32) x 2 x m: per 32-row group
   float* flbox32;        // ceil(R/32) x 2 x m: per 32-entry front-list group
+  unsigned long long* stats;  // nullable, 4: (i, j) pairs evaluated -- COUNT fast/full, DEC fast/full
 };
 
 // Morton presort of the boxed mode (F -> perm, FS, SS, S block range, boxes)

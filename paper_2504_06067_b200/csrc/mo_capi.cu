@@ -42,7 +42,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, fcand, fctl, blkbox, flbox, blkbox32, flbox32, cbox, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, fcand, fctl, blkbox, flbox, blkbox32, flbox32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -119,6 +119,7 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.blkbox32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * m * 4 : 0);
   L.flbox32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * m * 4 : 0);
   L.cbox = bump(c, 32 * 4);
+  L.sstats = bump(c, 4 * 8);
   L.tkey = bump(c, st ? (size_t)R * 4 : 0);
   L.tval = bump(c, st ? (size_t)R * 4 : 0);
   L.cnt = bump(c, st ? (size_t)R * 4 : 0);
@@ -464,6 +465,7 @@ static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   sa.flbox = at<float>(ws, L.flbox);
   sa.blkbox32 = at<float>(ws, L.blkbox32);
   sa.flbox32 = at<float>(ws, L.flbox32);
+  sa.stats = at<unsigned long long>(ws, L.sstats);
   return sa;
 }
 
@@ -763,6 +765,13 @@ int mo_workspace_bytes_ex(int64_t n, int32_t m, int32_t d, int64_t w, int32_t so
   if (!bytes || n < 1 || m < 1 || w < 1 || shard_count < 0) return MO_ERR_PARAM;
   if (sort_mode != MO_SORT_BITS && sort_mode != MO_SORT_STREAM) return MO_ERR_PARAM;
   *bytes = make_layout(2 * n, w, m, sort_mode, shards_of(shard_count)).total;
+  return MO_OK;
+}
+
+int mo_stream_stats_offset(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count,
+                           int64_t* stats_off) {
+  if (n < 1 || m < 1 || w < 1 || shard_count < 0 || !stats_off) return MO_ERR_PARAM;
+  *stats_off = (int64_t)make_layout(2 * n, w, m, sort_mode, shards_of(shard_count)).sstats;
   return MO_OK;
 }
 
