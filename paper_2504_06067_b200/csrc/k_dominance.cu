@@ -550,7 +550,7 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     maxb = sms * (per > 0 ? (per > 1 ? 1 : per) : 1);
   }
   const int NB = presort_buckets(args.R);
-  int blocks = (int)ceil_div(args.R > NB ? args.R : NB, PRESORT_THREADS * 2);
+  int blocks = (int)ceil_div(args.R > NB ? args.R : NB, PRESORT_THREADS / 2);
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
   if (!args.in_step) {
