@@ -180,6 +180,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
     }
     const float jmin = __ldg(a.blkmin + bj);
     float wjmn[M], wjmx[M];  // bounding box of this warp's 64 j rows (boxed mode)
+    float wjS = 0.0f;        // min S over the warp's 64 j rows (boxed mode)
     if (a.boxed) {
       const int q = (j0 + 64 * (tid >> 5)) / 32;
       const int q2 = min(q + 1, (a.R - 1) / 32);
@@ -189,6 +190,7 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
         wjmx[k] = fmaxf(__ldg(a.blkbox32 + (int64_t)q * 2 * M + M + k),
                         __ldg(a.blkbox32 + (int64_t)q2 * 2 * M + M + k));
       }
+      wjS = fminf(__ldg(a.blkS32 + (int64_t)q * 2), __ldg(a.blkS32 + (int64_t)q2 * 2));
     }
     const int bend = a.boxed ? a.R : block_bend(a, bj);
     int e0, e1;  // i range: positions (COUNT) or front-list entries (DEC)
@@ -256,7 +258,10 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
             continue;
           }
         }
-        if (fast) {
+        // S-separated at the (32 i, 64 j) level: the <= chain suffices
+        const bool fast32 = fast || (a.boxed && ldx<FUSED>((MODE == MODE_COUNT ? a.blkS32 : a.flS32) +
+                                                           (int64_t)((s0 + g0) / 32) * 2 + 1) < wjS);
+        if (fast32) {
           nfast += 2 * (g1 - g0);
           for (int i = g0; i < g1; i += 8) {
 #pragma unroll
@@ -366,6 +371,19 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
     }
     __syncthreads();
     if (a.boxed) {
+      {  // S range of every 32-entry group (the warp-level <= test of the DEC sweep)
+        const float sv = act ? __ldg(a.SS + p) : 0.0f;
+        float mn = act ? sv : __int_as_float(0x7f800000), mx = act ? sv : -__int_as_float(0x7f800000);
+        for (int o = 16; o > 0; o >>= 1) {
+          mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
+          mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+        }
+        if ((threadIdx.x & 31) == 0 && threadIdx.x < STREAM_BLK) {
+          const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + (threadIdx.x >> 5);
+          a.flS32[q32 * 2] = mn;
+          a.flS32[q32 * 2 + 1] = mx;
+        }
+      }
       for (int k = 0; k < a.m; ++k) {
         const float f = act ? __ldg(a.FS + (int64_t)p * a.m + k) : 0.0f;
         float mn = act ? f : __int_as_float(0x7f800000), mx = act ? f : -__int_as_float(0x7f800000);
@@ -522,10 +540,15 @@ __device__ void chunk_boxes(const StreamArgs& a, int fk, float* sRedMin, float* 
           gmn = fminf(gmn, __shfl_xor_sync(MO_FULL, gmn, o));
           gmx = fmaxf(gmx, __shfl_xor_sync(MO_FULL, gmx, o));
         }
-        if (k >= 0 && lane == 0) {
+        if (lane == 0) {
           const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + wid + 4 * u;
-          a.flbox32[q32 * 2 * M + k] = gmn;
-          a.flbox32[q32 * 2 * M + M + k] = gmx;
+          if (k >= 0) {
+            a.flbox32[q32 * 2 * M + k] = gmn;
+            a.flbox32[q32 * 2 * M + M + k] = gmx;
+          } else if (a.boxed) {
+            a.flS32[q32 * 2] = gmn;
+            a.flS32[q32 * 2 + 1] = gmx;
+          }
         }
         mn = fminf(mn, gmn);
         mx = fmaxf(mx, gmx);
@@ -735,10 +758,15 @@ __global__ void __launch_bounds__(MORTON_THREADS) k_presort_morton(MortonArgs a)
         mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
         mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
       }
-      if (lane == 0 && k >= 0 && tid < STREAM_BLK) {
+      if (lane == 0 && tid < STREAM_BLK) {
         const int64_t q32 = (int64_t)b * (STREAM_BLK / 32) + (tid >> 5);
-        a.blkbox32[q32 * 2 * m + k] = mn;
-        a.blkbox32[q32 * 2 * m + m + k] = mx;
+        if (k >= 0) {
+          a.blkbox32[q32 * 2 * m + k] = mn;
+          a.blkbox32[q32 * 2 * m + m + k] = mx;
+        } else {
+          a.blkS32[q32 * 2] = mn;
+          a.blkS32[q32 * 2 + 1] = mx;
+        }
       }
       if (lane == 0) {
         sRed[0][tid >> 5] = mn;

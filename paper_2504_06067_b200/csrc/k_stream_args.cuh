@@ -50,6 +50,8 @@ struct StreamArgs {
   float* blkbox32;       // ceil(R/32) x 2 x m: per 32-row group
   float* flbox32;        // ceil(R/32) x 2 x m: per 32-entry front-list group
   unsigned long long* stats;  // nullable, 4: (i, j) pairs evaluated -- COUNT fast/full, DEC fast/full
+  float* blkS32;         // ceil(R/32) x 2: S min / max per 32-row group (boxed)
+  float* flS32;          // ceil(R/32) x 2: S min / max per 32-entry front-list group (boxed)
 };
 
 // Morton presort of the boxed mode (F -> perm, FS, SS, S block range, boxes)
@@ -68,6 +70,7 @@ struct MortonArgs {
   float* blkmax;
   float* blkbox;
   float* blkbox32;
+  float* blkS32;
   GridCtx g;
 };
 

@@ -42,7 +42,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, fcand, fctl, blkbox, flbox, blkbox32, flbox32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -118,6 +118,8 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.flbox = bump(c, st ? (size_t)(nb + 1) * 2 * m * 4 : 0);
   L.blkbox32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * m * 4 : 0);
   L.flbox32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * m * 4 : 0);
+  L.blkS32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * 4 : 0);
+  L.flS32 = bump(c, st ? (size_t)(R / 32 + 16) * 2 * 4 : 0);
   L.cbox = bump(c, 32 * 4);
   L.sstats = bump(c, 4 * 8);
   L.tkey = bump(c, st ? (size_t)R * 4 : 0);
@@ -466,6 +468,8 @@ static StreamArgs stream_args(const mo_step_args* a, const Layout& L) {
   sa.blkbox32 = at<float>(ws, L.blkbox32);
   sa.flbox32 = at<float>(ws, L.flbox32);
   sa.stats = at<unsigned long long>(ws, L.sstats);
+  sa.blkS32 = at<float>(ws, L.blkS32);
+  sa.flS32 = at<float>(ws, L.flS32);
   return sa;
 }
 
@@ -489,6 +493,7 @@ static int stream_presort(const mo_step_args* a, const Layout& L, cudaStream_t s
   ma.blkmax = at<float>(ws, L.blkmax);
   ma.blkbox = at<float>(ws, L.blkbox);
   ma.blkbox32 = at<float>(ws, L.blkbox32);
+  ma.blkS32 = at<float>(ws, L.blkS32);
   ma.g.bar = at<unsigned>(ws, L.bar) + BAR_PRESORT;
   ma.g.part = at<int>(ws, L.part);
   ma.g.hist = at<int>(ws, L.hist);

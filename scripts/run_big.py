@@ -27,5 +27,13 @@ for g in range(gens):
     eng.step(profile=prof)
     torch.cuda.synchronize()
     dt = time.time() - t0
+    extra = {}
+    if eng.sort_mode == 1:
+        import ctypes
+        from paper_2504_06067_b200 import _lib
+        off = ctypes.c_int64(0)
+        _lib.lib().mo_stream_stats_offset(n, m, eng.w, eng.sort_mode, eng.shard_count, ctypes.byref(off))
+        st = eng.ws[off.value: off.value + 32].view(torch.int64).cpu().tolist()
+        extra = {"pairs_count_le": st[0], "pairs_count_full": st[1], "pairs_dec_le": st[2], "pairs_dec_full": st[3]}
     print(json.dumps({"gen": g, "wall_s": round(dt, 4), **{k: round(v, 5) for k, v in prof.items()},
-                      **eng.info_dict()}), flush=True)
+                      **eng.info_dict(), **extra}), flush=True)
