@@ -101,6 +101,15 @@ __device__ __forceinline__ int block_items(const StreamArgs& a, int t, int fln) 
   return (lo + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
 }
 
+// Boxed mode: every owned block has the same number of items (no bound per block), so items decode
+// as (t, c) = (item / per, item % per) without a plan search; blocks with nothing to do are skipped
+// when their item comes up.
+template <int MODE>
+__host__ __device__ __forceinline__ int boxed_items_per_block(int nb, int fln) {
+  return MODE == MODE_COUNT ? (nb + STREAM_CHUNK - 1) / STREAM_CHUNK
+                            : (fln + STREAM_BLK * STREAM_CHUNK - 1) / (STREAM_BLK * STREAM_CHUNK);
+}
+
 // One CTA: items per owned block, exclusive prefix into plan[0..T].
 template <int MODE>
 __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
@@ -108,6 +117,13 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_stream_plan(StreamArgs a) {
   const int tid = threadIdx.x;
   const bool done = __ldcg(a.ctl + SC_DONE) != 0;
   const int fln = __ldcg(a.ctl + SC_FLN);
+  if (a.boxed) {
+    if (tid == 0) {
+      a.ctl[SC_ITEMS] = done ? 0 : a.T * boxed_items_per_block<MODE>(nblocks(a.R), fln);
+      a.ctl[SC_WORK] = 0;
+    }
+    return;
+  }
   const int per = (a.T + PLAN_THREADS - 1) / PLAN_THREADS;
   const int t0 = min(a.T, tid * per), t1 = min(a.T, t0 + per);
   int mine = 0;
@@ -162,12 +178,22 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
     const int item = *sItem;
     __syncthreads();
     if (item >= items) break;
-    int lo = 0, hi = a.T;  // largest t with plan[t] <= item
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (ldx<FUSED>(a.plan + mid) <= item) lo = mid; else hi = mid;
+    int t, c;
+    if (a.boxed) {
+      const int per = boxed_items_per_block<MODE>(nblocks(a.R), fln);
+      t = item / per;
+      c = item - t * per;
+      if (owned_block(a, t) >= nblocks(a.R)) continue;
+      if (MODE == MODE_DEC && ldx<FUSED>(a.ucnt + t) == 0) continue;   // uniform over the CTA
+    } else {
+      int lo = 0, hi = a.T;  // largest t with plan[t] <= item
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (ldx<FUSED>(a.plan + mid) <= item) lo = mid; else hi = mid;
+      }
+      t = lo;
+      c = item - ldx<FUSED>(a.plan + t);
     }
-    const int t = lo, c = item - ldx<FUSED>(a.plan + t);
     const int bj = owned_block(a, t);
     const int j0 = bj * STREAM_BLK;
     // two adjacent rows per thread: a warp owns 64 consecutive positions (one j box per warp)
@@ -489,6 +515,11 @@ __device__ int grid_scan_all(GridCtx& g, int64_t N, ValueF value, EmitF emit, in
 // plan[t] = exclusive prefix of the items of owned block t; returns the total (all CTAs).
 __device__ __noinline__ int plan_all(const StreamArgs& a, GridCtx& g, int mode, int fln, int* sh) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  if (a.boxed) {   // uniform items per block, no plan (the caller's barrier publishes earlier writes)
+    grid_sync(g.bar);
+    return a.T * (mode == MODE_COUNT ? boxed_items_per_block<MODE_COUNT>(nblocks(a.R), fln)
+                                     : boxed_items_per_block<MODE_DEC>(nblocks(a.R), fln));
+  }
   for (int t = gt; t < a.T; t += gs)
     a.plan[t] = mode == MODE_COUNT ? block_items<MODE_COUNT>(a, t, fln) : block_items<MODE_DEC>(a, t, fln);
   grid_sync(g.bar);
