@@ -166,25 +166,32 @@ __device__ __forceinline__ T ldx(const T* p) {
   return __ldg(p);
 }
 
+// Warp-centric: a work item is (owned j block t, chunk c of i rows, quarter wq of the block's 256 j
+// rows); each warp pulls its own items and stages its 32-row i groups in a private shared-memory slice
+// with __syncwarp -- no CTA barriers, so warps whose boxes skip most groups never wait for busy ones.
+// Lane = 2 adjacent j rows; the warp owns 64 j rows (one j box).
 template <int M, int MODE, bool FUSED>
-__device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* sItem, int items, int fln,
-                                          int* counter, int base) {
+__device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFw, int items, int fln, int* counter,
+                                          int base) {
   constexpr int MP = (M + 3) & ~3;
-  const int tid = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  float* sF = sFw + (threadIdx.x >> 5) * 32 * MP;   // this warp's 32-row staging slice
   const float PINF = __int_as_float(0x7f800000);
+  const int nbk = nblocks(a.R);
   for (;;) {
-    if (tid == 0) *sItem = atomicAdd(counter, 1) - base;
-    __syncthreads();
-    const int item = *sItem;
-    __syncthreads();
-    if (item >= items) break;
+    int item = 0;
+    if (lane == 0) item = atomicAdd(counter, 1) - base;
+    item = __shfl_sync(MO_FULL, item, 0);
+    if (item >= 4 * items) break;
+    const int wq = item & 3;
+    item >>= 2;
     int t, c;
     if (a.boxed) {
-      const int per = boxed_items_per_block<MODE>(nblocks(a.R), fln);
+      const int per = boxed_items_per_block<MODE>(nbk, fln);
       t = item / per;
       c = item - t * per;
-      if (owned_block(a, t) >= nblocks(a.R)) continue;
-      if (MODE == MODE_DEC && ldx<FUSED>(a.ucnt + t) == 0) continue;   // uniform over the CTA
+      if (owned_block(a, t) >= nbk) continue;
+      if (MODE == MODE_DEC && ldx<FUSED>(a.ucnt + t) == 0) continue;
     } else {
       int lo = 0, hi = a.T;  // largest t with plan[t] <= item
       while (hi - lo > 1) {
@@ -196,8 +203,8 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
     }
     const int bj = owned_block(a, t);
     const int j0 = bj * STREAM_BLK;
-    // two adjacent rows per thread: a warp owns 64 consecutive positions (one j box per warp)
-    const int ja = j0 + 2 * tid, jb = ja + 1;
+    const int ja = j0 + 64 * wq + 2 * lane, jb = ja + 1;
+    if (j0 + 64 * wq >= a.R) continue;
     float fa[M], fb[M];
 #pragma unroll
     for (int k = 0; k < M; ++k) {
@@ -206,9 +213,9 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
     }
     const float jmin = __ldg(a.blkmin + bj);
     float wjmn[M], wjmx[M];  // bounding box of this warp's 64 j rows (boxed mode)
-    float wjS = 0.0f;        // min S over the warp's 64 j rows (boxed mode)
+    float wjS = 0.0f;        // min S over them
     if (a.boxed) {
-      const int q = (j0 + 64 * (tid >> 5)) / 32;
+      const int q = (j0 + 64 * wq) / 32;
       const int q2 = min(q + 1, (a.R - 1) / 32);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -229,12 +236,12 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
       e0 = c * STREAM_CHUNK * STREAM_BLK;
       e1 = min(fln, e0 + STREAM_CHUNK * STREAM_BLK);
     }
-    float ca = 0.0f, cb = 0.0f;   // predicated-FADD counts (full dominance chains)
-    unsigned long long nfast = 0, nfull = 0;   // (i, j) pairs evaluated by this thread (measurement)
-    int na = 0, nb2 = 0;          // popcount counts (sign-of-difference chains, box "all")
+    float ca = 0.0f, cb = 0.0f;   // predicated-FADD counts
+    unsigned long long nfast = 0, nfull = 0;   // (i, j) pairs evaluated by this lane (measurement)
+    int na = 0, nb2 = 0;          // box "all" counts
     for (int s0 = e0; s0 < e1; s0 += STREAM_BLK) {
       const int nv = min(STREAM_BLK, e1 - s0);
-      if (a.boxed) {  // block-pair classification from the bounding boxes (uniform over the CTA)
+      if (a.boxed) {  // block-pair classification from the 256-level bounding boxes
         const float* ib = (MODE == MODE_COUNT ? a.blkbox : a.flbox) + (int64_t)(s0 / STREAM_BLK) * 2 * M;
         const float* jb2 = a.blkbox + (int64_t)bj * 2 * M;
         bool none = false, all = true, strict = false;
@@ -248,25 +255,16 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
         }
         if (none) continue;
         if (all && strict) {
-          ca += (float)nv;
-          cb += (float)nv;
+          na += nv;
+          nb2 += nv;
           continue;
         }
       }
-      for (int e = tid; e < STREAM_BLK; e += ST_THREADS) {
-        int src = -1;
-        if (e < nv) src = MODE == MODE_COUNT ? s0 + e : ldx<FUSED>(a.fl + s0 + e);
-        float* dst = sFi + e * MP;
-#pragma unroll
-        for (int k = 0; k < MP; ++k) dst[k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
-      }
       const float imax = MODE == MODE_COUNT ? __ldg(a.blkmax + s0 / STREAM_BLK) : ldx<FUSED>(a.flmax + s0 / STREAM_BLK);
       const bool fast = (MODE == MODE_COUNT && !a.boxed ? (s0 / STREAM_BLK < bj) : true) && imax < jmin;
-      __syncthreads();
-      const int nv8 = (nv + 7) & ~7;  // pads are +inf rows: they dominate no finite row
-      for (int g0 = 0; g0 < nv8; g0 += 32) {
-        const int g1 = min(nv8, g0 + 32);
-        if (a.boxed) {  // warp-uniform: 32 i rows (their box) against this warp's 64 j rows
+      for (int g0 = 0; g0 < nv; g0 += 32) {
+        const int gn = min(32, nv - g0);
+        if (a.boxed) {  // 32 i rows (their box) against this warp's 64 j rows
           const float* ib = (MODE == MODE_COUNT ? a.blkbox32 : a.flbox32) + (int64_t)((s0 + g0) / 32) * 2 * M;
           bool none = false, all = true, strict = false;
 #pragma unroll
@@ -278,47 +276,56 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
           }
           if (none) continue;
           if (all && strict) {
-            const int cnt = min(32, nv - g0);
-            na += cnt;
-            nb2 += cnt;
+            na += gn;
+            nb2 += gn;
             continue;
           }
         }
+        // stage the group: lane l loads i row g0 + l (pads: +inf, never <= a finite row)
+        {
+          int src = -1;
+          if (lane < gn) src = MODE == MODE_COUNT ? s0 + g0 + lane : ldx<FUSED>(a.fl + s0 + g0 + lane);
+          __syncwarp();
+#pragma unroll
+          for (int k = 0; k < MP; ++k)
+            sF[lane * MP + k] = (src >= 0 && k < M) ? __ldg(a.FS + (int64_t)src * M + k) : PINF;
+          __syncwarp();
+        }
+        const int gn8 = (gn + 7) & ~7;
         // S-separated at the (32 i, 64 j) level: the <= chain suffices
         const bool fast32 = fast || (a.boxed && ldx<FUSED>((MODE == MODE_COUNT ? a.blkS32 : a.flS32) +
                                                            (int64_t)((s0 + g0) / 32) * 2 + 1) < wjS);
         if (fast32) {
-          nfast += 2 * (g1 - g0);
-          for (int i = g0; i < g1; i += 8) {
+          nfast += 2 * gn8;
+          for (int i = 0; i < gn8; i += 8) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               float v[M];
 #pragma unroll
-              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+              for (int k = 0; k < M; ++k) v[k] = sF[(i + u) * MP + k];
               Chain<M>::le_cnt(v, fa, ca);
               Chain<M>::le_cnt(v, fb, cb);
             }
           }
         } else {
-          nfull += 2 * (g1 - g0);
-          for (int i = g0; i < g1; i += 8) {
+          nfull += 2 * gn8;
+          for (int i = 0; i < gn8; i += 8) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               float v[M];
 #pragma unroll
-              for (int k = 0; k < M; ++k) v[k] = sFi[(i + u) * MP + k];
+              for (int k = 0; k < M; ++k) v[k] = sF[(i + u) * MP + k];
               Chain<M>::dom_cnt(v, fa, ca);
               Chain<M>::dom_cnt(v, fb, cb);
             }
           }
         }
       }
-      __syncthreads();
     }
     if (a.stats) {   // executed pairs, for the roofline (one atomic per warp and item)
       nfast = warp_sum(nfast);
       nfull = warp_sum(nfull);
-      if ((tid & 31) == 0) {
+      if (lane == 0) {
         if (nfast) atomicAdd(a.stats + (MODE == MODE_COUNT ? 0 : 2), nfast);
         if (nfull) atomicAdd(a.stats + (MODE == MODE_COUNT ? 1 : 3), nfull);
       }
@@ -332,10 +339,9 @@ __device__ __forceinline__ void tiles_run(const StreamArgs& a, float* sFi, int* 
 template <int M, int MODE>
 __global__ void __launch_bounds__(ST_THREADS) k_stream_tiles(StreamArgs a) {
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
-  __shared__ int sItem;
-  tiles_run<M, MODE, false>(a, sFi, &sItem, __ldcg(a.ctl + SC_ITEMS),
-                            MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0, a.ctl + SC_WORK, 0);
+  __shared__ __align__(16) float sFw[(ST_THREADS / 32) * 32 * MP];
+  tiles_run<M, MODE, false>(a, sFw, __ldcg(a.ctl + SC_ITEMS), MODE == MODE_DEC ? __ldcg(a.ctl + SC_FLN) : 0,
+                            a.ctl + SC_WORK, 0);
 }
 
 // Owned unranked rows with no unranked dominator left -> local mask slice.
@@ -627,8 +633,7 @@ __device__ __noinline__ int apply_front_local(const StreamArgs& a, GridCtx& g, i
 template <int M>
 __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sFi[STREAM_BLK * MP];
-  __shared__ int sItem;
+  __shared__ __align__(16) float sFw[(ST_THREADS / 32) * 32 * MP];
   __shared__ int sh[40];
   __shared__ float sRedMin[ST_THREADS / 32], sRedMax[ST_THREADS / 32];
   GridCtx g = a.gc;
@@ -650,8 +655,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
   // dominator counts, front 0
   int base = 0;
   int items = plan_all(a, g, MODE_COUNT, 0, sh);
-  tiles_run<M, MODE_COUNT, true>(a, sFi, &sItem, items, 0, a.ctl + SC_WORK, base);
-  base += items + (int)gridDim.x;
+  tiles_run<M, MODE_COUNT, true>(a, sFw, items, 0, a.ctl + SC_WORK, base);
+  base += 4 * items + (int)gridDim.x * (ST_THREADS / 32);   // every warp overshoots once
   grid_sync(g.bar);
   mark_all(a);
   grid_sync(g.bar);
@@ -678,8 +683,8 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
     grid_sync(g.bar);            // fl / rank_pos / ucnt of front k visible
     chunk_boxes<M>(a, fk, sRedMin, sRedMax);
     items = plan_all(a, g, MODE_DEC, fk, sh);  // (its first barrier also publishes the chunk boxes)
-    tiles_run<M, MODE_DEC, true>(a, sFi, &sItem, items, fk, a.ctl + SC_WORK, base);
-    base += items + (int)gridDim.x;
+    tiles_run<M, MODE_DEC, true>(a, sFw, items, fk, a.ctl + SC_WORK, base);
+    base += 4 * items + (int)gridDim.x * (ST_THREADS / 32);
     grid_sync(g.bar);
     mark_all(a);
     grid_sync(g.bar);
