@@ -49,6 +49,8 @@
 namespace mo {
 
 constexpr int ST_THREADS = STREAM_BLK / 2;   // two j columns per thread
+// k_stream_fused: big CTAs (the sweep is warp-centric) so its grid barriers have few participants
+constexpr int FUSED_THREADS = 512;
 constexpr int PLAN_THREADS = 1024;
 constexpr int APPLY_THREADS = 512;
 enum { MODE_COUNT = 0, MODE_DEC = 1 };
@@ -553,14 +555,15 @@ __device__ void mark_all(const StreamArgs& a) {
 template <int M>
 __device__ void chunk_boxes(const StreamArgs& a, int fk, float* sRedMin, float* sRedMax) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int bd = blockDim.x, nw = bd >> 5;
   const int nq = (fk + STREAM_BLK - 1) / STREAM_BLK;
   for (int q = blockIdx.x; q < nq; q += gridDim.x) {
     int p[2];
     bool act[2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {   // entry q*256 + tid + 128u: warp w covers 32-groups w and w+4
-      const int e = q * STREAM_BLK + tid + ST_THREADS * u;
-      act[u] = e < fk;
+    for (int u = 0; u < 2; ++u) {   // chunk entry tid + bd*u: warp w covers the 32-group w + nw*u
+      const int el = tid + bd * u, e = q * STREAM_BLK + el;
+      act[u] = el < STREAM_BLK && e < fk;
       p[u] = act[u] ? __ldcg(a.fl + e) : 0;
     }
     for (int k = -1; k < (a.boxed ? M : 0); ++k) {
@@ -577,8 +580,8 @@ __device__ void chunk_boxes(const StreamArgs& a, int fk, float* sRedMin, float* 
           gmn = fminf(gmn, __shfl_xor_sync(MO_FULL, gmn, o));
           gmx = fmaxf(gmx, __shfl_xor_sync(MO_FULL, gmx, o));
         }
-        if (lane == 0) {
-          const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + wid + 4 * u;
+        if (lane == 0 && wid + nw * u < STREAM_BLK / 32) {
+          const int64_t q32 = (int64_t)q * (STREAM_BLK / 32) + wid + nw * u;
           if (k >= 0) {
             a.flbox32[q32 * 2 * M + k] = gmn;
             a.flbox32[q32 * 2 * M + M + k] = gmx;
@@ -596,7 +599,7 @@ __device__ void chunk_boxes(const StreamArgs& a, int fk, float* sRedMin, float* 
       }
       __syncthreads();
       if (tid == 0) {
-        for (int w = 1; w < ST_THREADS / 32; ++w) {
+        for (int w = 1; w < nw; ++w) {
           mn = fminf(mn, sRedMin[w]);
           mx = fmaxf(mx, sRedMax[w]);
         }
@@ -631,11 +634,11 @@ __device__ __noinline__ int apply_front_local(const StreamArgs& a, GridCtx& g, i
 }
 
 template <int M>
-__global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
+__global__ void __launch_bounds__(FUSED_THREADS, 2) k_stream_fused(StreamArgs a) {
   constexpr int MP = (M + 3) & ~3;
-  __shared__ __align__(16) float sFw[(ST_THREADS / 32) * 32 * MP];
+  __shared__ __align__(16) float sFw[(FUSED_THREADS / 32) * 32 * MP];
   __shared__ int sh[40];
-  __shared__ float sRedMin[ST_THREADS / 32], sRedMax[ST_THREADS / 32];
+  __shared__ float sRedMin[FUSED_THREADS / 32], sRedMax[FUSED_THREADS / 32];
   GridCtx g = a.gc;
   const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
   const int R = a.R;
@@ -656,7 +659,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
   int base = 0;
   int items = plan_all(a, g, MODE_COUNT, 0, sh);
   tiles_run<M, MODE_COUNT, true>(a, sFw, items, 0, a.ctl + SC_WORK, base);
-  base += 4 * items + (int)gridDim.x * (ST_THREADS / 32);   // every warp overshoots once
+  base += 4 * items + (int)gridDim.x * (FUSED_THREADS / 32);   // every warp overshoots once
   grid_sync(g.bar);
   mark_all(a);
   grid_sync(g.bar);
@@ -684,7 +687,7 @@ __global__ void __launch_bounds__(ST_THREADS) k_stream_fused(StreamArgs a) {
     chunk_boxes<M>(a, fk, sRedMin, sRedMax);
     items = plan_all(a, g, MODE_DEC, fk, sh);  // (its first barrier also publishes the chunk boxes)
     tiles_run<M, MODE_DEC, true>(a, sFw, items, fk, a.ctl + SC_WORK, base);
-    base += 4 * items + (int)gridDim.x * (ST_THREADS / 32);
+    base += 4 * items + (int)gridDim.x * (FUSED_THREADS / 32);
     grid_sync(g.bar);
     mark_all(a);
     grid_sync(g.bar);
@@ -954,7 +957,7 @@ int launch_stream_fused(StreamArgs a, cudaStream_t s) {
   if (cudaMemsetAsync(a.gc.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   a.gc.parity = 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(ST_THREADS);
+  cfg.blockDim = dim3(FUSED_THREADS);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -967,8 +970,8 @@ int launch_stream_fused(StreamArgs a, cudaStream_t s) {
   case MM: {                                                                                      \
     if (!blocks[MM]) {                                                                            \
       int per = 0;                                                                                \
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fused<MM>, ST_THREADS, 0);     \
-      per = per > 6 ? 6 : (per < 1 ? 1 : per);   /* grid <= MAX_GRID (GridCtx part) */        \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream_fused<MM>, FUSED_THREADS, 0);     \
+      per = per > 2 ? 2 : (per < 1 ? 1 : per);   /* few barrier participants */        \
       blocks[MM] = sms * per;                                                                     \
     }                                                                                             \
     cfg.gridDim = dim3(blocks[MM]);                                                               \

@@ -111,12 +111,16 @@ class Engine:
         self.poll = max(1, int(poll))
         self.prune_r = int(prune_r)          # lattice box radius (0 = the library default for m)
         # streamed sort, one shard: the front loop either runs on the device inside mo_step (one
-        # cooperative launch, graph-capturable) or front by front from the host (full-occupancy sweep
-        # launches; faster today at C4 scale, so the default unless a graph is captured).  Sharded runs
+        # cooperative launch, graph-capturable; ~30 us per front) or front by front from the host
+        # (full-occupancy sweep launches, ~50 us per front; faster when the sweeps dominate, e.g. C4).
+        # host_fronts=None (auto, eager): host-driven while the previous generation had <= 300 fronts,
+        # device-side beyond (profiles/r01_sort_modes.jsonl: DTLZ4 m=3 has thousands).  Sharded runs
         # are always host-driven: the collectives sit between the fronts.
+        self._auto_fronts = host_fronts is None and not graph
         if host_fronts is None:
             host_fronts = not graph
         self.host_fronts = self.sort_mode == _lib.SORT_STREAM and (self.shard_count > 1 or bool(host_fronts))
+        self._fronts_hint = 0
         if graph and self.host_fronts:
             raise ConfigError("graph", "CUDA-graph replay needs the device-side front loop (one shard)")
         with torch.cuda.device(self.dev):
@@ -226,10 +230,20 @@ class Engine:
     # ------------------------------------------------------------- stepping
     def step(self, profile=None):
         """Advance one generation (eager launch).  ``profile``: dict receiving per-phase seconds."""
-        if self.host_fronts:
+        device_fronts = (self._auto_fronts and self.shard_count == 1 and self.sort_mode == _lib.SORT_STREAM
+                         and self._fronts_hint > 300)
+        if self.host_fronts and not device_fronts:
             for req in self.step_gen(profile):
                 run_collective(req, self.group)
             return
+        if device_fronts:
+            self._step_device(profile)
+            self._fronts_hint = int(self.info[_lib.INFO["NFRONTS"]].item())
+            return
+        self._step_device(profile)
+
+    def _step_device(self, profile=None):
+        """One generation through mo_step / mo_step_phases (device-side front loop when streamed)."""
         if profile is None:
             self._launch(self.cur, self.generation)
         else:
@@ -276,7 +290,9 @@ class Engine:
             _lib.check(L.mo_sort_stream_front(a, k, s), "mo_sort_stream_front")
             k += 1
             if k % self.poll == 0 or k == 1:
-                if int(self.info[_lib.INFO["NFRONTS"]].item()) > 0:   # identical on every shard
+                nf = int(self.info[_lib.INFO["NFRONTS"]].item())
+                if nf > 0:   # identical on every shard
+                    self._fronts_hint = nf
                     break
         _lib.check(L.mo_sort_stream_end(a, s), "mo_sort_stream_end")
         if ev:

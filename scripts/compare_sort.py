@@ -13,9 +13,11 @@ gens = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 for prob, m, n in cases:
     m, n = int(m), int(n)
     out = {"problem": prob, "m": m, "n": n}
-    for sort in ("bits", "stream"):
+    for sort in ("bits", "stream", "stream_dev"):
         cfg = engine.RunConfig(problem=prob, n=n, m=m, d=m + (19 if prob == "DTLZ7" else 9), generations=gens, seed=0)
-        eng = engine.Engine(cfg, sort=sort)
+        if sort == "bits" and 2 * n > 300_000:
+            continue
+        eng = engine.Engine(cfg, sort=sort.replace("_dev", ""), host_fronts=(sort == "stream"))
         for _ in range(3):
             eng.step()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

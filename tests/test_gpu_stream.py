@@ -225,3 +225,18 @@ def test_stream_many_fronts(M):
         want = Odom.non_dominated_sort(F, stop_at=512)
         assert np.array_equal(r, want), stream
         assert eng.info_dict()["nfronts"] == 512
+
+
+def test_stream_auto_front_loop_switch(M):
+    """Eager streamed runs switch to the device-side front loop once a generation has > 300 fronts
+    (DTLZ4 m=3: hundreds); every generation still equals the bit-matrix engine."""
+    cfg = M.engine.RunConfig(problem="DTLZ4", n=8000, m=3, d=12, generations=4, seed=1)
+    a = M.engine.Engine(cfg, sort="bits")
+    b = M.engine.Engine(cfg, sort="stream")
+    switched = False
+    for _ in range(4):
+        switched |= b._fronts_hint > 300
+        a.step()
+        b.step()
+        assert torch.equal(a.X, b.X) and torch.equal(a.F, b.F)
+    assert switched, b._fronts_hint
