@@ -439,31 +439,40 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
   bool ok = live && s > 0.0 && isfinite(s);
 #pragma unroll
   for (int k = 0; k < M; ++k) ok = ok && fn[k] >= 0.0f;
-  float best = -__int_as_float(0x7f800000);
-  int bp = 0x7fffffff;
-  // the box (lo, extent per coordinate) is computed once per group, by its leader, in FP64, and broadcast
-  int lo[M], ext[M];
-  float inv[M];
-  int total = 0;
-  if (sub == 0 && ok) {
-    total = 1;
+  // rows the box cannot serve (f = 0, non-finite) go straight to the fallback list
+  if (live && !ok && sub == 0) {
+    a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row;
+    atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
+  }
+  bool done = !ok;   // group-uniform
+  // radius r, then r+1, r+2 for the rows whose certificate failed (no separate full scan for them)
+  for (int it = 0; it < 3; ++it) {
+    if (__all_sync(MO_FULL, done)) break;
+    const int rr = r + it;
+    float best = -__int_as_float(0x7f800000);
+    int bp = 0x7fffffff;
+    // the box (lo, extent per coordinate) is computed once per group, by its leader, in FP64, and broadcast
+    int lo[M], ext[M];
+    float inv[M];
+    int total = 0;
+    if (sub == 0 && !done) {
+      total = 1;
+#pragma unroll
+      for (int k = 0; k < M - 1; ++k) {
+        const double x = (double)fn[k] / s * (double)H;
+        lo[k] = max(0, (int)floor(x - (double)rr) + 1);
+        const int hi = min(H, (int)ceil(x + (double)rr) - 1);
+        ext[k] = max(0, hi - lo[k] + 1);
+        total *= ext[k];
+      }
+    }
+    total = __shfl_sync(MO_FULL, total, 0, LPR);
 #pragma unroll
     for (int k = 0; k < M - 1; ++k) {
-      const double x = (double)fn[k] / s * (double)H;
-      lo[k] = max(0, (int)floor(x - (double)r) + 1);
-      const int hi = min(H, (int)ceil(x + (double)r) - 1);
-      ext[k] = max(0, hi - lo[k] + 1);
-      total *= ext[k];
+      lo[k] = __shfl_sync(MO_FULL, lo[k], 0, LPR);
+      ext[k] = __shfl_sync(MO_FULL, ext[k], 0, LPR);
+      inv[k] = ext[k] > 0 ? 1.0f / (float)ext[k] : 0.0f;
     }
-  }
-  total = __shfl_sync(MO_FULL, total, 0, LPR);
-#pragma unroll
-  for (int k = 0; k < M - 1; ++k) {
-    lo[k] = __shfl_sync(MO_FULL, lo[k], 0, LPR);
-    ext[k] = __shfl_sync(MO_FULL, ext[k], 0, LPR);
-    inv[k] = ext[k] > 0 ? 1.0f / (float)ext[k] : 0.0f;
-  }
-  if (ok) {
     for (int q = sub; q < total; q += LPR) {
       int rem = q, rest, idx = 0;
       int kv[M];  // mixed-radix decode of the box index, k_{m-2} fastest; (rem + .5) / ext is exact in
@@ -488,28 +497,30 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
         bp = p;
       }
     }
-  }
-  // group reduction: max key, lowest position on ties
+    // group reduction: max key, lowest position on ties
 #pragma unroll
-  for (int o = LPR / 2; o > 0; o >>= 1) {
-    const float tb = __shfl_xor_sync(MO_FULL, best, o);
-    const int pb = __shfl_xor_sync(MO_FULL, bp, o);
-    if (tb > best || (tb == best && pb < bp)) {
-      best = tb;
-      bp = pb;
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      const float tb = __shfl_xor_sync(MO_FULL, best, o);
+      const int pb = __shfl_xor_sync(MO_FULL, bp, o);
+      if (tb > best || (tb == best && pb < bp)) {
+        best = tb;
+        bp = pb;
+      }
     }
+    int cert = 0;
+    if (sub == 0 && !done) {
+      const double un = sqrt(nn) / s;                       // ||u||, u = f / sum(f)
+      double se = ((double)rr - 1e-6) / (double)H / (sqrt((double)M) * un);
+      se = se < 1.0 ? se : 1.0;
+      const double bound = sqrt(nn) * sqrt(1.0 - se * se) * (1.0 + (M + 2) * 5.9604644775390625e-8);
+      cert = bp != 0x7fffffff && (double)best > bound;
+      if (cert)
+        a.akey[row] = ((unsigned long long)f2ord(best) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp);
+    }
+    const int cert_g = __shfl_sync(MO_FULL, cert, 0, LPR);   // every lane joins (no short circuit)
+    done = done || cert_g != 0;
   }
-  if (sub != 0 || !live) return;
-  if (ok) {
-    const double un = sqrt(nn) / s;                       // ||u||, u = f / sum(f)
-    double se = ((double)r - 1e-6) / (double)H / (sqrt((double)M) * un);
-    se = se < 1.0 ? se : 1.0;
-    const double bound = sqrt(nn) * sqrt(1.0 - se * se) * (1.0 + (M + 2) * 5.9604644775390625e-8);
-    ok = bp != 0x7fffffff && (double)best > bound;
-  }
-  if (ok) {
-    a.akey[row] = ((unsigned long long)f2ord(best) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp);
-  } else {
+  if (!done && sub == 0) {
     a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row;
     atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
   }
