@@ -14,6 +14,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # lazy submodule import: the GPU modules pull in torch
     import importlib
-    if name in ("batchcore", "dominance", "engine", "metrics", "niche", "problems", "refpoints", "variation"):
+    if name in ("batchcore", "bench", "cli", "dominance", "engine", "metrics", "niche", "problems", "refpoints",
+                "variation"):
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

@@ -1,0 +1,180 @@
+"""Experiment harness (the reference's ``bench`` module).
+
+* :class:`ExperimentPlan` -- a grid of RunConfigs (problems x sizes x generations x seeds),
+  repetitions, a per-cell time limit and an output path.
+* :func:`run_plan` -- runs every cell on the GPU engine and writes one CSV row per generation with
+  the SPEC schema (fingerprint, seed, generation, igd, hv_raw, hv_normalized, t_variation, t_sort,
+  t_niche, t_eval, timed_out).  IGD (GPU, FP64) against 10^4 front points; HV by the GPU Monte-Carlo
+  estimator (exact m <= 3 HV is not implemented on the GPU: the column is the MC estimate with
+  10^5 samples for every m).  The CSV is written atomically (temp file + rename).
+* :func:`summarize` -- per fingerprint: mean, standard deviation and 95 % t-interval of the final IGD /
+  HV and of the per-generation runtime (generation 1 excluded: one-time setup).
+* ``compare_backends`` of the reference times the batched against the scalar Alg. 1 back-end; the Alg. 1
+  back-end is CPU test infrastructure here (oracle/), so this harness does not offer it.
+"""
+import csv
+import dataclasses
+import hashlib
+import json
+import math
+import os
+import tempfile
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import ConfigError
+
+COLUMNS = ("fingerprint", "seed", "generation", "igd", "hv_raw", "hv_normalized", "t_variation", "t_sort",
+           "t_niche", "t_eval", "timed_out")
+
+
+@dataclass(frozen=True)
+class ExperimentPlan:
+    """SPEC.md:658-661."""
+    problems: tuple = ("DTLZ2",)
+    m: int = 3
+    d: int = 12
+    sizes: tuple = (92,)
+    generations: tuple = (100,)
+    seeds: tuple = (0,)
+    repetitions: int = 1
+    time_limit_s: float = 600.0
+    out: str = "results.csv"
+    ref_points: int = 10_000
+    hv_ref: tuple = None            # reference point for HV (default 1.1 x the front's nadir sample)
+    hv_samples: int = 100_000
+
+    def cells(self):
+        for p in self.problems:
+            for n in self.sizes:
+                for g in self.generations:
+                    yield p, n, g
+
+    def validate(self):
+        if self.repetitions < 1:
+            raise ConfigError("repetitions", "must be >= 1")
+        if not (self.problems and self.sizes and self.generations and self.seeds):
+            raise ConfigError("plan", "the grid has no cell")
+
+
+def fingerprint(cfg):
+    """Stable hash of a RunConfig's fields (seed excluded: it is its own column)."""
+    d = dataclasses.asdict(cfg)
+    d.pop("seed", None)
+    return hashlib.sha1(json.dumps(d, sort_keys=True, default=str).encode()).hexdigest()[:12]
+
+
+def _metrics(F, ref, hv_ref, hv_samples, seed):
+    from . import metrics
+    q = metrics.igd(F, ref)
+    hv, _ = metrics.hv_mc(F, hv_ref, samples=hv_samples, seed=seed, lower=np.zeros(len(hv_ref)))
+    vol = float(np.prod(hv_ref))
+    return q, hv, hv / vol if vol > 0 else 0.0
+
+
+def run_plan(plan, progress=None):
+    """Run every (cell, seed, repetition); write the CSV atomically; return the output path."""
+    import torch
+
+    from . import engine, metrics
+    plan.validate()
+    rows = []
+    for prob, n, gens in plan.cells():
+        pf = metrics.dtlz_pf_sample(prob, plan.m, plan.ref_points).astype(np.float32)
+        hv_ref = tuple(plan.hv_ref) if plan.hv_ref else tuple(1.1 * pf.max(axis=0))
+        for seed in plan.seeds:
+            for _ in range(plan.repetitions):
+                cfg = engine.RunConfig(problem=prob, n=n, m=plan.m, d=plan.d, generations=gens, seed=seed)
+                fp = fingerprint(cfg)
+                state = engine.initialize(cfg)
+                t0 = time.time()
+                for g in range(1, gens + 1):
+                    state = engine.step(state, cfg, profile=True)
+                    prof = state.timings
+                    timed_out = (time.time() - t0) > plan.time_limit_s
+                    q, hv, hvn = _metrics(state.F, pf, hv_ref, plan.hv_samples, seed)
+                    rows.append({"fingerprint": fp, "seed": seed, "generation": g, "igd": q, "hv_raw": hv,
+                                 "hv_normalized": hvn,
+                                 **{k: prof.get(k, 0.0) for k in ("t_variation", "t_sort", "t_niche", "t_eval")},
+                                 "timed_out": int(timed_out)})
+                    state = dataclasses.replace(state, timings={})
+                    if timed_out:
+                        break
+                torch.cuda.synchronize()
+                if progress:
+                    progress(prob, n, gens, seed)
+    return write_rows(rows, plan.out)
+
+
+def write_rows(rows, path):
+    d = os.path.dirname(os.path.abspath(path))
+    fd, tmp = tempfile.mkstemp(dir=d, suffix=".tmp")
+    try:
+        with os.fdopen(fd, "w", newline="") as f:
+            w = csv.DictWriter(f, fieldnames=COLUMNS)
+            w.writeheader()
+            for r in rows:
+                w.writerow({k: r[k] for k in COLUMNS})
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+    return path
+
+
+def _tci(x):
+    """mean, sample std, 95 % t-interval half width."""
+    from scipy import stats
+    x = np.asarray(x, np.float64)
+    mean = float(x.mean())
+    if x.size < 2:
+        return mean, 0.0, 0.0
+    sd = float(x.std(ddof=1))
+    return mean, sd, float(stats.t.ppf(0.975, x.size - 1) * sd / math.sqrt(x.size))
+
+
+def read_rows(path):
+    rows = []
+    with open(path, newline="") as f:
+        r = csv.DictReader(f)
+        if tuple(r.fieldnames or ()) != COLUMNS:
+            raise ConfigError("csv", f"unexpected header {r.fieldnames}")
+        for lineno, row in enumerate(r, start=2):
+            try:
+                rows.append({"fingerprint": row["fingerprint"], "seed": int(row["seed"]),
+                             "generation": int(row["generation"]),
+                             **{k: float(row[k]) for k in COLUMNS[3:10]}, "timed_out": int(row["timed_out"])})
+            except (TypeError, ValueError) as e:
+                raise ConfigError("csv", f"line {lineno}: {e}") from None
+    return rows
+
+
+def summarize(path):
+    """per fingerprint, statistics over seeds of the final IGD / HV and of the
+    per-generation runtime (generation 1 excluded)."""
+    rows = read_rows(path)
+    out = {}
+    by = {}
+    for r in rows:
+        by.setdefault(r["fingerprint"], []).append(r)
+    for fp, rs in by.items():
+        final = {}
+        times = []
+        for r in rs:
+            key = r["seed"]
+            if key not in final or r["generation"] > final[key]["generation"]:
+                final[key] = r
+            if r["generation"] > 1:
+                times.append(r["t_variation"] + r["t_sort"] + r["t_niche"] + r["t_eval"])
+        fin = list(final.values())
+        out[fp] = {"runs": len(fin),
+                   "igd": _tci([r["igd"] for r in fin]),
+                   "hv_normalized": _tci([r["hv_normalized"] for r in fin]),
+                   "s_per_generation": _tci(times) if times else (float("nan"), 0.0, 0.0)}
+    return out
+
+
+__all__ = ["ExperimentPlan", "COLUMNS", "fingerprint", "run_plan", "write_rows", "read_rows", "summarize"]
