@@ -374,7 +374,7 @@ def run_ours(args, rank, world):
     d2h = n * d * 4 + n * m * 4 + m * 4 + _lib.INFO_COUNT * 4
 
     result = {"ms": ms, "clk": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "info": info,
-              "w": eng.w, "sharded": sharded, "sort": wl["sort"]}
+              "w": eng.w, "sharded": sharded, "sort": wl["sort"], "lattice": eng.lattice is not None}
     kern = time_kernels(torch, eng, _lib) if (rank == 0 or sharded) else None
     if rank == 0:
         result["kernels"] = kern
@@ -447,7 +447,11 @@ def main():
     dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
     kname = ("k_stream_tiles<COUNT> (dominator-count sweep, streamed sort)" if r["sort"] == "stream"
              else "k_dom_tile_sorted (dominance bit-matrix)")
-    launches = K * 8 if r["sort"] == "bits" else K * (14 + 4 * int(kern.get("fronts_issued") or 0))
+    # our kernels per generation: vary, presort, dominance, peel, prep, association (lattice + fallback
+    # scan, or the full scan), assoc_final, select; streamed: + reset/plan/count/mark + 4 per front
+    assoc_kernels = 2 if r.get("lattice") else 1
+    launches = (K * (7 + assoc_kernels) if r["sort"] == "bits"
+                else K * (10 + assoc_kernels + 4 * int(kern.get("fronts_issued") or 0)))
     traffic = (committed_traffic("k_stream_tiles<3, 0>", "r01_ncu_full_c4_count_raw.csv") if args.workload == "c4"
                else committed_traffic("k_dom_tile_sorted<5", "r01_ncu_full_c2_raw.csv") if args.workload == "c2"
                else None)
