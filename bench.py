@@ -395,9 +395,16 @@ def main():
         if rank != 0:
             return
         cores = len(os.sched_getaffinity(0))
+        # bound the whole run to a few minutes: calibrate the per-row cost of the O(R^2) parts once,
+        # then size every step's row sample so that warmup + steps fit in ~180 s
+        cal = cpu_generation_estimate(wl, seed=0, sample_rows=32)
+        fixed = cal["t_variation_eval"] + cal["t_linear"]
+        per_row = (cal["t_dominance"] + cal["t_association"]) * 32 / (2 * wl["n"]) / 32
+        budget = 180.0 / max(1, args.warmup + args.steps)
+        rows = args.cpu_sample_rows or int(max(8, min(256, (budget - fixed) / max(per_row, 1e-9))))
         per = []
         for i in range(args.warmup + args.steps):
-            est = cpu_generation_estimate(wl, seed=0, sample_rows=args.cpu_sample_rows or 256)
+            est = cpu_generation_estimate(wl, seed=i, sample_rows=rows)
             if i >= args.warmup:
                 per.append(est["seconds_per_generation"])
         spg = float(np.mean(per))
