@@ -393,3 +393,38 @@ def test_engine_rejects_oracle_backend(M):
     with pytest.raises(errors.ConfigError) as ei:
         M.engine.initialize(M.engine.RunConfig(backend="oracle"))
     assert ei.value.field == "backend"
+
+
+# ------------------------------------------------ broad state-injection sweep (all engine paths)
+
+SWEEP = [(k, n, m, d, sort) for (k, n, m, d) in [("DTLZ2", 300, 2, 11), ("DTLZ1", 400, 3, 7), ("DTLZ7", 500, 4, 23),
+                                                   ("DTLZ4", 300, 5, 14), ("DTLZ3", 300, 6, 15), ("DTLZ5", 200, 8, 17),
+                                                   ("DTLZ6", 250, 10, 19), ("DTLZ2", 2000, 3, 12)]
+         for sort in ("bits", "stream")]
+
+
+@pytest.mark.parametrize("kind,n,m,d,sort", SWEEP)
+def test_engine_sweep_state_injection(M, kind, n, m, d, sort):
+    """m = 2 .. 10 (single- and two-layer reference sets, lattice pruning where it applies), both sort
+    modes: every generation the oracle's selection on the GPU's merged objectives picks the GPU's
+    survivors exactly."""
+    gens = 3
+    cfg = M.engine.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=23)
+    ocfg = Oeng.RunConfig(problem=kind, n=n, m=m, d=d, generations=gens, seed=23)
+    eng = M.engine.Engine(cfg, sort=sort, prune=True if m <= 5 and eng_prunable(m, n) else "auto")
+    for g in range(gens):
+        st = _gpu_state_to_oracle(eng)
+        cur = eng.cur
+        eng.step()
+        O = np_(eng.XR[cur][n:]).copy()
+        FO = np_(eng.FR[cur][n:]).copy()
+        nxt = Oeng.step(st, ocfg, offspring=(O, FO))
+        info = eng.info_dict()
+        assert info["l"] == nxt.info["l"] and info["k"] == nxt.info["k"], (g, info)
+        assert np.array_equal(np_(eng.X), nxt.X), f"generation {g}"
+        assert np.array_equal(np_(eng.ideal), nxt.ideal)
+
+
+def eng_prunable(m, n):
+    from paper_2504_06067_b200 import refpoints
+    return refpoints.choose_divisions(m, n)[1] == 0
