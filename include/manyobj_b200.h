@@ -325,6 +325,16 @@ size_t mo_hv_mc_workspace_bytes(int64_t samples);
 int mo_hv_mc(const float* front, int64_t nf, int32_t m, const double* lower, const double* upper, int64_t samples,
              uint64_t seed, unsigned long long* hits_out, void* workspace, size_t workspace_bytes, void* stream_);
 
+/* metrics.hv, exact branch (m <= 3): rows that do not weakly
+ * dominate ref (F_i <= ref componentwise) are discarded; the FP64 volume of the
+ * region dominated by the rest and bounded by ref is written to out[0] (0 when
+ * none is retained).  Deterministic (slab decomposition along f3, fixed-order
+ * sums).  Workspace: mo_hv_exact_workspace_bytes(nf).  m outside 1..3 ->
+ * MO_ERR_PARAM.  Replaces the reference's exact sweep. */
+size_t mo_hv_exact_workspace_bytes(int64_t nf);
+int mo_hv_exact(const float* front, int64_t nf, int32_t m, const double* ref, double* out, void* workspace,
+                size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------- measurement helper */
 
 /* Issue-rate microbenchmark for the roofline of the CUDA-core kernels (not a

@@ -50,3 +50,16 @@ def hv(front, ref_point):
             total += _hv2(F[F[:, 2] <= a][:, :2], r[:2]) * (b - a)
         return total
     raise ValueError("exact hv only for m <= 3")
+
+
+def normalized_hv(fronts):
+    """SPEC.md:619-627 (Appendix E Eqs. 3-5): ref = 1.01 f^max, ideal = 0.9 f^min over all fronts,
+    HV_max = prod(ref - ideal); each front's exact hv / HV_max (m <= 3); HV_max = 0 -> zeros."""
+    Fs = [np.asarray(f, np.float64) for f in fronts]
+    allf = np.concatenate([f for f in Fs if f.size])
+    ref = 1.01 * allf.max(axis=0)
+    ideal = 0.9 * allf.min(axis=0)
+    hv_max = float(np.prod(ref - ideal))
+    if not hv_max > 0.0:
+        return [0.0] * len(Fs)
+    return [hv(f, ref) / hv_max for f in Fs]

@@ -77,6 +77,8 @@ _PROTOS = {
     "mo_igd": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_i32, c_vp, c_vp, c_sz, c_vp]),
     "mo_hv_mc_workspace_bytes": (c_sz, [c_i64]),
     "mo_hv_mc": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_i64, c_u64, c_vp, c_vp, c_sz, c_vp]),
+    "mo_hv_exact_workspace_bytes": (c_sz, [c_i64]),
+    "mo_hv_exact": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_sort_stream_begin": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
     "mo_sort_stream_front": (c_i32, [ctypes.POINTER(StepArgs), c_i32, c_vp]),
     "mo_sort_stream_end": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),

@@ -4,9 +4,10 @@
   repetitions, a per-cell time limit and an output path.
 * :func:`run_plan` -- runs every cell on the GPU engine and writes one CSV row per generation with
   the SPEC schema (fingerprint, seed, generation, igd, hv_raw, hv_normalized, t_variation, t_sort,
-  t_niche, t_eval, timed_out).  IGD (GPU, FP64) against 10^4 front points; HV by the GPU Monte-Carlo
-  estimator (exact m <= 3 HV is not implemented on the GPU: the column is the MC estimate with
-  10^5 samples for every m).  The CSV is written atomically (temp file + rename).
+  t_niche, t_eval, timed_out).  IGD (GPU, FP64) against 10^4 front points; HV on the GPU: exact for
+  m <= 3, Monte-Carlo (``hv_samples``, fixed seed) for m > 3; hv_normalized = hv_raw / HV_max with
+  HV_max = prod(ref - 0.9 f^min) over the true-front sample (Appendix E Eqs. 3-5).  The CSV is
+  written atomically (temp file + rename).
 * :func:`summarize` -- per fingerprint: mean, standard deviation and 95 % t-interval of the final IGD /
   HV and of the per-generation runtime (generation 1 excluded: one-time setup).
 * ``compare_backends`` of the reference times the batched against the scalar Alg. 1 back-end; the Alg. 1
@@ -66,11 +67,11 @@ def fingerprint(cfg):
     return hashlib.sha1(json.dumps(d, sort_keys=True, default=str).encode()).hexdigest()[:12]
 
 
-def _metrics(F, ref, hv_ref, hv_samples, seed):
+def _metrics(F, ref, hv_ref, hv_ideal, hv_samples, seed):
     from . import metrics
     q = metrics.igd(F, ref)
-    hv, _ = metrics.hv_mc(F, hv_ref, samples=hv_samples, seed=seed, lower=np.zeros(len(hv_ref)))
-    vol = float(np.prod(hv_ref))
+    hv = metrics.hv(F, hv_ref, samples=hv_samples, seed=seed)
+    vol = float(np.prod(np.asarray(hv_ref) - hv_ideal))
     return q, hv, hv / vol if vol > 0 else 0.0
 
 
@@ -84,6 +85,7 @@ def run_plan(plan, progress=None):
     for prob, n, gens in plan.cells():
         pf = metrics.dtlz_pf_sample(prob, plan.m, plan.ref_points).astype(np.float32)
         hv_ref = tuple(plan.hv_ref) if plan.hv_ref else tuple(1.1 * pf.max(axis=0))
+        hv_ideal = 0.9 * pf.astype(np.float64).min(axis=0)
         for seed in plan.seeds:
             for _ in range(plan.repetitions):
                 cfg = engine.RunConfig(problem=prob, n=n, m=plan.m, d=plan.d, generations=gens, seed=seed)
@@ -94,7 +96,7 @@ def run_plan(plan, progress=None):
                     state = engine.step(state, cfg, profile=True)
                     prof = state.timings
                     timed_out = (time.time() - t0) > plan.time_limit_s
-                    q, hv, hvn = _metrics(state.F, pf, hv_ref, plan.hv_samples, seed)
+                    q, hv, hvn = _metrics(state.F, pf, hv_ref, hv_ideal, plan.hv_samples, seed)
                     rows.append({"fingerprint": fp, "seed": seed, "generation": g, "igd": q, "hv_raw": hv,
                                  "hv_normalized": hvn,
                                  **{k: prof.get(k, 0.0) for k in ("t_variation", "t_sort", "t_niche", "t_eval")},

@@ -15,6 +15,17 @@
 // (Philox) sample stream over the box [lower, ref]; a sample counts when some
 // retained front point weakly dominates it.  Per-block hit counts are summed
 // in fixed order; hv = box volume * hits / samples.
+//
+// HV exact (m <= 3 branch; m = 1, 2 are padded to m = 3
+// with a zero coordinate and a unit reference extent, which multiplies the
+// volume by exactly 1): slab decomposition along the third objective.
+// k_hv_rank ranks the retained rows (F <= ref) in (f1, f2, row) order and in
+// (f3, row) order by tiled all-pairs counting (no sort library; deterministic
+// dense positions) and scatters them; k_hv_slab gives slab k = [z_(k),
+// z_(k+1)) the 2-D staircase area of the rows with z-rank <= k, swept in
+// (f1, f2) order in FP64 (area += (r1 - x) * max(0, ymin - y)), times its
+// thickness; the slabs are added in a fixed order.  O(n^2) work, all of it
+// parallel: ~ms at n = 10^5.
 #include "mo_common.cuh"
 #include "mo_rng.cuh"
 
@@ -148,6 +159,130 @@ __global__ void k_hv_sum(const unsigned long long* __restrict__ hits, int64_t nb
   }
 }
 
+// ------------------------------------------------------------------ HV (exact)
+
+constexpr int HVX_THREADS = 256;
+
+struct HvExactWs {
+  double2* xy;      // [nf] retained rows in (x, y, row) order
+  int32_t* zr;      // [nf] their z-ranks
+  double* zs;       // [nf] z values in (z, row) order
+  double* slab;     // [nf]
+  int32_t* nv;      // retained count
+};
+
+__device__ __forceinline__ void hv_row(const float* F, int m, int64_t i, double& x, double& y, double& z) {
+  x = (double)F[i * m];
+  y = m > 1 ? (double)F[i * m + 1] : 0.0;
+  z = m > 2 ? (double)F[i * m + 2] : 0.0;
+}
+
+__global__ void __launch_bounds__(HVX_THREADS) k_hv_rank(const float* __restrict__ F, int64_t nf, int m,
+                                                         const double* __restrict__ ref, HvExactWs w) {
+  __shared__ double sX[HVX_THREADS], sY[HVX_THREADS], sZ[HVX_THREADS];
+  __shared__ int sV[HVX_THREADS];
+  const double r0 = ref[0], r1 = m > 1 ? ref[1] : 1.0, r2 = m > 2 ? ref[2] : 1.0;
+  const int64_t i = (int64_t)blockIdx.x * HVX_THREADS + threadIdx.x;
+  double x = 0, y = 0, z = 0;
+  bool vi = false;
+  if (i < nf) {
+    hv_row(F, m, i, x, y, z);
+    vi = x <= r0 && y <= r1 && z <= r2;
+  }
+  int px = 0, pz = 0;
+  for (int64_t t0 = 0; t0 < nf; t0 += HVX_THREADS) {
+    __syncthreads();
+    const int64_t j = t0 + threadIdx.x;
+    double a = 0, b = 0, c = 0;
+    bool vj = false;
+    if (j < nf) {
+      hv_row(F, m, j, a, b, c);
+      vj = a <= r0 && b <= r1 && c <= r2;
+    }
+    sX[threadIdx.x] = a; sY[threadIdx.x] = b; sZ[threadIdx.x] = c; sV[threadIdx.x] = vj;
+    __syncthreads();
+    const int tn = (int)min((int64_t)HVX_THREADS, nf - t0);
+    for (int q = 0; q < tn; ++q) {
+      if (!sV[q]) continue;
+      const int64_t jj = t0 + q;
+      const double a2 = sX[q], b2 = sY[q], c2 = sZ[q];
+      px += (a2 < x) || (a2 == x && (b2 < y || (b2 == y && jj < i)));
+      pz += (c2 < z) || (c2 == z && jj < i);
+    }
+  }
+  if (vi) {
+    w.xy[px] = make_double2(x, y);
+    w.zr[px] = pz;
+    w.zs[pz] = z;
+    atomicAdd(w.nv, 1);
+  }
+}
+
+__global__ void __launch_bounds__(HVX_THREADS) k_hv_slab(int m, const double* __restrict__ ref, HvExactWs w) {
+  __shared__ double2 sXY[HVX_THREADS];
+  __shared__ int sZR[HVX_THREADS];
+  const int nv = *w.nv;
+  if ((int64_t)blockIdx.x * HVX_THREADS >= nv) return;  // uniform per block
+  const double r0 = ref[0], r1 = m > 1 ? ref[1] : 1.0, r2 = m > 2 ? ref[2] : 1.0;
+  const int k = blockIdx.x * HVX_THREADS + threadIdx.x;
+  double thick = 0.0;
+  if (k < nv) thick = (k + 1 < nv ? w.zs[k + 1] : r2) - w.zs[k];
+  double area = 0.0, ymin = r1;
+  const bool busy = __syncthreads_or(thick > 0.0);
+  if (!busy) {
+    if (k < nv) w.slab[k] = 0.0;
+    return;
+  }
+  for (int t0 = 0; t0 < nv; t0 += HVX_THREADS) {
+    __syncthreads();
+    if (t0 + (int)threadIdx.x < nv) {
+      sXY[threadIdx.x] = w.xy[t0 + threadIdx.x];
+      sZR[threadIdx.x] = w.zr[t0 + threadIdx.x];
+    }
+    __syncthreads();
+    const int tn = min(HVX_THREADS, nv - t0);
+    if (thick > 0.0) {
+      for (int q = 0; q < tn; ++q) {
+        const double2 p = sXY[q];
+        if (sZR[q] <= k && p.y < ymin) {
+          area = __fma_rn(r0 - p.x, ymin - p.y, area);
+          ymin = p.y;
+        }
+      }
+    }
+  }
+  if (k < nv) w.slab[k] = thick > 0.0 ? area * thick : 0.0;
+}
+
+__global__ void __launch_bounds__(SUM_THREADS) k_hv_exact_sum(HvExactWs w, double* __restrict__ out) {
+  __shared__ double sh[SUM_THREADS];
+  const int nv = *w.nv;
+  double s = 0.0;
+  for (int r = threadIdx.x; r < nv; r += SUM_THREADS) s = __dadd_rn(s, w.slab[r]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int q = SUM_THREADS / 2; q > 0; q >>= 1) {
+    if ((int)threadIdx.x < q) sh[threadIdx.x] = __dadd_rn(sh[threadIdx.x], sh[threadIdx.x + q]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+static HvExactWs hv_exact_layout(void* ws, int64_t nf) {
+  char* p = reinterpret_cast<char*>(ws);
+  HvExactWs w;
+  w.xy = reinterpret_cast<double2*>(p);
+  p += (size_t)nf * 16;
+  w.zs = reinterpret_cast<double*>(p);
+  p += (size_t)nf * 8;
+  w.slab = reinterpret_cast<double*>(p);
+  p += (size_t)nf * 8;
+  w.zr = reinterpret_cast<int32_t*>(p);
+  p += (size_t)((nf + 1) & ~1ll) * 4;
+  w.nv = reinterpret_cast<int32_t*>(p);
+  return w;
+}
+
 }  // namespace mo
 
 using namespace mo;
@@ -214,6 +349,30 @@ int mo_hv_mc(const float* front, int64_t nf, int32_t m, const double* lower, con
   }
   MO_CHECK_LAUNCH();
   k_hv_sum<<<1, 32, 0, s>>>(hits, blocks, hits_out);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+size_t mo_hv_exact_workspace_bytes(int64_t nf) {
+  const int64_t n = nf > 0 ? nf : 1;
+  return (size_t)n * 32 + (size_t)((n + 1) & ~1ll) * 4 + 16;
+}
+
+int mo_hv_exact(const float* front, int64_t nf, int32_t m, const double* ref, double* out, void* workspace,
+                size_t workspace_bytes, void* stream_) {
+  if (m < 1 || m > 3 || nf < 0 || !ref || !out) return MO_ERR_PARAM;
+  if (nf > 0x7ffffffe || (nf > 0 && (!front || !workspace || workspace_bytes < mo_hv_exact_workspace_bytes(nf))))
+    return MO_ERR_PARAM;
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (nf == 0) return cudaMemsetAsync(out, 0, 8, s) == cudaSuccess ? MO_OK : MO_ERR_CUDA;
+  HvExactWs w = hv_exact_layout(workspace, nf);
+  if (cudaMemsetAsync(w.nv, 0, 4, s) != cudaSuccess) return MO_ERR_CUDA;
+  const unsigned blocks = (unsigned)ceil_div(nf, (int64_t)HVX_THREADS);
+  k_hv_rank<<<blocks, HVX_THREADS, 0, s>>>(front, nf, m, ref, w);
+  MO_CHECK_LAUNCH();
+  k_hv_slab<<<blocks, HVX_THREADS, 0, s>>>(m, ref, w);
+  MO_CHECK_LAUNCH();
+  k_hv_exact_sum<<<1, SUM_THREADS, 0, s>>>(w, out);
   MO_CHECK_LAUNCH();
   return MO_OK;
 }

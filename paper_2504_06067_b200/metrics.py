@@ -4,8 +4,11 @@ SPEC.md:529-537) -- SURVEY.md 8(f) item 1.
 
 * :func:`igd` runs on the GPU (``mo_igd``: fused min-distance reduction in
   FP64, deterministic), like the association kernel it resembles.
-* :func:`hv_mc` is the Monte-Carlo branch of ``metrics.hv`` (m > 3,
-  SPEC.md:614) on the GPU (``mo_hv_mc``: Philox samples, dominance counts).
+* :func:`hv`: exact for m <= 3 on the GPU (``mo_hv_exact``:
+  slab decomposition, FP64, deterministic), Monte-Carlo with 10^6 samples and
+  a fixed seed for m > 3 (:func:`hv_mc`, ``mo_hv_mc``: Philox samples,
+  dominance counts; it also returns the standard error).
+* :func:`normalized_hv` (the paper's Appendix E Eqs. 3-5).
 * :func:`dtlz_pf_sample` is host set-up code like ``refpoints``: FP64 points
   on the true front from the problems' own parametrisations at g = 0,
   positions from the R_(m-1) Kronecker sequence (deterministic, low
@@ -13,6 +16,7 @@ SPEC.md:529-537) -- SURVEY.md 8(f) item 1.
   surface, so candidates are filtered (in order) until ``count`` remain.
 """
 import ctypes
+import warnings
 
 import numpy as np
 import torch
@@ -62,6 +66,53 @@ def hv_mc(front, ref_point, samples=10 ** 6, seed=0, lower=None):
     vol = float(torch.prod(r - lo).item())
     p = int(hits.item()) / float(samples)
     return vol * p, vol * np.sqrt(max(p * (1.0 - p), 0.0) / samples)
+
+
+def hv(front, ref_point, samples=10 ** 6, seed=0):
+    """Hypervolume dominated by ``front`` and bounded by ``ref_point``: rows that do
+    not weakly dominate ``ref_point`` are discarded (empty -> 0).  m <= 3: exact; m > 3: the
+    Monte-Carlo estimate of :func:`hv_mc` (``samples``, fixed ``seed``)."""
+    F = as_matrix(front)
+    m = F.shape[1]
+    r = np.asarray(ref_point, np.float64).reshape(-1)
+    if r.size != m:
+        raise ShapeError("ref_point must have one component per objective")
+    if m > 3:
+        return hv_mc(F, r, samples=samples, seed=seed)[0]
+    if F.shape[0] == 0:
+        return 0.0
+    L = _lib.lib()
+    rd = torch.as_tensor(r, device=F.device)
+    ws = torch.empty(int(L.mo_hv_exact_workspace_bytes(F.shape[0])), dtype=torch.uint8, device=F.device)
+    out = torch.empty(1, dtype=torch.float64, device=F.device)
+    _lib.check(L.mo_hv_exact(_lib.ptr(F), F.shape[0], m, _lib.ptr(rd), _lib.ptr(out), _lib.ptr(ws), ws.numel(),
+                             _lib.stream_ptr()), "mo_hv_exact")
+    return float(out.item())
+
+
+def normalized_hv(fronts, samples=10 ** 6, seed=0):
+    """SPEC.md:619-627 / Appendix E Eqs. (3)-(5): f^max, f^min over ALL fronts; ref = 1.01 f^max,
+    ideal = 0.9 f^min (applied literally, also to negative minima), HV_max = prod(ref - ideal); each
+    front's hv(front, ref) / HV_max.  HV_max = 0 -> all zeros and a RuntimeWarning."""
+    Fs = [as_matrix(f) for f in fronts]
+    if not Fs:
+        raise EmptySelectionError("normalized_hv needs at least one front")
+    m = Fs[0].shape[1]
+    if any(f.shape[1] != m for f in Fs):
+        raise ShapeError("all fronts must have the same number of objectives")
+    rows = [f.double() for f in Fs if f.shape[0] > 0]
+    if not rows:
+        raise EmptySelectionError("normalized_hv needs a nonempty front")
+    allf = torch.cat(rows)
+    fmax = allf.amax(dim=0).cpu().numpy()
+    fmin = allf.amin(dim=0).cpu().numpy()
+    ref = 1.01 * fmax
+    ideal = 0.9 * fmin
+    hv_max = float(np.prod(ref - ideal))
+    if not hv_max > 0.0:
+        warnings.warn("normalized_hv: HV_max = 0 (degenerate fronts); all values set to 0", RuntimeWarning)
+        return [0.0] * len(Fs)
+    return [hv(f, ref, samples=samples, seed=seed) / hv_max for f in Fs]
 
 
 # ------------------------------------------------------------- front samplers
@@ -144,4 +195,4 @@ def dtlz_pf_sample(kind, m, count):
     raise ParameterError(f"no closed-form front for {kind!r}")
 
 
-__all__ = ["igd", "hv_mc", "dtlz_pf_sample"]
+__all__ = ["igd", "hv", "hv_mc", "normalized_hv", "dtlz_pf_sample"]
