@@ -185,6 +185,53 @@ def cpu_generation_estimate(wl, seed=0, sample_rows=0, threads=None):
             "split_k": split.k}
 
 
+def cpu_generation_c(wl, seed=0, threads=0, max_pairs=4e9):
+    """Seconds per generation with the quadratic stages in the C/OpenMP restatement (oracle/c, all host
+    cores; SURVEY.md 8(d)'s "fair multi-core CPU"): non-dominated sort with stop_at = n and the
+    canonical association over all R rows run in full when R^2 (resp. R w) <= max_pairs, else on a row
+    sample scaled by rows; variation, evaluation and normalisation as in the numpy oracle."""
+    from oracle import c as oc
+    from oracle.manyobj_ref import engine as Oeng
+    from oracle.manyobj_ref import niche as On
+    from oracle.manyobj_ref import rng as Orng
+    from oracle.manyobj_ref import variation as Ov
+
+    cfg = Oeng.RunConfig(problem=wl["problem"], n=wl["n"], m=wl["m"], d=wl["d"], generations=1, seed=seed)
+    st = Oeng.initialize(cfg)
+    n = wl["n"]
+    R = 2 * n
+    t0 = time.perf_counter()
+    O = Ov.vary(st.X, cfg.variation, seed, 0)
+    FO = Oeng.evaluate(cfg, O)
+    t_vary = time.perf_counter() - t0
+    FR = np.ascontiguousarray(np.concatenate([st.F, FO]), np.float32)
+    rs = np.random.default_rng(seed)
+    t0 = time.perf_counter()
+    if float(R) * R <= max_pairs:
+        oc.nds(FR, stop_at=n, threads=threads)
+        dom_rows = R
+    else:
+        dom_rows = max(256, int(max_pairs / R))
+        oc.dominator_counts(FR, rows=np.sort(rs.choice(R, dom_rows, replace=False)), threads=threads)
+    t_dom = (time.perf_counter() - t0) * R / dom_rows
+    zh = np.ascontiguousarray(st.zhat, np.float32)
+    w = zh.shape[0]
+    pos_ref = Orng.positions(w, seed, 0, Orng.STREAM_REF_SHUFFLE)
+    Fn = ((FR - FR.min(0)) / np.maximum(FR.max(0) - FR.min(0), 1e-10)).astype(np.float32)
+    as_rows = R if float(R) * w <= max_pairs else max(256, int(max_pairs / w))
+    t0 = time.perf_counter()
+    oc.associate(Fn, zh, pos_ref, rows=None if as_rows == R else np.sort(rs.choice(R, as_rows, replace=False)),
+                 threads=threads)
+    t_assoc = (time.perf_counter() - t0) * R / as_rows
+    t0 = time.perf_counter()
+    On.normalize_objectives(FR, st.ideal, np.ones(R, bool), Orng.positions(R, seed, 0, Orng.STREAM_POP_SHUFFLE))
+    t_lin = time.perf_counter() - t0
+    total = t_vary + t_dom + t_assoc + t_lin
+    return {"seconds_per_generation": total, "t_variation_eval": t_vary, "t_dominance": t_dom,
+            "t_association": t_assoc, "t_linear": t_lin, "cores": threads or oc.max_threads(),
+            "dominance_rows": dom_rows, "association_rows": as_rows}
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def measure_peaks(torch, L, _lib):
@@ -495,6 +542,17 @@ def main():
                                 "sample": f"numpy oracle: dominance + association on {est['sample_rows']} of {R} "
                                           "rows scaled by rows; variation, evaluation, normalisation in full",
                                 "detail_s": {k: round(v, 3) for k, v in est.items() if k.startswith("t_")}}
+        try:
+            ce = cpu_generation_c(wl, seed=0, threads=len(os.sched_getaffinity(0)))
+            line["cpu_baseline"]["fair_multicore"] = {
+                "value": 1.0 / ce["seconds_per_generation"], "unit": "generations/s", "cores": ce["cores"],
+                "kind": "port",
+                "sample": (f"C/OpenMP restatement (oracle/c): non-dominated sort on {ce['dominance_rows']} and "
+                           f"association on {ce['association_rows']} of {R} rows (scaled by rows when sampled); "
+                           "numpy variation / evaluation / normalisation"),
+                "detail_s": {k: round(v, 4) for k, v in ce.items() if k.startswith("t_")}}
+        except (OSError, RuntimeError, subprocess.CalledProcessError) as e:     # no gcc / libgomp on the host
+            line["cpu_baseline"]["fair_multicore"] = {"unavailable": f"{type(e).__name__}: {e}"}
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
