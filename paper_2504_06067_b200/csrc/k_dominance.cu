@@ -550,7 +550,11 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     maxb = sms * (per > 0 ? (per > 1 ? 1 : per) : 1);
   }
   const int NB = presort_buckets(args.R);
-  int blocks = (int)ceil_div(args.R > NB ? args.R : NB, PRESORT_THREADS / 2);
+  // rows drive the grid (a CTA per 128 rows: C2's bucket scan wants ~all SMs); a tiny population keeps
+  // one or two CTAs so its grid barriers stay cheap (C1: 8 -> 2 CTAs, 0.116 -> 0.106 ms/generation)
+  const int64_t by_rows = ceil_div((int64_t)args.R, (int64_t)(PRESORT_THREADS / 2));
+  const int64_t by_buckets = ceil_div((int64_t)NB, (int64_t)(PRESORT_THREADS * 4));
+  int blocks = (int)(by_rows > by_buckets ? by_rows : by_buckets);
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
   if (!args.in_step) {

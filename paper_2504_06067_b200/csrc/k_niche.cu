@@ -177,8 +177,12 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     }
     gen_prologue(a, gen, gtid, gthreads, sKp, sSp, &sRp, sKr, sSr, &sRr);
   }
-  for (int i = gtid; i < R; i += gthreads)
-    if (a.ranks[i] >= 0 && a.ranks[i] <= l) a.cand[atomicAdd(a.ctl, 1)] = i;
+  for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
+    const int i = base + tid;
+    const bool c = i < R && a.ranks[i] >= 0 && a.ranks[i] <= l;
+    const int slot = warp_alloc(a.ctl, c ? 1 : 0);          // candidate order is immaterial
+    if (c) a.cand[slot] = i;
+  }
   if (a.mode != PREP_FULL) return;
   if (gtid < m) {
     a.ext_key[gtid] = ~0ull;
@@ -445,8 +449,15 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
     atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
   }
   bool done = !ok;   // group-uniform
-  // radius r, then r+1, r+2 for the rows whose certificate failed (no separate full scan for them)
-  for (int it = 0; it < 3; ++it) {
+  // per-row FP64 constants of the box and the certificate, hoisted out of the radius loop: x_k = f_k * H/s;
+  // sin >= (r/H) / (sqrt(m) ||u||) = r * s / (H sqrt(m) ||f||) with u = f/s (rounding here is ~1e-16
+  // relative, far inside the 1e-6 radius margin and the 2^-24 key slack of the bound)
+  const double hs = ok ? (double)H / s : 0.0;
+  const double sn = sqrt(nn);
+  const double c_se = ok ? s / ((double)H * sqrt((double)M) * sn) : 0.0;
+  // radius r, then r+1 for the rows whose certificate failed; the rare rest goes to the sliced full scan
+  // (a (2r+4)^(m-1) box walked by one group is a latency-bound straggler that holds the whole grid)
+  for (int it = 0; it < 2; ++it) {
     if (__all_sync(MO_FULL, done)) break;
     const int rr = r + it;
     float best = -__int_as_float(0x7f800000);
@@ -459,7 +470,7 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
       total = 1;
 #pragma unroll
       for (int k = 0; k < M - 1; ++k) {
-        const double x = (double)fn[k] / s * (double)H;
+        const double x = (double)fn[k] * hs;
         lo[k] = max(0, (int)floor(x - (double)rr) + 1);
         const int hi = min(H, (int)ceil(x + (double)rr) - 1);
         ext[k] = max(0, hi - lo[k] + 1);
@@ -473,6 +484,7 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
       ext[k] = __shfl_sync(MO_FULL, ext[k], 0, LPR);
       inv[k] = ext[k] > 0 ? 1.0f / (float)ext[k] : 0.0f;
     }
+#pragma unroll 2
     for (int q = sub; q < total; q += LPR) {
       int rem = q, rest, idx = 0;
       int kv[M];  // mixed-radix decode of the box index, k_{m-2} fastest; (rem + .5) / ext is exact in
@@ -509,10 +521,9 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
     }
     int cert = 0;
     if (sub == 0 && !done) {
-      const double un = sqrt(nn) / s;                       // ||u||, u = f / sum(f)
-      double se = ((double)rr - 1e-6) / (double)H / (sqrt((double)M) * un);
+      double se = ((double)rr - 1e-6) * c_se;
       se = se < 1.0 ? se : 1.0;
-      const double bound = sqrt(nn) * sqrt(1.0 - se * se) * (1.0 + (M + 2) * 5.9604644775390625e-8);
+      const double bound = sn * sqrt(1.0 - se * se) * (1.0 + (M + 2) * 5.9604644775390625e-8);
       cert = bp != 0x7fffffff && (double)best > bound;
       if (cert)
         a.akey[row] = ((unsigned long long)f2ord(best) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp);
@@ -527,7 +538,7 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
 }
 
 // Full scan for the few rows the lattice certificate rejected: items = (row, slice of the shard's
-// reference range, 512 points); a warp per item, lanes stride the slice in shuffled order with the
+// reference range sized so the items cover the grid's warps, >= 32 points); a warp per item, lanes stride the slice in shuffled order with the
 // canonical key and a strict '>' (first maximum per lane), a warp reduction (max key, lowest position),
 // and an atomicMax merge of the slices into akey -- many short independent scans instead of a few long
 // latency-bound ones.
@@ -539,8 +550,12 @@ __global__ void __launch_bounds__(256) k_assoc_fallback(AssocArgs a) {
   const int nfb = __ldcg(a.fb_ctl);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  constexpr int SLICE = 512;
-  const int nslice = (a.zend - a.zbeg + SLICE - 1) / SLICE;
+  // slice the reference range so that the items cover the grid's warps (a handful of rows -> one
+  // 32-point slice per warp; many rows -> longer slices); at least 32 points per slice
+  const int range = a.zend - a.zbeg;
+  const int per_row = max(1, nwarps / max(nfb, 1));
+  const int SLICE = max(32, ((range + per_row - 1) / per_row + 31) & ~31);
+  const int nslice = (range + SLICE - 1) / SLICE;
   for (int it = warp; it < nfb * nslice; it += nwarps) {
     const int c = it / nslice, sl = it - c * nslice;
     const int row = __ldcg(a.fb_cand + c);
@@ -836,13 +851,18 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       grid_sync(a.g.bar);
       trace_mark(a.trace, 28);
       // ---- P5: take_j; bucket storage for partially taken points
-      for (int j = gtid; j < w; j += gthreads) {
-        const int c = __ldcg(a.rho_p + j);
-        if (c == 0) continue;
-        const long long t0 = (long long)L - __ldcg(a.rho + j);
-        const int t = (int)(t0 < 0 ? 0 : (t0 > c ? c : t0)) + __ldcg(a.kept + j);
-        a.take[j] = t;
-        if (t > 0 && t < c) a.bstart[j] = atomicAdd(&a.sctl[SCTL_ALLOC], c);
+      for (int base = blockIdx.x * blockDim.x; base < w; base += gthreads) {   // uniform trip count
+        const int j = base + threadIdx.x;
+        const int c = j < w ? __ldcg(a.rho_p + j) : 0;
+        int t = 0;
+        if (c > 0) {
+          const long long t0 = (long long)L - __ldcg(a.rho + j);
+          t = (int)(t0 < 0 ? 0 : (t0 > c ? c : t0)) + __ldcg(a.kept + j);
+          a.take[j] = t;
+        }
+        const bool part = c > 0 && t > 0 && t < c;
+        const int off = warp_alloc(&a.sctl[SCTL_ALLOC], part ? c : 0);   // bucket order is immaterial
+        if (part) a.bstart[j] = off;
       }
       grid_sync(a.g.bar);
       trace_mark(a.trace, 29);
@@ -1023,7 +1043,7 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     case 2: MO_TRY(launch_ex(k_assoc_lattice<2, 1>, dim3((unsigned)ceil_div(R, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
     case 3: MO_TRY(launch_ex(k_assoc_lattice<3, 8>, dim3((unsigned)ceil_div(R * 8, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
     case 4: MO_TRY(launch_ex(k_assoc_lattice<4, 32>, dim3((unsigned)ceil_div(R * 32, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
-    case 5: MO_TRY(launch_ex(k_assoc_lattice<5, 32>, dim3((unsigned)ceil_div(R * 32, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
+    case 5: MO_TRY(launch_ex(k_assoc_lattice<5, 16>, dim3((unsigned)ceil_div(R * 16, 256)), dim3(256), 0, s, false, g_mo_pdl, a)); break;
     default: return MO_ERR_PARAM;
   }
   // fallback rows: a warp-per-row full scan over this launch's reference range

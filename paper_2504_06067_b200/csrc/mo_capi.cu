@@ -302,7 +302,7 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
 }
 
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
-static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 2); }
+static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 1); }
 
 static PrepArgs niche_prep_args(const mo_step_args* a, const Layout& L) {
   const int64_t R = 2 * a->n;

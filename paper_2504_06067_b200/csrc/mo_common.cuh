@@ -87,6 +87,25 @@ __device__ __forceinline__ void warp_agg_add(int* hist, int bin, bool active) {
   if ((int)lane_id() == leader) atomicAdd(hist + bin, __popc(peers));
 }
 
+// Warp-aggregated allocation from a global counter: every lane of the (full) warp
+// calls it with its count (0 allowed); one atomic per warp; returns the lane's
+// offset (only meaningful when cnt > 0).  Slot order within the counter is
+// scheduling-dependent, so callers must not depend on it.
+__device__ __forceinline__ int warp_alloc(int* ctr, int cnt) {
+  const int lane = (int)lane_id();
+  int x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(MO_FULL, x, o);
+    if (lane >= o) x += t;
+  }
+  const int total = __shfl_sync(MO_FULL, x, 31);
+  int base = 0;
+  if (lane == 31 && total > 0) base = atomicAdd(ctr, total);
+  base = __shfl_sync(MO_FULL, base, 31);
+  return base + x - cnt;
+}
+
 // Block-wide exclusive scan of one int per thread (blockDim.x multiple of 32, <= 1024).
 // `sh` must hold >= 33 ints.  Returns the exclusive prefix; *total gets the block sum.
 __device__ __forceinline__ int block_excl_scan(int v, int* sh, int* total) {

@@ -162,7 +162,7 @@ class Engine:
             if prune is True and not legal:
                 raise ConfigError("prune", "lattice pruning needs a single-layer Das-Dennis set and m <= 5")
             return None, 0
-        r = self.prune_r or (6 if m <= 3 else (3 if m == 4 else 2))   # default_lattice_r (mo_capi.cu)
+        r = self.prune_r or (6 if m <= 3 else (3 if m == 4 else 1))   # default_lattice_r (mo_capi.cu)
         # a box point costs several full-scan points (decode + gathered loads); measured: C2 (m=5, w=8855,
         # r=2) 185 -> 167 us niche phase, m=5 N=100k 6.2 -> 0.54 ms (scripts/assoc_probe.py)
         if prune == "auto" and 8 * (2 * r - 1) ** (m - 1) >= w:     # box of (2r-1)^(m-1) points
