@@ -19,6 +19,8 @@
 // across all fronts every word of a row is read once plus one re-check per
 // front.  Eight lanes scan one row 128 bytes at a time.
 #include "mo_chains.cuh"
+#include <cstdlib>
+
 #include "mo_common.cuh"
 #include "mo_grid.cuh"
 #include "k_dominance_args.cuh"
@@ -540,6 +542,128 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   trace_mark(a.trace, 5);
 }
 
+// k_presort_small: the same counting sort for R <= PS_MAXR rows in ONE 1024-thread CTA with the keys and
+// bucket counters in shared memory -- no grid barriers (the multi-CTA version spends most of its ~22 us at
+// C2 in six of them).  Buckets: min(presort_buckets(R), PS_MAXNB); as in k_presort the order inside a
+// bucket is arbitrary and only S-monotonicity of the buckets matters.  Row state in shared memory:
+// key (P0) -> bucket (P1) -> (bucket << 15 | position) (P3).
+constexpr int PS_THREADS = 1024;
+constexpr int PS_MAXR = 32768;
+constexpr int PS_MAXNB = 16384;
+
+size_t presort_small_smem(int R) {
+  const int nb = presort_buckets(R) < PS_MAXNB ? presort_buckets(R) : PS_MAXNB;
+  return (size_t)R * 4 + (size_t)nb * 4;
+}
+
+__global__ void __launch_bounds__(PS_THREADS, 1) k_presort_small(PresortArgs a) {
+  pdl_wait();
+  extern __shared__ uint32_t ps_smem[];
+  __shared__ unsigned sMin, sMax;
+  __shared__ int sh[40];
+  const int R = a.R, m = a.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NB = presort_buckets(R) < PS_MAXNB ? presort_buckets(R) : PS_MAXNB;
+  uint32_t* sKQ = ps_smem;
+  int* sCnt = reinterpret_cast<int*>(ps_smem + R);
+  trace_mark(a.trace, 0);
+  if (tid == 0) {
+    sMin = 0xffffffffu;
+    sMax = 0u;
+  }
+  for (int q = tid; q < NB; q += PS_THREADS) sCnt[q] = 0;
+  if (a.hasdom)
+    for (int p = tid; p < R; p += PS_THREADS) a.hasdom[p] = 0;
+  __syncthreads();
+  // P0: S, key, key range
+  unsigned kmin = 0xffffffffu, kmax = 0u;
+#pragma unroll 4
+  for (int i = tid; i < R; i += PS_THREADS) {
+    const float* f = a.F + (int64_t)i * m;
+    float sm = f[0];
+    for (int k = 1; k < m; ++k) sm = __fadd_rn(sm, f[k]);
+    const uint32_t key = f2ord(sm);
+    sKQ[i] = key;
+    kmin = min(kmin, key);
+    kmax = max(kmax, key);
+  }
+  kmin = warp_min_u32(kmin);
+  kmax = warp_max_u32(kmax);
+  if (lane == 0) {
+    atomicMin(&sMin, kmin);
+    atomicMax(&sMax, kmax);
+  }
+  __syncthreads();
+  trace_mark(a.trace, 1);
+  // P1: bucket + histogram (shared-memory atomics)
+  const uint32_t lo = sMin;
+  const uint64_t span = (uint64_t)(sMax - lo) + 1ull;
+  for (int i = tid; i < R; i += PS_THREADS) {
+    const uint32_t q = (uint32_t)(((uint64_t)(sKQ[i] - lo) * (uint64_t)NB) / span);
+    sKQ[i] = q;
+    atomicAdd(&sCnt[q], 1);
+  }
+  __syncthreads();
+  trace_mark(a.trace, 2);
+  // P2: exclusive scan of the counts (NB is a multiple of PS_THREADS: consecutive runs per thread)
+  {
+    const int per = NB / PS_THREADS, q0 = tid * per;
+    int run = 0;
+    for (int q = q0; q < q0 + per; ++q) run += sCnt[q];
+    int total;
+    int pre = block_excl_scan(run, sh, &total);
+    for (int q = q0; q < q0 + per; ++q) {
+      const int c = sCnt[q];
+      sCnt[q] = pre;
+      pre += c;
+    }
+  }
+  __syncthreads();
+  trace_mark(a.trace, 3);
+  // P3: scatter (after it sCnt[q] = end of bucket q)
+#pragma unroll 2
+  for (int i = tid; i < R; i += PS_THREADS) {
+    const uint32_t q = sKQ[i];
+    const int pos = atomicAdd(&sCnt[q], 1);
+    sKQ[i] = (q << 15) | (uint32_t)pos;
+    const float* f = a.F + (int64_t)i * m;
+    float* fs = a.FS + (int64_t)pos * m;
+    float sm = f[0];
+    fs[0] = __fadd_rn(sm, 0.0f);   // -0 -> +0
+    for (int k = 1; k < m; ++k) {
+      const float v = f[k];
+      sm = __fadd_rn(sm, v);
+      fs[k] = __fadd_rn(v, 0.0f);
+    }
+    a.perm[pos] = i;
+    a.SS[pos] = sm;                // == ord2f(key): the same FP32 sum
+  }
+  __syncthreads();
+  trace_mark(a.trace, 4);
+  // P4: wend, then per-256-row S range (SS written above by this CTA)
+  for (int i = tid; i < R; i += PS_THREADS) {
+    const uint32_t v = sKQ[i];
+    a.wend[v & 0x7fffu] = (sCnt[v >> 15] - 1) / 32 + 1;
+  }
+  const int nblk = (R + 255) / 256;
+  for (int b = warp; b < nblk; b += PS_THREADS / 32) {
+    float mn = 3.402823466e38f, mx = -3.402823466e38f;
+    for (int p = b * 256 + lane; p < min(R, b * 256 + 256); p += 32) {
+      const float v = a.SS[p];
+      mn = fminf(mn, v);
+      mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(MO_FULL, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(MO_FULL, mx, o));
+    }
+    if (lane == 0) {
+      a.blkmin[b] = mn;
+      a.blkmax[b] = mx;
+    }
+  }
+  trace_mark(a.trace, 5);
+}
+
 int launch_presort(const PresortArgs& args, cudaStream_t s) {
   static int maxb = 0;
   if (!maxb) {
@@ -548,6 +672,23 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_presort, PRESORT_THREADS, 0);
     maxb = sms * (per > 0 ? (per > 1 ? 1 : per) : 1);
+  }
+  static int small_max = -1;
+  if (small_max < 0) {   // crossover (rows) below which the single-CTA presort wins; MO_PRESORT_SMALL_MAX overrides
+    const char* e = getenv("MO_PRESORT_SMALL_MAX");
+    small_max = e ? atoi(e) : 2048;
+    if (small_max > PS_MAXR) small_max = PS_MAXR;
+  }
+  if (!args.stable && args.R <= small_max) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(k_presort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)presort_small_smem(PS_MAXR)) != cudaSuccess)
+        return MO_ERR_CUDA;
+      attr = true;
+    }
+    return launch_ex(k_presort_small, dim3(1), dim3(PS_THREADS), presort_small_smem(args.R), s, false,
+                     g_mo_pdl && args.in_step, args);
   }
   const int NB = presort_buckets(args.R);
   // rows drive the grid (a CTA per 128 rows: C2's bucket scan wants ~all SMs); a tiny population keeps
