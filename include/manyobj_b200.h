@@ -232,6 +232,13 @@ typedef struct mo_step_args {
   int32_t* lattice_pos;
   int32_t lattice_H;
   int32_t lattice_r;
+  int32_t pad3;
+  /* Tensor-core filter of the full-scan association (no lattice, one shard,
+   * w >= 1024): the unit directions packed by mo_pack_refs_bf16 (device,
+   * mo_pack_refs_bytes(w) bytes, static).  NULL = FP32 scan only.  The
+   * association stays bit-identical: the bf16 MMA only selects which
+   * references get the canonical FP32 key. */
+  const void* zhat_frag;
 } mo_step_args;
 
 enum { MO_SORT_BITS = 0, MO_SORT_STREAM = 1 };
@@ -334,6 +341,15 @@ int mo_hv_mc(const float* front, int64_t nf, int32_t m, const double* lower, con
 size_t mo_hv_exact_workspace_bytes(int64_t nf);
 int mo_hv_exact(const float* front, int64_t nf, int32_t m, const double* ref, double* out, void* workspace,
                 size_t workspace_bytes, void* stream);
+
+/* bf16 hi/lo m16n8k16 B-fragments of the w unit directions zhat (w x m FP32,
+ * device) for mo_step_args.zhat_frag, in the packed column order `order`
+ * (device int32[w], a permutation of the reference indices; NULL = identity;
+ * a random order makes the filter's running maximum converge in a few steps):
+ * 544 bytes per 8 columns (fragments + the columns' reference indices).
+ * m <= 16. */
+size_t mo_pack_refs_bytes(int64_t w);
+int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
 
 /* ---------------------------------------------------- measurement helper */
 

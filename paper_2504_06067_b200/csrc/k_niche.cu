@@ -20,6 +20,8 @@
 //             shuffled positions are promoted, and the stable survivor
 //             compaction.  (Niche counts are warp-aggregated atomics fused
 //             into k_assoc_final.)
+#include <cuda_bf16.h>
+
 #include "mo_common.cuh"
 #include "mo_grid.cuh"
 #include "mo_rng.cuh"
@@ -592,6 +594,275 @@ __global__ void __launch_bounds__(256) k_assoc_fallback(AssocArgs a) {
   }
 }
 
+// ------------------------------------------- association: tensor-core filter + exact FP32 keys
+//
+// The full-scan association (no lattice) is a GEMM, Fn (rows x m) x Zhat^T (m x w), followed by a row
+// argmax of the canonical FP32 key.  k_assoc_hmma evaluates the dots on the tensor cores as a FILTER and
+// the canonical key only where it can matter:
+//   * the m <= 16 coordinates are padded to K = 16 and split into bf16 hi + lo parts (x = hi + lo +
+//     O(2^-17 |x|)); three m16n8k16 bf16 MMAs with FP32 accumulation (hi.hi + hi.lo + lo.hi) give
+//     t~ with |t~ - t| <= 2^-13 sum_k |f_k z_k| <= 2^-13 ||f|| for the canonical key t (products of
+//     bf16 are exact in FP32; <= 48 accumulations; the dropped lo.lo and residual terms) -- the filter
+//     uses eps = 2^-12 ||f||, twice that;
+//   * a reference is a candidate when t~ >= (running max of t~ seen by this lane) - 2 eps; the exact
+//     argmax j* and every exact tie satisfy t~ >= T* - eps >= max t~ - 2 eps, so each is a candidate
+//     when it is reached; candidates get the canonical key (ord(t) << 32 | ~position), the same
+//     atomicMax merge as the FP32 scan -> bit-identical association;
+//   * rows with ||f|| = 0 or non-finite values (every reference ties / no order) go to the sliced
+//     full scan (fb_cand), like the lattice rejects.
+// Layout: a warp owns 16 candidate rows (A fragments in registers for the whole sweep) and walks a chunk
+// of 8-reference tiles; the 8 warps of a CTA take 8 row tiles of the SAME chunk so the fragment stream
+// (544 B per tile: hi, lo, reference indices) is read once per CTA from L2 and hit in L1 by the other warps.  mma.sync
+// (HMMA) rather than tcgen05: K = 16 is a single MMA step and the work is the per-element filter and
+// running max on the accumulators, which needs them in registers anyway.
+constexpr int HMMA_WARPS = 8;
+
+__device__ __forceinline__ uint32_t bf16x2_bits(float lo_k, float hi_k) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo_k, hi_k);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void split_bf16(float x, float& h, float& l) {
+  h = __bfloat162float(__float2bfloat16_rn(x));
+  l = __fsub_rn(x, h);
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// fragments of tile t (refs 8t..8t+7, static order): lane L holds ref n = L / 4 and k pairs (2(L%4), +1),
+// (2(L%4) + 8, +9): [t][0..31] hi parts, [t][32..63] lo parts
+constexpr int HMMA_TS = 68;   // uint2 per packed tile: 32 hi + 32 lo fragments, then 8 int32 reference indices
+
+__global__ void k_pack_refs(const float* __restrict__ zhat, int64_t w, int m, const int32_t* __restrict__ order,
+                            uint2* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t ntiles = (w + 7) / 8;
+  if (e >= ntiles * 32) return;
+  const int64_t t = e >> 5;
+  const int lane = (int)(e & 31), tg = lane & 3, n = lane >> 2;
+  const int64_t q = t * 8 + n;                       // packed column
+  const int64_t j = q < w ? (order ? (int64_t)order[q] : q) : -1;
+  float v[4], h[4], l[4];
+  const int ks[4] = {2 * tg, 2 * tg + 1, 2 * tg + 8, 2 * tg + 9};
+  for (int c = 0; c < 4; ++c) {
+    v[c] = (j >= 0 && ks[c] < m) ? zhat[j * m + ks[c]] : 0.0f;
+    split_bf16(v[c], h[c], l[c]);
+  }
+  out[t * HMMA_TS + lane] = make_uint2(bf16x2_bits(h[0], h[1]), bf16x2_bits(h[2], h[3]));
+  out[t * HMMA_TS + 32 + lane] = make_uint2(bf16x2_bits(l[0], l[1]), bf16x2_bits(l[2], l[3]));
+  if (tg == 0) reinterpret_cast<int32_t*>(out + t * HMMA_TS + 64)[n] = (int32_t)j;
+}
+
+template <int M>
+__device__ __forceinline__ void hmma_load_fn(const AssocArgs& a, int row, float (&fn)[M]) {
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    float v = a.F[(int64_t)row * M + k];
+    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+    fn[k] = v;
+  }
+}
+
+// exact canonical keys of the candidates among the step's filter values of one row (packed columns
+// 2tg, 2tg + 1 of tiles t .. t+U-1; the reference index of a column is stored after the tile's fragments);
+// fn: the row's normalised objectives (shared memory, written once per item)
+template <int M, int U>
+__device__ __forceinline__ void hmma_exact(const AssocArgs& a, const float* fn, const float (&v)[U][2], int t, int tg,
+                                           float thr, unsigned long long& best) {
+  uint32_t mask = 0;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) mask |= (v[u][e] >= thr ? 1u : 0u) << (2 * u + e);
+  while (mask) {
+    const int b = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int j = __ldg(reinterpret_cast<const int*>(a.zfrag + (int64_t)(t + (b >> 1)) * HMMA_TS + 64) +
+                        2 * tg + (b & 1));
+    if (j < 0) continue;
+    const int p = __ldg(a.pos_ref + j);
+    float f[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) f[k] = fn[k];
+    const float tk = canon_dot<M>(f, a.zs + (int64_t)p * M);
+    const unsigned long long key = ((unsigned long long)f2ord(tk) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
+    best = key > best ? key : best;
+  }
+}
+
+constexpr int HMMA_U = 8;   // tiles per filter step
+
+// one filter step over U tiles t .. t+U-1: 3U independent MMAs (fragment loads issued first), one max per
+// row; rows whose step maximum reaches (running max - 2 eps) get their candidates' exact keys (rare after
+// the first steps)
+template <int M, int U, bool WARM>
+__device__ __forceinline__ void hmma_step(const AssocArgs& a, int t, int lane, int tg, const uint32_t (&ah)[4],
+                                          const uint32_t (&al)[4], const bool (&act)[2], const float* fn0,
+                                          const float* fn1, const float (&marg)[2], float& mx0, float& mx1,
+                                          unsigned long long& best0, unsigned long long& best1) {
+  uint2 bh[U], bl[U];
+  const uint2* fr = a.zfrag + (int64_t)t * HMMA_TS + lane;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    bh[u] = __ldg(fr + u * HMMA_TS);
+    bl[u] = __ldg(fr + u * HMMA_TS + 32);
+  }
+  float v0[U][2], v1[U][2];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    mma_bf16_16816(c, ah, bh[u].x, bh[u].y);
+    mma_bf16_16816(c, ah, bl[u].x, bl[u].y);
+    mma_bf16_16816(c, al, bh[u].x, bh[u].y);
+    v0[u][0] = c[0];   // row gid, packed columns 2tg, 2tg + 1 of tile t + u
+    v0[u][1] = c[1];
+    v1[u][0] = c[2];   // row gid + 8
+    v1[u][1] = c[3];
+  }
+  float s0 = fmaxf(v0[0][0], v0[0][1]), s1 = fmaxf(v1[0][0], v1[0][1]);
+#pragma unroll
+  for (int u = 1; u < U; ++u) {
+    s0 = fmaxf(s0, fmaxf(v0[u][0], v0[u][1]));
+    s1 = fmaxf(s1, fmaxf(v1[u][0], v1[u][1]));
+  }
+  if (!WARM) {
+    const float th0 = mx0 - marg[0], th1 = mx1 - marg[1];
+    if (act[0] && s0 >= th0) hmma_exact<M, U>(a, fn0, v0, t, tg, th0, best0);
+    if (act[1] && s1 >= th1) hmma_exact<M, U>(a, fn1, v1, t, tg, th1, best1);
+  }
+  // the quad's four lanes see disjoint columns of the same rows: share the step maxima, so a new record
+  // triggers one exact pass per row rather than one per lane
+  s0 = fmaxf(s0, __shfl_xor_sync(MO_FULL, s0, 1));
+  s1 = fmaxf(s1, __shfl_xor_sync(MO_FULL, s1, 1));
+  s0 = fmaxf(s0, __shfl_xor_sync(MO_FULL, s0, 2));
+  s1 = fmaxf(s1, __shfl_xor_sync(MO_FULL, s1, 2));
+  mx0 = fmaxf(mx0, s0);
+  mx1 = fmaxf(mx1, s1);
+}
+
+template <int M>
+__global__ void __launch_bounds__(HMMA_WARPS * 32) k_assoc_hmma(AssocArgs a, int chunks) {
+  pdl_wait();
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tg = lane & 3;
+  const int nrt = (ncand + 15) / 16;                    // 16-row tiles
+  const int ngrp = (nrt + HMMA_WARPS - 1) / HMMA_WARPS;  // CTA items: 8 row tiles x one chunk
+  const int ntiles = (a.w + 7) / 8;
+  const int per_chunk = (ntiles + chunks - 1) / chunks;
+  __shared__ float sFn[HMMA_WARPS][16][M];
+  for (int item = blockIdx.x; item < ngrp * chunks; item += gridDim.x) {
+    const int grp = item / chunks, ch = item - grp * chunks;
+    const int rt = grp * HMMA_WARPS + warp;
+    const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
+    if (rt >= nrt || t0 >= t1) continue;   // warp-uniform
+    // the lane's two rows: gid and gid + 8 of the tile
+    int row[2];
+    bool act[2];
+    float marg[2];
+    uint32_t ah[4], al[4];
+    float av[2][4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int c = rt * 16 + gid + 8 * r;
+      act[r] = c < ncand;
+      row[r] = act[r] ? __ldcg(a.cand + c) : 0;
+      float fn[M];
+      hmma_load_fn<M>(a, row[r], fn);
+      __syncwarp();
+      if (tg == 0)
+#pragma unroll
+        for (int k = 0; k < M; ++k) sFn[warp][gid + 8 * r][k] = fn[k];
+      float nn = 0.0f;
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        fin = fin && isfinite(fn[k]);
+        nn = fmaf(fn[k], fn[k], nn);
+      }
+      const float norm = sqrtf(nn);
+      const bool ok = fin && norm > 1e-30f && isfinite(norm);   // (tiny rows: bf16 subnormal flushes)
+      if (act[r] && !ok) {
+        if (ch == 0 && tg == 0) {
+          a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row[r];
+          atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
+        }
+        act[r] = false;
+      }
+      marg[r] = act[r] ? ldexpf(norm, -11) : 0.0f;    // 2 eps
+      // A-fragment coordinates of this lane: k = 2tg, 2tg+1, 2tg+8, 2tg+9 (0 past m or for idle rows)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) av[r][q] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const float v = act[r] ? fn[k] : 0.0f;
+        if (k == 2 * tg) av[r][0] = v;
+        if (k == 2 * tg + 1) av[r][1] = v;
+        if (k == 2 * tg + 8) av[r][2] = v;
+        if (k == 2 * tg + 9) av[r][3] = v;
+      }
+    }
+    {
+      float h[2][4], l[2][4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) split_bf16(av[r][q], h[r][q], l[r][q]);
+      // a0: (row gid, k 2tg..+1), a1: (row gid+8, same k), a2: (row gid, k +8), a3: (row gid+8, k +8)
+      ah[0] = bf16x2_bits(h[0][0], h[0][1]);
+      ah[1] = bf16x2_bits(h[1][0], h[1][1]);
+      ah[2] = bf16x2_bits(h[0][2], h[0][3]);
+      ah[3] = bf16x2_bits(h[1][2], h[1][3]);
+      al[0] = bf16x2_bits(l[0][0], l[0][1]);
+      al[1] = bf16x2_bits(l[1][0], l[1][1]);
+      al[2] = bf16x2_bits(l[0][2], l[0][3]);
+      al[3] = bf16x2_bits(l[1][2], l[1][3]);
+    }
+    __syncwarp();
+    if (!__any_sync(MO_FULL, act[0] || act[1])) continue;
+    const float* fn0 = sFn[warp][gid];
+    const float* fn1 = sFn[warp][gid + 8];
+    float mx0 = -__int_as_float(0x7f800000), mx1 = mx0;
+    unsigned long long best0 = 0ull, best1 = 0ull;
+    // filter steps of HMMA_U tiles: 3U independent MMAs, then one max per row; the (rare after the first
+    // steps) rows whose step maximum reaches the running max - 2 eps get their candidates' exact keys
+    const int tfull = t0 + (t1 - t0) / HMMA_U * HMMA_U;
+    // warm-up: the filter maxima of the first steps (packed order is a fixed random permutation of the
+    // references, so a few steps already sit near the row's maximum) shared across the quad; any value
+    // actually seen is a valid running maximum, so the sweep below starts with a tight threshold and
+    // evaluates few exact keys
+    {
+      const int tw = min(tfull, t0 + 4 * HMMA_U);
+      for (int t = t0; t < tw; t += HMMA_U)
+        hmma_step<M, HMMA_U, true>(a, t, lane, tg, ah, al, act, fn0, fn1, marg, mx0, mx1, best0, best1);
+    }
+    for (int t = t0; t < tfull; t += HMMA_U)
+      hmma_step<M, HMMA_U, false>(a, t, lane, tg, ah, al, act, fn0, fn1, marg, mx0, mx1, best0, best1);
+    for (int t = tfull; t < t1; ++t)
+      hmma_step<M, 1, false>(a, t, lane, tg, ah, al, act, fn0, fn1, marg, mx0, mx1, best0, best1);
+    // the four lanes of a quad hold the same two rows: max key, then one atomic per row
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const unsigned long long b0 = __shfl_xor_sync(MO_FULL, best0, o);
+      const unsigned long long b1 = __shfl_xor_sync(MO_FULL, best1, o);
+      best0 = b0 > best0 ? b0 : best0;
+      best1 = b1 > best1 ? b1 : best1;
+    }
+    if (tg == 0) {
+      if (act[0] && best0) atomicMax(&a.akey[row[0]], best0);
+      if (act[1] && best1) atomicMax(&a.akey[row[1]], best1);
+    }
+  }
+}
+
 __global__ void k_assoc_final(AssocFinalArgs a) {
   pdl_wait();
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
@@ -1029,6 +1300,57 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   }
   MO_CHECK_LAUNCH();
   return MO_OK;
+}
+
+int launch_pack_refs(const float* zhat, int64_t w, int m, const int32_t* order, uint2* out, cudaStream_t s) {
+  if (w < 1 || m < 1 || m > 16) return MO_ERR_PARAM;
+  const int64_t n = (w + 7) / 8 * 32;
+  k_pack_refs<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(zhat, w, m, order, out);
+  MO_CHECK_LAUNCH();
+  return MO_OK;
+}
+
+// tensor-core filtered full scan + the sliced FP32 scan for its rejects (zero / non-finite rows)
+int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  if (!a.zfrag || m < 2 || m > 16 || a.zbeg != 0 || a.zend != a.w) return MO_ERR_PARAM;
+  if (!a.in_step) {
+    if (cudaMemsetAsync(a.fb_ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
+      return MO_ERR_CUDA;
+  }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // chunks of the reference range: enough CTA items (8 row tiles x chunk) for ~4 waves of 2 CTAs per SM
+  // at the worst-case candidate count R, each chunk >= 64 tiles
+  const int64_t grp = ceil_div(ceil_div(R, (int64_t)16), (int64_t)HMMA_WARPS);
+  const int64_t ntiles = ceil_div((int64_t)a.w, (int64_t)8);
+  int64_t chunks = ceil_div((int64_t)sms * 16, grp);
+  if (chunks > ntiles / 64) chunks = ntiles / 64;
+  if (chunks < 1) chunks = 1;
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assoc_hmma<16>, HMMA_WARPS * 32, 0);
+  const dim3 grid((unsigned)(sms * (per > 1 ? per : 2))), blk(HMMA_WARPS * 32);
+  switch (m) {
+#define MO_HM_CASE(MM) \
+  case MM: MO_TRY(launch_ex(k_assoc_hmma<MM>, grid, blk, 0, s, false, g_mo_pdl, a, (int)chunks)); break;
+    MO_HM_CASE(2) MO_HM_CASE(3) MO_HM_CASE(4) MO_HM_CASE(5) MO_HM_CASE(6) MO_HM_CASE(7) MO_HM_CASE(8)
+    MO_HM_CASE(9) MO_HM_CASE(10) MO_HM_CASE(11) MO_HM_CASE(12) MO_HM_CASE(13) MO_HM_CASE(14)
+    MO_HM_CASE(15) MO_HM_CASE(16)
+#undef MO_HM_CASE
+    default: return MO_ERR_PARAM;
+  }
+  const dim3 fg((unsigned)sms), fb(256);
+  switch (m) {
+#define MO_FB_CASE(MM) \
+  case MM: return launch_ex(k_assoc_fallback<MM>, fg, fb, 0, s, false, g_mo_pdl, a);
+    MO_FB_CASE(2) MO_FB_CASE(3) MO_FB_CASE(4) MO_FB_CASE(5) MO_FB_CASE(6) MO_FB_CASE(7) MO_FB_CASE(8)
+    MO_FB_CASE(9) MO_FB_CASE(10) MO_FB_CASE(11) MO_FB_CASE(12) MO_FB_CASE(13) MO_FB_CASE(14)
+    MO_FB_CASE(15) MO_FB_CASE(16)
+#undef MO_FB_CASE
+    default: return MO_ERR_PARAM;
+  }
 }
 
 int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {

@@ -76,6 +76,9 @@ struct AssocArgs {
   int* fb_cand;
   int* fb_ctl;
   int in_step;           // fb_ctl / info[MO_INFO_ASSOC_FALLBACK] already cleared by k_prep
+  // tensor-core filter (k_assoc_hmma): bf16 hi/lo fragments of the unit directions in static reference
+  // order (mo_pack_refs_bf16); nullptr = FP32 full scan only
+  const uint2* zfrag;
 };
 
 struct AssocFinalArgs {
@@ -134,6 +137,8 @@ struct SelectArgs {
 
 int launch_prep(const PrepArgs& a, cudaStream_t s);
 int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
+int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
+int launch_pack_refs(const float* zhat, int64_t w, int m, const int32_t* order, uint2* out, cudaStream_t s);
 int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s);
 int launch_select(const SelectArgs& a, cudaStream_t s);

@@ -301,6 +301,17 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
                            at<int>(ws, L.rank_pos), ps.trace, s, true);
 }
 
+// tensor-core filtered association: full reference range (one shard), packed fragments, enough points
+// for the filter to pay (below ~1k points the FP32 scan's smem tiles are as fast); MO_NO_HMMA=1 disables
+static bool use_hmma(const AssocArgs& aa, int m) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("MO_NO_HMMA");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !off && aa.zfrag && m >= 2 && m <= 16 && aa.zbeg == 0 && aa.zend == aa.w && aa.w >= 1024;
+}
+
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
 static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 1); }
 
@@ -330,6 +341,7 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   if (mask & MO_PHASE_NICHE_ASSOC) {
   const int G = shards_of(a->shard_count);
   AssocArgs aa;
+  memset(&aa, 0, sizeof(aa));
   aa.F = a->FR;
   aa.ideal = a->ideal;
   aa.a32 = pa.a32;
@@ -350,8 +362,11 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.fb_cand = at<int>(ws, L.fcand);
   aa.fb_ctl = at<int>(ws, L.fctl);
   aa.in_step = 1;
+  aa.zfrag = reinterpret_cast<const uint2*>(a->zhat_frag);
   if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
+  else if (use_hmma(aa, m))
+    MO_TRY(launch_assoc_hmma(aa, m, R, s));
   else
     MO_TRY(launch_assoc(aa, m, R, s));
   }
@@ -527,6 +542,14 @@ using namespace mo;
 
 extern "C" {
 
+size_t mo_pack_refs_bytes(int64_t w) { return w > 0 ? (size_t)((w + 7) / 8) * 544 : 0; }
+
+int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream_) {
+  if (!zhat || !out) return MO_ERR_PARAM;
+  return launch_pack_refs(zhat, w, m, order, reinterpret_cast<uint2*>(out), (cudaStream_t)stream_);
+}
+
+
 const char* mo_version(void) { return "manyobj_b200 0.1.0 (sm_100a)"; }
 
 int64_t mo_bits_words_per_row(int64_t R) { return words_per_row(R); }
@@ -666,6 +689,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
                           nullptr, PREP_PERMS_CAND);
   MO_TRY(launch_prep(pa, s));
   AssocArgs aa;
+  memset(&aa, 0, sizeof(aa));
   aa.F = Fn;
   aa.ideal = nullptr;
   aa.a32 = nullptr;
