@@ -1319,9 +1319,13 @@ int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     if (cudaMemsetAsync(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 0, sizeof(int), s) != cudaSuccess)
       return MO_ERR_CUDA;
   }
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int sms = 0, per = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assoc_hmma<16>, HMMA_WARPS * 32, 0);
+  }
   // chunks of the reference range: enough CTA items (8 row tiles x chunk) for ~4 waves of 2 CTAs per SM
   // at the worst-case candidate count R, each chunk >= 64 tiles
   const int64_t grp = ceil_div(ceil_div(R, (int64_t)16), (int64_t)HMMA_WARPS);
@@ -1329,8 +1333,6 @@ int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   int64_t chunks = ceil_div((int64_t)sms * 16, grp);
   if (chunks > ntiles / 64) chunks = ntiles / 64;
   if (chunks < 1) chunks = 1;
-  int per = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assoc_hmma<16>, HMMA_WARPS * 32, 0);
   const dim3 grid((unsigned)(sms * (per > 1 ? per : 2))), blk(HMMA_WARPS * 32);
   switch (m) {
 #define MO_HM_CASE(MM) \
