@@ -138,6 +138,50 @@ __device__ void gauss_solve_warp(double* A, double* rhs, int m, int* singular) {
   __syncwarp();
 }
 
+// phase 1 of k_prep for m = M (register arrays): ASF extreme-point keys and column maxima of the
+// translated candidates, merged by warp reductions + one atomic per warp
+template <int M>
+__device__ __forceinline__ void prep_extremes(const PrepArgs& a, int ncand, int gthreads) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  float idl[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) idl[k] = __ldcg(a.ideal + k);
+  for (int base = blockIdx.x * blockDim.x; base < ncand; base += gthreads) {
+    const int c = base + tid;
+    const bool act = c < ncand;
+    float ft[M], q[M];
+    int row = 0, pp = 0;
+    if (act) {
+      row = __ldcg(a.cand + c);
+      pp = __ldcg(a.pos_pop + row);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        ft[k] = __fsub_rn(a.F[(int64_t)row * M + k], idl[k]);
+        q[k] = __fdiv_rn(ft[k], ASF_EPS);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      uint32_t v = act ? f2ord(ft[k]) : 0u;
+      v = warp_max_u32(v);
+      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
+    }
+#pragma unroll
+    for (int ax = 0; ax < M; ++ax) {
+      unsigned long long key = ~0ull;
+      if (act) {
+        float s = ft[ax];  // w_ax,ax = 1: f / 1 is exact
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k != ax) s = fmaxf(s, q[k]);
+        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+      }
+      key = warp_min_u64(key);
+      if (lane == 0 && key != ~0ull) atomicMin(&a.ext_key[ax], key);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   pdl_wait();
   __shared__ uint32_t sKp[MAX_SHUFFLE_ROUNDS], sSp[MAX_SHUFFLE_ROUNDS], sKr[MAX_SHUFFLE_ROUNDS],
@@ -195,37 +239,14 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 
   // ---- phase 1: ASF extreme points + column maxima of translated candidates
   const int ncand = __ldcg(a.ctl);
-  float idl[MAXM];
-  for (int k = 0; k < m; ++k) idl[k] = __ldcg(a.ideal + k);
-  for (int base = blockIdx.x * blockDim.x; base < ncand; base += gthreads) {
-    const int c = base + tid;
-    const bool act = c < ncand;
-    float ft[MAXM], q[MAXM];
-    int row = 0, pp = 0;
-    if (act) {
-      row = __ldcg(a.cand + c);
-      pp = __ldcg(a.pos_pop + row);
-      for (int k = 0; k < m; ++k) {
-        ft[k] = __fsub_rn(a.F[(int64_t)row * m + k], idl[k]);
-        q[k] = __fdiv_rn(ft[k], ASF_EPS);
-      }
-    }
-    for (int k = 0; k < m; ++k) {
-      uint32_t v = act ? f2ord(ft[k]) : 0u;
-      v = warp_max_u32(v);
-      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
-    }
-    for (int ax = 0; ax < m; ++ax) {
-      unsigned long long key = ~0ull;
-      if (act) {
-        float s = ft[ax];  // w_ax,ax = 1: f / 1 is exact
-        for (int k = 0; k < m; ++k)
-          if (k != ax) s = fmaxf(s, q[k]);
-        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
-      }
-      key = warp_min_u64(key);
-      if (lane == 0 && key != ~0ull) atomicMin(&a.ext_key[ax], key);
-    }
+  switch (m) {
+#define MO_PX_CASE(MM) \
+  case MM: prep_extremes<MM>(a, ncand, gthreads); break;
+    MO_PX_CASE(1) MO_PX_CASE(2) MO_PX_CASE(3) MO_PX_CASE(4) MO_PX_CASE(5) MO_PX_CASE(6) MO_PX_CASE(7)
+    MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
+    MO_PX_CASE(15) MO_PX_CASE(16)
+#undef MO_PX_CASE
+    default: break;
   }
   grid_sync(a.bar);
   trace_mark(a.trace, 18);
@@ -863,6 +884,7 @@ __global__ void __launch_bounds__(HMMA_WARPS * 32) k_assoc_hmma(AssocArgs a, int
   }
 }
 
+template <int M>   // m = M: register arrays (the runtime-m version kept fn[] on the stack)
 __global__ void k_assoc_final(AssocFinalArgs a) {
   pdl_wait();
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
@@ -872,10 +894,11 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
   if (base >= ncand) return;  // whole block idle (uniform)
   const int c = base + threadIdx.x;
   const bool act = c < ncand;
-  const int m = a.m;
+  constexpr int m = M;
   const int row = act ? __ldcg(a.cand + c) : 0;
-  float fn[MAXM];
+  float fn[M];
   if (act) {
+#pragma unroll
     for (int k = 0; k < m; ++k) {
       float v = a.F[(int64_t)row * m + k];
       if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
@@ -891,8 +914,10 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
     const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
     const float* z = a.zs + (int64_t)p * m;
     float t = __fmul_rn(fn[0], z[0]);
+#pragma unroll
     for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn[k], z[k]));
     float s2 = 0.0f;
+#pragma unroll
     for (int k = 0; k < m; ++k) {
       const float e = __fsub_rn(fn[k], __fmul_rn(t, z[k]));
       s2 = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s2, __fmul_rn(e, e));
@@ -1386,7 +1411,16 @@ int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
 
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
   if (R <= 0) return MO_OK;
-  return launch_ex(k_assoc_final, dim3((unsigned)ceil_div(R, 128)), dim3(128), 0, s, false, g_mo_pdl, a);
+  const dim3 grid((unsigned)ceil_div(R, 128)), blk(128);
+  switch (a.m) {
+#define MO_AF_CASE(MM) \
+  case MM: return launch_ex(k_assoc_final<MM>, grid, blk, 0, s, false, g_mo_pdl, a);
+    MO_AF_CASE(1) MO_AF_CASE(2) MO_AF_CASE(3) MO_AF_CASE(4) MO_AF_CASE(5) MO_AF_CASE(6) MO_AF_CASE(7)
+    MO_AF_CASE(8) MO_AF_CASE(9) MO_AF_CASE(10) MO_AF_CASE(11) MO_AF_CASE(12) MO_AF_CASE(13) MO_AF_CASE(14)
+    MO_AF_CASE(15) MO_AF_CASE(16)
+#undef MO_AF_CASE
+    default: return MO_ERR_PARAM;
+  }
 }
 
 int launch_select(const SelectArgs& a, cudaStream_t s) {
