@@ -479,8 +479,14 @@ __global__ void __launch_bounds__(256) k_assoc_lattice(AssocArgs a) {
   const double sn = sqrt(nn);
   const double c_se = ok ? s / ((double)H * sqrt((double)M) * sn) : 0.0;
   // radius r, then r+1 for the rows whose certificate failed; the rare rest goes to the sliced full scan
-  // (a (2r+4)^(m-1) box walked by one group is a latency-bound straggler that holds the whole grid)
-  for (int it = 0; it < 2; ++it) {
+  // (a (2r+4)^(m-1) box walked by one group is a latency-bound straggler that holds the whole grid) --
+  // unless the reference set is so large that a full-scan row costs more than 64 such boxes, where the
+  // third radius r+2 is tried in the group first
+  int box3 = 1;
+#pragma unroll
+  for (int k = 0; k < M - 1; ++k) box3 *= 2 * (r + 2);
+  const int tries = (int64_t)box3 * 64 < (int64_t)a.w ? 3 : 2;
+  for (int it = 0; it < tries; ++it) {
     if (__all_sync(MO_FULL, done)) break;
     const int rr = r + it;
     float best = -__int_as_float(0x7f800000);
