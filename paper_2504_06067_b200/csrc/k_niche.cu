@@ -1222,22 +1222,17 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         return (int)s;
       },
       [&](int64_t i, int pre) {
-        if (a.X_next) a.bucket[pre] = (int)i;   // source row of survivor `pre` (bucket storage is free now)
+        // survivor `pre` <- merged row i, copied by the emitting thread (the rows are L2-resident; no
+        // barrier + second pass for a separate gather)
+        if (a.X_next) {
+          const int d = a.dvars, mm = a.m;
+          const float* xs = a.XR + i * d;
+          float* xd = a.X_next + (int64_t)pre * d;
+          for (int v = 0; v < d; ++v) xd[v] = xs[v];
+          for (int k = 0; k < mm; ++k) a.F_next[(int64_t)pre * mm + k] = a.FR[i * mm + k];
+        }
       },
       sh);
-  grid_sync(a.g.bar);
-  if (a.X_next) {
-    // coalesced gather, one warp per survivor row: lanes stride the d + m columns
-    const int d = a.dvars, mm = a.m;
-    for (int r = gwarp; r < nsurv; r += nwarps) {
-      const int64_t src = __ldcg(a.bucket + r);
-      const float* xs = a.XR + src * d;
-      float* xd = a.X_next + (int64_t)r * d;
-#pragma unroll 4
-      for (int v = lane; v < d; v += 32) xd[v] = xs[v];
-      if (lane < mm) a.F_next[(int64_t)r * mm + lane] = a.FR[src * mm + lane];
-    }
-  }
   trace_mark(a.trace, 35);
   for (int i = gtid; i < R; i += gthreads) {
     const int r = a.ranks[i];
