@@ -139,20 +139,26 @@ __device__ void gauss_solve_warp(double* A, double* rhs, int m, int* singular) {
 }
 
 // phase 1 of k_prep for m = M (register arrays): ASF extreme-point keys and column maxima of the
-// translated candidates, merged by warp reductions + one atomic per warp
+// translated candidate rows (rank in [0, l]), merged by warp reductions + one atomic per warp.  The keys
+// are stored complemented (atomicMax of ~key: 0 is neutral, so a zeroed workspace needs no reset node;
+// phase 2 restores 0 after reading).  build_cand: also append the candidates to cand (engine path:
+// phase 0's list pass and its grid barrier are folded in here).
 template <int M>
-__device__ __forceinline__ void prep_extremes(const PrepArgs& a, int ncand, int gthreads) {
+__device__ __forceinline__ void prep_extremes(const PrepArgs& a, int R, int l, int gthreads, bool build_cand) {
   const int tid = threadIdx.x, lane = tid & 31;
   float idl[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) idl[k] = __ldcg(a.ideal + k);
-  for (int base = blockIdx.x * blockDim.x; base < ncand; base += gthreads) {
-    const int c = base + tid;
-    const bool act = c < ncand;
+  for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
+    const int row = base + tid;
+    const bool act = row < R && a.ranks[row] >= 0 && a.ranks[row] <= l;
+    if (build_cand) {
+      const int slot = warp_alloc(a.ctl, act ? 1 : 0);   // candidate order is immaterial
+      if (act) a.cand[slot] = row;
+    }
     float ft[M], q[M];
-    int row = 0, pp = 0;
+    int pp = 0;
     if (act) {
-      row = __ldcg(a.cand + c);
       pp = __ldcg(a.pos_pop + row);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -177,7 +183,7 @@ __device__ __forceinline__ void prep_extremes(const PrepArgs& a, int ncand, int 
         key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
       }
       key = warp_min_u64(key);
-      if (lane == 0 && key != ~0ull) atomicMin(&a.ext_key[ax], key);
+      if (lane == 0 && key != ~0ull) atomicMax(&a.ext_key[ax], ~key);
     }
   }
 }
@@ -223,25 +229,28 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     }
     gen_prologue(a, gen, gtid, gthreads, sKp, sSp, &sRp, sKr, sSr, &sRr);
   }
-  for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
-    const int i = base + tid;
-    const bool c = i < R && a.ranks[i] >= 0 && a.ranks[i] <= l;
-    const int slot = warp_alloc(a.ctl, c ? 1 : 0);          // candidate order is immaterial
-    if (c) a.cand[slot] = i;
+  // engine path (ideal and positions final at launch): the candidate list is built inside phase 1
+  const bool fused = a.mode == PREP_FULL && a.ideal_done && a.pro_done;
+  if (!fused) {
+    for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
+      const int i = base + tid;
+      const bool c = i < R && a.ranks[i] >= 0 && a.ranks[i] <= l;
+      const int slot = warp_alloc(a.ctl, c ? 1 : 0);          // candidate order is immaterial
+      if (c) a.cand[slot] = i;
+    }
+    if (a.mode != PREP_FULL) return;
+    if (gtid < m) {
+      a.ext_key[gtid] = 0ull;
+      a.colmax[gtid] = 0u;
+    }
+    grid_sync(a.bar);
   }
-  if (a.mode != PREP_FULL) return;
-  if (gtid < m) {
-    a.ext_key[gtid] = ~0ull;
-    a.colmax[gtid] = 0u;
-  }
-  grid_sync(a.bar);
   trace_mark(a.trace, 17);
 
   // ---- phase 1: ASF extreme points + column maxima of translated candidates
-  const int ncand = __ldcg(a.ctl);
   switch (m) {
 #define MO_PX_CASE(MM) \
-  case MM: prep_extremes<MM>(a, ncand, gthreads); break;
+  case MM: prep_extremes<MM>(a, R, l, gthreads, fused); break;
     MO_PX_CASE(1) MO_PX_CASE(2) MO_PX_CASE(3) MO_PX_CASE(4) MO_PX_CASE(5) MO_PX_CASE(6) MO_PX_CASE(7)
     MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
     MO_PX_CASE(15) MO_PX_CASE(16)
@@ -250,6 +259,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   }
   grid_sync(a.bar);
   trace_mark(a.trace, 18);
+  const int ncand = __ldcg(a.ctl);
 
   // ---- phase 2: hyperplane solve (one thread) on the extreme rows loaded by the block,
   //      per-component fallbacks
@@ -257,7 +267,8 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     __shared__ double sFb[MAXM];
     for (int e = tid; e < m * m; e += blockDim.x) {
       const int r = e / m, c = e - r * m;
-      const int row = __ldcg(a.perm_pop + (uint32_t)(__ldcg(a.ext_key + r) & 0xffffffffull));
+      const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
+      const int row = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
       sA[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
     }
     for (int k = tid; k < m; k += blockDim.x) {
@@ -266,6 +277,10 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       sRhs[k] = 1.0;
     }
     __syncthreads();
+    if (tid < m) {   // every reader of this generation's keys is done: neutral values for the next launch
+      a.ext_key[tid] = 0ull;
+      a.colmax[tid] = 0u;
+    }
     __shared__ int sSing;
     if (tid < 32) {
       if (tid == 0) sSing = 0;
