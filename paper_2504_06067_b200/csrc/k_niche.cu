@@ -257,13 +257,14 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 #undef MO_PX_CASE
     default: break;
   }
-  grid_sync(a.bar);
-  trace_mark(a.trace, 18);
+  // phase 2 runs in the last block to finish phase 1
+  if (!grid_last(a.bar)) return;
+  trace_mark_any(a.trace, 18);
   const int ncand = __ldcg(a.ctl);
 
-  // ---- phase 2: hyperplane solve (one thread) on the extreme rows loaded by the block,
+  // ---- phase 2: hyperplane solve (one warp) on the extreme rows loaded by the block,
   //      per-component fallbacks
-  if (blockIdx.x == 0) {
+  {
     __shared__ double sFb[MAXM];
     for (int e = tid; e < m * m; e += blockDim.x) {
       const int r = e / m, c = e - r * m;
@@ -294,13 +295,11 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      const int singular = sSing;
-      bool bad = singular != 0;
-      if (!bad)
-        for (int k = 0; k < m; ++k)
-          if (!isfinite(sRhs[k])) bad = true;
-      for (int k = 0; k < m; ++k) {
+    if (tid < 32) {   // one lane per component (m <= 32 here; larger m loops), same arithmetic per k
+      bool fin = true;
+      for (int k = tid; k < m; k += 32) fin = fin && isfinite(sRhs[k]);
+      const bool bad = sSing != 0 || !__all_sync(MO_FULL, fin);
+      for (int k = tid; k < m; k += 32) {
         double ak;
         if (bad) {
           ak = sFb[k];
@@ -312,10 +311,10 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
         a.a32[k] = __double2float_rn(ak);
         if (a.icpt_out) a.icpt_out[k] = ak;
       }
-      a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
+      if (tid == 0) a.info[MO_INFO_SINGULAR] = bad ? 1 : 0;
     }
   }
-  trace_mark(a.trace, 19);
+  trace_mark_any(a.trace, 19);
 }
 
 // ---------------------------------------------------------- association

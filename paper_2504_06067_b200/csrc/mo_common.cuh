@@ -157,6 +157,26 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
 }
 
+// "Last block out": true in exactly one block, the last to arrive; every other block's writes before
+// its arrival are visible to it.  Nobody waits, so a final single-block phase starts as soon as the
+// grid's work is done (no barrier release round trip) and the other blocks retire.  Shares the
+// self-resetting count of grid_sync's slot (the last block restores 0).
+__device__ __forceinline__ bool grid_last(unsigned* bar) {
+  __shared__ int sLast;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u) + 1u;
+    sLast = arrived == gridDim.x;
+    if (sLast) {
+      atomicExch(bar, 0u);
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  return sLast != 0;
+}
+
 // Programmatic dependent launch (PDL): kernels of a generation are launched
 // with cudaLaunchAttributeProgrammaticStreamSerialization, so the next
 // kernel's CTAs are scheduled while the previous one drains.  pdl_wait()
@@ -202,6 +222,14 @@ inline int launch_ex(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 // Phase trace for the persistent kernels: block 0 / thread 0 stamps the
 // global nanosecond timer into tr[slot] (tr == nullptr: no-op).  Read back by
 // the host (engine.Engine.trace()) to time phases inside one launch.
+__device__ __forceinline__ void trace_mark_any(unsigned long long* tr, int slot) {   // any block
+  if (tr != nullptr && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[slot] = t;
+  }
+}
+
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int slot) {
   if (tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
