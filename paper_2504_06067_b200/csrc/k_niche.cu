@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       sRhs[k] = 1.0;
     }
     __syncthreads();
+    trace_mark_any(a.trace, 20);
     if (tid < m) {   // every reader of this generation's keys is done: neutral values for the next launch
       a.ext_key[tid] = 0ull;
       a.colmax[tid] = 0u;
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       }
     }
     __syncthreads();
+    trace_mark_any(a.trace, 21);
     if (tid < 32) {   // one lane per component (m <= 32 here; larger m loops), same arithmetic per k
       bool fin = true;
       for (int k = tid; k < m; k += 32) fin = fin && isfinite(sRhs[k]);

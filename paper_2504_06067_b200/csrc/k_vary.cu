@@ -83,11 +83,16 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   const int npairs = n / 2;
   const int q0 = vblock * ppb;
   const int tid = threadIdx.x;
-  if (tid < ppb && q0 + tid < npairs) {
-    const int q = q0 + tid;
-    shA[tid] = (int)prp_inv(2u * q, shK, shS, shR, (uint32_t)n);
-    shB[tid] = (int)prp_inv(2u * q + 1u, shK, shS, shR, (uint32_t)n);
-    shCross[tid] = u01(philox4x32((uint32_t)q, PAIR_SLOT, gen, STREAM_SBX, seed).x) < cfg.p_c;
+  // the two parents of a pair on two threads (each inverse shuffle is ~74 dependent rounds)
+  if (tid < 2 * ppb && q0 + (tid >> 1) < npairs) {
+    const int ql = tid >> 1, q = q0 + ql;
+    const int par = (int)prp_inv(2u * q + (uint32_t)(tid & 1), shK, shS, shR, (uint32_t)n);
+    if (tid & 1) {
+      shB[ql] = par;
+    } else {
+      shA[ql] = par;
+      shCross[ql] = u01(philox4x32((uint32_t)q, PAIR_SLOT, gen, STREAM_SBX, seed).x) < cfg.p_c;
+    }
   }
   __syncthreads();
   const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
@@ -201,7 +206,9 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
   if (pro) {
     p = *pro;
     const int64_t items = pro->R > pro->w ? pro->R : pro->w;
-    pblocks = (int)ceil_div(items, (int64_t)VARY_THREADS * 4);
+    // one item (a row / reference-point shuffle: 2 x ~74 dependent rounds) per thread: the prologue
+    // CTAs are the kernel's critical path when they loop (4 items per thread: ~26 us at C2)
+    pblocks = (int)ceil_div(items, (int64_t)VARY_THREADS);
     pblocks = pblocks < 1 ? 1 : (pblocks > 296 ? 296 : pblocks);
   }
   k_vary_eval<<<(unsigned)(vblocks + pblocks), VARY_THREADS, 0, s>>>(problem, X, (int)n, d, m, seed, gen, gen_ptr,

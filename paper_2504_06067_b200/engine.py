@@ -367,6 +367,7 @@ class Engine:
         "presort.bounds": (4, 5),
         "peel.prologue": (8, 9), "peel.fronts": (9, 10),
         "prep.phase0": (16, 17), "prep.extremes": (17, 18), "prep.solve": (18, 19),
+        "prep.solve_loads": (18, 20), "prep.solve_gauss": (20, 21), "prep.solve_icpt": (21, 19),
         "select.nearest_keys": (24, 25), "select.nearest": (25, 26), "select.level": (26, 27),
         "select.marked": (27, 28), "select.take": (28, 29), "select.cache": (29, 30), "select.topk": (30, 31),
         "select.compact": (31, 35), "select.ranks": (35, 36), "select.total": (24, 36),
