@@ -46,6 +46,10 @@ struct PrepArgs {
   // barrier is self-resetting, and the lattice fallback counters (nullable) are cleared here
   int in_step;
   int* fb_ctl;
+  // mating parents precomputed one generation ahead by the prologue CTAs of k_vary_eval (the mating
+  // shuffle depends on (seed, generation, n) only): [4p .. 4p+3] tag of the buffer of parity p =
+  // (~generation, seed lo, seed hi, n), [8] completion counter, [16 + p * n ..) parent of slot q.  nullable
+  int* mate;
   int pro_done;    // gen_prologue already ran (in k_vary_eval): only the candidate list in phase 0
   int ideal_done;  // the running ideal was already lowered by the offspring (k_vary_eval)
 };

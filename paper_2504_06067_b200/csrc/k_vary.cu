@@ -67,17 +67,52 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   if ((int)blockIdx.x < pro_blocks) {   // first CTAs (scheduled first): the generation prologue
     __shared__ uint32_t shK2[MAX_SHUFFLE_ROUNDS], shS2[MAX_SHUFFLE_ROUNDS];
     __shared__ int shR2;
+    if (blockIdx.x == 0) trace_mark_any(pro.trace, 46);
     const uint32_t g = gen_ptr ? *gen_ptr : gen_val;
-    gen_prologue(pro, g, (int)blockIdx.x * VARY_THREADS + (int)threadIdx.x, pro_blocks * VARY_THREADS, shK, shS,
-                 &shR, shK2, shS2, &shR2);
+    const int gtid = (int)blockIdx.x * VARY_THREADS + (int)threadIdx.x, gthreads = pro_blocks * VARY_THREADS;
+    gen_prologue(pro, g, gtid, gthreads, shK, shS, &shR, shK2, shS2, &shR2);
+    if (pro.mate) {
+      // next generation's mating parents (off this generation's critical path)
+      const uint32_t gn = g + 1u;
+      __syncthreads();
+      load_shuffle_keys_smem(shK2, shS2, &shR2, (uint32_t)n, seed, gn, STREAM_MATING);
+      __syncthreads();
+      int* buf = pro.mate + 16 + (int64_t)(gn & 1u) * n;
+      int* tag = pro.mate + 4 * (gn & 1u);
+      // continue the prologue's index space (rows, reference points, then mating slots) so that the
+      // slots go to threads that had no row / reference item when the grid covers all three
+      const int off = (pro.R + pro.w) % gthreads;
+      for (int q = (gtid - off + gthreads) % gthreads; q < n; q += gthreads)
+        buf[q] = (int)prp_inv((uint32_t)q, shK2, shS2, shR2, (uint32_t)n);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(pro.mate + 8, 1) == pro_blocks - 1) {   // last prologue CTA: publish
+          pro.mate[8] = 0;
+          tag[1] = (int)(uint32_t)seed;
+          tag[2] = (int)(uint32_t)(seed >> 32);
+          tag[3] = n;
+          __threadfence();
+          tag[0] = (int)~gn;                                   // written last: the validity flag
+        }
+      }
+    }
+    if (blockIdx.x == 0) trace_mark_any(pro.trace, 45);
     return;
   }
+  const bool tb = (int)blockIdx.x == pro_blocks;   // traced vary block
+  if (tb) trace_mark_any(pro.trace, 40);
   const int vblock = (int)blockIdx.x - pro_blocks;
   __shared__ float shMin[16];
   __shared__ int shA[VARY_PAIRS], shB[VARY_PAIRS];
   __shared__ uint8_t shCross[VARY_PAIRS];
   const uint32_t gen = gen_ptr ? *gen_ptr : gen_val;
-  load_shuffle_keys_smem(shK, shS, &shR, (uint32_t)n, seed, gen, STREAM_MATING);
+  // parents precomputed by the previous generation's prologue CTAs, when their tag matches
+  const int* mtag = pro.mate ? pro.mate + 4 * (gen & 1u) : nullptr;
+  const int* mbuf = (mtag && __ldcg(mtag) == (int)~gen && __ldcg(mtag + 1) == (int)(uint32_t)seed &&
+                     __ldcg(mtag + 2) == (int)(uint32_t)(seed >> 32) && __ldcg(mtag + 3) == n)
+                        ? pro.mate + 16 + (int64_t)(gen & 1u) * n : nullptr;
+  if (!mbuf) load_shuffle_keys_smem(shK, shS, &shR, (uint32_t)n, seed, gen, STREAM_MATING);
   if (threadIdx.x < 16) shMin[threadIdx.x] = __int_as_float(0x7f800000);
   __syncthreads();
   const int npairs = n / 2;
@@ -86,7 +121,8 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   // the two parents of a pair on two threads (each inverse shuffle is ~74 dependent rounds)
   if (tid < 2 * ppb && q0 + (tid >> 1) < npairs) {
     const int ql = tid >> 1, q = q0 + ql;
-    const int par = (int)prp_inv(2u * q + (uint32_t)(tid & 1), shK, shS, shR, (uint32_t)n);
+    const uint32_t slot = 2u * q + (uint32_t)(tid & 1);
+    const int par = mbuf ? __ldcg(mbuf + slot) : (int)prp_inv(slot, shK, shS, shR, (uint32_t)n);
     if (tid & 1) {
       shB[ql] = par;
     } else {
@@ -95,6 +131,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     }
   }
   __syncthreads();
+  if (tb) trace_mark_any(pro.trace, 41);
   const float p_m = cfg.p_m < 0.0f ? 1.0f / (float)d : cfg.p_m;
   const double eta_c = (double)cfg.eta_c, eta_m = (double)cfg.eta_m;
   const int npb = min(ppb, npairs - q0);
@@ -119,6 +156,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     Xo[(int64_t)(2 * q + 1) * d + v] = o2;
   }
   __syncthreads();
+  if (tb) trace_mark_any(pro.trace, 42);
   // Phase 3a: g of every child by a group of 8 lanes (strided partial sums + the pinned xor
   // butterfly, = dtlz_g), and the domain check; 256 threads = 32 children x 8 lanes
   static_assert(VARY_THREADS == 2 * VARY_PAIRS * G_LANES, "one 8-lane group per child");
@@ -141,6 +179,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     if (!ok) atomicOr(domain_flag, 1);
   }
   __syncthreads();
+  if (tb) trace_mark_any(pro.trace, 43);
   // Phase 3b: one thread per (child, objective)
   const int etasks = nch * m;
   for (int e = tid; e < etasks; e += VARY_THREADS) {
@@ -157,6 +196,10 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   if (ideal) {
     __syncthreads();
     if (tid < m && tid < 16) atomic_min_float(&ideal[tid], shMin[tid]);
+  }
+  if (tb) {
+    __syncthreads();
+    trace_mark_any(pro.trace, 44);
   }
 }
 
@@ -205,9 +248,9 @@ int launch_vary_eval(int problem, const float* X, int64_t n, int d, int m, uint6
   memset(&p, 0, sizeof(p));
   if (pro) {
     p = *pro;
-    const int64_t items = pro->R > pro->w ? pro->R : pro->w;
-    // one item (a row / reference-point shuffle: 2 x ~74 dependent rounds) per thread: the prologue
-    // CTAs are the kernel's critical path when they loop (4 items per thread: ~26 us at C2)
+    // one shuffle item (row, reference point or next generation's mating slot: ~74 dependent rounds)
+    // per thread: the prologue CTAs are the kernel's critical path when they loop
+    const int64_t items = (int64_t)pro->R + pro->w + (pro->mate ? n : 0);
     pblocks = (int)ceil_div(items, (int64_t)VARY_THREADS);
     pblocks = pblocks < 1 ? 1 : (pblocks > 296 ? 296 : pblocks);
   }

@@ -42,7 +42,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, mate, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -106,6 +106,7 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.fill = bump(c, (size_t)(w + 1) * 4);
   L.lvl = bump(c, (size_t)2 * LVL_BINS * 4);
   L.sctl = bump(c, 16 * 4);
+  L.mate = bump(c, (size_t)(R + 16) * 4);   // [0..7] two tags, [8] counter, [16..): two n-slot mating buffers
   // streamed / sharded sort (sort_mode == MO_SORT_STREAM)
   const bool st = sort_mode == MO_SORT_STREAM;
   const int64_t nb = ceil_div(R, STREAM_BLK);
@@ -196,6 +197,7 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.fb_ctl = nullptr;
   a.pro_done = 0;
   a.ideal_done = 0;
+  a.mate = at<int>(ws, L.mate);
   return a;
 }
 

@@ -20,14 +20,19 @@ __device__ inline void gen_prologue(const PrepArgs& a, uint32_t gen, int gtid, i
   load_shuffle_keys_smem(sKp, sSp, sRp, (uint32_t)R, a.seed, gen, STREAM_POP_SHUFFLE);
   load_shuffle_keys_smem(sKr, sSr, sRr, (uint32_t)w, a.seed, gen, STREAM_REF_SHUFFLE);
   __syncthreads();
-  for (int i = gtid; i < R; i += gthreads) {
-    const int p = (int)prp((uint32_t)i, sKp, sSp, *sRp, (uint32_t)R);
-    a.pos_pop[i] = p;
-    a.perm_pop[p] = i;
-    if (a.prom) a.prom[i] = 0;
-    if (a.akey) a.akey[i] = 0ull;
-  }
-  for (int j = gtid; j < w; j += gthreads) {
+  // one index space over rows then reference points, so a thread runs one shuffle chain (~74 dependent
+  // rounds) rather than one of each when the grid covers R + w
+  for (int t = gtid; t < R + w; t += gthreads) {
+    if (t < R) {
+      const int i = t;
+      const int p = (int)prp((uint32_t)i, sKp, sSp, *sRp, (uint32_t)R);
+      a.pos_pop[i] = p;
+      a.perm_pop[p] = i;
+      if (a.prom) a.prom[i] = 0;
+      if (a.akey) a.akey[i] = 0ull;
+      continue;
+    }
+    const int j = t - R;
     const int p = (int)prp((uint32_t)j, sKr, sSr, *sRr, (uint32_t)w);
     a.pos_ref[j] = p;
     if (a.lat_pos) a.lat_pos[__ldg(a.lat_index + j)] = p;

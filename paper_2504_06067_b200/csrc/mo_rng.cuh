@@ -93,18 +93,20 @@ __host__ __device__ inline void make_shuffle_keys(ShuffleKeys& sk, uint32_t n, u
   }
 }
 
+// x' = (k - x) mod n with k, x < n: 32-bit wrap-around then + n when k < x (same value as the signed form)
 __device__ __forceinline__ uint32_t sn_round(uint32_t x, uint32_t n, uint32_t k, uint32_t s) {
-  int64_t xp = (int64_t)k - (int64_t)x;
-  if (xp < 0) xp += n;
-  uint32_t xpu = (uint32_t)xp;
+  uint32_t xpu = k - x;
+  if (k < x) xpu += n;
   uint32_t xh = x > xpu ? x : xpu;
   return (lowbias32(xh ^ s) & 1u) ? xpu : x;
 }
 
-// Shuffled position of item x (keys in shared or global memory).
+// Shuffled position of item x (keys in shared or global memory).  The round chain is the latency of a
+// shuffle (~74 dependent rounds); unrolling lets the key loads of later rounds issue early.
 __device__ __forceinline__ uint32_t prp(uint32_t x, const uint32_t* K, const uint32_t* S, int rounds,
                                         uint32_t n) {
   if (n <= 1) return x;
+#pragma unroll 4
   for (int r = 0; r < rounds; ++r) x = sn_round(x, n, K[r], S[r]);
   return x;
 }
@@ -113,6 +115,7 @@ __device__ __forceinline__ uint32_t prp(uint32_t x, const uint32_t* K, const uin
 __device__ __forceinline__ uint32_t prp_inv(uint32_t p, const uint32_t* K, const uint32_t* S, int rounds,
                                             uint32_t n) {
   if (n <= 1) return p;
+#pragma unroll 4
   for (int r = rounds - 1; r >= 0; --r) p = sn_round(p, n, K[r], S[r]);
   return p;
 }

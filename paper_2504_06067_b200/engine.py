@@ -363,6 +363,8 @@ class Engine:
         return self.FR[self.cur][: self.cfg.n]
 
     TRACE_SLOTS = {
+        "vary.parents": (40, 41), "vary.sbx_pm": (41, 42), "vary.g": (42, 43), "vary.objectives": (43, 44),
+        "vary.prologue": (46, 45), "vary.prologue_end_to_vary_end": (45, 44),
         "presort.sum": (0, 1), "presort.hist": (1, 2), "presort.scan": (2, 3), "presort.scatter": (3, 4),
         "presort.bounds": (4, 5),
         "peel.prologue": (8, 9), "peel.fronts": (9, 10),
