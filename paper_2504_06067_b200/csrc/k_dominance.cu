@@ -465,7 +465,13 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   // P2: exclusive scan of the bucket counts -> bucket starts (in fill[] to keep counts)
   grid_scan(
       a.g, NB, [&](int64_t q) { return __ldcg(a.valB + q); },
-      [&](int64_t q, int pre) { a.fill[q] = pre; }, sh);
+      [&](int64_t q, int pre) {
+        // atomic path: valB[q] becomes the bucket END (its count is not needed any more), so P3 can
+        // write wend and the block S bounds itself (no P3 -> P4 barrier)
+        if (!a.stable) a.valB[q] = pre + __ldcg(a.valB + q);
+        a.fill[q] = pre;
+      },
+      sh);
   grid_sync(a.g.bar);
   trace_mark(a.trace, 3);
   // every block has read the key range (P1): restore its neutral values for the next launch
@@ -499,7 +505,22 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
       a.perm[pos] = i;
       a.SS[pos] = ord2f(__ldcg(a.keyB + i));
       for (int k = 0; k < m; ++k) a.FS[(int64_t)pos * m + k] = __fadd_rn(a.F[(int64_t)i * m + k], 0.0f);  // -0 -> +0
+      // P4 folded in: wend from the bucket end; the 256-row block S range from the key range of the
+      // buckets at the block's first / last position (conservative: the fast-tile test max S(bi) <
+      // min S(bj) stays sound, adjacent blocks sharing a bucket are simply not fast)
+      a.wend[pos] = (__ldcg(a.valB + q) - 1) / 32 + 1;
+      if ((pos & 255) == 0) {
+        const uint64_t kmin = (uint64_t)q * span;
+        a.blkmin[pos >> 8] = ord2f(lo + (uint32_t)((kmin + NB - 1) / NB));
+      }
+      if ((pos & 255) == 255 || pos == R - 1) {
+        const uint64_t kmax = ((uint64_t)q + 1) * span;
+        a.blkmax[pos >> 8] = ord2f(lo + (uint32_t)((kmax + NB - 1) / NB) - 1u);
+      }
     }
+    trace_mark(a.trace, 4);
+    trace_mark(a.trace, 5);
+    return;
   }
   grid_sync(a.g.bar);
   const uint32_t* rowq = a.stable ? a.tkey : a.keyA;
