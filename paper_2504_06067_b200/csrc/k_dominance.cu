@@ -764,13 +764,34 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   int* rk = a.perm ? a.rank_pos : a.ranks;   // ranks indexed by bit-matrix row
   trace_mark(a.trace, 8);
 
-  // prologue: ranks / resume / ranked mask (invalid rows count as ranked so they never block)
-  int nvalid_local = 0;
+  // prologue: ranks / resume / ranked mask (invalid rows count as ranked so they never block).
+  // pre0 (all rows valid, hasdom from the tile kernel): front 0 is found here too -- its rows are the
+  // ones without a dominator, a per-row test on the same thread-to-row mapping -- and counted into a
+  // spare slot of front_sizes, so the first barrier publishes it (one barrier less per generation)
+  const bool pre0 = a.valid == nullptr && a.hasdom != nullptr;
+  int* fs0 = a.front_sizes + R + 3;   // zero at entry; reset by the last block after every read
+  int nvalid_local = 0, ready0 = 0;
   for (int j = gtid; j < R; j += gthreads) {
     bool v = a.valid == nullptr || a.valid[j];
-    rk[j] = v ? MO_RANK_UNRANKED : MO_RANK_DROPPED;
+    int r = v ? MO_RANK_UNRANKED : MO_RANK_DROPPED;
+    if (pre0 && a.hasdom[j] == 0) {
+      r = 0;
+      ready0++;
+    }
+    rk[j] = r;
     a.resume[j] = 0;
     nvalid_local += v;
+  }
+  if (pre0) {
+    ready0 = warp_sum(ready0);
+    if (lane == 0) sCount[wib] = ready0;
+    __syncthreads();
+    if (tid == 0) {
+      int s0 = 0;
+      for (int w = 0; w < PEEL_THREADS / 32; ++w) s0 += sCount[w];
+      if (s0) atomicAdd(fs0, s0);
+    }
+    if (gtid == 0) a.front_sizes[2] = 0;   // front 1's counter (phase A of front 0 is skipped)
   }
   for (int64_t w = gtid; w < W; w += gthreads) {
     uint32_t m = 0;
@@ -786,11 +807,11 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
     a.ranked[w] = m;
   }
   nvalid_local = warp_sum(nvalid_local);
-  if (lane == 0) atomicAdd(&a.front_sizes[0], nvalid_local);
-  if (gtid == 0) a.front_sizes[1] = 0;
+  if (!pre0 && lane == 0) atomicAdd(&a.front_sizes[0], nvalid_local);
+  if (!pre0 && gtid == 0) a.front_sizes[1] = 0;
   grid_sync(a.bar);
   trace_mark(a.trace, 9);
-  const int nvalid = __ldcg(a.front_sizes);
+  const int nvalid = pre0 ? R : __ldcg(a.front_sizes);
   const int64_t target = a.stop_at > 0 ? a.stop_at : (int64_t)nvalid;
   if (a.stop_at > 0 && nvalid < a.stop_at) {
     grid_sync(a.bar);            // everyone has read front_sizes[0]
@@ -798,6 +819,7 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
       a.info[MO_INFO_ERROR] = MO_ERR_INFEASIBLE;
       a.info[MO_INFO_L] = -1;
       a.front_sizes[0] = 0;      // neutral for the next launch (no memset node)
+      if (pre0) *fs0 = 0;
     }
     return;
   }
@@ -810,7 +832,9 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   for (;;) {
     // ---- phase A: find front k
     int ready_local = 0;
-    if (k == 0 && a.hasdom) {
+    if (k == 0 && pre0) {
+      // found in the prologue
+    } else if (k == 0 && a.hasdom) {
       // front 0 = rows without any dominator, known from the tile kernel
       for (int j = gtid; j < R; j += gthreads) {
         if (rk[j] == MO_RANK_UNRANKED && a.hasdom[j] == 0) {
@@ -859,18 +883,24 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
         }
       }
     }
-    ready_local = warp_sum(ready_local);
-    if (lane == 0) sCount[wib] = ready_local;
-    __syncthreads();
-    if (tid == 0) {
-      int s = 0;
-      for (int w = 0; w < PEEL_THREADS / 32; ++w) s += sCount[w];
-      if (s) atomicAdd(&a.front_sizes[k + 1], s);
+    int fk;
+    if (k == 0 && pre0) {
+      fk = __ldcg(fs0);
+      if (gtid == 0) a.front_sizes[1] = fk;   // the front-size record later readers use
+    } else {
+      ready_local = warp_sum(ready_local);
+      if (lane == 0) sCount[wib] = ready_local;
+      __syncthreads();
+      if (tid == 0) {
+        int s = 0;
+        for (int w = 0; w < PEEL_THREADS / 32; ++w) s += sCount[w];
+        if (s) atomicAdd(&a.front_sizes[k + 1], s);
+      }
+      if (gtid == 0) a.front_sizes[k + 2] = 0;
+      grid_sync(a.bar);
+      // ---- phase B: decide, then publish front k into the ranked mask
+      fk = __ldcg(a.front_sizes + k + 1);
     }
-    if (gtid == 0) a.front_sizes[k + 2] = 0;
-    grid_sync(a.bar);
-    // ---- phase B: decide, then publish front k into the ranked mask
-    const int fk = __ldcg(a.front_sizes + k + 1);
     cum += fk;
     const bool done = (cum >= target) || (fk == 0);
     if (done) {
@@ -891,8 +921,10 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
         a.info[MO_INFO_FL_SIZE] = fk;
         a.info[MO_INFO_SKIPPED] = (a.stop_at > 0 && sel + fk == a.stop_at) ? 1 : 0;
         a.info[MO_INFO_ERROR] = 0;
-        a.front_sizes[0] = 0;    // read by every block after the prologue barrier, long passed
+        if (!pre0) a.front_sizes[0] = 0;    // read by every block after the prologue barrier, long passed
       }
+      // pre0: every block has read fs0 before getting here; the last one restores its neutral value
+      if (pre0 && grid_last(a.bar) && tid == 0) *fs0 = 0;
       trace_mark(a.trace, 10);
       return;
     }
@@ -903,6 +935,7 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
       if (lane == 0 && m) a.ranked[w] |= m;
     }
     grid_sync(a.bar);
+    if (k == 0 && pre0 && gtid == 0) *fs0 = 0;   // every block read it before this barrier
     ++k;
   }
 }
@@ -929,6 +962,7 @@ int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int
              perm, hasdom, wend, rank_pos, trace};
   if (!in_step) {
     if (cudaMemsetAsync(front_sizes, 0, 2 * sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
+    if (cudaMemsetAsync(front_sizes + R + 3, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
     if (cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
   }
   int blocks = peel_grid_blocks();
