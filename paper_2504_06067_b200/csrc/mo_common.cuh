@@ -137,22 +137,30 @@ __device__ __forceinline__ int block_excl_scan(int v, int* sh, int* total) {
 
 // Sense-reversing software grid barrier for persistent kernels launched with
 // cudaLaunchAttributeCooperative (all CTAs co-resident).  `bar` = {count, gen}.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid barrier for co-resident (cooperative) grids, self-resetting: bar[0] counts arrivals, bar[1] is
+// the generation.  Arrival is one acq_rel atomic (it releases this CTA's writes -- ordered before it by
+// the __syncthreads -- and acquires those of the earlier arrivals); the last arriver restores the count
+// and bumps the generation with a release atomic; the others spin on an acquire load of the generation.
+// (The previous fence + relaxed-atomic form paid two full MEMBAR.GPU on the critical path.)
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
   if (gridDim.x == 1) return;
   if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    unsigned gen = *vgen;
-    __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u) + 1u;
-    if (arrived == gridDim.x) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    const unsigned gen = ld_acquire_gpu(bar + 1);
+    unsigned arrived;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+    if (arrived + 1u == gridDim.x) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
-      while (*vgen == gen) __nanosleep(32);
+      while (ld_acquire_gpu(bar + 1) == gen) __nanosleep(20);
     }
-    __threadfence();
   }
   __syncthreads();
 }
