@@ -173,13 +173,10 @@ __device__ __forceinline__ bool grid_last(unsigned* bar) {
   __shared__ int sLast;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u) + 1u;
-    sLast = arrived == gridDim.x;
-    if (sLast) {
-      atomicExch(bar, 0u);
-      __threadfence();
-    }
+    unsigned arrived;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(bar) : "memory");
+    sLast = arrived + 1u == gridDim.x;
+    if (sLast) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
   }
   __syncthreads();
   return sLast != 0;
