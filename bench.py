@@ -421,7 +421,9 @@ def run_ours(args, rank, world):
     d2h = n * d * 4 + n * m * 4 + m * 4 + _lib.INFO_COUNT * 4
 
     result = {"ms": ms, "clk": clk.summary(), "e2e_ms": e2e_ms, "h2d": h2d, "d2h": d2h, "info": info,
-              "w": eng.w, "sharded": sharded, "sort": wl["sort"], "lattice": eng.lattice is not None}
+              "w": eng.w, "sharded": sharded, "sort": wl["sort"], "lattice": eng.lattice is not None,
+              "hmma": (getattr(eng, "zfrag", None) is not None and eng.w >= 1024
+                       and os.environ.get("MO_NO_HMMA") != "1")}
     kern = time_kernels(torch, eng, _lib) if (rank == 0 or sharded) else None
     if rank == 0:
         result["kernels"] = kern
@@ -503,7 +505,8 @@ def main():
              else "k_dom_tile_sorted (dominance bit-matrix)")
     # our kernels per generation: vary, presort, dominance, peel, prep, association (lattice + fallback
     # scan, or the full scan), assoc_final, select; streamed: + reset/plan/count/mark + 4 per front
-    assoc_kernels = 2 if r.get("lattice") else 1
+    # lattice or tensor-core filter: the filtered kernel + the sliced fallback scan; else the FP32 scan
+    assoc_kernels = 2 if (r.get("lattice") or r.get("hmma")) else 1
     launches = (K * (7 + assoc_kernels) if r["sort"] == "bits"
                 else K * (10 + assoc_kernels + 4 * int(kern.get("fronts_issued") or 0)))
     traffic = (committed_traffic("k_stream_tiles<3, 0>", "r01_ncu_full_c4_count_raw.csv") if args.workload == "c4"
