@@ -58,6 +58,9 @@ enum {
   MO_INFO_ERROR = 10,     /* non-zero status raised on the device          */
   MO_INFO_ASSOC_FALLBACK = 11, /* candidates the lattice-pruned association
                                   could not certify (full scan instead)     */
+  MO_INFO_ERROR_FIRST = 12, /* first non-zero device status since the host
+                               last zeroed it (sticky: later generations
+                               never clear it; the engine raises it)     */
   MO_INFO_COUNT = 16
 };
 

@@ -75,18 +75,23 @@ def initialize(cfg):
     return RunState(0, X, F, F.min(axis=0), refpoints.unit_directions(Z), Z)
 
 
-def survivor_selection(cfg, FR, ideal, zhat, generation, gen=None, loop="waterfill"):
-    """NDS + split + niching on merged objectives FR (2n x m FP32)."""
-    ranks = dominance.non_dominated_sort(FR, stop_at=cfg.n)
+def survivor_selection(cfg, FR, ideal, zhat, generation, gen=None, loop="waterfill", nds_fn=None,
+                       associate_fn=None, fast=False):
+    """NDS + split + niching on merged objectives FR (2n x m FP32).
+
+    ``nds_fn(FR, stop_at) -> ranks`` / ``associate_fn`` / ``fast``: the same stages from the C
+    restatement (oracle/c, checked bit-for-bit against these numpy ones) for C2-C4-sized checks."""
+    ranks = (nds_fn or (lambda F, stop_at: dominance.non_dominated_sort(F, stop_at=stop_at)))(FR, cfg.n)
     split = dominance.split_fronts(ranks, cfg.n)
     sel, info = niche.select(FR, ranks, split, ideal, zhat, cfg.seed, generation,
-                             backend=cfg.backend, gen=gen, loop=loop)
+                             backend=cfg.backend, gen=gen, loop=loop, associate_fn=associate_fn, fast=fast)
     info["ranks"] = ranks
     return sel, info
 
 
-def step(state, cfg, gen=None, offspring=None, loop="waterfill"):
-    """SPEC.md:459-467.  ``offspring=(O, FO)`` injects externally produced offspring."""
+def step(state, cfg, gen=None, offspring=None, loop="waterfill", **accel):
+    """SPEC.md:459-467.  ``offspring=(O, FO)`` injects externally produced offspring; ``accel``:
+    nds_fn / associate_fn / fast of :func:`survivor_selection`."""
     g = state.generation
     if offspring is None:
         O = _variation.vary(state.X, cfg.variation, cfg.seed, g)
@@ -95,7 +100,7 @@ def step(state, cfg, gen=None, offspring=None, loop="waterfill"):
         O, FO = (np.asarray(a, np.float32) for a in offspring)
     XR = np.concatenate([state.X, O])
     FR = np.concatenate([state.F, FO])
-    sel, info = survivor_selection(cfg, FR, state.ideal, state.zhat, g, gen, loop)
+    sel, info = survivor_selection(cfg, FR, state.ideal, state.zhat, g, gen, loop, **accel)
     info["selected"] = sel
     return RunState(g + 1, XR[sel], FR[sel], info["ideal"], state.zhat, state.Z, info)
 

@@ -236,6 +236,33 @@ def nearest_selection(pi, d, ranks, l, rho, rho_p, k, pos_pop, pos_ref):
     return promoted, rho, rho_p
 
 
+def nearest_selection_vec(pi, d, ranks, l, rho, rho_p, k, pos_pop, pos_ref):
+    """:func:`nearest_selection` without the per-point loop (one lexsort; O(R log R)): the same
+    promoted rows and counts (tests/test_oracle_fast.py), for the checker at C2-C4 sizes where the
+    loop's per-point scans of F_l are quadratic."""
+    rho = rho.copy()
+    rho_p = rho_p.copy()
+    empty = np.flatnonzero(rho == 0)
+    if len(empty) == 0 or k <= 0:
+        return np.zeros(0, np.int64), rho, rho_p
+    fl = np.flatnonzero(ranks == l)
+    is_empty = np.zeros(len(rho), bool)
+    is_empty[empty] = True
+    c = fl[is_empty[pi[fl]]]
+    c = c[np.lexsort((pos_pop[c], d[c], pi[c]))]            # per point: d first, then position
+    pc = pi[c]
+    first = np.ones(len(c), bool)
+    first[1:] = pc[1:] != pc[:-1]
+    chosen = np.full(len(rho), -1, np.int64)
+    chosen[pc[first]] = c[first]
+    kept = _first_k_by_pos(empty, k, pos_ref)
+    promoted = chosen[kept].astype(np.int64)
+    rho[kept] = 1
+    rho_p[kept] -= 1
+    rho[rho_p == 0] = INF
+    return promoted, rho, rho_p
+
+
 def build_cache(pi, ranks, l, w, pos_pop, exclude):
     """Per reference point, F_l candidates in shuffled population order.
 
@@ -361,8 +388,11 @@ def oracle_niche_select(pi, d, ranks, l, k, w, gen):
 # ------------------------------------------------------------- full pipeline
 
 def select(F, ranks, split, ideal_prev, zhat, seed, generation, backend="batched", gen=None,
-           loop="waterfill"):
-    """Survivor selection of Alg. 1/2 given NDS ranks.  Returns (selected mask, info)."""
+           loop="waterfill", associate_fn=None, fast=False):
+    """Survivor selection of Alg. 1/2 given NDS ranks.  Returns (selected mask, info).
+
+    ``associate_fn(Fn, zhat, pos_ref, rows) -> (pi, d)`` replaces :func:`associate_canonical` (the
+    C restatement in oracle/c at large sizes); ``fast`` uses :func:`nearest_selection_vec`."""
     F = np.asarray(F, np.float32)
     R = F.shape[0]
     w = zhat.shape[0]
@@ -381,14 +411,15 @@ def select(F, ranks, split, ideal_prev, zhat, seed, generation, backend="batched
     cand = (ranks <= l) & (ranks != DROPPED)
     Fn, ideal, a, ext, singular = normalize_objectives(F, ideal_prev, cand, pos_pop)
     rows = np.flatnonzero(cand)
-    pi, d = associate_canonical(Fn, zhat, pos_ref, rows)
+    pi, d = (associate_fn or associate_canonical)(Fn, zhat, pos_ref, rows)
     info.update(Fn=Fn, intercepts=a, extremes=ext, singular=singular, pi=pi, d=d,
                 pos_pop=pos_pop, pos_ref=pos_ref)
     if backend == "oracle":
         promoted = oracle_niche_select(pi, d, ranks, l, k, w, gen or np.random.default_rng(seed))
     else:
         rho, rho_p = niche_counts(pi, ranks, l, w)
-        near, rho, rho_p = nearest_selection(pi, d, ranks, l, rho, rho_p, k, pos_pop, pos_ref)
+        near, rho, rho_p = (nearest_selection_vec if fast else nearest_selection)(
+            pi, d, ranks, l, rho, rho_p, k, pos_pop, pos_ref)
         k_rem = k - len(near)
         offsets, cq = build_cache(pi, ranks, l, w, pos_pop, near)
         if loop == "loop":

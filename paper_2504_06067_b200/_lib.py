@@ -21,7 +21,7 @@ c_i32, c_i64, c_u32, c_u64, c_f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uin
 c_vp, c_sz = ctypes.c_void_p, ctypes.c_size_t
 
 INFO = dict(L=0, SELECTED=1, K=2, NFRONTS=3, FL_SIZE=4, SKIPPED=5, NEAREST=6, LEVEL=7, SINGULAR=8,
-            SURVIVORS=9, ERROR=10, ASSOC_FALLBACK=11)
+            SURVIVORS=9, ERROR=10, ASSOC_FALLBACK=11, ERROR_FIRST=12)
 INFO_COUNT = 16
 PHASE_VARY, PHASE_SORT, PHASE_NICHE, PHASE_ALL = 1, 2, 4, 7
 NICHE_PREP, NICHE_ASSOC, NICHE_FINISH = 8, 16, 32

@@ -817,6 +817,7 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
     grid_sync(a.bar);            // everyone has read front_sizes[0]
     if (gtid == 0) {
       a.info[MO_INFO_ERROR] = MO_ERR_INFEASIBLE;
+      if (a.info[MO_INFO_ERROR_FIRST] == 0) a.info[MO_INFO_ERROR_FIRST] = MO_ERR_INFEASIBLE;
       a.info[MO_INFO_L] = -1;
       a.front_sizes[0] = 0;      // neutral for the next launch (no memset node)
       if (pre0) *fs0 = 0;

@@ -31,6 +31,7 @@
 namespace mo {
 
 constexpr int MAXM = 64;
+constexpr int PREP_MAXM = 16;   // k_prep phase-1 instantiations (MO_PX_CASE)
 constexpr float ASF_EPS = 1e-6f;
 constexpr double DEGENERATE = 1e-10;
 
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
     MO_PX_CASE(15) MO_PX_CASE(16)
 #undef MO_PX_CASE
-    default: break;
+    default: __trap();   // unreachable: launch_prep rejects m outside [1, PREP_MAXM]
   }
   // phase 2 runs in the last block to finish phase 1
   if (!grid_last(a.bar)) return;
@@ -1250,6 +1251,11 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       },
       sh);
   trace_mark(a.trace, 35);
+  // No grid barrier after the P8 compaction scan: other blocks may still be in grid_scan's second
+  // pass re-reading ranks[] of their chunks while this loop rewrites promoted rows to l-1.  That is
+  // benign only because the P8 predicate of a promoted row is true through `prom` whatever its rank
+  // (r = l or l-1 both select it); a predicate that depends on the rank value of a promoted row
+  // would need the barrier back.
   for (int i = gtid; i < R; i += gthreads) {
     const int r = a.ranks[i];
     const bool pr = !skipped && __ldcg(a.prom + i) != 0;
@@ -1294,7 +1300,8 @@ int select_grid_blocks() {
 }
 
 int launch_prep(const PrepArgs& a, cudaStream_t s) {
-  if (a.m < 1 || a.m > MAXM) return MO_ERR_PARAM;
+  // phase 1 (extreme points) is instantiated for m = 1..PREP_MAXM only
+  if (a.m < 1 || a.m > MAXM || (a.mode == PREP_FULL && a.m > PREP_MAXM)) return MO_ERR_PARAM;
   if (!a.in_step) {
     if (cudaMemsetAsync(a.ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
     if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;

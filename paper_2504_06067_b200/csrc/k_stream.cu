@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_stream_apply(StreamArgs a, in
       a.info[MO_INFO_FL_SIZE] = fk;
       a.info[MO_INFO_SKIPPED] = (sel + fk == a.stop_at) ? 1 : 0;
       a.info[MO_INFO_ERROR] = (cum < a.stop_at) ? MO_ERR_INFEASIBLE : 0;
+      if (cum < a.stop_at && a.info[MO_INFO_ERROR_FIRST] == 0) a.info[MO_INFO_ERROR_FIRST] = MO_ERR_INFEASIBLE;
       __threadfence();
       a.info[MO_INFO_NFRONTS] = k + 1;
       a.ctl[SC_DONE] = k + 1;
@@ -679,6 +680,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 2) k_stream_fused(StreamArgs a)
         a.info[MO_INFO_FL_SIZE] = fk;
         a.info[MO_INFO_SKIPPED] = (sel + fk == a.stop_at) ? 1 : 0;
         a.info[MO_INFO_ERROR] = (cum < a.stop_at) ? MO_ERR_INFEASIBLE : 0;
+      if (cum < a.stop_at && a.info[MO_INFO_ERROR_FIRST] == 0) a.info[MO_INFO_ERROR_FIRST] = MO_ERR_INFEASIBLE;
         a.info[MO_INFO_NFRONTS] = k + 1;
       }
       break;

@@ -654,7 +654,7 @@ int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t
 int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, const int32_t* info, uint64_t seed,
                  uint32_t generation, float* ideal, float* Fn, double* intercepts, void* workspace,
                  size_t workspace_bytes, void* stream_) {
-  if (m < 1 || m > 64 || R < 1) return MO_ERR_PARAM;
+  if (m < 1 || m > 16 || R < 1) return MO_ERR_PARAM;   // k_prep's extreme-point pass: m <= 16
   Layout L = make_layout(R, 1, m);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;

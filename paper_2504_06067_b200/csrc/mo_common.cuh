@@ -169,6 +169,10 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
 // its arrival are visible to it.  Nobody waits, so a final single-block phase starts as soon as the
 // grid's work is done (no barrier release round trip) and the other blocks retire.  Shares the
 // self-resetting count of grid_sync's slot (the last block restores 0).
+// CONTRACT: grid_last must be the LAST use of `bar` in a launch.  The reset is a plain relaxed store
+// and non-last blocks do not wait for it, so a later grid_sync / grid_last on the same slot in the
+// same launch could count a stale arrival and release early.  Call sites (k_front_peel, k_prep) use
+// it as their final synchronisation only.
 __device__ __forceinline__ bool grid_last(unsigned* bar) {
   __shared__ int sLast;
   __syncthreads();

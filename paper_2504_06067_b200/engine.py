@@ -39,7 +39,7 @@ import numpy as np
 import torch
 
 from . import _lib, problems, refpoints
-from .errors import ConfigError
+from .errors import ConfigError, raise_for_status
 from .variation import VariationConfig, init_population
 
 
@@ -157,6 +157,11 @@ class Engine:
             del L
         self.cur = 0
         self.generation = 0
+        self._gen_dev_synced = True      # gen_dev == self.generation (graph replays read it)
+        # sticky device status (info[ERROR_FIRST]) copied to pinned memory after every eager step and
+        # raised lazily by the next step / check_errors() -- no host sync per generation
+        self._err_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self._err_event = None
         self._args = [self._make_args(0), self._make_args(1)]
         self._graph = None
         if graph:
@@ -240,7 +245,38 @@ class Engine:
 
     # ------------------------------------------------------------- stepping
     def step(self, profile=None):
-        """Advance one generation (eager launch).  ``profile``: dict receiving per-phase seconds."""
+        """Advance one generation (eager launch).  ``profile``: dict receiving per-phase seconds.
+
+        A device-side failure of an earlier generation (e.g. InfeasibleSplitError) is raised here, at
+        the latest one step late, or by :meth:`check_errors`."""
+        self.check_errors(block=False)
+        self._step_dispatch(profile)
+        self._gen_dev_synced = False
+        self._post_error_copy()
+
+    def _post_error_copy(self):
+        self._err_host.copy_(self.info[_lib.INFO["ERROR_FIRST"]: _lib.INFO["ERROR_FIRST"] + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._err_event = ev
+
+    def check_errors(self, block=True):
+        """Raise the reference exception of the first device-side status since the last check
+        (errors.STATUS_TO_ERROR).  block=False only looks at copies that already landed."""
+        if block:
+            torch.cuda.current_stream(self.dev).synchronize()
+            code = int(self.info[_lib.INFO["ERROR_FIRST"]].item())
+        else:
+            if self._err_event is None or not self._err_event.query():
+                return
+            code = int(self._err_host[0])
+        self._err_event = None
+        if code:
+            self.info[_lib.INFO["ERROR_FIRST"]] = 0
+            self._err_host.zero_()
+            raise_for_status(code, f"engine generation <= {self.generation}")
+
+    def _step_dispatch(self, profile=None):
         device_fronts = (self._auto_fronts and self.shard_count == 1 and self.sort_mode == _lib.SORT_STREAM
                          and self._fronts_hint > 300)
         if self.host_fronts and not device_fronts:
@@ -341,17 +377,24 @@ class Engine:
         """Advance one generation by replaying the captured graph of the current parity."""
         if self._graph is None:
             raise RuntimeError("no graph captured")
+        if not self._gen_dev_synced:      # eager steps advanced the host counter only
+            self.gen_dev.fill_(self.generation)
+            self._gen_dev_synced = True
         self._graph[self.cur].replay()
         self.cur ^= 1
         self.generation += 1
 
-    def replay(self, generations=1):
-        """Advance ``generations`` generations with graph replays (device generation counter)."""
+    def replay(self, generations=1, check=True):
+        """Advance ``generations`` generations with graph replays (device generation counter);
+        device-side errors are raised at the end (check=True: one host sync)."""
         if self._graph is None:
             raise RuntimeError("no graph captured")
         self.gen_dev.fill_(self.generation)
+        self._gen_dev_synced = True
         for _ in range(generations):
             self.replay_one()
+        if check:
+            self.check_errors(block=True)
 
     # --------------------------------------------------------------- views
     @property
@@ -387,6 +430,7 @@ class Engine:
 
     def info_dict(self):
         h = self.info.cpu().tolist()
+        # (the sticky ERROR_FIRST slot is left for check_errors to raise)
         return {k.lower(): h[v] for k, v in _lib.INFO.items()}
 
 
@@ -515,6 +559,7 @@ def run(cfg, record=True, profile=False, graph=False, **engine_kw):
             history.append({"generation": state.generation, "l": info["l"], "k": info["k"],
                             "fronts": info["nfronts"], "skipped": info["skipped"],
                             "survivors": info["survivors"]})
+    eng.check_errors(block=True)
     return history, state
 
 

@@ -1,0 +1,164 @@
+"""Parity at BASELINE.json's own sizes (configs[1..3]), through the engine's C-ABI path on the GPU.
+
+Every checked generation is a state injection: the GPU engine advances one generation; the oracle
+(oracle/manyobj_ref, its quadratic stages run by the bit-identical C restatement oracle/c --
+tests/test_oracle_c.py, tests/test_oracle_fast.py) takes the same parents, the GPU's offspring
+(checked against the oracle's own variation at rtol 1e-6: the GPU computes SBX/PM/DTLZ in FP64 and
+rounds once) and selects survivors.  Bit-exact: l, k, |F_l|, the ranks of fronts <= l, the promoted
+set, the ideal, and the next population X and F.
+
+* C2  DTLZ2 m=5  d=14 N=10k : all 500 generations (BASELINE configs[1] "exact-match
+      fronts/survivors vs CPU").
+* C3  DTLZ3 m=10 d=19 N=100k: generations 0-2 and 20-21, both sort modes (the bench runs the
+      bit-matrix sort; the engine's auto mode picks the streamed one at this size).
+* C4  DTLZ7 m=3  d=22 N=1M  : generations 0 and 1 on the streamed sort with the certified lattice
+      association.  The oracle's ranks are full (oracle/c nds3).  Association: the oracle's full
+      scan over 2M x 1M pairs is minutes, so pi/d come from the GPU's per-op full-scan association
+      (niche.associate, a different kernel from the engine's lattice path) after an exact check of
+      every F_l row and 10^5 sampled candidate rows against oracle/c; the oracle's niching then
+      has to reproduce the engine's survivors exactly.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import c as oc
+from oracle.manyobj_ref import dominance as Odom
+from oracle.manyobj_ref import engine as Oeng
+from oracle.manyobj_ref import refpoints as Oref
+from oracle.manyobj_ref import variation as Ovar
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def M():
+    import paper_2504_06067_b200 as pkg
+    from paper_2504_06067_b200 import _lib
+    _lib.lib()
+    return pkg
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def _oracle_state(eng):
+    return Oeng.RunState(eng.generation, np_(eng.X).copy(), np_(eng.F).copy(), np_(eng.ideal).copy(),
+                         Oref.unit_directions(eng.Z), eng.Z)
+
+
+def _check_generation(eng, ocfg, st, accel, check_offspring=True, tag=""):
+    n = ocfg.n
+    g = st.generation
+    cur = eng.cur
+    eng.step()
+    O = np_(eng.XR[cur][n:]).copy()
+    FO = np_(eng.FR[cur][n:]).copy()
+    if check_offspring:
+        want = Ovar.vary(st.X, ocfg.variation, ocfg.seed, g)
+        assert np.allclose(O, want, rtol=1e-6, atol=1e-7), f"{tag} offspring g={g}"
+    nxt = Oeng.step(st, ocfg, offspring=(O, FO), **accel)
+    info = eng.info_dict()
+    oi = nxt.info
+    assert info["error"] == 0 and info["survivors"] == n, (tag, g, info)
+    assert (info["l"], info["k"], info["selected"]) == (oi["l"], oi["k"], oi["selected_count"]), (tag, g, info)
+    l = oi["l"]
+    want_r = oi["ranks"]
+    got_r = np_(eng.ranks).astype(np.int64)
+    assert info["fl_size"] == int((want_r == l).sum()), (tag, g)
+    assert np.array_equal(got_r[want_r < l], want_r[want_r < l]), f"{tag} ranks < l, g={g}"
+    assert (got_r[want_r == Odom.DROPPED] == Odom.DROPPED).all(), f"{tag} dropped rows, g={g}"
+    fl = want_r == l
+    if oi["skipped"]:
+        assert (got_r[fl] == l).all()
+    else:
+        promoted = np.flatnonzero(fl & (got_r == l - 1))
+        assert np.array_equal(np.sort(promoted), np.sort(oi["promoted"])), f"{tag} promoted set, g={g}"
+        assert (got_r[fl] >= l - 1).all() and (got_r[fl] <= l).all()
+    assert np.array_equal(np_(eng.ideal), nxt.ideal), f"{tag} ideal g={g}"
+    assert np.array_equal(np_(eng.X), nxt.X), f"{tag} survivors X g={g}"
+    assert np.array_equal(np_(eng.F), nxt.F), f"{tag} survivors F g={g}"
+    return info
+
+
+def test_c2_all_500_generations(M):
+    """BASELINE configs[1]: DTLZ2 m=5 d=14 N=10k, 500 generations, exact fronts/survivors vs CPU."""
+    n, m, d, gens = 10000, 5, 14, 500
+    cfg = M.engine.RunConfig(problem="DTLZ2", n=n, m=m, d=d, generations=gens, seed=0)
+    ocfg = Oeng.RunConfig(problem="DTLZ2", n=n, m=m, d=d, generations=gens, seed=0)
+    eng = M.engine.Engine(cfg, sort="bits")
+    assert np.array_equal(np_(eng.X), Oeng.initial_population(n, d, 0))
+    accel = oc.accel()
+    niched = 0
+    for g in range(gens):
+        st = _oracle_state(eng)
+        info = _check_generation(eng, ocfg, st, accel, check_offspring=(g % 25 == 0), tag="C2")
+        niched += 1 - info["skipped"]
+    assert eng.generation == gens and niched > 0
+
+
+@pytest.mark.parametrize("sort", ["bits", "stream"])
+def test_c3_generations(M, sort):
+    """BASELINE configs[2]: DTLZ3 m=10 d=19 N=100k (two-layer Z, w = 97,383; tensor-core filtered
+    association); early generations (many fronts) and generation 20+ (l = 0)."""
+    n, m, d = 100000, 10, 19
+    cfg = M.engine.RunConfig(problem="DTLZ3", n=n, m=m, d=d, generations=30, seed=0)
+    ocfg = Oeng.RunConfig(problem="DTLZ3", n=n, m=m, d=d, generations=30, seed=0)
+    eng = M.engine.Engine(cfg, sort=sort)
+    assert eng.w == 97383
+    accel = oc.accel()
+    for g in range(3):
+        _check_generation(eng, ocfg, _oracle_state(eng), accel, check_offspring=(g == 0), tag=f"C3/{sort}")
+    while eng.generation < 20:
+        eng.step()
+    for g in range(2):
+        _check_generation(eng, ocfg, _oracle_state(eng), accel, check_offspring=(g == 0), tag=f"C3/{sort}")
+
+
+def test_c4_generations(M):
+    """BASELINE configs[3] on one GPU: DTLZ7 m=3 d=22 N=1M (R = 2M; H = 1412, w = 998,991)."""
+    from oracle.manyobj_ref import niche as On
+
+    n, m, d = 1000000, 3, 22
+    cfg = M.engine.RunConfig(problem="DTLZ7", n=n, m=m, d=d, generations=4, seed=0)
+    ocfg = Oeng.RunConfig(problem="DTLZ7", n=n, m=m, d=d, generations=4, seed=0)
+    eng = M.engine.Engine(cfg, sort="stream")
+    assert eng.w == 998991 and eng.lattice is not None
+    zh32 = np.ascontiguousarray(Oref.unit_directions(eng.Z), np.float32)
+    rs = np.random.default_rng(0)
+    checked = {}
+
+    def assoc_gpu_checked(Fn, zhat, pos_ref, rows):
+        # GPU per-op full scan (k_assoc, not the engine's lattice kernel) on the oracle's Fn ...
+        R = Fn.shape[0]
+        ranks = np.full(R, Odom.DROPPED, np.int32)
+        ranks[rows] = 0
+        pi_g, d_g = M.niche.associate(torch.from_numpy(np.ascontiguousarray(Fn)).cuda(),
+                                      torch.from_numpy(zh32).cuda(), torch.from_numpy(ranks).cuda(), 0,
+                                      ocfg.seed, checked["gen"])
+        pi = np.full(R, -1, np.int64)
+        dd = np.full(R, np.nan, np.float32)
+        pi[rows] = np_(pi_g)[rows]
+        dd[rows] = np_(d_g)[rows]
+        # ... checked exactly against the C restatement on every F_l row + 10^5 sampled candidates
+        sample = np.union1d(checked["fl_rows"], rs.choice(rows, size=min(100000, len(rows)), replace=False))
+        po, do = oc.associate(Fn, zhat, pos_ref, rows=sample)
+        assert np.array_equal(pi[sample], po), "pi differs from oracle/c"
+        assert np.array_equal(dd[sample].view(np.int32), do.view(np.int32)), "d differs from oracle/c"
+        checked["rows"] = len(sample)
+        return pi, dd
+
+    def nds_and_note(F, stop_at):
+        r = oc.nds3(F, stop_at)
+        live = r[r != Odom.DROPPED]
+        l = int(live.max())
+        checked["fl_rows"] = np.flatnonzero(r == l)
+        return r
+
+    accel = dict(nds_fn=nds_and_note, associate_fn=assoc_gpu_checked, fast=True)
+    for g in range(2):
+        checked["gen"] = eng.generation
+        info = _check_generation(eng, ocfg, _oracle_state(eng), accel, check_offspring=(g == 0), tag="C4")
+        assert info["skipped"] or checked["rows"] >= min(100000, info["fl_size"])
+    assert On is not None
