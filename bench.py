@@ -247,13 +247,20 @@ def time_kernels(torch, eng, _lib):
     W = int(L.mo_bits_words_per_row(R))
     bits = torch.empty((R, W), dtype=torch.int32, device="cuda")
     hasdom = torch.empty(R, dtype=torch.uint8, device="cuda")
+    tb = int(L.mo_dominance_tables_bytes(R, m))
+    tables = torch.empty(max(tb, 1), dtype=torch.uint8, device="cuda")
     ts = []
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
-                                              _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
-                                              _lib.stream_ptr()), "dom")
+        if tb:     # the engine's kernel: rank-mask tables + sweep (k_dom_tables + k_dom_rank)
+            _lib.check(L.mo_dominance_bits_ranked(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
+                                                  _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
+                                                  _lib.ptr(tables), tb, _lib.stream_ptr()), "dom")
+        else:
+            _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
+                                                  _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
+                                                  _lib.stream_ptr()), "dom")
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))

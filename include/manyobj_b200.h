@@ -143,6 +143,17 @@ int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* 
                              int64_t R, int32_t m,
                              uint32_t* bits, uint8_t* hasdom, void* stream_);
 
+/* Same bit-matrix and hasdom as mo_dominance_bits_sorted, by per-objective
+ * rank masks (k_dom_rank.cu, the engine's kernel for 2 <= m <= 16): for every
+ * 256-row block and objective, the sorted values (Eytzinger order) and the 257
+ * prefix masks; a row's dominators in a block are the AND over objectives of
+ * the prefix masks selected by m binary searches.  tables: device scratch of
+ * mo_dominance_tables_bytes(R, m) bytes (0 = unsupported m). */
+size_t mo_dominance_tables_bytes(int64_t R, int32_t m);
+int mo_dominance_bits_ranked(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
+                             int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* tables,
+                             size_t tables_bytes, void* stream);
+
 /* dominance.non_dominated_sort + split_fronts, peeling the
  * bit-matrix.  stop_at > 0 stops at the first front whose cumulative size
  * reaches stop_at (later rows get 0x7fffffff = dropped); stop_at <= 0 ranks
@@ -353,6 +364,71 @@ int mo_hv_exact(const float* front, int64_t nf, int32_t m, const double* ref, do
  * m <= 16. */
 size_t mo_pack_refs_bytes(int64_t w);
 int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
+
+/* ------------------------------------------- op-level API (k_ops.cu)
+ * The reference's per-op functions as device kernels, for callers of the
+ * per-op API (the engine runs these stages fused inside mo_step).  Index and
+ * count arrays are int64 (the reference's integer vectors), outputs follow the
+ * reference oracle's order (oracle/manyobj_ref/niche.py:157-278).  Stream
+ * ordered; the caller owns every buffer; workspace from
+ * mo_ops_workspace_bytes(rows, points). */
+int mo_ops_workspace_bytes(int64_t R, int64_t w, size_t* bytes);
+
+/* batchcore.step_mask: out[i] = x[i] > 0. */
+int mo_step_mask(const double* x, int64_t n, int8_t* out, void* stream);
+/* batchcore.masked_argmin: *out (device int64) = lowest index
+ * of the minimum over valid slots (valid NULL = all), -1 when none is valid
+ * (the caller raises EmptySelectionError). */
+int mo_masked_argmin(const double* values, const uint8_t* valid, int64_t n, int64_t* out, void* workspace,
+                     size_t workspace_bytes, void* stream);
+/* batchcore.segment_count: counts[j] = valid labels == j;
+ * a valid label outside [0, segments) sets *status (device) = MO_ERR_BOUNDS. */
+int mo_segment_count(const int64_t* labels, const uint8_t* valid, int64_t n, int64_t segments, int64_t* counts,
+                     int32_t* status, void* stream);
+/* niche.associate over a materialised distance matrix D
+ * (R x w FP64): pi = first column of the row minimum, d = that minimum;
+ * invalid rows -> (-1, NaN). */
+int mo_associate_matrix(const double* D, const uint8_t* valid, int64_t R, int64_t w, int64_t* pi, double* d,
+                        void* stream);
+/* niche.niche_counts: rho over rank < l (l > 0), rho' over
+ * rank == l, rho = 2^31-1 (infinity) where rho' == 0. */
+int mo_niche_counts(const int64_t* pi, const int64_t* ranks, int64_t R, int64_t l, int64_t w, int64_t* rho,
+                    int64_t* rho_p, void* stream);
+/* niche.nearest_selection: for every point with rho == 0
+ * the rank-l candidate of smallest (d, pos_pop); all of them when they are
+ * <= k (ascending point order), else the first k by pos_ref.  promoted:
+ * device int64[w], *n_promoted (device) entries; rho / rho_p updated in place
+ * (rho = 1, rho' - 1, infinity when rho' reaches 0). */
+int mo_nearest_selection(const int64_t* pi, const float* d, const int64_t* ranks, int64_t R, int64_t l,
+                         int64_t* rho, int64_t* rho_p, int64_t w, int64_t k, const int64_t* pos_pop,
+                         const int64_t* pos_ref, int64_t* promoted, int64_t* n_promoted, void* workspace,
+                         size_t workspace_bytes, void* stream);
+/* niche.build_cache as CSR: offsets[w+1], cand = rank-l
+ * rows not flagged in `exclude` (uint8 per row, may be NULL), grouped by pi,
+ * shuffled population order inside a point. */
+int mo_build_cache(const int64_t* pi, const int64_t* ranks, int64_t R, int64_t l, int64_t w, const int64_t* pos_pop,
+                   const uint8_t* exclude, int64_t* offsets, int64_t* cand, void* workspace, size_t workspace_bytes,
+                   void* stream);
+/* niche.batched_random_selection: the k rows Alg. 2's loop
+ * takes from the CSR cache, in the loop's order; info (device int64[3]) =
+ * (rows taken, loop iterations, status: MO_ERR_INFEASIBLE when the loop
+ * cannot fill k). */
+int mo_batched_random_selection(const int64_t* offsets, const int64_t* cand, const int64_t* rho, const int64_t* rho_p,
+                                int64_t w, int64_t k, const int64_t* pos_ref, int64_t* taken, int64_t* info,
+                                void* workspace, size_t workspace_bytes, void* stream);
+/* variation.sbx_pair over npairs pairs of d variables,
+ * FP64: with u (npairs x d) SBX on every variable; u == NULL draws the
+ * engine's Philox streams (pair Bernoulli(p_c), one u per variable) for
+ * (seed, generation).  clamp != 0 clamps to [lo, hi]. */
+int mo_sbx_pairs(const double* P1, const double* P2, int64_t npairs, int32_t d, const double* u, double eta_c,
+                 float p_c, double lo, double hi, int32_t clamp, uint64_t seed, uint32_t generation, double* C1,
+                 double* C2, void* stream);
+/* variation.polynomial_mutation, FP64, clamped to [lo, hi]:
+ * with u (n x d) mutate where flag (uint8, NULL = everywhere); u == NULL
+ * draws the engine's PM stream (flag = u < p_m, then a second draw). */
+int mo_polynomial_mutation(const double* X, int64_t n, int32_t d, const double* u, const uint8_t* flag, double eta_m,
+                           float p_m, double lo, double hi, uint64_t seed, uint32_t generation, double* out,
+                           void* stream);
 
 /* ---------------------------------------------------- measurement helper */
 

@@ -64,6 +64,8 @@ _PROTOS = {
     "mo_front_peel": (c_i32, [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_presort": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_dominance_bits_sorted": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "mo_dominance_tables_bytes": (c_sz, [c_i64, c_i32]),
+    "mo_dominance_bits_ranked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_normalize": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_associate": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_sz,
                              c_vp]),
@@ -90,6 +92,22 @@ _PROTOS = {
     "mo_workspace_bytes_ex": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_sz)]),
     "mo_stream_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    # op-level API (k_ops.cu)
+    "mo_ops_workspace_bytes": (c_i32, [c_i64, c_i64, ctypes.POINTER(c_sz)]),
+    "mo_step_mask": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
+    "mo_masked_argmin": (c_i32, [c_vp, c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "mo_segment_count": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "mo_associate_matrix": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "mo_niche_counts": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp]),
+    "mo_nearest_selection": (c_i32, [c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                                     c_vp, c_vp, c_sz, c_vp]),
+    "mo_build_cache": (c_i32, [c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_batched_random_selection": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_sz,
+                                            c_vp]),
+    "mo_sbx_pairs": (c_i32, [c_vp, c_vp, c_i64, c_i32, c_vp, ctypes.c_double, c_f32, ctypes.c_double,
+                             ctypes.c_double, c_i32, c_u64, c_u32, c_vp, c_vp, c_vp]),
+    "mo_polynomial_mutation": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, ctypes.c_double, c_f32, ctypes.c_double,
+                                       ctypes.c_double, c_u64, c_u32, c_vp, c_vp]),
 }
 
 EXPORTED = tuple(_PROTOS)
@@ -138,6 +156,12 @@ def workspace_rows(R, m, w, device=None):
     nbytes = c_sz(0)
     check(lib().mo_workspace_bytes_rows(int(R), int(m), int(w), ctypes.byref(nbytes)), "mo_workspace_bytes_rows")
     return torch.empty(int(nbytes.value), dtype=torch.uint8, device=device or "cuda")
+
+
+def workspace_ops(R, w, device=None):
+    nbytes = c_sz(0)
+    check(lib().mo_ops_workspace_bytes(int(R), int(w), ctypes.byref(nbytes)), "mo_ops_workspace_bytes")
+    return torch.empty(max(1, int(nbytes.value)), dtype=torch.uint8, device=device or "cuda")
 
 
 def workspace_step(n, m, d, w, device=None):

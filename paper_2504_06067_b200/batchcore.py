@@ -4,7 +4,8 @@ These are the reference's L1 building blocks; inside the engine they exist
 only fused into the kernels (warp argmin reductions, warp-aggregated
 histograms, keyed shuffles).  The standalone versions below keep the
 reference API for callers and tests: shuffles run the library's keyed
-swap-or-not kernel, the reductions are single device tensor expressions.
+swap-or-not kernel, step_mask / masked_argmin / segment_count their own small
+kernels (k_ops.cu).
 """
 from dataclasses import dataclass
 
@@ -39,32 +40,42 @@ class SeedableRng:
 
 
 def step_mask(x):
-    """Heaviside H(x) = 1 where x > 0."""
-    return (as_cuda(x, torch.float32) > 0).to(torch.int8)
+    """Heaviside H(x) = 1 where x > 0; int8 CUDA tensor (k_step_mask)."""
+    x = as_cuda(x, torch.float64).reshape(-1)
+    out = torch.empty(x.numel(), dtype=torch.int8, device=x.device)
+    _lib.check(_lib.lib().mo_step_mask(_lib.ptr(x), x.numel(), _lib.ptr(out), _lib.stream_ptr()), "mo_step_mask")
+    return out
 
 
 def masked_argmin(values, valid=None):
-    """Lowest-index minimum over valid slots."""
-    v = as_cuda(values, torch.float64)
-    ok = torch.ones_like(v, dtype=torch.bool) if valid is None else as_cuda(valid, torch.bool)
-    if ok.shape != v.shape:
+    """Lowest-index minimum over valid slots; EmptySelectionError when none is valid."""
+    v = as_cuda(values, torch.float64).reshape(-1)
+    ok = None if valid is None else as_cuda(valid, torch.uint8).reshape(-1)
+    if ok is not None and ok.shape != v.shape:
         raise ShapeError("values/valid length mismatch")
-    if not bool(ok.any()):
+    out = torch.empty(1, dtype=torch.int64, device=v.device)
+    ws = _lib.workspace_ops(v.numel(), 1, v.device)
+    _lib.check(_lib.lib().mo_masked_argmin(_lib.ptr(v), _lib.ptr(ok), v.numel(), _lib.ptr(out), _lib.ptr(ws),
+                                           ws.numel(), _lib.stream_ptr()), "mo_masked_argmin")
+    i = int(out.item())
+    if i < 0:
         raise EmptySelectionError("masked_argmin over zero valid slots")
-    masked = torch.where(ok, v, torch.full_like(v, float("inf")))
-    mn = masked.min()
-    hit = ok & (masked == mn)
-    return int(torch.nonzero(hit)[0, 0].item())
+    return i
 
 
 def segment_count(labels, valid, segments):
-    """Count of valid labels per segment."""
-    lab = as_cuda(labels, torch.int64)
-    ok = torch.ones_like(lab, dtype=torch.bool) if valid is None else as_cuda(valid, torch.bool)
-    lab = lab[ok]
-    if lab.numel() and (int(lab.min()) < 0 or int(lab.max()) >= segments):
+    """Count of valid labels per segment; BoundsError for a valid label out of range."""
+    lab = as_cuda(labels, torch.int64).reshape(-1)
+    ok = None if valid is None else as_cuda(valid, torch.uint8).reshape(-1)
+    if ok is not None and ok.shape != lab.shape:
+        raise ShapeError("labels/valid length mismatch")
+    counts = torch.empty(int(segments), dtype=torch.int64, device=lab.device)
+    status = torch.zeros(1, dtype=torch.int32, device=lab.device)
+    _lib.check(_lib.lib().mo_segment_count(_lib.ptr(lab), _lib.ptr(ok), lab.numel(), int(segments), _lib.ptr(counts),
+                                           _lib.ptr(status), _lib.stream_ptr()), "mo_segment_count")
+    if int(status.item()):
         raise BoundsError("label out of range")
-    return torch.bincount(lab, minlength=segments)
+    return counts
 
 
 def shuffle_rows(m, rng):

@@ -1,0 +1,399 @@
+// Dominance bit-matrix by per-objective rank masks (K1, engine path for m = 2..16).
+//
+// Reference: dominance.dominance_matrix, the input of non_dominated_sort
+// (SPEC.md:196-204).  Same output as k_dom_tile_sorted (k_dominance.cu) -- the dominated-major
+// bit-matrix over presorted positions plus hasdom -- with far fewer instructions per pair.
+//
+// For a 256-row block I of the S-presorted rows and one objective k, the set {i in I : a_ik <= b}
+// is the prefix of I's rows sorted by objective k whose length c is the number of values <= b.
+// So per block and objective we precompute (k_dom_tables):
+//   * the sorted values in Eytzinger (BFS) order, 511 slots padded with NaN -> c by 9 branch-free
+//     probes, conflict-free in shared memory (level t of the tree is 2^t contiguous words);
+//   * the 257 prefix masks P_k[c] (256 bits = 8 words each).
+// Then, for a row j, the 256 bits "a_i <= b_j in every objective" are AND_k P_k[c_k(j)]: m searches
+// and m x 8 word ANDs for 256 pairs instead of 256 m-long compare chains (about 1.6 instructions per
+// pair at m = 10 instead of ~11).  In S-separated tiles (max S(I) < min S(J)) that weak relation is
+// already "i dominates j" (S differs, so the rows differ).  Tiles with overlapping S ranges (the
+// diagonal) also need the reverse relation: {i : a_ik >= b} = complement of the strict prefix
+// P_k[#{a < b}], giving both dominance directions with the exact compare semantics of the pairwise
+// kernel (IEEE <=, -0 == +0; a row with a NaN objective dominates nothing and is dominated by
+// nothing).
+//
+// k_dom_rank: persistent grid over items (I block, run of J blocks).  The CTA pulls block I's m
+// tables (m x 10,272 B) into shared memory with ONE bulk TMA copy (cp.async.bulk + mbarrier), then
+// sweeps its J blocks, one row j per thread: b_j from FS (L2), m Eytzinger searches (unrolled across
+// the m objectives for ILP), the mask ANDs, 8 words stored to row j.  Reverse-direction words of the
+// overlapping tiles are transposed through warp ballots and shared memory.
+#include <cuda_runtime.h>
+
+#include "mo_common.cuh"
+#include "k_dominance_args.cuh"
+
+namespace mo {
+
+constexpr int DR_BLK = 256;                        // rows per block (= the bit-matrix tile)
+constexpr int DR_EYT = 512;                        // Eytzinger slots (1..511 used)
+constexpr int DR_MASKS = DR_BLK + 1;               // prefix masks c = 0..256
+constexpr int DR_TBL_WORDS = DR_EYT + DR_MASKS * 8;
+constexpr int DR_TBL_BYTES = DR_TBL_WORDS * 4;     // 10,272 (16-byte multiple)
+static_assert(DR_TBL_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
+
+__host__ __device__ inline int64_t dom_rank_blocks(int64_t R) { return (R + DR_BLK - 1) / DR_BLK; }
+
+// 16-byte half h of prefix mask c: swizzled so that 8 lanes loading random masks spread over all 8
+// bank groups of a 128-bit shared-memory phase
+__device__ __forceinline__ int mask_slot(int c, int h) { return 2 * c + (h ^ ((c >> 2) & 1)); }
+
+// ------------------------------------------------------------------ tables
+// grid (nb, M): block bi, objective k.  vmask[bi*8 + w]: rows of block bi that exist and have no NaN.
+template <int M>
+__global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__ FS, int R,
+                                                        uint32_t* __restrict__ tables, uint32_t* __restrict__ vmask) {
+  pdl_wait();
+  __shared__ uint32_t sKey[DR_BLK];
+  __shared__ int sIdx[DR_BLK];
+  const int bi = blockIdx.x, k = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int i = bi * DR_BLK + t;
+  const float x = i < R ? FS[(int64_t)i * M + k] : __int_as_float(0x7fc00000);
+  sKey[t] = x != x ? 0xffffffffu : f2ord(__fadd_rn(x, 0.0f));   // NaN last; -0 -> +0
+  sIdx[t] = t;
+  if (k == 0) {
+    bool ok = i < R;
+    if (ok)
+      for (int q = 0; q < M; ++q) {
+        const float v = FS[(int64_t)i * M + q];
+        ok = ok && v == v;
+      }
+    const uint32_t bal = __ballot_sync(MO_FULL, ok);
+    if (lane == 0) vmask[(int64_t)bi * 8 + warp] = bal;
+  }
+  __syncthreads();
+  // bitonic sort of (key, idx), ascending
+  for (int size = 2; size <= DR_BLK; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const int p = t ^ stride;
+      if (p > t) {
+        const bool up = (t & size) == 0;
+        const uint32_t a = sKey[t], b = sKey[p];
+        if ((a > b) == up) {
+          sKey[t] = b;
+          sKey[p] = a;
+          const int ia = sIdx[t];
+          sIdx[t] = sIdx[p];
+          sIdx[p] = ia;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  uint32_t* tab = tables + ((int64_t)bi * M + k) * DR_TBL_WORDS;
+  // Eytzinger: node n at depth d holds sorted position ((2 (n - 2^d) + 1) << (8 - d)) - 1
+  for (int n = t; n < DR_EYT; n += DR_BLK) {
+    float v = __int_as_float(0x7fc00000);
+    if (n >= 1) {
+      const int d = 31 - __clz(n);
+      const int pos = ((2 * (n - (1 << d)) + 1) << (8 - d)) - 1;
+      if (pos < DR_BLK && sKey[pos] != 0xffffffffu) v = ord2f(sKey[pos]);
+    }
+    tab[n] = __float_as_uint(v);
+  }
+  // prefix masks: warp w builds word w of P[0..256] by an inclusive OR-scan over the sorted order
+  uint32_t* P = tab + DR_EYT;
+  uint32_t carry = 0;
+  for (int q = 0; q < DR_BLK / 32; ++q) {
+    const int s = q * 32 + lane;
+    const int idx = sIdx[s];
+    uint32_t v = (idx >> 5) == warp ? 1u << (idx & 31) : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(MO_FULL, v, o);
+      if (lane >= o) v |= y;
+    }
+    v |= carry;
+    const int c = s + 1;   // P[c] = first c sorted rows
+    P[mask_slot(c, warp >> 2) * 4 + (warp & 3)] = v;
+    carry = __shfl_sync(MO_FULL, v, 31);
+  }
+  if (lane == 0) P[mask_slot(0, warp >> 2) * 4 + (warp & 3)] = 0u;
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------- main sweep
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk TMA copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+struct DomRankArgs {
+  const float* FS;
+  const float* blkmin;
+  const float* blkmax;
+  const int* wend;
+  const uint32_t* tables;
+  const uint32_t* vmask;
+  uint32_t* bits;
+  uint8_t* hasdom;
+  int R, nb, ch;           // rows, blocks, J blocks per item
+  int64_t W;               // words per bit-matrix row
+  int64_t items;
+};
+
+// items of block row bi: ceil((nb - bi) / ch); G(n) = sum_{x=1..n} ceil(x / ch)
+__device__ __forceinline__ int64_t dr_G(int64_t n, int ch) {
+  const int64_t q = n / ch, r = n % ch;
+  return ch * q * (q + 1) / 2 + r * (q + 1);
+}
+__device__ __forceinline__ void dr_decode(int64_t t, int nb, int ch, int& bi, int& bj0, int& bj1) {
+  const int64_t Gn = dr_G(nb, ch);
+  int lo = 0, hi = nb - 1;   // largest bi with cum(bi) = Gn - G(nb - bi) <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (Gn - dr_G(nb - mid, ch) <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  bi = lo;
+  const int64_t off = t - (Gn - dr_G(nb - bi, ch));
+  bj0 = bi + (int)off * ch;
+  bj1 = min(nb, bj0 + ch);
+}
+
+template <int M>
+__global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
+  pdl_wait();
+  extern __shared__ __align__(128) uint32_t sTab[];   // M tables of block I
+  __shared__ __align__(8) uint64_t sBar;
+  __shared__ uint32_t sT[DR_BLK * 9];                  // reverse-direction words (row i, J word w)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) mbar_init(&sBar, 1);
+  __syncthreads();
+  unsigned parity = 0;
+  for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+    int bi, bj0, bj1;
+    dr_decode(item, a.nb, a.ch, bi, bj0, bj1);
+    __syncthreads();   // the previous item is done with sTab / sT
+    if (tid == 0) {
+      mbar_expect_tx(&sBar, (unsigned)(M * DR_TBL_BYTES));
+      bulk_g2s(sTab, a.tables + (int64_t)bi * M * DR_TBL_WORDS, (unsigned)(M * DR_TBL_BYTES), &sBar);
+    }
+    uint32_t vI[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) vI[w] = __ldg(a.vmask + (int64_t)bi * 8 + w);
+    const float smaxI = __ldg(a.blkmax + bi);
+    const int i0 = bi * DR_BLK;
+    // first J row's objectives while the tables land
+    float bnext[M];
+    {
+      const int j = bj0 * DR_BLK + tid;
+#pragma unroll
+      for (int k = 0; k < M; ++k) bnext[k] = j < a.R ? __ldg(a.FS + (int64_t)j * M + k) : 0.0f;
+    }
+    mbar_wait(&sBar, parity);
+    parity ^= 1u;
+    for (int bj = bj0; bj < bj1; ++bj) {
+      const int j = bj * DR_BLK + tid;
+      float b[M];
+      bool jnan = false;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        b[k] = bnext[k];
+        jnan = jnan || (b[k] != b[k]);
+      }
+      if (bj + 1 < bj1) {   // prefetch the next J block's row
+        const int jn = j + DR_BLK;
+#pragma unroll
+        for (int k = 0; k < M; ++k) bnext[k] = jn < a.R ? __ldg(a.FS + (int64_t)jn * M + k) : 0.0f;
+      }
+      const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
+      // weak relation a_i <= b_j in every objective: AND of the prefix masks
+      int node[M];
+#pragma unroll
+      for (int k = 0; k < M; ++k) node[k] = 1;
+#pragma unroll
+      for (int s = 0; s < 9; ++s) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + node[k]]);
+          node[k] = 2 * node[k] + (e <= b[k] ? 1 : 0);
+        }
+      }
+      uint32_t le[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const int c = node[k] - DR_EYT;
+        const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
+        const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+        le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
+        le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+      }
+      uint32_t out[8];
+      if (fast) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) out[w] = le[w];
+      } else {
+        // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
+        int nd[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) nd[k] = 1;
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + nd[k]]);
+            nd[k] = 2 * nd[k] + (e < b[k] ? 1 : 0);
+          }
+        }
+        uint32_t ge[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const int c = nd[k] - DR_EYT;
+          const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
+          const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+          ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
+          ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w) out[w] = le[w] & ~ge[w];   // i dominates j
+        if (bi != bj) {
+          // j dominates i: transpose the per-j masks into rows i (word bj*8 + warp) by ballots
+          const bool jok = j < a.R;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const uint32_t rev = jok ? (ge[w] & ~le[w]) : 0u;
+            uint32_t mine = 0;
+#pragma unroll
+            for (int b2 = 0; b2 < 32; ++b2) {
+              const uint32_t bal = __ballot_sync(MO_FULL, (rev >> b2) & 1u);
+              mine = lane == b2 ? bal : mine;
+            }
+            sT[(w * 32 + lane) * 9 + warp] = mine;   // row i = w*32 + lane, word warp of block bj
+          }
+        }
+      }
+      if (j < a.R) {
+        uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)j * a.W + (int64_t)bi * 8);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        if ((out[0] | out[1] | out[2] | out[3] | out[4] | out[5] | out[6] | out[7]) != 0u) a.hasdom[j] = 1;
+      }
+      if (fast) {
+        // rows i of I's last S bucket may share it with rows of J: their words of block bj lie below
+        // wend and are read by the peel, so they must hold zeros (no j of a fast tile dominates an i)
+        const int ilast = min(a.R, i0 + DR_BLK) - 1;
+        if (__ldg(a.wend + ilast) > bj * 8) {
+          const int i = i0 + tid;
+          if (i < a.R && __ldg(a.wend + i) > bj * 8) {
+            uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
+            dst[0] = make_uint4(0u, 0u, 0u, 0u);
+            dst[1] = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+      } else if (bi != bj) {
+        __syncthreads();
+        const int i = i0 + tid;
+        if (i < a.R) {
+          const uint32_t* sw = sT + tid * 9;
+          uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
+          dst[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+          dst[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
+          if ((sw[0] | sw[1] | sw[2] | sw[3] | sw[4] | sw[5] | sw[6] | sw[7]) != 0u) a.hasdom[i] = 1;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+size_t dom_rank_tables_bytes(int64_t R, int m) {
+  const int64_t nb = dom_rank_blocks(R);
+  return (size_t)nb * (size_t)m * DR_TBL_BYTES + (size_t)nb * 8 * 4 + 256;
+}
+
+template <int M>
+static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
+                             uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+  const int nb = (int)dom_rank_blocks(R);
+  uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
+  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask));
+  const size_t smem = (size_t)M * DR_TBL_BYTES;
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    if (cudaFuncSetAttribute(k_dom_rank<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return MO_ERR_CUDA;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dom_rank<M>, DR_BLK, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
+  // ~4 items per resident CTA: each item re-loads block I's tables (M x 10 KB), so runs of J blocks
+  // amortise the copy while the item count keeps the triangular work balanced
+  int ch = (int)ceil_div(pairs, 4 * slots);
+  ch = ch < 1 ? 1 : (ch > nb ? nb : ch);
+  DomRankArgs a;
+  a.FS = FS;
+  a.blkmin = blkmin;
+  a.blkmax = blkmax;
+  a.wend = wend;
+  a.tables = tables;
+  a.vmask = vmask;
+  a.bits = bits;
+  a.hasdom = hasdom;
+  a.R = (int)R;
+  a.nb = nb;
+  a.ch = ch;
+  a.W = words_per_row(R);
+  int64_t items = 0;
+  for (int bi = 0; bi < nb; ++bi) items += (nb - bi + ch - 1) / ch;
+  a.items = items;
+  const int64_t grid = items < slots ? items : slots;
+  return launch_ex(k_dom_rank<M>, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a);
+}
+
+int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R, int m,
+                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+  if (R <= 0) return MO_OK;
+  if (R > (1ll << 31) - 1 - DR_BLK) return MO_ERR_PARAM;
+  switch (m) {
+#define MO_DR_CASE(MM) \
+  case MM: return launch_dom_rank_m<MM>(FS, blkmin, blkmax, wend, R, bits, hasdom, tables, s);
+    MO_DR_CASE(2) MO_DR_CASE(3) MO_DR_CASE(4) MO_DR_CASE(5) MO_DR_CASE(6) MO_DR_CASE(7) MO_DR_CASE(8)
+    MO_DR_CASE(9) MO_DR_CASE(10) MO_DR_CASE(11) MO_DR_CASE(12) MO_DR_CASE(13) MO_DR_CASE(14) MO_DR_CASE(15)
+    MO_DR_CASE(16)
+#undef MO_DR_CASE
+    default:
+      return MO_ERR_PARAM;
+  }
+}
+
+}  // namespace mo

@@ -47,6 +47,9 @@ int launch_presort(const PresortArgs& args, cudaStream_t s);
 int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint32_t* bits, cudaStream_t s);
 int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
                            int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s, bool clear_hasdom = true);
+size_t dom_rank_tables_bytes(int64_t R, int m);
+int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R, int m,
+                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s);
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,

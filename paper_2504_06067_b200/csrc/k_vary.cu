@@ -14,6 +14,7 @@
 #include "mo_dtlz.cuh"
 #include "mo_rng.cuh"
 #include "mo_prologue.cuh"
+#include "mo_variation.cuh"
 
 namespace mo {
 
@@ -24,28 +25,6 @@ __device__ __forceinline__ void atomic_min_float(float* addr, float v) {
     atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
 }
 
-__device__ __forceinline__ double sbx_beta(double u, double eta) {
-  double e = 1.0 / (eta + 1.0);
-  return u <= 0.5 ? pow(2.0 * u, e) : pow(1.0 / (2.0 * (1.0 - u)), e);
-}
-
-__device__ __forceinline__ double pm_apply(double x, double u, double eta) {
-  // bounds [0,1]: span = 1, d1 = x, d2 = 1 - x  (oracle variation.pm_delta)
-  const double lo = 0.0, hi = 1.0, span = hi - lo;
-  double d1 = (x - lo) / span, d2 = (hi - x) / span;
-  double mp = 1.0 / (eta + 1.0);
-  double dq;
-  if (u < 0.5) {
-    double v = 2.0 * u + (1.0 - 2.0 * u) * pow(1.0 - d1, eta + 1.0);
-    dq = pow(v, mp) - 1.0;
-  } else {
-    double v = 2.0 * (1.0 - u) + 2.0 * (u - 0.5) * pow(1.0 - d2, eta + 1.0);
-    dq = 1.0 - pow(v, mp);
-  }
-  return x + dq * span;
-}
-
-__device__ __forceinline__ double clamp01(double v) { return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v); }
 
 // One block = ppb <= VARY_PAIRS mating pairs, VARY_THREADS threads.  Phase 1: one
 // thread per pair draws the parents (keyed MATING permutation) into shared

@@ -42,7 +42,7 @@ struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
       colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
-      lvl, sctl, mate, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
+      lvl, sctl, mate, dtab, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
 };
 
@@ -54,6 +54,9 @@ static size_t bump(size_t& cur, size_t bytes) {
 
 static int shards_of(int32_t count) { return count < 1 ? 1 : count; }
 
+// sort_mode LAYOUT_OPS: the per-op entry points (mo_normalize, mo_associate, mo_niche_select, ...) -- no
+// bit-matrix (mo_front_peel takes the caller's) and no streamed-sort regions.
+constexpr int LAYOUT_OPS = -1;
 static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_BITS, int G = 1) {
   Layout L;
   size_t c = 0;
@@ -107,6 +110,9 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.lvl = bump(c, (size_t)2 * LVL_BINS * 4);
   L.sctl = bump(c, 16 * 4);
   L.mate = bump(c, (size_t)(R + 16) * 4);   // [0..7] two tags, [8] counter, [16..): two n-slot mating buffers
+  // rank-mask dominance tables (k_dom_rank.cu): per 256-row block and objective, Eytzinger values +
+  // prefix masks (bit-matrix sort, 2 <= m <= 16)
+  L.dtab = bump(c, sort_mode == MO_SORT_BITS && m >= 2 && m <= 16 ? dom_rank_tables_bytes(R, m) : 0);
   // streamed / sharded sort (sort_mode == MO_SORT_STREAM)
   const bool st = sort_mode == MO_SORT_STREAM;
   const int64_t nb = ceil_div(R, STREAM_BLK);
@@ -287,6 +293,17 @@ static PresortArgs presort_args(const mo_step_args* a, const Layout& L) {
   return ps;
 }
 
+// rank-mask dominance (k_dom_rank.cu) for 2 <= m <= 16; MO_DOM_PAIRWISE=1 selects the pairwise
+// compare-chain tiles (k_dom_tile_sorted) instead
+static bool use_dom_rank(int m) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("MO_DOM_PAIRWISE");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  return !off && m >= 2 && m <= 16;
+}
+
 static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   const int64_t n = a->n, R = 2 * n;
   void* ws = a->workspace;
@@ -297,7 +314,10 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   ps.in_step = 1;
   ps.hasdom = hasdom;
   MO_TRY(launch_presort(ps, s));
-  MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s, false));
+  if (use_dom_rank(a->m))
+    MO_TRY(launch_dom_rank(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, at<uint32_t>(ws, L.dtab), s));
+  else
+    MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s, false));
   return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
                            at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, ps.perm, hasdom, ps.wend,
                            at<int>(ws, L.rank_pos), ps.trace, s, true);
@@ -567,7 +587,7 @@ int mo_workspace_bytes(int64_t n, int32_t m, int32_t d, int64_t w, size_t* bytes
 
 int mo_workspace_bytes_rows(int64_t R, int32_t m, int64_t w, size_t* bytes) {
   if (!bytes || R < 1 || m < 1 || w < 0) return MO_ERR_PARAM;
-  *bytes = make_layout(R, w > 0 ? w : 1, m).total;
+  *bytes = make_layout(R, w > 0 ? w : 1, m, LAYOUT_OPS).total;
   return MO_OK;
 }
 
@@ -604,7 +624,7 @@ int mo_dominance_bits(const float* F, int64_t R, int32_t m, const uint8_t* valid
 int mo_presort(const float* F, int64_t R, int32_t m, int32_t* perm, float* FS, float* SS, int32_t* wend,
                float* blkmin, float* blkmax, void* workspace, size_t workspace_bytes, void* stream_) {
   if (R < 1 || m < 1 || !F || !perm || !FS || !SS || !wend || !blkmin || !blkmax) return MO_ERR_PARAM;
-  Layout L = make_layout(R, 1, m);
+  Layout L = make_layout(R, 1, m, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   PresortArgs ps;
   ps.F = F;
@@ -641,9 +661,23 @@ int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* 
   return launch_dom_tile_sorted(FS, blkmin, blkmax, wend, R, m, bits, hasdom, (cudaStream_t)stream_);
 }
 
+size_t mo_dominance_tables_bytes(int64_t R, int32_t m) {
+  return (R < 1 || m < 2 || m > 16) ? 0 : dom_rank_tables_bytes(R, m);
+}
+
+int mo_dominance_bits_ranked(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
+                             int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* tables,
+                             size_t tables_bytes, void* stream_) {
+  if (!FS || !blkmin || !blkmax || !wend || !bits || !hasdom || !tables || m < 2 || m > 16) return MO_ERR_PARAM;
+  if (tables_bytes < dom_rank_tables_bytes(R, m)) return MO_ERR_PARAM;
+  cudaStream_t s = (cudaStream_t)stream_;
+  if (cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
+  return launch_dom_rank(FS, blkmin, blkmax, wend, R, m, bits, hasdom, static_cast<uint32_t*>(tables), s);
+}
+
 int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int32_t* ranks,
                   int32_t* info, void* workspace, size_t workspace_bytes, void* stream_) {
-  Layout L = make_layout(R, 1, 1);
+  Layout L = make_layout(R, 1, 1, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   return launch_front_peel(bits, R, valid, stop_at, ranks, info, at<int>(workspace, L.resume),
                            at<uint32_t>(workspace, L.ranked), at<int>(workspace, L.fsizes),
@@ -655,7 +689,7 @@ int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, con
                  uint32_t generation, float* ideal, float* Fn, double* intercepts, void* workspace,
                  size_t workspace_bytes, void* stream_) {
   if (m < 1 || m > 16 || R < 1) return MO_ERR_PARAM;   // k_prep's extreme-point pass: m <= 16
-  Layout L = make_layout(R, 1, m);
+  Layout L = make_layout(R, 1, m, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;
   // w = 1 dummy reference point set: only the row shuffle matters here
@@ -684,7 +718,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
                  const int32_t* info, uint64_t seed, uint32_t generation, int32_t* pi, float* d, void* workspace,
                  size_t workspace_bytes, void* stream_) {
   if (m < 1 || m > 16 || R < 1 || w < 1) return MO_ERR_PARAM;
-  Layout L = make_layout(R, w, m);
+  Layout L = make_layout(R, w, m, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;
   PrepArgs pa = prep_args(L, workspace, Fn, R, m, w, ranks, const_cast<int*>(info), nullptr, seed, generation, zhat,
@@ -726,7 +760,7 @@ int mo_niche_select(const int32_t* pi, const float* d, int64_t R, int64_t w, int
                     int32_t* info, uint64_t seed, uint32_t generation, uint8_t* selected, void* workspace,
                     size_t workspace_bytes, void* stream_) {
   if (R < 1 || w < 1 || n < 1) return MO_ERR_PARAM;
-  Layout L = make_layout(R, w, 1);
+  Layout L = make_layout(R, w, 1, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;
   // shuffles only (rows and reference points)

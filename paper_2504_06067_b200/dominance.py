@@ -10,7 +10,7 @@ import torch
 
 from . import _lib
 from ._tensor import as_cuda, as_mask, as_matrix, device
-from .errors import InfeasibleSplitError, ShapeError
+from .errors import InfeasibleSplitError, ParameterError, ShapeError
 
 DROPPED = _lib.DROPPED
 
@@ -59,18 +59,30 @@ def presort(F):
     return out
 
 
-def dominance_bits_sorted(ps, poison=False):
+def dominance_bits_sorted(ps, poison=False, method="ranked"):
     """Bit-matrix of presorted rows (position space) + has-a-dominator flags, from :func:`presort`.
-    ``poison`` pre-fills the matrix with ones (tests: words below wend must all be written)."""
+    ``method``: "ranked" (per-objective rank masks, k_dom_rank.cu -- the engine's kernel) or
+    "pairwise" (compare-chain tiles, k_dom_tile_sorted).  ``poison`` pre-fills the matrix with ones
+    (tests: words below wend must all be written)."""
     FS = ps["FS"]
     R, m = FS.shape
-    W = int(_lib.lib().mo_bits_words_per_row(R))
+    L = _lib.lib()
+    W = int(L.mo_bits_words_per_row(R))
     bits = torch.full((R, W), -1 if poison else 0, dtype=torch.int32, device=FS.device)
     hasdom = torch.empty(R, dtype=torch.uint8, device=FS.device)
-    _lib.check(_lib.lib().mo_dominance_bits_sorted(_lib.ptr(FS), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
-                                                   _lib.ptr(ps["wend"]), R,
-                                                   m, _lib.ptr(bits), _lib.ptr(hasdom), _lib.stream_ptr()),
-               "mo_dominance_bits_sorted")
+    args = (_lib.ptr(FS), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]), _lib.ptr(ps["wend"]), R, m,
+            _lib.ptr(bits), _lib.ptr(hasdom))
+    if method == "ranked":
+        nbytes = int(L.mo_dominance_tables_bytes(R, m))
+        if nbytes == 0:
+            raise ParameterError("the rank-mask kernel needs 2 <= m <= 16")
+        tables = torch.empty(nbytes, dtype=torch.uint8, device=FS.device)
+        _lib.check(L.mo_dominance_bits_ranked(*args, _lib.ptr(tables), nbytes, _lib.stream_ptr()),
+                   "mo_dominance_bits_ranked")
+    elif method == "pairwise":
+        _lib.check(L.mo_dominance_bits_sorted(*args, _lib.stream_ptr()), "mo_dominance_bits_sorted")
+    else:
+        raise ParameterError(f"unknown method {method!r}")
     return bits, hasdom
 
 

@@ -11,7 +11,7 @@ it is the CPU test oracle (oracle/manyobj_ref/niche.py), not an engine path.
 import torch
 
 from . import _lib
-from ._tensor import as_cuda, as_matrix
+from ._tensor import as_cuda, as_mask, as_matrix
 from .dominance import DROPPED
 from .errors import ParameterError, ShapeError
 
@@ -51,8 +51,10 @@ def normalize_objectives(F, ideal=None, ranks=None, l=None, seed=0, generation=0
     return Fn, ideal, icpt
 
 
-def associate(Fn, zhat, ranks=None, l=None, seed=0, generation=0):
-    """(pi, d) per candidate row -- fused Eq. (2) distance + argmin.
+def associate_canonical(Fn, zhat, ranks=None, l=None, seed=0, generation=0):
+    """(pi, d) per candidate row -- fused Eq. (2) distance + argmin; the oracle's
+    ``associate_canonical`` (oracle/manyobj_ref/niche.py:168) with the shuffles keyed by (seed,
+    generation) as in the engine.
 
     pi = nearest reference point by the canonical FP32 key (ties -> lowest
     shuffled reference position), d = perpendicular distance.  Rows that are
@@ -73,6 +75,98 @@ def associate(Fn, zhat, ranks=None, l=None, seed=0, generation=0):
                                        int(seed), int(generation), _lib.ptr(pi), _lib.ptr(d), _lib.ptr(ws),
                                        ws.numel(), _lib.stream_ptr()), "mo_associate")
     return pi, d
+
+
+def associate(D, valid=None):
+    """SPEC.md:349-357 over a materialised distance matrix (R x w): per valid row pi = argmin (lowest
+    column on ties), d = the minimum; invalid rows get the sentinel (-1, NaN).  int64 / FP64 CUDA
+    tensors.  (The engine never builds D; see :func:`associate_canonical`.)"""
+    D = as_matrix(D, torch.float64)
+    R, w = D.shape
+    if w < 1:
+        raise ShapeError("D needs at least one column")
+    v = as_mask(valid, R)
+    pi = torch.empty(R, dtype=torch.int64, device=D.device)
+    d = torch.empty(R, dtype=torch.float64, device=D.device)
+    _lib.check(_lib.lib().mo_associate_matrix(_lib.ptr(D), _lib.ptr(v), R, w, _lib.ptr(pi), _lib.ptr(d),
+                                              _lib.stream_ptr()), "mo_associate_matrix")
+    return pi, d
+
+
+def _i64(x):
+    return as_cuda(x, torch.int64)
+
+
+def niche_counts(pi, ranks, l, w):
+    """SPEC.md:358-366: (rho, rho') int64 over w points; rho counts rank < l (when l > 0), rho' counts
+    rank == l, and rho = INF (2^31 - 1) wherever rho' = 0."""
+    pi, ranks = _i64(pi), _i64(ranks)
+    if pi.shape != ranks.shape:
+        raise ShapeError("pi and ranks need one entry per row")
+    dev = pi.device
+    rho = torch.empty(int(w), dtype=torch.int64, device=dev)
+    rho_p = torch.empty(int(w), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().mo_niche_counts(_lib.ptr(pi), _lib.ptr(ranks), pi.numel(), int(l), int(w), _lib.ptr(rho),
+                                          _lib.ptr(rho_p), _lib.stream_ptr()), "mo_niche_counts")
+    return rho, rho_p
+
+
+def nearest_selection(pi, d, ranks, l, rho, rho_p, k, pos_pop, pos_ref):
+    """SPEC.md:367-375 (Alg. 2 lines 8-12): returns (promoted rows, rho, rho') -- for every point with
+    rho = 0 its rank-l candidate of smallest (d, shuffled position); all of them when they fit in
+    k (point order), else the first k in shuffled reference order."""
+    pi, ranks, pos_pop, pos_ref = _i64(pi), _i64(ranks), _i64(pos_pop), _i64(pos_ref)
+    d = as_cuda(d, torch.float32)
+    rho, rho_p = _i64(rho).clone(), _i64(rho_p).clone()
+    R, w = pi.numel(), rho.numel()
+    dev = pi.device
+    promoted = torch.empty(w, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = _lib.workspace_ops(R, w, dev)
+    _lib.check(_lib.lib().mo_nearest_selection(_lib.ptr(pi), _lib.ptr(d), _lib.ptr(ranks), R, int(l), _lib.ptr(rho),
+                                               _lib.ptr(rho_p), w, int(k), _lib.ptr(pos_pop), _lib.ptr(pos_ref),
+                                               _lib.ptr(promoted), _lib.ptr(cnt), _lib.ptr(ws), ws.numel(),
+                                               _lib.stream_ptr()), "mo_nearest_selection")
+    return promoted[: int(cnt.item())], rho, rho_p
+
+
+def build_cache(pi, ranks, l, w, pos_pop, exclude=None):
+    """the cache table as CSR (offsets[w+1], cand) -- rank-l rows not in ``exclude``
+    (row indices), grouped by reference point, shuffled population order inside a point."""
+    pi, ranks, pos_pop = _i64(pi), _i64(ranks), _i64(pos_pop)
+    R = pi.numel()
+    dev = pi.device
+    ex = None
+    if exclude is not None:
+        e = _i64(exclude)
+        ex = torch.zeros(R, dtype=torch.uint8, device=dev)
+        if e.numel():
+            ex[e] = 1
+    offsets = torch.empty(int(w) + 1, dtype=torch.int64, device=dev)
+    cand = torch.empty(max(R, 1), dtype=torch.int64, device=dev)
+    ws = _lib.workspace_ops(R, w, dev)
+    _lib.check(_lib.lib().mo_build_cache(_lib.ptr(pi), _lib.ptr(ranks), R, int(l), int(w), _lib.ptr(pos_pop),
+                                         _lib.ptr(ex), _lib.ptr(offsets), _lib.ptr(cand), _lib.ptr(ws), ws.numel(),
+                                         _lib.stream_ptr()), "mo_build_cache")
+    return offsets, cand[: int(offsets[-1].item())]
+
+
+def batched_random_selection(offsets, cand, rho, rho_p, k, pos_ref):
+    """SPEC.md:385-393 (Alg. 2 lines 15-26): (taken rows in the loop's order, loop iterations).
+    Raises InfeasibleSplitError when the points run out before k rows are taken."""
+    offsets, cand, rho, rho_p, pos_ref = _i64(offsets), _i64(cand), _i64(rho), _i64(rho_p), _i64(pos_ref)
+    w, k = rho.numel(), int(k)
+    dev = rho.device
+    taken = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
+    info = torch.zeros(3, dtype=torch.int64, device=dev)
+    ws = _lib.workspace_ops(k, w, dev)
+    _lib.check(_lib.lib().mo_batched_random_selection(_lib.ptr(offsets), _lib.ptr(cand), _lib.ptr(rho),
+                                                      _lib.ptr(rho_p), w, k, _lib.ptr(pos_ref), _lib.ptr(taken),
+                                                      _lib.ptr(info), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+               "mo_batched_random_selection")
+    h = info.tolist()
+    _lib.check(h[2], "batched_random_selection")
+    return taken[: h[0]], h[1]
 
 
 def niche_select(pi, d, ranks, split, n, w, seed=0, generation=0):
@@ -116,4 +210,5 @@ def perpendicular_distance_matrix(Fn, Z):
     return E.norm(dim=2)
 
 
-__all__ = ["normalize_objectives", "associate", "niche_select", "perpendicular_distance_matrix", "DROPPED"]
+__all__ = ["normalize_objectives", "associate", "associate_canonical", "niche_counts", "nearest_selection",
+           "build_cache", "batched_random_selection", "niche_select", "perpendicular_distance_matrix", "DROPPED"]

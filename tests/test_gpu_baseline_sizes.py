@@ -14,7 +14,7 @@ set, the ideal, and the next population X and F.
 * C4  DTLZ7 m=3  d=22 N=1M  : generations 0 and 1 on the streamed sort with the certified lattice
       association.  The oracle's ranks are full (oracle/c nds3).  Association: the oracle's full
       scan over 2M x 1M pairs is minutes, so pi/d come from the GPU's per-op full-scan association
-      (niche.associate, a different kernel from the engine's lattice path) after an exact check of
+      (niche.associate_canonical, a different kernel from the engine's lattice path) after an exact check of
       every F_l row and 10^5 sampled candidate rows against oracle/c; the oracle's niching then
       has to reproduce the engine's survivors exactly.
 """
@@ -134,7 +134,7 @@ def test_c4_generations(M):
         R = Fn.shape[0]
         ranks = np.full(R, Odom.DROPPED, np.int32)
         ranks[rows] = 0
-        pi_g, d_g = M.niche.associate(torch.from_numpy(np.ascontiguousarray(Fn)).cuda(),
+        pi_g, d_g = M.niche.associate_canonical(torch.from_numpy(np.ascontiguousarray(Fn)).cuda(),
                                       torch.from_numpy(zh32).cuda(), torch.from_numpy(ranks).cuda(), 0,
                                       ocfg.seed, checked["gen"])
         pi = np.full(R, -1, np.int64)

@@ -118,11 +118,16 @@ def test_dominance_with_valid_mask(M):
     assert np.array_equal(r, Odom.non_dominated_sort(F, valid))
 
 
-def test_sorted_path_bits(M):
+@pytest.mark.parametrize("method", ["ranked", "pairwise"])
+def test_sorted_path_bits(M, method):
     """Engine sort path: S-ordered buckets, bits of every row up to wend, hasdom flags."""
     rs = np.random.default_rng(12)
+    signed0 = rs.integers(-1, 2, size=(520, 3)).astype(np.float32)
+    signed0[rs.random((520, 3)) < 0.5] *= -0.0                         # -0 == +0 ties
     cases = [rs.random((700, 3)), rs.integers(0, 3, size=(600, 4)), rs.random((1300, 5)),
-             np.repeat(rs.random((300, 2)), 3, axis=0), rs.random((257, 10))]
+             np.repeat(rs.random((300, 2)), 3, axis=0), rs.random((257, 10)), signed0,
+             rs.integers(0, 2, size=(900, 16)), np.round(rs.random((1100, 12)) * 3) / 3,
+             np.full((300, 6), 0.5)]
     for F in cases:
         F = F.astype(np.float32)
         R, m = F.shape
@@ -139,12 +144,14 @@ def test_sorted_path_bits(M):
         # ... but no later position outside p's bucket may have S <= S[p]
         for p in range(R):
             later = np.arange((we[p]) * 32, R)
-            assert (SS[later] > SS[p]).all()
+            # (an S = -0 bucket precedes the S = +0 one: FP-equal sums, no dominance either way)
+            eq = SS[later] == SS[p]
+            assert (SS[later] >= SS[p]).all() and not (eq & (np.signbit(SS[later]) == np.signbit(SS[p]))).any()
         bmin, bmax = np_(ps["blkmin"]), np_(ps["blkmax"])
         for b in range(len(bmin)):
             blk = SS[b * 256:(b + 1) * 256]
             assert bmin[b] == blk.min() and bmax[b] == blk.max()
-        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True)
+        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True, method=method)
         D = Odom.dominance_matrix(F[perm])                      # D[i][j]: i dominates j (position space)
         dense = np_(M.dominance.unpack_bits(bits, R))
         for j in range(R):
@@ -154,7 +161,8 @@ def test_sorted_path_bits(M):
         assert np.array_equal(np_(hasdom).astype(bool), D.any(axis=0))
 
 
-def test_sorted_bits_bucket_straddling_fast_tile(M):
+@pytest.mark.parametrize("method", ["ranked", "pairwise"])
+def test_sorted_bits_bucket_straddling_fast_tile(M, method):
     """A S-bucket straddling a block boundary whose tile is fast: the i rows' words of the later block
     lie below wend and must be written (zeros), not left stale (regression: stale bits from the previous
     generation made the peel see phantom dominators)."""
@@ -173,7 +181,7 @@ def test_sorted_bits_bucket_straddling_fast_tile(M):
         we = np_(ps["wend"])
         bmin, bmax = np_(ps["blkmin"]), np_(ps["blkmax"])
         hit += int(we[255] > 8 and bmax[0] < bmin[1])
-        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True)
+        bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True, method=method)
         D = Odom.dominance_matrix(F[perm])
         dense = np_(M.dominance.unpack_bits(bits, R))
         for j in range(R):
@@ -182,6 +190,38 @@ def test_sorted_bits_bucket_straddling_fast_tile(M):
         r = np_(M.dominance.non_dominated_sort(F, stop_at=R // 2))
         assert np.array_equal(r, Odom.non_dominated_sort(F, stop_at=R // 2))
     assert hit > 0, "construction never produced a straddling fast tile"
+
+
+def test_ranked_bits_nan_rows(M):
+    """A row with a NaN objective dominates nothing and is dominated by nothing (the oracle's
+    (A <= B).all() & (A < B).any() with IEEE compares); the rank-mask kernel keeps that."""
+    rs = np.random.default_rng(9)
+    F = rs.integers(0, 3, size=(700, 4)).astype(np.float32)
+    F[rs.random((700, 4)) < 0.02] = np.nan
+    ps = M.dominance.presort(F)
+    perm = np_(ps["perm"])
+    we = np_(ps["wend"])
+    bits, hasdom = M.dominance.dominance_bits_sorted(ps, poison=True, method="ranked")
+    D = Odom.dominance_matrix(F[perm])
+    dense = np_(M.dominance.unpack_bits(bits, 700))
+    for j in range(700):
+        lim = min(700, we[j] * 32)
+        assert np.array_equal(dense[:lim, j], D[:lim, j]), j
+
+
+def test_ranked_bits_large_many_blocks(M):
+    """Multi-block sweep (items spanning several J blocks), C3-like m = 10 and a tie-heavy m = 5."""
+    rs = np.random.default_rng(21)
+    for F in (rs.random((9000, 10)).astype(np.float32),
+              (np.round(rs.random((7000, 5)) * 6) / 6).astype(np.float32)):
+        R = F.shape[0]
+        ps = M.dominance.presort(F)
+        a, ha = M.dominance.dominance_bits_sorted(ps, method="ranked")
+        b, hb = M.dominance.dominance_bits_sorted(ps, method="pairwise")
+        we = torch.as_tensor(np_(ps["wend"])).cuda().long()
+        cols = torch.arange(a.shape[1], device="cuda")[None, :]
+        live = cols < we[:, None]
+        assert torch.equal(a[live], b[live]) and torch.equal(ha, hb)
 
 
 def test_nds_bit_exact(M):
@@ -285,7 +325,7 @@ def test_associate_bit_exact(M, seed, R, m, w_target):
     Fn, *_ = Oniche.normalize_objectives(F, np.full(m, np.inf, np.float32), cand, pos_pop)
     pi, d = Oniche.associate_canonical(Fn, zh, pos_ref, np.flatnonzero(cand))
     Fn_in = np.where(cand[:, None], Fn, 0).astype(np.float32)
-    gpi, gd = M.niche.associate(Fn_in, zh, ranks.astype(np.int32), sp.l, seed, gen)
+    gpi, gd = M.niche.associate_canonical(Fn_in, zh, ranks.astype(np.int32), sp.l, seed, gen)
     assert np.array_equal(np_(gpi)[cand], pi[cand])
     assert np.array_equal(np_(gd)[cand], d[cand])
     assert (np_(gpi)[~cand] == -1).all()
