@@ -10,8 +10,11 @@
   written atomically (temp file + rename).
 * :func:`summarize` -- per fingerprint: mean, standard deviation and 95 % t-interval of the final IGD /
   HV and of the per-generation runtime (generation 1 excluded: one-time setup).
-* ``compare_backends`` of the reference times the batched against the scalar Alg. 1 back-end; the Alg. 1
-  back-end is CPU test infrastructure here (oracle/), so this harness does not offer it.
+* :func:`compare_backends` -- SPEC.md:686-694 (Table I's analogue): per population size, the mean
+  per-generation time of two back-ends on identical seeds and their ratio.  "batched" is this package's
+  GPU engine; the scalar Alg. 1 back-end ("oracle") is the CPU restatement under ``oracle/`` -- test
+  infrastructure that the product path never calls -- and is only *timed* here, loaded lazily by
+  module name (``MANYOBJ_ORACLE``, default ``oracle.manyobj_ref.engine``) when a comparison names it.
 """
 import csv
 import dataclasses
@@ -179,4 +182,78 @@ def summarize(path):
     return out
 
 
-__all__ = ["ExperimentPlan", "COLUMNS", "fingerprint", "run_plan", "write_rows", "read_rows", "summarize"]
+# ------------------------------------------------------------------ compare_backends
+
+def _gpu_backend(cfg, generations):
+    """Per-generation seconds of the GPU engine (generation 1 excluded: one-time setup)."""
+    import torch
+
+    from . import engine
+    state = engine.initialize(cfg)
+    per = []
+    for _ in range(generations):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        state = engine.step(state)
+        state.engine.check_errors(block=True)
+        per.append(time.perf_counter() - t0)
+    return per
+
+
+def _cpu_backend(niching):
+    def run(cfg, generations):
+        import importlib
+        O = importlib.import_module(os.environ.get("MANYOBJ_ORACLE", "oracle.manyobj_ref.engine"))
+        ocfg = O.RunConfig(problem=cfg.problem, n=cfg.n, m=cfg.m, d=cfg.d, generations=generations,
+                           seed=cfg.seed, backend=niching)
+        st = O.initialize(ocfg)
+        per = []
+        for _ in range(generations):
+            t0 = time.perf_counter()
+            st = O.step(st, ocfg)
+            per.append(time.perf_counter() - t0)
+        return per
+    return run
+
+
+BACKENDS = {"batched": _gpu_backend,
+            # the CPU restatements (timing only): Alg. 1 scalar niching, and the batched CPU loop
+            "oracle": _cpu_backend("oracle"),
+            "batched-cpu": _cpu_backend("batched")}
+
+
+def compare_backends(problem="DTLZ2", m=3, d=12, sizes=(92,), reps=1, generations=5,
+                     backends=("batched", "oracle"), seed=0):
+    """for each population size, the mean per-generation time (generation 1 excluded)
+    of ``backends[0]`` and ``backends[1]`` over ``reps`` identical-seed runs (seeds seed..seed+reps-1),
+    and the ratio t(backends[1]) / t(backends[0]) (the speed-up of the first over the second).
+    Returns one row per size."""
+    from . import engine
+    if reps < 1 or generations < 2:
+        raise ConfigError("reps", "reps >= 1 and generations >= 2 (generation 1 is excluded)")
+    if len(backends) != 2 or any(b not in BACKENDS for b in backends):
+        raise ConfigError("backend", f"two of {sorted(BACKENDS)}")
+    if not sizes:
+        raise ConfigError("sizes", "at least one population size")
+    rows = []
+    for n in sizes:
+        times = {}
+        for b in backends:
+            per = []
+            for r in range(reps):
+                cfg = engine.RunConfig(problem=problem, n=int(n), m=m, d=d, generations=generations,
+                                       seed=seed + r)
+                engine.validate(cfg)
+                per.extend(BACKENDS[b](cfg, generations)[1:])
+            times[b] = _tci(per)
+        t0, t1 = times[backends[0]][0], times[backends[1]][0]
+        rows.append({"problem": problem, "m": m, "d": d, "n": int(n), "reps": reps,
+                     "generations": generations,
+                     f"s_per_gen_{backends[0]}": t0, f"ci95_{backends[0]}": times[backends[0]][2],
+                     f"s_per_gen_{backends[1]}": t1, f"ci95_{backends[1]}": times[backends[1]][2],
+                     "ratio": t1 / t0 if t0 > 0 else float("inf")})
+    return rows
+
+
+__all__ = ["ExperimentPlan", "COLUMNS", "fingerprint", "run_plan", "write_rows", "read_rows", "summarize",
+           "compare_backends", "BACKENDS"]

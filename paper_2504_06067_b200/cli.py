@@ -2,11 +2,13 @@
 
   python -m paper_2504_06067_b200.cli run --config plan.yaml --out results.csv [--seeds 0,1,2]
   python -m paper_2504_06067_b200.cli summarize results.csv
+  python -m paper_2504_06067_b200.cli compare --problem DTLZ2 --m 3 --d 12 --sizes 800,3200 [--reps 3]
 
 ``run`` reads an ExperimentPlan from a YAML key-value file (fields of bench.ExperimentPlan).  Exit
 code 0 on success; 2 for a bad configuration / input (ConfigError), 3 for any other failure.
-``compare`` (batched vs the scalar Alg. 1 back-end) is not offered: the Alg. 1 back-end is CPU test
-infrastructure in this package (oracle/).
+``compare`` prints one JSON row per population size: the GPU batched engine's mean
+per-generation time against the scalar Alg. 1 back-end (or ``--against batched-cpu``) and the ratio.
+The CPU back-ends are timed only; see bench.compare_backends.
 """
 import argparse
 import json
@@ -50,6 +52,15 @@ def main(argv=None):
     r.add_argument("--time-limit", type=float)
     s = sub.add_parser("summarize")
     s.add_argument("csv")
+    c = sub.add_parser("compare")
+    c.add_argument("--problem", default="DTLZ2")
+    c.add_argument("--m", type=int, default=3)
+    c.add_argument("--d", type=int, default=12)
+    c.add_argument("--sizes", default="92")
+    c.add_argument("--reps", type=int, default=1)
+    c.add_argument("--generations", type=int, default=5)
+    c.add_argument("--against", default="oracle")
+    c.add_argument("--seed", type=int, default=0)
     a = p.parse_args(argv)
     try:
         if a.cmd == "run":
@@ -61,6 +72,15 @@ def main(argv=None):
                 plan = dataclasses.replace(plan, time_limit_s=a.time_limit)
             from .bench import run_plan
             print(run_plan(plan))
+        elif a.cmd == "compare":
+            from .bench import compare_backends
+            try:
+                sizes = tuple(int(x) for x in a.sizes.split(","))
+            except ValueError:
+                raise ConfigError("sizes", f"comma-separated integers expected, got {a.sizes!r}") from None
+            for row in compare_backends(a.problem, a.m, a.d, sizes, a.reps, a.generations,
+                                        ("batched", a.against), a.seed):
+                print(json.dumps(row))
         else:
             from .bench import summarize
             print(json.dumps(summarize(a.csv), indent=1))

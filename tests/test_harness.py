@@ -84,3 +84,35 @@ def test_run_plan_end_to_end(tmp_path):
         assert (x["igd"], x["hv_raw"], x["hv_normalized"]) == (y["igd"], y["hv_raw"], y["hv_normalized"])
     s = H.summarize(plan.out)
     assert list(s.values())[0]["runs"] == 2
+
+
+def test_compare_backends_rows_and_self_ratio():
+    """one row per size; a back-end against itself -> ratio 1 +- noise (CPU back-ends)."""
+    rows = H.compare_backends("DTLZ2", 3, 12, sizes=(16, 40), reps=1, generations=3,
+                              backends=("oracle", "oracle"))
+    assert [r["n"] for r in rows] == [16, 40]
+    for r in rows:
+        assert r["s_per_gen_oracle"] > 0
+        assert r["ratio"] == 1.0          # same key: the same mean
+    rows = H.compare_backends("DTLZ2", 3, 12, sizes=(40,), reps=2, generations=3,
+                              backends=("batched-cpu", "oracle"))
+    assert len(rows) == 1 and 0.05 < rows[0]["ratio"] < 50
+    with pytest.raises(errors.ConfigError):
+        H.compare_backends(sizes=(40,), backends=("batched", "nope"))
+    with pytest.raises(errors.ConfigError):
+        H.compare_backends(sizes=(40,), generations=1)
+
+
+def test_cli_compare_bad_sizes(capsys):
+    from paper_2504_06067_b200 import cli
+    assert cli.main(["compare", "--sizes", "12,x"]) == 2
+
+
+@pytest.mark.gpu
+def test_compare_backends_gpu_vs_alg1():
+    """batched / oracle ratio at n = 3200, DTLZ2 m = 3 must be >= 5 (here: GPU engine vs
+    the scalar Alg. 1 CPU back-end)."""
+    rows = H.compare_backends("DTLZ2", 3, 12, sizes=(800, 3200), reps=1, generations=3,
+                              backends=("batched", "oracle"))
+    assert [r["n"] for r in rows] == [800, 3200]
+    assert rows[1]["ratio"] >= 5, rows
