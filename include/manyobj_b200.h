@@ -40,6 +40,11 @@ enum {
   MO_ERR_CUDA = 7        /* CUDA runtime failure (no reference analogue) */
 };
 
+/* Objective-count limits: the engine (mo_step) runs 2 <= m <= MO_MAX_M
+ * (Appendix D studies m = 4 ... 512); m <= 16 runs register-array
+ * kernels, 16 < m <= MO_MAX_M the runtime-m ("wide") kernels. */
+enum { MO_MAX_M = 512 };
+
 /* Problems (DTLZ1/4/6 per the standard suite). */
 enum { MO_DTLZ1 = 1, MO_DTLZ2, MO_DTLZ3, MO_DTLZ4, MO_DTLZ5, MO_DTLZ6, MO_DTLZ7 };
 
@@ -144,7 +149,8 @@ int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* 
                              uint32_t* bits, uint8_t* hasdom, void* stream_);
 
 /* Same bit-matrix and hasdom as mo_dominance_bits_sorted, by per-objective
- * rank masks (k_dom_rank.cu, the engine's kernel for 2 <= m <= 16): for every
+ * rank masks (k_dom_rank.cu, the engine's kernel for 2 <= m <= MO_MAX_M; m > 16
+ * streams the tables in chunks of 8 objectives): for every
  * 256-row block and objective, the sorted values (Eytzinger order) and the 257
  * prefix masks; a row's dominators in a block are the AND over objectives of
  * the prefix masks selected by m binary searches.  tables: device scratch of

@@ -46,22 +46,25 @@ __device__ __forceinline__ int mask_slot(int c, int h) { return 2 * c + (h ^ ((c
 
 // ------------------------------------------------------------------ tables
 // grid (nb, M): block bi, objective k.  vmask[bi*8 + w]: rows of block bi that exist and have no NaN.
+// M = 0: runtime m (the wide-m path, m > 16)
 template <int M>
 __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__ FS, int R,
-                                                        uint32_t* __restrict__ tables, uint32_t* __restrict__ vmask) {
+                                                        uint32_t* __restrict__ tables, uint32_t* __restrict__ vmask,
+                                                        int m_rt) {
   pdl_wait();
+  const int m = M > 0 ? M : m_rt;
   __shared__ uint32_t sKey[DR_BLK];
   __shared__ int sIdx[DR_BLK];
   const int bi = blockIdx.x, k = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int i = bi * DR_BLK + t;
-  const float x = i < R ? FS[(int64_t)i * M + k] : __int_as_float(0x7fc00000);
+  const float x = i < R ? FS[(int64_t)i * m + k] : __int_as_float(0x7fc00000);
   sKey[t] = x != x ? 0xffffffffu : f2ord(__fadd_rn(x, 0.0f));   // NaN last; -0 -> +0
   sIdx[t] = t;
   if (k == 0) {
     bool ok = i < R;
     if (ok)
-      for (int q = 0; q < M; ++q) {
-        const float v = FS[(int64_t)i * M + q];
+      for (int q = 0; q < m; ++q) {
+        const float v = FS[(int64_t)i * m + q];
         ok = ok && v == v;
       }
     const uint32_t bal = __ballot_sync(MO_FULL, ok);
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__
       __syncthreads();
     }
   }
-  uint32_t* tab = tables + ((int64_t)bi * M + k) * DR_TBL_WORDS;
+  uint32_t* tab = tables + ((int64_t)bi * m + k) * DR_TBL_WORDS;
   // Eytzinger: node n at depth d holds sorted position ((2 (n - 2^d) + 1) << (8 - d)) - 1
   for (int n = t; n < DR_EYT; n += DR_BLK) {
     float v = __int_as_float(0x7fc00000);
@@ -332,6 +335,179 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
   pdl_trigger();
 }
 
+// ------------------------------------------------------------ wide m (m > 16)
+//
+// The same rank-mask relation for any m (Appendix D: m up to 512): the m tables of block I do
+// not fit in shared memory, so each (I, J) tile walks the objectives in chunks of DRW_MC tables (one
+// bulk copy per chunk) and keeps the running AND of the prefix masks -- le (a_i <= b_j) and ge
+// (a_i >= b_j) -- in registers.  Output identical to k_dom_rank (same words, hasdom, zeroed straddle
+// words); objectives are visited in ascending order, so no result depends on the chunking.
+constexpr int DRW_MC = 8;
+
+__global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) {
+  pdl_wait();
+  extern __shared__ __align__(128) uint32_t sTab[];   // DRW_MC tables of block I
+  __shared__ __align__(8) uint64_t sBar;
+  __shared__ uint32_t sT[DR_BLK * 9];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) mbar_init(&sBar, 1);
+  __syncthreads();
+  unsigned parity = 0;
+  for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
+    int bi, bj0, bj1;
+    dr_decode(item, a.nb, a.ch, bi, bj0, bj1);
+    uint32_t vI[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) vI[w] = __ldg(a.vmask + (int64_t)bi * 8 + w);
+    const float smaxI = __ldg(a.blkmax + bi);
+    const int i0 = bi * DR_BLK;
+    for (int bj = bj0; bj < bj1; ++bj) {
+      const int j = bj * DR_BLK + tid;
+      const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
+      uint32_t le[8], ge[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        le[w] = 0xffffffffu;
+        ge[w] = vI[w];
+      }
+      bool jnan = false;
+      for (int k0 = 0; k0 < m; k0 += DRW_MC) {
+        const int mc = min(DRW_MC, m - k0);
+        __syncthreads();   // everyone is done with the previous chunk / item
+        if (tid == 0) {
+          mbar_expect_tx(&sBar, (unsigned)(mc * DR_TBL_BYTES));
+          bulk_g2s(sTab, a.tables + ((int64_t)bi * m + k0) * DR_TBL_WORDS, (unsigned)(mc * DR_TBL_BYTES), &sBar);
+        }
+        float b[DRW_MC];
+#pragma unroll
+        for (int q = 0; q < DRW_MC; ++q) {
+          b[q] = (j < a.R && q < mc) ? __ldg(a.FS + (int64_t)j * m + k0 + q) : 0.0f;
+          jnan = jnan || (b[q] != b[q]);
+        }
+        mbar_wait(&sBar, parity);
+        parity ^= 1u;
+#pragma unroll
+        for (int q = 0; q < DRW_MC; ++q) {
+          if (q < mc) {
+            const uint32_t* tab = sTab + q * DR_TBL_WORDS;
+            int node = 1, nd = 1;
+#pragma unroll
+            for (int st = 0; st < 9; ++st) {
+              const float e = __uint_as_float(tab[node]);
+              node = 2 * node + (e <= b[q] ? 1 : 0);
+              if (!fast) {
+                const float e2 = __uint_as_float(tab[nd]);
+                nd = 2 * nd + (e2 < b[q] ? 1 : 0);
+              }
+            }
+            const uint4* P = reinterpret_cast<const uint4*>(tab + DR_EYT);
+            {
+              const int c = node - DR_EYT;
+              const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+              le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
+              le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+            }
+            if (!fast) {
+              const int c = nd - DR_EYT;
+              const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+              ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
+              ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
+            }
+          }
+        }
+      }
+      uint32_t out[8];
+      if (fast) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) out[w] = le[w];
+      } else {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          if (jnan) ge[w] = 0u;
+          out[w] = le[w] & ~ge[w];
+        }
+        if (bi != bj) {
+          const bool jok = j < a.R;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const uint32_t rev = jok ? (ge[w] & ~le[w]) : 0u;
+            uint32_t mine = 0;
+#pragma unroll
+            for (int b2 = 0; b2 < 32; ++b2) {
+              const uint32_t bal = __ballot_sync(MO_FULL, (rev >> b2) & 1u);
+              mine = lane == b2 ? bal : mine;
+            }
+            sT[(w * 32 + lane) * 9 + warp] = mine;
+          }
+        }
+      }
+      if (j < a.R) {
+        uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)j * a.W + (int64_t)bi * 8);
+        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+        if ((out[0] | out[1] | out[2] | out[3] | out[4] | out[5] | out[6] | out[7]) != 0u) a.hasdom[j] = 1;
+      }
+      if (fast) {
+        const int ilast = min(a.R, i0 + DR_BLK) - 1;
+        if (__ldg(a.wend + ilast) > bj * 8) {
+          const int i = i0 + tid;
+          if (i < a.R && __ldg(a.wend + i) > bj * 8) {
+            uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
+            dst[0] = make_uint4(0u, 0u, 0u, 0u);
+            dst[1] = make_uint4(0u, 0u, 0u, 0u);
+          }
+        }
+      } else if (bi != bj) {
+        __syncthreads();
+        const int i = i0 + tid;
+        if (i < a.R) {
+          const uint32_t* sw = sT + tid * 9;
+          uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
+          dst[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
+          dst[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
+          if ((sw[0] | sw[1] | sw[2] | sw[3] | sw[4] | sw[5] | sw[6] | sw[7]) != 0u) a.hasdom[i] = 1;
+        }
+      }
+    }
+  }
+  pdl_trigger();
+}
+
+static int launch_dom_rank_wide(const float* FS, const float* blkmin, const float* blkmax, const int* wend,
+                                int64_t R, int m, uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+  const int nb = (int)dom_rank_blocks(R);
+  uint32_t* vmask = tables + (int64_t)nb * m * DR_TBL_WORDS;
+  MO_TRY(launch_ex(k_dom_tables<0>, dim3(nb, m), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, m));
+  const size_t smem = (size_t)DRW_MC * DR_TBL_BYTES;
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    if (cudaFuncSetAttribute(k_dom_rank_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return MO_ERR_CUDA;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dom_rank_wide, DR_BLK, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  DomRankArgs a;
+  a.FS = FS;
+  a.blkmin = blkmin;
+  a.blkmax = blkmax;
+  a.wend = wend;
+  a.tables = tables;
+  a.vmask = vmask;
+  a.bits = bits;
+  a.hasdom = hasdom;
+  a.R = (int)R;
+  a.nb = nb;
+  a.ch = 1;   // one (I, J) tile per item: every tile re-streams block I's m tables anyway
+  a.W = words_per_row(R);
+  a.items = (int64_t)nb * (nb + 1) / 2;
+  const int64_t slots = (int64_t)sms * per_sm;
+  const int64_t grid = a.items < slots ? a.items : slots;
+  return launch_ex(k_dom_rank_wide, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a, m);
+}
+
 size_t dom_rank_tables_bytes(int64_t R, int m) {
   const int64_t nb = dom_rank_blocks(R);
   return (size_t)nb * (size_t)m * DR_TBL_BYTES + (size_t)nb * 8 * 4 + 256;
@@ -342,7 +518,7 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
                              uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
   const int nb = (int)dom_rank_blocks(R);
   uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
-  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask));
+  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M));
   const size_t smem = (size_t)M * DR_TBL_BYTES;
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
@@ -392,6 +568,8 @@ int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, c
     MO_DR_CASE(16)
 #undef MO_DR_CASE
     default:
+      if (m > 16 && m <= MO_MAX_M)
+        return launch_dom_rank_wide(FS, blkmin, blkmax, wend, R, m, bits, hasdom, tables, s);
       return MO_ERR_PARAM;
   }
 }

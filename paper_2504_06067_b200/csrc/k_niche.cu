@@ -31,7 +31,6 @@
 namespace mo {
 
 constexpr int MAXM = 64;
-constexpr int PREP_MAXM = 16;   // k_prep phase-1 instantiations (MO_PX_CASE)
 constexpr float ASF_EPS = 1e-6f;
 constexpr double DEGENERATE = 1e-10;
 
@@ -139,6 +138,146 @@ __device__ void gauss_solve_warp(double* A, double* rhs, int m, int* singular) {
   __syncwarp();
 }
 
+// gauss_solve with a whole block (wide m, 32 < m <= MO_MAX_M): the same operations on the same elements
+// as the one-thread version -- pivot = first row with the strictly largest |A[r][c]|; every multiplier
+// f_r = A[r][c] / A[c][c] is taken from the unchanged column before the rows are updated; each element
+// A[r][q] - f_r * A[c][q] and rhs[r] - f_r * rhs[c] is rounded once per operation (-fmad=false) -- so
+// the solution is bit-identical; back substitution forms the products in parallel and subtracts them
+// in the sequential order (q ascending) on one thread.  sF: shared scratch of m doubles.
+__device__ void gauss_solve_block(double* A, double* rhs, int m, int* singular, double* sF) {
+  __shared__ double sV[32];
+  __shared__ int sP[32];
+  __shared__ int sPiv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = (blockDim.x + 31) >> 5;
+  for (int c = 0; c < m; ++c) {
+    double v = -1.0;
+    int p = 0x7fffffff;
+    for (int r = c + tid; r < m; r += blockDim.x) {
+      const double x = fabs(A[(int64_t)r * m + c]);
+      if (x > v) {
+        v = x;
+        p = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double vo = __shfl_xor_sync(MO_FULL, v, o);
+      const int po = __shfl_xor_sync(MO_FULL, p, o);
+      if (vo > v || (vo == v && po < p)) {
+        v = vo;
+        p = po;
+      }
+    }
+    if (lane == 0) {
+      sV[warp] = v;
+      sP[warp] = p;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = sV[0];
+      int bp = sP[0];
+      for (int q = 1; q < nw; ++q)
+        if (sV[q] > bv || (sV[q] == bv && sP[q] < bp)) {
+          bv = sV[q];
+          bp = sP[q];
+        }
+      sPiv = bv == 0.0 ? -1 : bp;
+    }
+    __syncthreads();
+    const int piv = sPiv;
+    if (piv < 0) {
+      if (tid == 0) *singular = 1;
+      __syncthreads();
+      return;
+    }
+    if (piv != c) {
+      for (int q = tid; q < m; q += blockDim.x) {
+        const double t = A[(int64_t)c * m + q];
+        A[(int64_t)c * m + q] = A[(int64_t)piv * m + q];
+        A[(int64_t)piv * m + q] = t;
+      }
+      if (tid == 0) {
+        const double t = rhs[c];
+        rhs[c] = rhs[piv];
+        rhs[piv] = t;
+      }
+      __syncthreads();
+    }
+    const double acc = A[(int64_t)c * m + c];
+    for (int r = c + 1 + tid; r < m; r += blockDim.x) sF[r] = A[(int64_t)r * m + c] / acc;
+    __syncthreads();
+    const int cols = m - c;
+    const int64_t cells = (int64_t)(m - c - 1) * cols;
+    for (int64_t e = tid; e < cells; e += blockDim.x) {
+      const int r = c + 1 + (int)(e / cols), q = c + (int)(e % cols);
+      A[(int64_t)r * m + q] = A[(int64_t)r * m + q] - sF[r] * A[(int64_t)c * m + q];
+    }
+    for (int r = c + 1 + tid; r < m; r += blockDim.x) rhs[r] = rhs[r] - sF[r] * rhs[c];
+    __syncthreads();
+  }
+  for (int c = m - 1; c >= 0; --c) {
+    for (int q = c + 1 + tid; q < m; q += blockDim.x) sF[q] = A[(int64_t)c * m + q] * rhs[q];
+    __syncthreads();
+    if (tid == 0) {
+      double s = rhs[c];
+      for (int q = c + 1; q < m; ++q) s = s - sF[q];
+      rhs[c] = s / A[(int64_t)c * m + c];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *singular = 0;
+  __syncthreads();
+}
+
+// phase 1 of k_prep for runtime m (wide m > 16): the same keys and column maxima as prep_extremes<M>.
+// The ASF of axis ax is max(ft[ax], max_{k != ax} q[k]) (fmaxf: exact, NaN-ignoring, order-free), so
+// one pass finds the largest q and the largest q outside its index and every axis takes one of them.
+__device__ __forceinline__ void prep_extremes_rt(const PrepArgs& a, int R, int l, int gthreads, bool build_cand,
+                                                 int m) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
+    const int row = base + tid;
+    const bool act = row < R && a.ranks[row] >= 0 && a.ranks[row] <= l;
+    if (build_cand) {
+      const int slot = warp_alloc(a.ctl, act ? 1 : 0);
+      if (act) a.cand[slot] = row;
+    }
+    const float* f = a.F + (int64_t)(act ? row : 0) * m;
+    int pp = 0;
+    float top1 = __int_as_float(0x7fc00000), top2 = top1;
+    int i1 = -1;
+    if (act) {
+      pp = __ldcg(a.pos_pop + row);
+      for (int k = 0; k < m; ++k) {
+        const float q = __fdiv_rn(__fsub_rn(f[k], __ldcg(a.ideal + k)), ASF_EPS);
+        if (q > top1 || top1 != top1) {          // new maximum (NaN q never enters)
+          if (q == q) {
+            top2 = top1;
+            top1 = q;
+            i1 = k;
+          }
+        } else {
+          top2 = fmaxf(top2, q);
+        }
+      }
+    }
+    for (int k = 0; k < m; ++k) {
+      uint32_t v = act ? f2ord(__fsub_rn(f[k], __ldcg(a.ideal + k))) : 0u;
+      v = warp_max_u32(v);
+      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
+    }
+    for (int ax = 0; ax < m; ++ax) {
+      unsigned long long key = ~0ull;
+      if (act) {
+        const float s = fmaxf(__fsub_rn(f[ax], __ldcg(a.ideal + ax)), ax == i1 ? top2 : top1);
+        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+      }
+      key = warp_min_u64(key);
+      if (lane == 0 && key != ~0ull) atomicMax(&a.ext_key[ax], ~key);
+    }
+  }
+}
+
 // phase 1 of k_prep for m = M (register arrays): ASF extreme-point keys and column maxima of the
 // translated candidate rows (rank in [0, l]), merged by warp reductions + one atomic per warp.  The keys
 // are stored complemented (atomicMax of ~key: 0 is neutral, so a zeroed workspace needs no reset node;
@@ -194,12 +333,18 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   __shared__ uint32_t sKp[MAX_SHUFFLE_ROUNDS], sSp[MAX_SHUFFLE_ROUNDS], sKr[MAX_SHUFFLE_ROUNDS],
       sSr[MAX_SHUFFLE_ROUNDS];
   __shared__ int sRp, sRr;
-  __shared__ float sMin[MAXM];
+  __shared__ float sMin0[MAXM];
   __shared__ double sA[MAXM * MAXM];
-  __shared__ double sRhs[MAXM];
+  __shared__ double sRhs0[MAXM];
   const int tid = threadIdx.x, lane = tid & 31;
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int R = a.R, m = a.m, w = a.w;
+  // m > MAXM (wide): the system lives in global memory (a.solveA) and sA's shared bytes hold the
+  // per-objective vectors instead (MO_MAX_M doubles each)
+  static_assert(MAXM * MAXM >= 3 * MO_MAX_M, "wide-m scratch must fit in sA");
+  const bool big = m > MAXM;
+  float* sMin = big ? reinterpret_cast<float*>(sA) : sMin0;
+  double* sRhs = big ? sA : sRhs0;
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   const int l = __ldcg(a.info + MO_INFO_L);
   const bool skipped = __ldcg(a.info + MO_INFO_SKIPPED) != 0;
@@ -240,9 +385,9 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
       if (c) a.cand[slot] = i;
     }
     if (a.mode != PREP_FULL) return;
-    if (gtid < m) {
-      a.ext_key[gtid] = 0ull;
-      a.colmax[gtid] = 0u;
+    for (int k = gtid; k < m; k += gthreads) {
+      a.ext_key[k] = 0ull;
+      a.colmax[k] = 0u;
     }
     grid_sync(a.bar);
   }
@@ -256,7 +401,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
     MO_PX_CASE(15) MO_PX_CASE(16)
 #undef MO_PX_CASE
-    default: __trap();   // unreachable: launch_prep rejects m outside [1, PREP_MAXM]
+    default: prep_extremes_rt(a, R, l, gthreads, fused, m);   // wide m (launch_prep: m <= MO_MAX_M)
   }
   // phase 2 runs in the last block to finish phase 1
   if (!grid_last(a.bar)) return;
@@ -266,12 +411,14 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   // ---- phase 2: hyperplane solve (one warp) on the extreme rows loaded by the block,
   //      per-component fallbacks
   {
-    __shared__ double sFb[MAXM];
+    __shared__ double sFb0[MAXM], sGF0[MAXM];
+    double* sFb = big ? sA + MO_MAX_M : sFb0;
+    double* A = big ? a.solveA : sA;
     for (int e = tid; e < m * m; e += blockDim.x) {
       const int r = e / m, c = e - r * m;
       const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
       const int row = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
-      sA[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
+      A[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
     }
     for (int k = tid; k < m; k += blockDim.x) {
       const double mx = (double)ord2f(__ldcg(a.colmax + k));
@@ -280,20 +427,19 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     }
     __syncthreads();
     trace_mark_any(a.trace, 20);
-    if (tid < m) {   // every reader of this generation's keys is done: neutral values for the next launch
-      a.ext_key[tid] = 0ull;
-      a.colmax[tid] = 0u;
+    for (int k = tid; k < m; k += blockDim.x) {   // every reader of this generation's keys is done:
+      a.ext_key[k] = 0ull;                        // neutral values for the next launch
+      a.colmax[k] = 0u;
     }
     __shared__ int sSing;
-    if (tid < 32) {
-      if (tid == 0) sSing = 0;
-      __syncwarp();
-      if (ncand == 0) {
-        if (tid == 0) sSing = 1;
-      } else if (m <= 32) {
-        gauss_solve_warp(sA, sRhs, m, &sSing);
-      } else if (tid == 0) {
-        gauss_solve(sA, sRhs, m, &sSing);
+    if (tid == 0) sSing = ncand == 0 ? 1 : 0;
+    __syncthreads();
+    if (ncand != 0) {
+      if (m <= 32) {
+        if (tid < 32) gauss_solve_warp(A, sRhs, m, &sSing);
+      } else {
+        // multipliers: sGF0 when the system is in shared memory (m <= 64), else sA after sRhs / sFb
+        gauss_solve_block(A, sRhs, m, &sSing, big ? sA + 2 * MO_MAX_M : sGF0);
       }
     }
     __syncthreads();
@@ -437,6 +583,81 @@ __global__ void __launch_bounds__(ASSOC_THREADS) k_assoc(AssocArgs a) {
   }
 }
 
+
+// Wide m (16 < m <= MO_MAX_M): the same canonical keys, tie rule and atomicMax merge as k_assoc with a
+// runtime objective count.  Item = (16 candidate rows, a split of the reference positions); the rows'
+// normalised objectives sit in shared memory (read as broadcasts), each thread walks the split's points
+// p = p0 + tid, p0 + tid + 256, ... (ascending, strict '>': its first maximum) reading the objective-major
+// directions zsT[k * w + p] (coalesced), 16 running keys in registers.
+constexpr int ASSOCW_ROWS = 16;
+
+__global__ void __launch_bounds__(ASSOC_THREADS) k_assoc_wide(AssocArgs a, int m) {
+  pdl_wait();
+  extern __shared__ float sFw[];   // ASSOCW_ROWS x m
+  __shared__ int sRow[ASSOCW_ROWS];
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int nrt = (ncand + ASSOCW_ROWS - 1) / ASSOCW_ROWS;
+  const int wr = a.zend - a.zbeg;
+  if (nrt == 0 || wr <= 0) return;
+  int splits = (4 * (int)gridDim.x + nrt - 1) / nrt;
+  const int maxsplit = (wr + ASSOC_THREADS - 1) / ASSOC_THREADS;
+  splits = splits < 1 ? 1 : (splits > maxsplit ? maxsplit : splits);
+  const int psplit = (wr + splits - 1) / splits;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int item = blockIdx.x; item < nrt * splits; item += gridDim.x) {
+    const int rbase = (item / splits) * ASSOCW_ROWS;
+    const int p0 = a.zbeg + (item % splits) * psplit, p1 = min(a.zend, p0 + psplit);
+    __syncthreads();   // previous item done with sFw / sRow
+    if (tid < ASSOCW_ROWS) sRow[tid] = rbase + tid < ncand ? __ldcg(a.cand + rbase + tid) : -1;
+    for (int e = tid; e < ASSOCW_ROWS * m; e += ASSOC_THREADS) {
+      const int r = e / m, k = e - r * m;
+      const int c = rbase + r;
+      float v = 0.0f;
+      if (c < ncand) {
+        const int row = __ldcg(a.cand + c);
+        v = a.F[(int64_t)row * m + k];
+        if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+        if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+      }
+      sFw[e] = v;
+    }
+    __syncthreads();
+    float best[ASSOCW_ROWS];
+    int bp[ASSOCW_ROWS];
+#pragma unroll
+    for (int r = 0; r < ASSOCW_ROWS; ++r) {
+      best[r] = -__int_as_float(0x7f800000);
+      bp[r] = p0;
+    }
+    for (int p = p0 + tid; p < p1; p += ASSOC_THREADS) {
+      float t[ASSOCW_ROWS];
+      {
+        const float z = __ldg(a.zsT + p);
+#pragma unroll
+        for (int r = 0; r < ASSOCW_ROWS; ++r) t[r] = __fmul_rn(sFw[r * m], z);
+      }
+      for (int k = 1; k < m; ++k) {
+        const float z = __ldg(a.zsT + (int64_t)k * a.w + p);
+#pragma unroll
+        for (int r = 0; r < ASSOCW_ROWS; ++r) t[r] = __fadd_rn(t[r], __fmul_rn(sFw[r * m + k], z));
+      }
+#pragma unroll
+      for (int r = 0; r < ASSOCW_ROWS; ++r)
+        if (t[r] > best[r]) {
+          best[r] = t[r];
+          bp[r] = p;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < ASSOCW_ROWS; ++r) {
+      unsigned long long key = ((unsigned long long)f2ord(best[r]) << 32) | (uint32_t)(0xffffffffu - (uint32_t)bp[r]);
+      key = warp_max_u64(key);
+      if (lane == 0 && sRow[r] >= 0) atomicMax(&a.akey[sRow[r]], key);
+    }
+  }
+}
 
 // ------------------------------------------------- lattice-pruned association
 //
@@ -957,6 +1178,51 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
   }
 }
 
+// k_assoc_final for runtime m (wide m > 16): identical arithmetic, objectives re-read from F (L1)
+__global__ void k_assoc_final_rt(AssocFinalArgs a) {
+  pdl_wait();
+  if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
+  if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
+  const int ncand = __ldcg(a.ctl);
+  const int base = blockIdx.x * blockDim.x;
+  if (base >= ncand) return;
+  const int c = base + threadIdx.x;
+  const bool act = c < ncand;
+  const int m = a.m;
+  const int row = act ? __ldcg(a.cand + c) : 0;
+  auto fn = [&](int k) {
+    float v = a.F[(int64_t)row * m + k];
+    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+    return v;
+  };
+  if (act && a.Fn_out)
+    for (int k = 0; k < m; ++k) a.Fn_out[(int64_t)row * m + k] = fn(k);
+  if (a.fn_only) return;
+  int j = 0;
+  if (act) {
+    const unsigned long long key = __ldcg(a.akey + row);
+    const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
+    const float* z = a.zs + (int64_t)p * m;
+    float t = __fmul_rn(fn(0), z[0]);
+    for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn(k), z[k]));
+    float s2 = 0.0f;
+    for (int k = 0; k < m; ++k) {
+      const float e = __fsub_rn(fn(k), __fmul_rn(t, z[k]));
+      s2 = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s2, __fmul_rn(e, e));
+    }
+    j = a.perm_ref[p];
+    a.pi[row] = j;
+    a.d[row] = __fsqrt_rn(s2);
+  }
+  if (a.ranks) {
+    const int l = __ldcg(a.info + MO_INFO_L);
+    const int r = act ? a.ranks[row] : -1;
+    warp_agg_add(a.rho, j, act && r < l);
+    warp_agg_add(a.rho_p, j, act && r == l);
+  }
+}
+
 // --------------------------------------------------------------- select
 
 
@@ -1300,8 +1566,9 @@ int select_grid_blocks() {
 }
 
 int launch_prep(const PrepArgs& a, cudaStream_t s) {
-  // phase 1 (extreme points) is instantiated for m = 1..PREP_MAXM only
-  if (a.m < 1 || a.m > MAXM || (a.mode == PREP_FULL && a.m > PREP_MAXM)) return MO_ERR_PARAM;
+  // phase 1 (extreme points): register arrays for m <= 16 (MO_PX_CASE), the runtime-m pass above; m > MAXM
+  // needs the global system buffer
+  if (a.m < 1 || a.m > MO_MAX_M || (a.mode == PREP_FULL && a.m > MAXM && !a.solveA)) return MO_ERR_PARAM;
   if (!a.in_step) {
     if (cudaMemsetAsync(a.ctl, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
     if (cudaMemsetAsync(a.bar, 0, 2 * sizeof(unsigned), s) != cudaSuccess) return MO_ERR_CUDA;
@@ -1344,8 +1611,18 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     MO_AS_CASE(15)
     MO_AS_CASE(16)
 #undef MO_AS_CASE
-    default:
-      return MO_ERR_PARAM;
+    default: {
+      if (m > MO_MAX_M || !a.zsT) return MO_ERR_PARAM;
+      const size_t smem = (size_t)ASSOCW_ROWS * m * sizeof(float);
+      static bool attr = false;
+      if (!attr) {
+        if (cudaFuncSetAttribute(k_assoc_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 ASSOCW_ROWS * MO_MAX_M * (int)sizeof(float)) != cudaSuccess)
+          return MO_ERR_CUDA;
+        attr = true;
+      }
+      MO_TRY(launch_ex(k_assoc_wide, grid, dim3(ASSOC_THREADS), smem, s, false, g_mo_pdl, b, m));
+    }
   }
   MO_CHECK_LAUNCH();
   return MO_OK;
@@ -1443,7 +1720,9 @@ int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
     MO_AF_CASE(8) MO_AF_CASE(9) MO_AF_CASE(10) MO_AF_CASE(11) MO_AF_CASE(12) MO_AF_CASE(13) MO_AF_CASE(14)
     MO_AF_CASE(15) MO_AF_CASE(16)
 #undef MO_AF_CASE
-    default: return MO_ERR_PARAM;
+    default:
+      if (a.m > MO_MAX_M) return MO_ERR_PARAM;
+      return launch_ex(k_assoc_final_rt, grid, blk, 0, s, false, g_mo_pdl, a);
   }
 }
 

@@ -52,6 +52,10 @@ struct PrepArgs {
   int* mate;
   int pro_done;    // gen_prologue already ran (in k_vary_eval): only the candidate list in phase 0
   int ideal_done;  // the running ideal was already lowered by the offspring (k_vary_eval)
+  // wide m (m > 16; nullable otherwise): the FP64 hyperplane system when m > 64 (m x m, global) and the
+  // objective-major copy of the shuffled directions, zsT[k * w + p] (written by gen_prologue)
+  double* solveA;
+  float* zsT;
 };
 
 constexpr int LVL_BINS = 1024;
@@ -83,6 +87,7 @@ struct AssocArgs {
   // tensor-core filter (k_assoc_hmma): bf16 hi/lo fragments of the unit directions in static reference
   // order (mo_pack_refs_bf16); nullptr = FP32 full scan only
   const uint2* zfrag;
+  const float* zsT;      // wide m: m x w objective-major shuffled directions (k_assoc_wide)
 };
 
 struct AssocFinalArgs {

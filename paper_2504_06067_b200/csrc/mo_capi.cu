@@ -40,7 +40,7 @@ constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/h
 
 struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
-      colmax, icpt, a32, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
+      colmax, icpt, a32, solve, zsT, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
       lvl, sctl, mate, dtab, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
@@ -73,10 +73,15 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.zs = bump(c, (size_t)w * m * 4);
   L.cand = bump(c, (size_t)R * 4);
   L.ctl = bump(c, 64 * 4);
-  L.ext_key = bump(c, 64 * 8);
-  L.colmax = bump(c, 64 * 4);
-  L.icpt = bump(c, 64 * 8);
-  L.a32 = bump(c, 64 * 4);
+  const int64_t mm = m > 64 ? m : 64;   // per-objective slots (wide m: up to MO_MAX_M)
+  L.ext_key = bump(c, (size_t)mm * 8);
+  L.colmax = bump(c, (size_t)mm * 4);
+  L.icpt = bump(c, (size_t)mm * 8);
+  L.a32 = bump(c, (size_t)mm * 4);
+  // wide m: the FP64 hyperplane system (m > 64 does not fit k_prep's shared arrays) and the
+  // objective-major copy of the shuffled directions read by k_assoc_wide
+  L.solve = bump(c, m > 64 ? (size_t)m * m * 8 : 0);
+  L.zsT = bump(c, m > 16 ? (size_t)w * m * 4 : 0);
   L.akey = bump(c, (size_t)R * 8);
   L.pi = bump(c, (size_t)R * 4);
   L.d = bump(c, (size_t)R * 4);
@@ -111,8 +116,8 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.sctl = bump(c, 16 * 4);
   L.mate = bump(c, (size_t)(R + 16) * 4);   // [0..7] two tags, [8] counter, [16..): two n-slot mating buffers
   // rank-mask dominance tables (k_dom_rank.cu): per 256-row block and objective, Eytzinger values +
-  // prefix masks (bit-matrix sort, 2 <= m <= 16)
-  L.dtab = bump(c, sort_mode == MO_SORT_BITS && m >= 2 && m <= 16 ? dom_rank_tables_bytes(R, m) : 0);
+  // prefix masks (bit-matrix sort, 2 <= m <= MO_MAX_M)
+  L.dtab = bump(c, sort_mode == MO_SORT_BITS && m >= 2 && m <= MO_MAX_M ? dom_rank_tables_bytes(R, m) : 0);
   // streamed / sharded sort (sort_mode == MO_SORT_STREAM)
   const bool st = sort_mode == MO_SORT_STREAM;
   const int64_t nb = ceil_div(R, STREAM_BLK);
@@ -204,6 +209,8 @@ static PrepArgs prep_args(const Layout& L, void* ws, const float* F, int64_t R, 
   a.pro_done = 0;
   a.ideal_done = 0;
   a.mate = at<int>(ws, L.mate);
+  a.solveA = m > 64 ? at<double>(ws, L.solve) : nullptr;
+  a.zsT = m > 16 && zhat ? at<float>(ws, L.zsT) : nullptr;
   return a;
 }
 
@@ -293,7 +300,7 @@ static PresortArgs presort_args(const mo_step_args* a, const Layout& L) {
   return ps;
 }
 
-// rank-mask dominance (k_dom_rank.cu) for 2 <= m <= 16; MO_DOM_PAIRWISE=1 selects the pairwise
+// rank-mask dominance (k_dom_rank.cu) for 2 <= m <= MO_MAX_M; MO_DOM_PAIRWISE=1 selects the pairwise
 // compare-chain tiles (k_dom_tile_sorted) instead
 static bool use_dom_rank(int m) {
   static int off = -1;
@@ -301,7 +308,7 @@ static bool use_dom_rank(int m) {
     const char* e = getenv("MO_DOM_PAIRWISE");
     off = (e && e[0] == '1') ? 1 : 0;
   }
-  return !off && m >= 2 && m <= 16;
+  return (!off || m > 16) && m >= 2 && m <= MO_MAX_M;   // the pairwise tiles stop at m = 16
 }
 
 static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
@@ -385,6 +392,7 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.fb_ctl = at<int>(ws, L.fctl);
   aa.in_step = 1;
   aa.zfrag = reinterpret_cast<const uint2*>(a->zhat_frag);
+  aa.zsT = pa.zsT;
   if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
   else if (use_hmma(aa, m))
@@ -546,7 +554,8 @@ static int check_stream(const mo_step_args* a, Layout& L) {
 
 static int check_step_args(const mo_step_args* a) {
   if (a == nullptr) return MO_ERR_PARAM;
-  if (a->n < 2 || (a->n & 1) || a->m < 2 || a->m > 16 || a->d < a->m || a->w < 1) return MO_ERR_PARAM;
+  if (a->n < 2 || (a->n & 1) || a->m < 2 || a->m > MO_MAX_M || a->d < a->m || a->w < 1) return MO_ERR_PARAM;
+  if (a->m > 16 && a->sort_mode != MO_SORT_BITS) return MO_ERR_PARAM;   // streamed kernels: m <= 16
   if (2 * a->n > (int64_t)0x7fffffff || a->w > (int64_t)0x7fffffff) return MO_ERR_PARAM;
   if (!a->zhat || !a->XR || !a->FR || !a->X_next || !a->F_next || !a->ideal || !a->ranks || !a->info)
     return MO_ERR_PARAM;
@@ -662,13 +671,13 @@ int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* 
 }
 
 size_t mo_dominance_tables_bytes(int64_t R, int32_t m) {
-  return (R < 1 || m < 2 || m > 16) ? 0 : dom_rank_tables_bytes(R, m);
+  return (R < 1 || m < 2 || m > MO_MAX_M) ? 0 : dom_rank_tables_bytes(R, m);
 }
 
 int mo_dominance_bits_ranked(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
                              int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* tables,
                              size_t tables_bytes, void* stream_) {
-  if (!FS || !blkmin || !blkmax || !wend || !bits || !hasdom || !tables || m < 2 || m > 16) return MO_ERR_PARAM;
+  if (!FS || !blkmin || !blkmax || !wend || !bits || !hasdom || !tables || m < 2 || m > MO_MAX_M) return MO_ERR_PARAM;
   if (tables_bytes < dom_rank_tables_bytes(R, m)) return MO_ERR_PARAM;
   cudaStream_t s = (cudaStream_t)stream_;
   if (cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
@@ -688,7 +697,7 @@ int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t
 int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, const int32_t* info, uint64_t seed,
                  uint32_t generation, float* ideal, float* Fn, double* intercepts, void* workspace,
                  size_t workspace_bytes, void* stream_) {
-  if (m < 1 || m > 16 || R < 1) return MO_ERR_PARAM;   // k_prep's extreme-point pass: m <= 16
+  if (m < 1 || m > MO_MAX_M || R < 1) return MO_ERR_PARAM;
   Layout L = make_layout(R, 1, m, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;
@@ -717,7 +726,7 @@ int mo_normalize(const float* F, int64_t R, int32_t m, const int32_t* ranks, con
 int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64_t w, const int32_t* ranks,
                  const int32_t* info, uint64_t seed, uint32_t generation, int32_t* pi, float* d, void* workspace,
                  size_t workspace_bytes, void* stream_) {
-  if (m < 1 || m > 16 || R < 1 || w < 1) return MO_ERR_PARAM;
+  if (m < 1 || m > MO_MAX_M || R < 1 || w < 1) return MO_ERR_PARAM;
   Layout L = make_layout(R, w, m, LAYOUT_OPS);
   MO_TRY(check_ws(L, workspace, workspace_bytes));
   cudaStream_t s = (cudaStream_t)stream_;
@@ -740,6 +749,7 @@ int mo_associate(const float* Fn, int64_t R, int32_t m, const float* zhat, int64
   aa.zend = (int)w;
   aa.lat_z = nullptr;
   aa.in_step = 0;
+  aa.zsT = pa.zsT;
   MO_TRY(launch_assoc(aa, m, R, s));
   AssocFinalArgs fa;
   memset(&fa, 0, sizeof(fa));

@@ -46,7 +46,11 @@ __device__ inline void gen_prologue(const PrepArgs& a, uint32_t gen, int gtid, i
       a.near_key[j] = ~0ull;
     }
     if (a.zhat)
-      for (int k = 0; k < m; ++k) a.zs[(int64_t)p * m + k] = a.zhat[(int64_t)j * m + k];
+      for (int k = 0; k < m; ++k) {
+        const float z = a.zhat[(int64_t)j * m + k];
+        a.zs[(int64_t)p * m + k] = z;
+        if (a.zsT) a.zsT[(int64_t)k * w + p] = z;
+      }
   }
   if (a.lvl)
     for (int q = gtid; q < 2 * LVL_BINS; q += gthreads) a.lvl[q] = 0;

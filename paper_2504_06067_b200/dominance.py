@@ -75,7 +75,7 @@ def dominance_bits_sorted(ps, poison=False, method="ranked"):
     if method == "ranked":
         nbytes = int(L.mo_dominance_tables_bytes(R, m))
         if nbytes == 0:
-            raise ParameterError("the rank-mask kernel needs 2 <= m <= 16")
+            raise ParameterError("the rank-mask kernel needs 2 <= m <= 512")
         tables = torch.empty(nbytes, dtype=torch.uint8, device=FS.device)
         _lib.check(L.mo_dominance_bits_ranked(*args, _lib.ptr(tables), nbytes, _lib.stream_ptr()),
                    "mo_dominance_bits_ranked")

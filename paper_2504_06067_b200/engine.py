@@ -43,6 +43,9 @@ from .errors import ConfigError, raise_for_status
 from .variation import VariationConfig, init_population
 
 
+MAX_M = 512   # include/manyobj_b200.h MO_MAX_M: m > 16 runs the runtime-m ("wide") kernels
+
+
 @dataclass(frozen=True)
 class RunConfig:
     """SPEC.md:440-443: problem, n (even, >= m), m, d, generations, seed, backend, variation."""
@@ -70,8 +73,8 @@ def validate(cfg):
         raise ConfigError("d", "d must be >= m")
     if cfg.generations < 1:
         raise ConfigError("generations", "must be >= 1")
-    if cfg.m > 16:
-        raise ConfigError("m", "the association kernels are instantiated for m <= 16")
+    if cfg.m > MAX_M:
+        raise ConfigError("m", f"m <= {MAX_M} (PAPER.md Appendix D's largest objective count)")
     if cfg.backend != "batched":
         raise ConfigError("backend", "the GPU engine implements the batched back-end only; the Alg. 1 "
                                      "oracle back-end is CPU test infrastructure (oracle/manyobj_ref)")
@@ -201,11 +204,17 @@ class Engine:
             R = 2 * self.cfg.n
             bits = R * ((R + 255) // 256 * 8) * 4
             budget = 0.5 * torch.cuda.get_device_properties(self.dev).total_memory
-            # measured crossovers (profiles/r01_sort_modes.jsonl): the boxed streamed sort overtakes
-            # the bit-matrix at n ~ 100k (m = 3) and n ~ 48k (m >= 4, e.g. C3: 20.0 vs 26.1 ms)
+            # measured crossovers: the boxed streamed sort overtakes the bit-matrix at n ~ 100k for m = 3
+            # (profiles/r01_sort_modes.jsonl); for m >= 4 the rank-mask bit-matrix sort (round 2) is
+            # faster wherever the matrix fits (C3: 9.9 ms per generation vs 25 ms streamed)
             n, m = self.cfg.n, self.cfg.m
-            boxed_wins = (m <= 3 and n >= 100_000) or (4 <= m <= 10 and n >= 48_000)
+            boxed_wins = m <= 3 and n >= 100_000
             sort = "bits" if self.shard_count == 1 and bits <= budget and not boxed_wins else "stream"
+            if sort == "stream" and m > 16:
+                raise ConfigError("m", "the streamed sort runs m <= 16; this population's bit-matrix does "
+                                       "not fit the device")
+        if sort == "stream" and self.cfg.m > 16:
+            raise ConfigError("sort", "the streamed / sharded sort runs m <= 16")
         return _lib.SORT_BITS if sort == "bits" else _lib.SORT_STREAM
 
     # ------------------------------------------------------------ C-ABI args
