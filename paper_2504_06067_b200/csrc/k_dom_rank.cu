@@ -50,9 +50,14 @@ __device__ __forceinline__ int mask_slot(int c, int h) { return 2 * c + (h ^ ((c
 template <int M>
 __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__ FS, int R,
                                                         uint32_t* __restrict__ tables, uint32_t* __restrict__ vmask,
-                                                        int m_rt) {
+                                                        int m_rt, uint32_t* __restrict__ tsum) {
   pdl_wait();
   const int m = M > 0 ? M : m_rt;
+  if (tsum && blockIdx.y == 0) {   // this generation's tile summary of block bi's rows starts empty
+    const int64_t TW = tsum_words(R);
+    const int64_t r0 = (int64_t)blockIdx.x * DR_BLK, r1 = min((int64_t)R, r0 + DR_BLK);
+    for (int64_t e = r0 * TW + threadIdx.x; e < r1 * TW; e += DR_BLK) tsum[e] = 0u;
+  }
   __shared__ uint32_t sKey[DR_BLK];
   __shared__ int sIdx[DR_BLK];
   const int bi = blockIdx.x, k = blockIdx.y, t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -163,7 +168,24 @@ struct DomRankArgs {
   int R, nb, ch;           // rows, blocks, J blocks per item
   int64_t W;               // words per bit-matrix row
   int64_t items;
+  uint32_t* tsum;          // nullable: tile summary (then zero word blocks are not stored)
+  int64_t TW;
 };
+
+// store the 8 words of block `blk` of row `row` (always without a summary; with one, only when nonzero,
+// flagging the block); hasdom[row] = 1 when nonzero
+__device__ __forceinline__ void dr_store(const DomRankArgs& a, int row, int blk, const uint32_t* v) {
+  const bool nz = (v[0] | v[1] | v[2] | v[3] | v[4] | v[5] | v[6] | v[7]) != 0u;
+  if (!a.tsum || nz) {
+    uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)row * a.W + (int64_t)blk * 8);
+    dst[0] = make_uint4(v[0], v[1], v[2], v[3]);
+    dst[1] = make_uint4(v[4], v[5], v[6], v[7]);
+  }
+  if (nz) {
+    a.hasdom[row] = 1;
+    if (a.tsum) atomicOr(a.tsum + (int64_t)row * a.TW + (blk >> 5), 1u << (blk & 31));
+  }
+}
 
 // items of block row bi: ceil((nb - bi) / ch); G(n) = sum_{x=1..n} ceil(x / ch)
 __device__ __forceinline__ int64_t dr_G(int64_t n, int ch) {
@@ -300,13 +322,8 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
           }
         }
       }
-      if (j < a.R) {
-        uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)j * a.W + (int64_t)bi * 8);
-        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-        if ((out[0] | out[1] | out[2] | out[3] | out[4] | out[5] | out[6] | out[7]) != 0u) a.hasdom[j] = 1;
-      }
-      if (fast) {
+      if (j < a.R) dr_store(a, j, bi, out);
+      if (fast && !a.tsum) {
         // rows i of I's last S bucket may share it with rows of J: their words of block bj lie below
         // wend and are read by the peel, so they must hold zeros (no j of a fast tile dominates an i)
         const int ilast = min(a.R, i0 + DR_BLK) - 1;
@@ -318,15 +335,14 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
             dst[1] = make_uint4(0u, 0u, 0u, 0u);
           }
         }
-      } else if (bi != bj) {
+      } else if (!fast && bi != bj) {
         __syncthreads();
         const int i = i0 + tid;
         if (i < a.R) {
-          const uint32_t* sw = sT + tid * 9;
-          uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
-          dst[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
-          dst[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
-          if ((sw[0] | sw[1] | sw[2] | sw[3] | sw[4] | sw[5] | sw[6] | sw[7]) != 0u) a.hasdom[i] = 1;
+          uint32_t sw[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sw[w] = sT[tid * 9 + w];
+          dr_store(a, i, bj, sw);
         }
         __syncthreads();
       }
@@ -441,13 +457,8 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
           }
         }
       }
-      if (j < a.R) {
-        uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)j * a.W + (int64_t)bi * 8);
-        dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-        dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-        if ((out[0] | out[1] | out[2] | out[3] | out[4] | out[5] | out[6] | out[7]) != 0u) a.hasdom[j] = 1;
-      }
-      if (fast) {
+      if (j < a.R) dr_store(a, j, bi, out);
+      if (fast && !a.tsum) {
         const int ilast = min(a.R, i0 + DR_BLK) - 1;
         if (__ldg(a.wend + ilast) > bj * 8) {
           const int i = i0 + tid;
@@ -457,15 +468,14 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
             dst[1] = make_uint4(0u, 0u, 0u, 0u);
           }
         }
-      } else if (bi != bj) {
+      } else if (!fast && bi != bj) {
         __syncthreads();
         const int i = i0 + tid;
         if (i < a.R) {
-          const uint32_t* sw = sT + tid * 9;
-          uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
-          dst[0] = make_uint4(sw[0], sw[1], sw[2], sw[3]);
-          dst[1] = make_uint4(sw[4], sw[5], sw[6], sw[7]);
-          if ((sw[0] | sw[1] | sw[2] | sw[3] | sw[4] | sw[5] | sw[6] | sw[7]) != 0u) a.hasdom[i] = 1;
+          uint32_t sw[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sw[w] = sT[tid * 9 + w];
+          dr_store(a, i, bj, sw);
         }
       }
     }
@@ -474,10 +484,12 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
 }
 
 static int launch_dom_rank_wide(const float* FS, const float* blkmin, const float* blkmax, const int* wend,
-                                int64_t R, int m, uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+                                int64_t R, int m, uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s,
+                                uint32_t* tsum) {
   const int nb = (int)dom_rank_blocks(R);
   uint32_t* vmask = tables + (int64_t)nb * m * DR_TBL_WORDS;
-  MO_TRY(launch_ex(k_dom_tables<0>, dim3(nb, m), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, m));
+  MO_TRY(launch_ex(k_dom_tables<0>, dim3(nb, m), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, m,
+                   tsum));
   const size_t smem = (size_t)DRW_MC * DR_TBL_BYTES;
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
@@ -498,6 +510,8 @@ static int launch_dom_rank_wide(const float* FS, const float* blkmin, const floa
   a.vmask = vmask;
   a.bits = bits;
   a.hasdom = hasdom;
+  a.tsum = tsum;
+  a.TW = tsum_words(R);
   a.R = (int)R;
   a.nb = nb;
   a.ch = 1;   // one (I, J) tile per item: every tile re-streams block I's m tables anyway
@@ -515,10 +529,11 @@ size_t dom_rank_tables_bytes(int64_t R, int m) {
 
 template <int M>
 static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
-                             uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+                             uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum) {
   const int nb = (int)dom_rank_blocks(R);
   uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
-  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M));
+  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M,
+                   tsum));
   const size_t smem = (size_t)M * DR_TBL_BYTES;
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
@@ -545,6 +560,8 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
   a.vmask = vmask;
   a.bits = bits;
   a.hasdom = hasdom;
+  a.tsum = tsum;
+  a.TW = tsum_words(R);
   a.R = (int)R;
   a.nb = nb;
   a.ch = ch;
@@ -557,19 +574,19 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
 }
 
 int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R, int m,
-                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s) {
+                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum) {
   if (R <= 0) return MO_OK;
   if (R > (1ll << 31) - 1 - DR_BLK) return MO_ERR_PARAM;
   switch (m) {
 #define MO_DR_CASE(MM) \
-  case MM: return launch_dom_rank_m<MM>(FS, blkmin, blkmax, wend, R, bits, hasdom, tables, s);
+  case MM: return launch_dom_rank_m<MM>(FS, blkmin, blkmax, wend, R, bits, hasdom, tables, s, tsum);
     MO_DR_CASE(2) MO_DR_CASE(3) MO_DR_CASE(4) MO_DR_CASE(5) MO_DR_CASE(6) MO_DR_CASE(7) MO_DR_CASE(8)
     MO_DR_CASE(9) MO_DR_CASE(10) MO_DR_CASE(11) MO_DR_CASE(12) MO_DR_CASE(13) MO_DR_CASE(14) MO_DR_CASE(15)
     MO_DR_CASE(16)
 #undef MO_DR_CASE
     default:
       if (m > 16 && m <= MO_MAX_M)
-        return launch_dom_rank_wide(FS, blkmin, blkmax, wend, R, m, bits, hasdom, tables, s);
+        return launch_dom_rank_wide(FS, blkmin, blkmax, wend, R, m, bits, hasdom, tables, s, tsum);
       return MO_ERR_PARAM;
   }
 }

@@ -748,9 +748,67 @@ struct PeelArgs {
   const int* wend;
   int* rank_pos;
   unsigned long long* trace;  // nullable phase trace (slots 8..11)
+  // nullable tile summary (k_dom_rank): only flagged 256-bit word blocks were stored; resume[] then
+  // counts word blocks instead of words
+  const uint32_t* tsum;
+  int64_t TW;
 };
 
 constexpr int PEEL_THREADS = 256;
+
+// Phase A of one row with a tile summary: 8 lanes (l8) walk row j's summary words from block `t0`
+// (8 summary words = 256 blocks per step); each lane tests its flagged blocks (2 x uint4 of the
+// dominators' words against the ranked mask) in ascending order and stops at its first unranked
+// dominator; the group keeps the smallest such block.  Returns the first blocking block, or -1 when
+// every flagged block below tlim holds ranked dominators only.
+__device__ __forceinline__ int64_t peel_row_summary(const PeelArgs& a, int64_t j, bool active, int64_t t0,
+                                                    int64_t tlim, int l8, uint32_t gmask) {
+  int64_t blocked_at = -1;
+  int64_t sw0 = t0 >> 5;
+  for (;;) {
+    const bool scanning = active && blocked_at < 0 && (sw0 << 5) < tlim;
+    if (__ballot_sync(MO_FULL, scanning) == 0) break;
+    int64_t hit = INT64_MAX;
+    if (scanning) {
+      const int64_t swi = sw0 + l8;
+      if ((swi << 5) < tlim) {
+        uint32_t f = __ldcg(a.tsum + j * a.TW + swi);
+        if (swi == (t0 >> 5)) f &= 0xffffffffu << (t0 & 31);              // blocks before the resume block
+        const int64_t rem = tlim - (swi << 5);
+        if (rem < 32) f &= (1u << rem) - 1u;
+        while (f) {
+          const int b = __ffs(f) - 1;
+          f &= f - 1u;
+          const int64_t t = (swi << 5) + b;
+          const uint4* bw = reinterpret_cast<const uint4*>(a.bits + j * a.W + t * 8);
+          const uint4* rw = reinterpret_cast<const uint4*>(a.ranked + t * 8);
+          const uint4 b0 = __ldg(bw), b1 = __ldg(bw + 1);
+          const uint4 r0 = __ldcg(rw), r1 = __ldcg(rw + 1);
+          const uint32_t h = (b0.x & ~r0.x) | (b0.y & ~r0.y) | (b0.z & ~r0.z) | (b0.w & ~r0.w) |
+                             (b1.x & ~r1.x) | (b1.y & ~r1.y) | (b1.z & ~r1.z) | (b1.w & ~r1.w);
+          if (h) {
+            hit = t;
+            break;
+          }
+        }
+      }
+    }
+    // smallest blocking block of the 8-lane group
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+      const int64_t oh = __shfl_xor_sync(MO_FULL, hit, o, 8);
+      hit = oh < hit ? oh : hit;
+    }
+    (void)gmask;
+    if (scanning) {
+      if (hit != INT64_MAX)
+        blocked_at = hit;
+      else
+        sw0 += 8;
+    }
+  }
+  return blocked_at;
+}
 
 __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
   pdl_wait();
@@ -841,6 +899,22 @@ __global__ void __launch_bounds__(PEEL_THREADS) k_front_peel(PeelArgs a) {
         if (rk[j] == MO_RANK_UNRANKED && a.hasdom[j] == 0) {
           rk[j] = 0;
           ready_local++;
+        }
+      }
+    } else if (a.tsum) {
+      for (int rb = gwarp * 4; rb < R; rb += nwarps * 4) {
+        const int j = rb + g8;
+        const bool active = (j < R) && (__ldcg(rk + j) == MO_RANK_UNRANKED);
+        const int64_t tlim = active ? ((int64_t)a.wend[j] + 7) / 8 : 0;
+        const int64_t t0 = active ? (int64_t)a.resume[j] : 0;
+        const int64_t bl = peel_row_summary(a, j, active, t0, tlim, l8, gmask);
+        if (active && l8 == 0) {
+          if (bl >= 0) {
+            a.resume[j] = (int)bl;
+          } else {
+            rk[j] = k;
+            ready_local++;
+          }
         }
       }
     } else {
@@ -957,10 +1031,11 @@ int peel_grid_blocks() {
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
-                      unsigned long long* trace, cudaStream_t s, bool in_step) {
+                      unsigned long long* trace, cudaStream_t s, bool in_step, const uint32_t* tsum) {
   if (R <= 0) return MO_ERR_PARAM;
+  if (tsum && !wend) return MO_ERR_PARAM;
   PeelArgs a{bits, (int)R, words_per_row(R), valid, stop_at, ranks, info, resume, ranked, front_sizes, bar,
-             perm, hasdom, wend, rank_pos, trace};
+             perm, hasdom, wend, rank_pos, trace, tsum, tsum_words(R)};
   if (!in_step) {
     if (cudaMemsetAsync(front_sizes, 0, 2 * sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;
     if (cudaMemsetAsync(front_sizes + R + 3, 0, sizeof(int), s) != cudaSuccess) return MO_ERR_CUDA;

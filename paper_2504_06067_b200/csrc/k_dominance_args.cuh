@@ -48,11 +48,16 @@ int launch_dom_tile(const float* F, int64_t R, int m, const uint8_t* valid, uint
 int launch_dom_tile_sorted(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
                            int m, uint32_t* bits, uint8_t* hasdom, cudaStream_t s, bool clear_hasdom = true);
 size_t dom_rank_tables_bytes(int64_t R, int m);
+// Tile summary (engine path): bit t of row p's tsum words = "word block t (256 dominators) of row p was
+// written and is nonzero".  With a summary the rank kernels store only nonzero word blocks and the peel
+// reads only flagged blocks (a C3 row has ~15 nonzero blocks of the ~390 below its S bound).
+__host__ __device__ inline int64_t tsum_words(int64_t R) { return (((R + 255) / 256) + 31) / 32; }
 int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R, int m,
-                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s);
+                    uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum = nullptr);
 int launch_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int* ranks,
                       int* info, int* resume, uint32_t* ranked, int* front_sizes, unsigned* bar,
                       const int* perm, const uint8_t* hasdom, const int* wend, int* rank_pos,
-                      unsigned long long* trace, cudaStream_t s, bool in_step = false);
+                      unsigned long long* trace, cudaStream_t s, bool in_step = false,
+                      const uint32_t* tsum = nullptr);
 
 }  // namespace mo

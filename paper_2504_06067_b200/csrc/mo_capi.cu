@@ -40,7 +40,7 @@ constexpr int MAX_GRID = 1024;  // upper bound on persistent-grid blocks (part/h
 
 struct Layout {
   size_t bits, resume, ranked, fsizes, bar, pos_pop, perm_pop, pos_ref, perm_ref, zs, cand, ctl, ext_key,
-      colmax, icpt, a32, solve, zsT, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
+      colmax, icpt, a32, solve, zsT, tsum, akey, pi, d, rho, rho_p, take, bstart, near_key, prom, keyA, valA, keyB, valB, part,
       hist, sel, FS, SS, perm_sort, wend, hasdom, rank_pos, trace, pcnt, pfill, blkmin, blkmax, pctl, kept, fill,
       lvl, sctl, mate, dtab, fcand, fctl, blkbox, flbox, blkbox32, flbox32, blkS32, flS32, cbox, sstats, tkey, tval, cnt, mask_local, mask_full, fl, flmax, plan, ucnt, stctl, total;
   int64_t T, mask_local_words, mask_full_words;
@@ -118,6 +118,7 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   // rank-mask dominance tables (k_dom_rank.cu): per 256-row block and objective, Eytzinger values +
   // prefix masks (bit-matrix sort, 2 <= m <= MO_MAX_M)
   L.dtab = bump(c, sort_mode == MO_SORT_BITS && m >= 2 && m <= MO_MAX_M ? dom_rank_tables_bytes(R, m) : 0);
+  L.tsum = bump(c, sort_mode == MO_SORT_BITS ? (size_t)R * tsum_words(R) * 4 : 0);
   // streamed / sharded sort (sort_mode == MO_SORT_STREAM)
   const bool st = sort_mode == MO_SORT_STREAM;
   const int64_t nb = ceil_div(R, STREAM_BLK);
@@ -321,13 +322,24 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   ps.in_step = 1;
   ps.hasdom = hasdom;
   MO_TRY(launch_presort(ps, s));
-  if (use_dom_rank(a->m))
-    MO_TRY(launch_dom_rank(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, at<uint32_t>(ws, L.dtab), s));
-  else
+  // rank-mask kernels: only nonzero 256-bit word blocks are stored, flagged in the tile summary that the
+  // peel walks (MO_NO_TSUM=1: full stores and the word-by-word peel)
+  static int no_tsum = -1;
+  if (no_tsum < 0) {
+    const char* e = getenv("MO_NO_TSUM");
+    no_tsum = (e && e[0] == '1') ? 1 : 0;
+  }
+  uint32_t* tsum = nullptr;
+  if (use_dom_rank(a->m)) {
+    tsum = no_tsum ? nullptr : at<uint32_t>(ws, L.tsum);
+    MO_TRY(launch_dom_rank(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, at<uint32_t>(ws, L.dtab), s,
+                           tsum));
+  } else {
     MO_TRY(launch_dom_tile_sorted(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, s, false));
+  }
   return launch_front_peel(bits, R, nullptr, n, a->ranks, a->info, at<int>(ws, L.resume), at<uint32_t>(ws, L.ranked),
                            at<int>(ws, L.fsizes), at<unsigned>(ws, L.bar) + BAR_PEEL, ps.perm, hasdom, ps.wend,
-                           at<int>(ws, L.rank_pos), ps.trace, s, true);
+                           at<int>(ws, L.rank_pos), ps.trace, s, true, tsum);
 }
 
 // tensor-core filtered association: full reference range (one shard), packed fragments, enough points
