@@ -259,6 +259,12 @@ typedef struct mo_step_args {
    * association stays bit-identical: the bf16 MMA only selects which
    * references get the canonical FP32 key. */
   const void* zhat_frag;
+  /* tcgen05 filter of the same full-scan association (k_assoc_umma.cu,
+   * preferred over zhat_frag when set): the unit directions as FP16 UMMA
+   * tiles packed by mo_pack_refs_f16 (device, mo_pack_refs_f16_bytes(w)
+   * bytes, static).  The association stays bit-identical: tcgen05.mma only
+   * selects which references get the canonical FP32 key. */
+  const void* zhat_umma;
 } mo_step_args;
 
 enum { MO_SORT_BITS = 0, MO_SORT_STREAM = 1 };
@@ -369,6 +375,12 @@ int mo_hv_exact(const float* front, int64_t nf, int32_t m, const double* ref, do
  * 544 bytes per 8 columns (fragments + the columns' reference indices).
  * m <= 16. */
 size_t mo_pack_refs_bytes(int64_t w);
+/* FP16 tiles for the tcgen05 filter: 128 directions x K16 per 4 KB tile in the
+ * UMMA K-major no-swizzle core-matrix layout (packed column order `order`,
+ * NULL = identity), followed by the reference index of every packed column
+ * (int32, -1 = padding).  m <= 16. */
+size_t mo_pack_refs_f16_bytes(int64_t w, int32_t m);
+int mo_pack_refs_f16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
 int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
 
 /* ------------------------------------------- op-level API (k_ops.cu)

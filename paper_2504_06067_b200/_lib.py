@@ -45,7 +45,7 @@ class StepArgs(ctypes.Structure):
         ("sort_mode", c_i32), ("shard_rank", c_i32), ("shard_count", c_i32), ("pad2", c_i32),
         ("lattice_z", c_vp), ("lattice_index", c_vp), ("lattice_pos", c_vp), ("lattice_H", c_i32),
         ("lattice_r", c_i32), ("pad3", c_i32),
-        ("zhat_frag", c_vp),
+        ("zhat_frag", c_vp), ("zhat_umma", c_vp),
     ]
 
 
@@ -83,6 +83,8 @@ _PROTOS = {
     "mo_hv_exact_workspace_bytes": (c_sz, [c_i64]),
     "mo_pack_refs_bytes": (c_sz, [c_i64]),
     "mo_pack_refs_bf16": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "mo_pack_refs_f16_bytes": (c_sz, [c_i64, c_i32]),
+    "mo_pack_refs_f16": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_hv_exact": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_sort_stream_begin": (c_i32, [ctypes.POINTER(StepArgs), c_vp]),
     "mo_sort_stream_front": (c_i32, [ctypes.POINTER(StepArgs), c_i32, c_vp]),

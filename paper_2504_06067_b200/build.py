@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmanyobj_b200.so")
-SOURCES = ["mo_capi.cu", "k_vary.cu", "k_dominance.cu", "k_stream.cu", "k_niche.cu", "k_metrics.cu", "k_peaks.cu", "k_ops.cu", "k_dom_rank.cu"]
+SOURCES = ["mo_capi.cu", "k_vary.cu", "k_dominance.cu", "k_stream.cu", "k_niche.cu", "k_metrics.cu", "k_peaks.cu", "k_ops.cu", "k_dom_rank.cu", "k_assoc_umma.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

@@ -1669,6 +1669,17 @@ int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
 #undef MO_HM_CASE
     default: return MO_ERR_PARAM;
   }
+  return launch_assoc_fallback(a, m, s);
+}
+
+// the sliced FP32 full scan of the rows a filtered association appended to fb_cand
+int launch_assoc_fallback(const AssocArgs& a, int m, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   const dim3 fg((unsigned)sms), fb(256);
   switch (m) {
 #define MO_FB_CASE(MM) \

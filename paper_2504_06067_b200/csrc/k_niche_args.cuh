@@ -88,6 +88,9 @@ struct AssocArgs {
   // order (mo_pack_refs_bf16); nullptr = FP32 full scan only
   const uint2* zfrag;
   const float* zsT;      // wide m: m x w objective-major shuffled directions (k_assoc_wide)
+  // tcgen05 filter (k_assoc_umma): FP16 reference tiles + packed-column reference indices
+  // (mo_pack_refs_f16); preferred over zfrag when set
+  const void* zumma;
 };
 
 struct AssocFinalArgs {
@@ -149,6 +152,10 @@ int launch_assoc(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
 int launch_assoc_hmma(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
 int launch_pack_refs(const float* zhat, int64_t w, int m, const int32_t* order, uint2* out, cudaStream_t s);
 int launch_assoc_lattice(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
+int launch_assoc_fallback(const AssocArgs& a, int m, cudaStream_t s);
+int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s);
+size_t pack_refs_f16_bytes(int64_t w, int m);
+int launch_pack_refs_f16(const float* zhat, int64_t w, int m, const int32_t* order, void* out, cudaStream_t s);
 int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s);
 int launch_select(const SelectArgs& a, cudaStream_t s);
 

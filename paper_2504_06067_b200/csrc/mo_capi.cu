@@ -353,6 +353,18 @@ static bool use_hmma(const AssocArgs& aa, int m) {
   return !off && aa.zfrag && m >= 2 && m <= 16 && aa.zbeg == 0 && aa.zend == aa.w && aa.w >= 1024;
 }
 
+// tcgen05 association filter (k_assoc_umma.cu): same eligibility, FP16 reference tiles present;
+// MO_ASSOC=hmma selects the mma.sync filter, MO_NO_HMMA=1 the FP32 scan
+static bool use_umma(const AssocArgs& aa, int m) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("MO_ASSOC");
+    const char* h = getenv("MO_NO_HMMA");
+    off = ((e && strcmp(e, "hmma") == 0) || (h && h[0] == '1')) ? 1 : 0;
+  }
+  return !off && aa.zumma && m >= 2 && m <= 16 && aa.zbeg == 0 && aa.zend == aa.w && aa.w >= 1024;
+}
+
 // box radius of the lattice-pruned association: (2r-1)^(m-1) points per row
 static int default_lattice_r(int m) { return m <= 3 ? 6 : (m == 4 ? 3 : 1); }
 
@@ -405,8 +417,11 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.in_step = 1;
   aa.zfrag = reinterpret_cast<const uint2*>(a->zhat_frag);
   aa.zsT = pa.zsT;
+  aa.zumma = a->zhat_umma;
   if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
+  else if (use_umma(aa, m))
+    MO_TRY(launch_assoc_umma(aa, m, R, s));
   else if (use_hmma(aa, m))
     MO_TRY(launch_assoc_hmma(aa, m, R, s));
   else
@@ -584,6 +599,12 @@ static int check_step_args(const mo_step_args* a) {
 using namespace mo;
 
 extern "C" {
+
+size_t mo_pack_refs_f16_bytes(int64_t w, int32_t m) { return (w < 1 || m < 1 || m > 16) ? 0 : pack_refs_f16_bytes(w, m); }
+
+int mo_pack_refs_f16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream_) {
+  return launch_pack_refs_f16(zhat, w, m, order, out, (cudaStream_t)stream_);
+}
 
 size_t mo_pack_refs_bytes(int64_t w) { return w > 0 ? (size_t)((w + 7) / 8) * 544 : 0; }
 

@@ -132,13 +132,17 @@ class Engine:
             self.lattice, self.lattice_H = self._lattice_table(prune)   # (z, index, pos) or None
             # bf16 hi/lo MMA fragments of the unit directions (tensor-core filter of the full-scan
             # association; static, packed once)
-            self.zfrag = None
+            # and the FP16 UMMA tiles of the tcgen05 filter, preferred by the library when both are set)
+            self.zfrag = self.zumma = None
             if self.lattice is None and 2 <= m <= 16 and self.shard_count == 1:
                 self.zfrag = torch.empty(int(L.mo_pack_refs_bytes(self.w)), dtype=torch.uint8, device=self.dev)
+                self.zumma = torch.empty(int(L.mo_pack_refs_f16_bytes(self.w, m)), dtype=torch.uint8, device=self.dev)
                 order = torch.from_numpy(np.random.default_rng(0x5EED).permutation(self.w).astype(np.int32))
                 order = order.to(self.dev)
                 _lib.check(L.mo_pack_refs_bf16(self.zhat.data_ptr(), self.w, m, order.data_ptr(),
                                                self.zfrag.data_ptr(), _lib.stream_ptr()), "mo_pack_refs_bf16")
+                _lib.check(L.mo_pack_refs_f16(self.zhat.data_ptr(), self.w, m, order.data_ptr(),
+                                              self.zumma.data_ptr(), _lib.stream_ptr()), "mo_pack_refs_f16")
                 torch.cuda.current_stream(self.dev).synchronize()   # `order` is freed on return
             self.XR = [torch.empty((2 * n, d), dtype=torch.float32, device=self.dev) for _ in range(2)]
             self.FR = [torch.empty((2 * n, m), dtype=torch.float32, device=self.dev) for _ in range(2)]
@@ -245,6 +249,7 @@ class Engine:
         a.lattice_H = self.lattice_H
         a.lattice_r = self.prune_r
         a.zhat_frag = self.zfrag.data_ptr() if self.zfrag is not None else None
+        a.zhat_umma = self.zumma.data_ptr() if self.zumma is not None else None
         return a
 
     def _launch(self, cur, generation, phases=_lib.PHASE_ALL, use_dev_gen=False):

@@ -18,6 +18,6 @@ if [ "${NCU}" != "0" ]; then
       --log-file gpurun_out/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_dom_rank -s 3 -c 1 \
       -o gpurun_out/c3_domrank python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_assoc_hmma -s 3 -c 1 \
-      -o gpurun_out/c3_hmma python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_hmma.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_assoc_umma -s 3 -c 1 \
+      -o gpurun_out/c3_umma python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_umma.log 2>&1
 fi

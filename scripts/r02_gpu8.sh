@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_hmma.py -x -q > gpurun_out/pytest_umma.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_umma.log
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_assoc_umma -s 3 -c 1 \
+    -o gpurun_out/c3_umma python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_umma.log 2>&1

@@ -1,5 +1,6 @@
-"""Tensor-core filtered association (k_assoc_hmma: bf16 hi/lo m16n8k16 MMAs select the candidates, the
-canonical FP32 key decides) against the FP32 full scan and the oracle (GPU).
+"""Tensor-core filtered association -- k_assoc_umma (tcgen05.mma FP16 -> FP32 in TMEM, the engine default)
+and k_assoc_hmma (bf16 hi/lo m16n8k16 mma.sync) select the candidates, the canonical FP32 key decides --
+against the FP32 full scan and the oracle (GPU).
 
 * adversarial objectives -- rows on reference directions, exact midpoints between two directions (key
   ties broken by shuffled position), the ideal point (zero rows -> the sliced fallback scan), duplicates,
@@ -60,23 +61,26 @@ def _assoc_outputs(M, eng, F, n, m):
     return akey, np_(eng.FR[eng.cur ^ 1][:n]).copy(), np_(eng.ranks).copy(), info
 
 
-@pytest.mark.parametrize("m,n", [(3, 1500), (6, 1500), (10, 1500), (16, 2000)])
+@pytest.mark.parametrize("m,n", [(3, 1500), (6, 1500), (10, 1500), (16, 2000), (2, 1200), (9, 5000)])
 def test_hmma_filter_bit_identical_adversarial(M, m, n):
     rs = np.random.default_rng(m)
     F = _adversarial(M, m, n, rs)
     cfg = M.engine.RunConfig(problem="DTLZ2", n=n, m=m, d=m + 9, generations=1, seed=4)
     outs = []
-    for use in (True, False):
+    for mode in ("umma", "hmma", "scan"):
         eng = M.engine.Engine(cfg, prune=False)
-        assert eng.w >= 1024 and eng.zfrag is not None
-        if not use:
+        assert eng.w >= 1024 and eng.zfrag is not None and eng.zumma is not None
+        if mode != "umma":
+            eng.zumma = None
+        if mode == "scan":
             eng.zfrag = None
-            eng._args = [eng._make_args(0), eng._make_args(1)]
+        eng._args = [eng._make_args(0), eng._make_args(1)]
         outs.append(_assoc_outputs(M, eng, F, n, m))
-    (k1, f1, r1, i1), (k2, f2, r2, i2) = outs
+    (k1, f1, r1, i1) = outs[2]
     assert (k1 != 0).sum() > n // 2
-    assert np.array_equal(k1, k2)
-    assert np.array_equal(f1, f2) and np.array_equal(r1, r2) and i1 == i2
+    for k2, f2, r2, i2 in outs[:2]:
+        assert np.array_equal(k1, k2)
+        assert np.array_equal(f1, f2) and np.array_equal(r1, r2) and i1 == i2
 
 
 def _gpu_state_to_oracle(eng):
