@@ -22,14 +22,18 @@
 // tiles)):
 //   warp 0        producer: 1-D bulk copies (cp.async.bulk + mbarrier complete_tx) of the pre-packed
 //                 reference tiles (128 directions x KS K16 steps of FP16, UMMA K-major no-swizzle
-//                 core-matrix layout, 4 KB per step) into a shared-memory ring;
+//                 core-matrix layout, 4 KB per step) into a shared-memory ring (a warm-up prefix of
+//                 UA_WARM tiles is streamed twice: running maxima first, candidates after);
 //   warp 1        TMEM owner (alloc 512 columns / dealloc) and MMA issuer: per reference tile and row
 //                 tile KS tcgen05.mma.cta_group::1.kind::f16 M128 N128 K16 (the two row tiles share the
 //                 B tile), tcgen05.commit to the ring slot's empty barrier and to the accumulator
 //                 buffer's full barrier; two accumulator buffers (2 x 2 x 128 columns);
-//   warps 2..17   epilogue: build the item's A tiles in shared memory, then per tile tcgen05.ld
-//                 32x32b.x32 of their TMEM lane quarter (warp % 4) and 32-column group (both row
-//                 tiles), release the buffer, FMNMX3 chunk maxima, candidate buffering.
+//   warps 2..9    epilogue: build the item's A tiles in shared memory, then per tile four tcgen05.ld
+//                 32x32b.x32 of their TMEM lane quarter (warp % 4) and 64-column half (both row
+//                 tiles), one wait, release the buffer, FMNMX3 trees, candidate buffering.
+// Measured (C3, ncu): tensor pipe ~17 %, issue ~39 %: the per-tile chain (commit -> mbarrier ->
+// tcgen05.ld -> release -> next MMA) bounds it, not the MMA or the FMNMX3 work; N = 64 with four buffers
+// and two CTAs per SM (N = 64, 256 TMEM columns each) both measured slower (2.7 / 2.5 ms vs 2.2 ms).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
