@@ -191,7 +191,8 @@ def measure_peaks(torch, L, _lib):
     inp = torch.rand(64, device="cuda") + 0.5
     out = torch.empty(1 << 20, dtype=torch.int32, device="cuda")
     res = {}
-    for which, per_iter, name in ((0, 64, "compare"), (1, 16, "fp32")):
+    # (which, work per thread-iteration, name): compares, flops, shared-memory bytes (8 x 16 B loads)
+    for which, per_iter, name in ((0, 64, "compare"), (1, 16, "fp32"), (2, 128, "smem_bytes")):
         blocks, iters = sm * 8, 4096
         best = 0.0
         for _ in range(4):
@@ -249,14 +250,15 @@ def time_kernels(torch, eng, _lib):
     hasdom = torch.empty(R, dtype=torch.uint8, device="cuda")
     tb = int(L.mo_dominance_tables_bytes(R, m))
     tables = torch.empty(max(tb, 1), dtype=torch.uint8, device="cuda")
+    tsum = torch.empty((R, int(L.mo_tile_summary_words(R))), dtype=torch.int32, device="cuda")
     ts = []
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        if tb:     # the engine's kernel: rank-mask tables + sweep (k_dom_tables + k_dom_rank)
+        if tb:     # the engine's kernels and configuration: rank-mask tables + sweep with the tile summary
             _lib.check(L.mo_dominance_bits_ranked(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
                                                   _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
-                                                  _lib.ptr(tables), tb, _lib.stream_ptr()), "dom")
+                                                  _lib.ptr(tables), tb, _lib.ptr(tsum), _lib.stream_ptr()), "dom")
         else:
             _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
                                                   _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
@@ -265,14 +267,15 @@ def time_kernels(torch, eng, _lib):
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     out["dom_tile_ms"] = float(np.median(ts))
-    del bits
+    out["dom_kernel"] = "rank" if tb else "pairwise"
+    del bits, tsum
     return out
 
 
 # (workload, sort) -> (kernel name prefix, committed `ncu --set full` raw export under profiles/)
 TRAFFIC_CAPTURES = {
-    ("c2", "bits"): ("k_dom_tile_sorted<5", "r01_ncu_full_c2_raw.csv"),
-    ("c3", "bits"): ("k_dom_tile_sorted<10", "r02_ncu_full_c3_dom_raw.csv"),
+    ("c2", "bits"): ("k_dom_rank<5", "r02_ncu_full_c2_domrank_raw.csv"),
+    ("c3", "bits"): ("k_dom_rank<10", "r02_ncu_full_c3_domrank_raw.csv"),
     ("c4", "stream"): ("k_stream_tiles<3, 0>", "r01_ncu_full_c4_count_raw.csv"),
 }
 _UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -290,7 +293,7 @@ def committed_traffic(kernel_prefix, capture):
     ix = {h: i for i, h in enumerate(hdr)}
     vals = []
     for r in rows[2:]:
-        if r[ix["Kernel Name"]].replace("void ", "").startswith(kernel_prefix):
+        if kernel_prefix in r[ix["Kernel Name"]]:
             b = 0.0
             for col in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 b += float(r[ix[col]]) * _UNITS.get(units[ix[col]], 1.0)
@@ -508,37 +511,48 @@ def main():
     kern = r["kernels"]
     peaks = r["peaks"]
     n, m, R = wl["n"], wl["m"], 2 * wl["n"]
-    step_ms = kern["t_variation"] + kern["t_sort"] + kern["t_niche"]
-    # unordered pairs x m FP32 compares (one direction after the S-sort); a shard sweeps 1/world of them
-    cmp_work = R * (R - 1) // 2 * m // (world if sharded else 1)
-    algorithmic = f"R(R-1)/2 * m{' / world' if sharded else ''} = {cmp_work:.3e} compares per launch"
+    cap = TRAFFIC_CAPTURES.get((args.workload, r["sort"]))
+    traffic = committed_traffic(*cap) if cap else None
+    # our kernels per generation: vary, presort, [rank-mask tables], dominance, peel, prep, association
+    # (filtered / lattice + the sliced fallback scan, or the FP32 scan), assoc_final, select; streamed: +
+    # reset/plan/count/mark + 4 per front
+    assoc_kernels = 2 if (r.get("lattice") or r.get("hmma")) else 1
     if r["sort"] == "stream":
         # the boxed sweep decides most block pairs from bounding boxes: the roofline counts the FSETPs it
         # executed (m per pair on the <= chain, 2m on the full dominance chain)
         pl, pf = kern.get("count_pairs_le", 0), kern.get("count_pairs_full", 0)
         cmp_work = pl * m + pf * 2 * m
-        algorithmic = (f"executed: {pl:.3e} pairs x m + {pf:.3e} pairs x 2m = {cmp_work:.3e} compares "
-                       f"({(pl + pf) / max(1, R * R // (world if sharded else 1)):.4f} of the R^2 ordered pairs; "
-                       "the rest decided by block bounding boxes)")
-    dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
-    kname = ("k_stream_tiles<COUNT> (dominator-count sweep, streamed sort)" if r["sort"] == "stream"
-             else "k_dom_tile_sorted (dominance bit-matrix)")
-    # our kernels per generation: vary, presort, dominance, peel, prep, association (lattice + fallback
-    # scan, or the full scan), assoc_final, select; streamed: + reset/plan/count/mark + 4 per front
-    # lattice or tensor-core filter: the filtered kernel + the sliced fallback scan; else the FP32 scan
-    assoc_kernels = 2 if (r.get("lattice") or r.get("hmma")) else 1
-    launches = (K * (7 + assoc_kernels) if r["sort"] == "bits"
-                else K * (10 + assoc_kernels + 4 * int(kern.get("fronts_issued") or 0)))
-    cap = TRAFFIC_CAPTURES.get((args.workload, r["sort"]))
-    traffic = committed_traffic(*cap) if cap else None
-    roof = {"kernel": kname, "bound": "fp32-compare-issue",
-            "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12, "unit": "Tcmp/s",
-            "frac": dom_achieved / peaks["compare"], "traffic": traffic,
-            "traffic_note": "DRAM bytes per launch (read + write) from the committed ncu --set full capture "
-                            "(profiles/r01_ncu_full_*_raw.csv); the bit-matrix / counts stay in the 126 MB L2",
-            "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
-            "share_of_step": kern["dom_tile_ms"] / step_ms if step_ms else None,
-            "algorithmic": algorithmic}
+        dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
+        roof = {"kernel": "k_stream_tiles<COUNT> (dominator-count sweep, streamed sort)",
+                "bound": "fp32-compare-issue", "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12,
+                "unit": "Tcmp/s", "frac": dom_achieved / peaks["compare"],
+                "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
+                "algorithmic": (f"executed: {pl:.3e} pairs x m + {pf:.3e} pairs x 2m = {cmp_work:.3e} compares "
+                                f"({(pl + pf) / max(1, R * R // (world if sharded else 1)):.4f} of the R^2 ordered "
+                                "pairs; the rest decided by block bounding boxes)")}
+        launches = K * (10 + assoc_kernels + 4 * int(kern.get("fronts_issued") or 0))
+    else:
+        # rank-mask sweep (k_dom_rank): per (row j, 256-row block I) of the upper block triangle and per
+        # objective, one 256-bit prefix mask (32 B) and a 9-level Eytzinger search (9 x 4 B) read from
+        # shared memory -- the minimum the algorithm must read; bound: shared-memory load bandwidth
+        nb = (R + 255) // 256
+        pairs = sum(min(256, R - bj * 256) * (bj + 1) for bj in range(nb))
+        smem_bytes = pairs * m * (32 + 9 * 4)
+        dom_achieved = smem_bytes / (kern["dom_tile_ms"] / 1e3)
+        roof = {"kernel": "k_dom_tables + k_dom_rank (rank-mask dominance sweep, tile summary)", "bound": "smem",
+                "achieved": dom_achieved / 1e9, "peak": peaks["smem_bytes"] / 1e9, "unit": "GB/s",
+                "frac": dom_achieved / peaks["smem_bytes"],
+                "peak_source": "measured: k_peak_smem conflict-free ld.shared.v4 bandwidth (148 SMs x 128 B/clk "
+                               "nominal); MEASURED_PEAKS.json has HBM and tensor peaks only",
+                "algorithmic": (f"{pairs:.4e} (row, 256-row block) pairs x m = {m} x (32 B mask + 36 B search) = "
+                                f"{smem_bytes:.4e} B of shared-memory reads per launch")}
+        launches = K * (8 + assoc_kernels)
+    roof["traffic"] = traffic
+    roof["traffic_note"] = ("DRAM bytes per launch (read + write) of the dominant kernel from the committed ncu "
+                            f"--set full capture profiles/{cap[1] if cap else '-'}; the bit-matrix stays in the "
+                            "126 MB L2 / is stored only where nonzero")
+    roof["kernel_ms"] = kern["dom_tile_ms"]
+    roof["share_of_step"] = kern["dom_tile_ms"] / ms_per
     cfg_out = dict(cfgd)
     assert cfg_out["w"] == r["w"] and cfg_out["sort"] == r["sort"]
     line = {"metric": METRIC, "value": value, "unit": "generations/s", "n_gpus": world, "steps": K,
@@ -551,8 +565,9 @@ def main():
                     "d2h_bytes_per_step": r["d2h"]},
             "gpu_launches": launches,
             "roofline": roof,
-            "phases_ms": {k: round(v, 4) for k, v in kern.items()},
-            "peaks": {"compare_per_s": peaks["compare"], "fp32_flop_per_s": peaks["fp32"]},
+            "phases_ms": {k: round(v, 4) for k, v in kern.items() if isinstance(v, (int, float))},
+            "peaks": {"compare_per_s": peaks["compare"], "fp32_flop_per_s": peaks["fp32"],
+                      "smem_bytes_per_s": peaks["smem_bytes"]},
             "last_info": r["info"]}
     if not args.no_cpu_baseline and "cpu_gen_s" in r:
         line["cpu_baseline"] = {

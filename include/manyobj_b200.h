@@ -97,6 +97,8 @@ int64_t mo_trace_offset(int64_t n, int32_t m, int64_t w);
 
 /* Library build/version string. */
 const char* mo_version(void);
+/* sizeof(mo_step_args) as compiled into the library (bindings check their mirror against it). */
+size_t mo_step_args_bytes(void);
 
 /* --------------------------------------------------- RNG / shuffles (L1) */
 
@@ -156,9 +158,14 @@ int mo_dominance_bits_sorted(const float* FS, const float* blkmin, const float* 
  * the prefix masks selected by m binary searches.  tables: device scratch of
  * mo_dominance_tables_bytes(R, m) bytes (0 = unsupported m). */
 size_t mo_dominance_tables_bytes(int64_t R, int32_t m);
+/* tsum: NULL = store every word block below the S bound (the op-level
+ * contract); else the engine's tile summary (R x mo_tile_summary_words(R)
+ * uint32, bit t of row p = word block t of row p is nonzero and stored): only
+ * nonzero blocks are stored. */
+int64_t mo_tile_summary_words(int64_t R);
 int mo_dominance_bits_ranked(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
                              int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* tables,
-                             size_t tables_bytes, void* stream);
+                             size_t tables_bytes, uint32_t* tsum, void* stream);
 
 /* dominance.non_dominated_sort + split_fronts, peeling the
  * bit-matrix.  stop_at > 0 stops at the first front whose cumulative size

@@ -51,6 +51,7 @@ class StepArgs(ctypes.Structure):
 
 _PROTOS = {
     "mo_version": (ctypes.c_char_p, []),
+    "mo_step_args_bytes": (c_sz, []),
     "mo_bits_words_per_row": (c_i64, [c_i64]),
     "mo_trace_offset": (c_i64, [c_i64, c_i32, c_i64]),
     "mo_workspace_bytes": (c_i32, [c_i64, c_i32, c_i32, c_i64, ctypes.POINTER(c_sz)]),
@@ -65,7 +66,9 @@ _PROTOS = {
     "mo_presort": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_dominance_bits_sorted": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "mo_dominance_tables_bytes": (c_sz, [c_i64, c_i32]),
-    "mo_dominance_bits_ranked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "mo_dominance_bits_ranked": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_sz, c_vp,
+                                         c_vp]),
+    "mo_tile_summary_words": (c_i64, [c_i64]),
     "mo_normalize": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "mo_associate": (c_i32, [c_vp, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_u64, c_u32, c_vp, c_vp, c_vp, c_sz,
                              c_vp]),

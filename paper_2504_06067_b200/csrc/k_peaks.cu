@@ -6,6 +6,9 @@
 //   iteration per thread (+ 8 selp to keep the chains live).
 // k_peak_fp32:  8 independent chains of mul.rn + add.rn (no FMA, like the
 //   canonical association dot product): 16 flops per chain-step.
+// k_peak_smem:  conflict-free ld.shared.v4 (each warp reads 512 contiguous
+//   bytes per instruction) from a 32 KB array: shared-memory load bandwidth,
+//   the bound of the rank-mask dominance sweep (k_dom_rank.cu).
 #include "mo_common.cuh"
 
 namespace mo {
@@ -79,8 +82,28 @@ __global__ void __launch_bounds__(256) k_peak_fp32(const float* __restrict__ in,
   if (s == 1234.5f) out[t] = s;
 }
 
+__global__ void __launch_bounds__(256) k_peak_smem(const float* __restrict__ in, int iters, unsigned* out) {
+  __shared__ __align__(16) uint4 sbuf[2048];   // 32 KB
+  for (int i = threadIdx.x; i < 2048; i += 256) sbuf[i] = make_uint4(i, i * 3, i * 5, i * 7);
+  __syncthreads();
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint4 v = sbuf[(threadIdx.x + (it * 8 + u) * 256 + it) & 2047];   // a warp: 512 contiguous bytes
+      acc.x ^= v.x;
+      acc.y ^= v.y;
+      acc.z ^= v.z;
+      acc.w ^= v.w;
+    }
+  }
+  if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x7fffffffu) out[blockIdx.x] = acc.x;
+}
+
 int launch_peak(int which, int blocks, int iters, const float* in, void* out, cudaStream_t s) {
-  if (which == 0)
+  if (which == 2)
+    k_peak_smem<<<blocks, 256, 0, s>>>(in, iters, (unsigned*)out);
+  else if (which == 0)
     k_peak_fsetp<<<blocks, 256, 0, s>>>(in, iters, (unsigned*)out);
   else
     k_peak_fp32<<<blocks, 256, 0, s>>>(in, iters, (float*)out);
@@ -92,6 +115,6 @@ int launch_peak(int which, int blocks, int iters, const float* in, void* out, cu
 
 extern "C" int mo_peak_issue(int32_t which, int32_t blocks, int32_t iters, const float* in64, void* out,
                              void* stream_) {
-  if (which < 0 || which > 1 || blocks < 1 || iters < 1 || !in64 || !out) return MO_ERR_PARAM;
+  if (which < 0 || which > 2 || blocks < 1 || iters < 1 || !in64 || !out) return MO_ERR_PARAM;
   return mo::launch_peak(which, blocks, iters, in64, out, (cudaStream_t)stream_);
 }

@@ -614,7 +614,8 @@ int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* or
 }
 
 
-const char* mo_version(void) { return "manyobj_b200 0.1.0 (sm_100a)"; }
+const char* mo_version(void) { return "manyobj_b200 0.2.0 (sm_100a)"; }
+size_t mo_step_args_bytes(void) { return sizeof(mo_step_args); }
 
 int64_t mo_bits_words_per_row(int64_t R) { return words_per_row(R); }
 
@@ -707,14 +708,16 @@ size_t mo_dominance_tables_bytes(int64_t R, int32_t m) {
   return (R < 1 || m < 2 || m > MO_MAX_M) ? 0 : dom_rank_tables_bytes(R, m);
 }
 
+int64_t mo_tile_summary_words(int64_t R) { return R < 1 ? 0 : tsum_words(R); }
+
 int mo_dominance_bits_ranked(const float* FS, const float* blkmin, const float* blkmax, const int32_t* wend,
                              int64_t R, int32_t m, uint32_t* bits, uint8_t* hasdom, void* tables,
-                             size_t tables_bytes, void* stream_) {
+                             size_t tables_bytes, uint32_t* tsum, void* stream_) {
   if (!FS || !blkmin || !blkmax || !wend || !bits || !hasdom || !tables || m < 2 || m > MO_MAX_M) return MO_ERR_PARAM;
   if (tables_bytes < dom_rank_tables_bytes(R, m)) return MO_ERR_PARAM;
   cudaStream_t s = (cudaStream_t)stream_;
   if (cudaMemsetAsync(hasdom, 0, (size_t)R, s) != cudaSuccess) return MO_ERR_CUDA;
-  return launch_dom_rank(FS, blkmin, blkmax, wend, R, m, bits, hasdom, static_cast<uint32_t*>(tables), s);
+  return launch_dom_rank(FS, blkmin, blkmax, wend, R, m, bits, hasdom, static_cast<uint32_t*>(tables), s, tsum);
 }
 
 int mo_front_peel(const uint32_t* bits, int64_t R, const uint8_t* valid, int64_t stop_at, int32_t* ranks,

@@ -59,11 +59,13 @@ def presort(F):
     return out
 
 
-def dominance_bits_sorted(ps, poison=False, method="ranked"):
+def dominance_bits_sorted(ps, poison=False, method="ranked", summary=None):
     """Bit-matrix of presorted rows (position space) + has-a-dominator flags, from :func:`presort`.
     ``method``: "ranked" (per-objective rank masks, k_dom_rank.cu -- the engine's kernel) or
     "pairwise" (compare-chain tiles, k_dom_tile_sorted).  ``poison`` pre-fills the matrix with ones
-    (tests: words below wend must all be written)."""
+    (tests: words below wend must all be written).  ``summary``: an int32 tensor of R x
+    mo_tile_summary_words(R) words receiving the engine's tile summary (ranked only; then only nonzero
+    256-bit word blocks are stored)."""
     FS = ps["FS"]
     R, m = FS.shape
     L = _lib.lib()
@@ -77,8 +79,9 @@ def dominance_bits_sorted(ps, poison=False, method="ranked"):
         if nbytes == 0:
             raise ParameterError("the rank-mask kernel needs 2 <= m <= 512")
         tables = torch.empty(nbytes, dtype=torch.uint8, device=FS.device)
-        _lib.check(L.mo_dominance_bits_ranked(*args, _lib.ptr(tables), nbytes, _lib.stream_ptr()),
-                   "mo_dominance_bits_ranked")
+        _lib.check(L.mo_dominance_bits_ranked(*args, _lib.ptr(tables), nbytes,
+                                              _lib.ptr(summary) if summary is not None else None,
+                                              _lib.stream_ptr()), "mo_dominance_bits_ranked")
     elif method == "pairwise":
         _lib.check(L.mo_dominance_bits_sorted(*args, _lib.stream_ptr()), "mo_dominance_bits_sorted")
     else:

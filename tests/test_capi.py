@@ -63,4 +63,7 @@ def test_step_args_layout_matches_header(so):
     assert A.n.offset == 16 and A.seed.offset == 32 and A.var.offset == 48 and A.zhat.offset == 64
     assert A.generation_dev.offset == A.workspace_bytes.offset + 8
     assert A.pad3.offset == A.lattice_r.offset + 4 and A.zhat_frag.offset % 8 == 0
-    assert ctypes.sizeof(A) == A.zhat_frag.offset + 8
+    assert A.zhat_umma.offset == A.zhat_frag.offset + 8
+    assert ctypes.sizeof(A) == A.zhat_umma.offset + 8
+    so.mo_step_args_bytes.restype = ctypes.c_size_t
+    assert so.mo_step_args_bytes() == ctypes.sizeof(A)
