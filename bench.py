@@ -248,7 +248,8 @@ def time_kernels(torch, eng, _lib):
     W = int(L.mo_bits_words_per_row(R))
     bits = torch.empty((R, W), dtype=torch.int32, device="cuda")
     hasdom = torch.empty(R, dtype=torch.uint8, device="cuda")
-    tb = int(L.mo_dominance_tables_bytes(R, m))
+    # the engine's choice (mo_capi.cu use_dom_rank): rank masks beyond R = 2048 rows, pairwise tiles below
+    tb = int(L.mo_dominance_tables_bytes(R, m)) if (R > 2048 or m > 16) else 0
     tables = torch.empty(max(tb, 1), dtype=torch.uint8, device="cuda")
     tsum = torch.empty((R, int(L.mo_tile_summary_words(R))), dtype=torch.int32, device="cuda")
     ts = []
@@ -531,10 +532,20 @@ def main():
                                 f"({(pl + pf) / max(1, R * R // (world if sharded else 1)):.4f} of the R^2 ordered "
                                 "pairs; the rest decided by block bounding boxes)")}
         launches = K * (10 + assoc_kernels + 4 * int(kern.get("fronts_issued") or 0))
+    elif kern.get("dom_kernel") == "pairwise":
+        # tiny populations: the pairwise compare-chain tiles (k_dom_tile_sorted), R(R-1)/2 * m compares
+        cmp_work = R * (R - 1) // 2 * m
+        dom_achieved = cmp_work / (kern["dom_tile_ms"] / 1e3)
+        roof = {"kernel": "k_dom_tile_sorted (pairwise dominance tiles)", "bound": "fp32-compare-issue",
+                "achieved": dom_achieved / 1e12, "peak": peaks["compare"] / 1e12, "unit": "Tcmp/s",
+                "frac": dom_achieved / peaks["compare"],
+                "peak_source": "measured: k_peak_fsetp issue microbenchmark (MEASURED_PEAKS.json has no CUDA-core peak)",
+                "algorithmic": f"R(R-1)/2 * m = {cmp_work:.3e} compares per launch"}
+        launches = K * (7 + assoc_kernels)
     else:
         # rank-mask sweep (k_dom_rank): per (row j, 256-row block I) of the upper block triangle and per
         # objective, one 256-bit prefix mask (32 B) and a 9-level Eytzinger search (9 x 4 B) read from
-        # shared memory -- the minimum the algorithm must read; bound: shared-memory load bandwidth
+        # shared memory -- the minimum the algorithm reads; bound: shared-memory load bandwidth
         nb = (R + 255) // 256
         pairs = sum(min(256, R - bj * 256) * (bj + 1) for bj in range(nb))
         smem_bytes = pairs * m * (32 + 9 * 4)
@@ -546,7 +557,7 @@ def main():
                                "nominal); MEASURED_PEAKS.json has HBM and tensor peaks only",
                 "algorithmic": (f"{pairs:.4e} (row, 256-row block) pairs x m = {m} x (32 B mask + 36 B search) = "
                                 f"{smem_bytes:.4e} B of shared-memory reads per launch")}
-        launches = K * (8 + assoc_kernels)
+        launches = K * (8 + assoc_kernels)   # + k_dom_tables
     roof["traffic"] = traffic
     roof["traffic_note"] = ("DRAM bytes per launch (read + write) of the dominant kernel from the committed ncu "
                             f"--set full capture profiles/{cap[1] if cap else '-'}; the bit-matrix stays in the "

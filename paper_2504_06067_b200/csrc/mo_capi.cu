@@ -303,13 +303,16 @@ static PresortArgs presort_args(const mo_step_args* a, const Layout& L) {
 
 // rank-mask dominance (k_dom_rank.cu) for 2 <= m <= MO_MAX_M; MO_DOM_PAIRWISE=1 selects the pairwise
 // compare-chain tiles (k_dom_tile_sorted) instead
-static bool use_dom_rank(int m) {
+// Tiny populations (R <= 2048, e.g. C1) keep the one-launch pairwise tiles: there the splitter / table
+// kernels cost more than the compare chains they replace (C1: 10.8k vs 9.1k generations/s).
+static bool use_dom_rank(int m, int64_t R) {
   static int off = -1;
   if (off < 0) {
     const char* e = getenv("MO_DOM_PAIRWISE");
     off = (e && e[0] == '1') ? 1 : 0;
   }
-  return (!off || m > 16) && m >= 2 && m <= MO_MAX_M;   // the pairwise tiles stop at m = 16
+  if (m > 16) return m <= MO_MAX_M;   // the pairwise tiles stop at m = 16
+  return !off && m >= 2 && R > 2048;
 }
 
 static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
@@ -330,7 +333,7 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
     no_tsum = (e && e[0] == '1') ? 1 : 0;
   }
   uint32_t* tsum = nullptr;
-  if (use_dom_rank(a->m)) {
+  if (use_dom_rank(a->m, R)) {
     tsum = no_tsum ? nullptr : at<uint32_t>(ws, L.tsum);
     MO_TRY(launch_dom_rank(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, at<uint32_t>(ws, L.dtab), s,
                            tsum));
