@@ -35,6 +35,7 @@
 // tcgen05.ld -> release -> next MMA) bounds it, not the MMA or the FMNMX3 work; N = 64 with four buffers
 // and two CTAs per SM (N = 64, 256 TMEM columns each) both measured slower (2.7 / 2.5 ms vs 2.2 ms).
 #include <cuda_fp16.h>
+#include <stdlib.h>
 #include <cuda_runtime.h>
 
 #include "mo_async.cuh"
@@ -197,7 +198,7 @@ __device__ __forceinline__ void ua_exact(const AssocArgs& a, const int32_t* colr
 }
 
 template <int M>
-__global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int chunks) {
+__global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int chunks, int dbg) {
   constexpr int KS = ua_ks(M);
   constexpr int TILE = KS * UA_STEP_BYTES;          // one packed reference tile
   constexpr int ATILE = KS * UA_A_STEP;             // one row tile of A
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
           for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
             for (int k = 0; k < KS; ++k)
+              if (!(dbg & 2))   // debug timing: 2 = no MMA issue (commits only)
               ua_mma(tmem + (uint32_t)(buf * 2 + rt) * UA_N, ua_desc(abase + (uint32_t)(rt * ATILE + k * UA_A_STEP)),
                      ua_desc(bbase + (uint32_t)(s * TILE + k * UA_STEP_BYTES)), k > 0 ? 1u : 0u);
           ua_commit(&sEmpty[s]);
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
       unsigned long long best[2] = {0ull, 0ull};
       const int wu = min(UA_WARM, t1 - t0);
       for (int ti = 0; ti < wu + (t1 - t0); ++ti) {
-        const bool warm = ti < wu;   // warm-up pass over the first tiles: running maxima only
+        const bool warm = ti < wu || (dbg & 1);   // warm-up pass: running maxima only (dbg 1: always)
         const int t = warm ? t0 + ti : t0 + ti - wu;
         mbar_wait(&sTFull[buf], tph);
         tc_fence_after();
@@ -486,6 +488,11 @@ int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
   }
   static int sms = 0;
   static bool attr[17] = {};
+  static int dbg = -1;   // MO_UMMA_DEBUG (timing experiments only; results invalid when set)
+  if (dbg < 0) {
+    const char* e = getenv("MO_UMMA_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -507,7 +514,7 @@ int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
         return MO_ERR_CUDA;                                                                                 \
       attr[MM] = true;                                                                                      \
     }                                                                                                       \
-    MO_TRY(launch_ex(k_assoc_umma<MM>, grid, blk, ua_smem(ua_ks(MM)), s, false, g_mo_pdl, a, (int)chunks)); \
+    MO_TRY(launch_ex(k_assoc_umma<MM>, grid, blk, ua_smem(ua_ks(MM)), s, false, g_mo_pdl, a, (int)chunks, dbg)); \
     break;
     MO_UA_CASE(2) MO_UA_CASE(3) MO_UA_CASE(4) MO_UA_CASE(5) MO_UA_CASE(6) MO_UA_CASE(7) MO_UA_CASE(8)
     MO_UA_CASE(9) MO_UA_CASE(10) MO_UA_CASE(11) MO_UA_CASE(12) MO_UA_CASE(13) MO_UA_CASE(14)
