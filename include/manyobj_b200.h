@@ -390,6 +390,12 @@ size_t mo_pack_refs_f16_bytes(int64_t w, int32_t m);
 int mo_pack_refs_f16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
 int mo_pack_refs_bf16(const float* zhat, int64_t w, int32_t m, const int32_t* order, void* out, void* stream);
 
+/* Byte offsets (into a mo_step workspace of the same sizing arguments) of the
+ * niche-selection state one step leaves behind -- for the debug bookkeeping
+ * check and niche trace of SPEC.md:406, :424 (niche.check_bookkeeping): out11 =
+ * {pi, d, rho, rho_p, take, kept, prom, pos_pop, perm_pop, pos_ref, perm_ref}. */
+int mo_niche_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count, int64_t* out11);
+
 /* ------------------------------------------- op-level API (k_ops.cu)
  * The reference's per-op functions as device kernels, for callers of the
  * per-op API (the engine runs these stages fused inside mo_step).  Index and

@@ -97,6 +97,7 @@ _PROTOS = {
     "mo_workspace_bytes_ex": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_sz)]),
     "mo_stream_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64),
                                   ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "mo_niche_offsets": (c_i32, [c_i64, c_i32, c_i64, c_i32, c_i32, ctypes.POINTER(c_i64)]),
     # op-level API (k_ops.cu)
     "mo_ops_workspace_bytes": (c_i32, [c_i64, c_i64, ctypes.POINTER(c_sz)]),
     "mo_step_mask": (c_i32, [c_vp, c_i64, c_vp, c_vp]),
@@ -188,6 +189,15 @@ def stream_offsets(n, m, w, sort_mode, shards):
     check(load_library_cached().mo_stream_offsets(int(n), int(m), int(w), int(sort_mode), int(shards),
                                                   *[ctypes.byref(o) for o in out]), "mo_stream_offsets")
     return tuple(int(o.value) for o in out)
+
+
+def niche_offsets(n, m, w, sort_mode, shards):
+    """Byte offsets of the niche state of one step in the workspace (mo_niche_offsets)."""
+    out = (c_i64 * 11)()
+    check(load_library_cached().mo_niche_offsets(int(n), int(m), int(w), int(sort_mode), int(shards), out),
+          "mo_niche_offsets")
+    keys = ("pi", "d", "rho", "rho_p", "take", "kept", "prom", "pos_pop", "perm_pop", "pos_ref", "perm_ref")
+    return dict(zip(keys, (int(x) for x in out)))
 
 
 _host_lib = None

@@ -900,4 +900,17 @@ int mo_stream_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_
   return MO_OK;
 }
 
+// byte offsets of the niche-selection state a step leaves in its workspace (debug bookkeeping check /
+// niche trace): [0] pi (int32 R), [1] d (f32 R), [2] rho, [3] rho_p, [4] take,
+// [5] kept (int32 w+1 each), [6] prom (u8 R), [7] pos_pop, [8] perm_pop (int32 R), [9] pos_ref,
+// [10] perm_ref (int32 w)
+int mo_niche_offsets(int64_t n, int32_t m, int64_t w, int32_t sort_mode, int32_t shard_count, int64_t* out11) {
+  if (n < 1 || m < 1 || w < 1 || shard_count < 0 || !out11) return MO_ERR_PARAM;
+  Layout L = make_layout(2 * n, w, m, sort_mode, shards_of(shard_count));
+  const size_t v[11] = {L.pi, L.d, L.rho, L.rho_p, L.take, L.kept, L.prom, L.pos_pop, L.perm_pop, L.pos_ref,
+                        L.perm_ref};
+  for (int i = 0; i < 11; ++i) out11[i] = (int64_t)v[i];
+  return MO_OK;
+}
+
 }  // extern "C"

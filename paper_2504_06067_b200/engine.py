@@ -39,7 +39,7 @@ import numpy as np
 import torch
 
 from . import _lib, problems, refpoints
-from .errors import ConfigError, raise_for_status
+from .errors import ConfigError, ShapeError, raise_for_status
 from .variation import VariationConfig, init_population
 
 
@@ -93,9 +93,14 @@ class Engine:
     """Device-resident NSGA-III run: buffers, workspace and (optionally) a CUDA graph."""
 
     def __init__(self, cfg, graph=False, device=None, sort="auto", group=None, shard=None, poll=4, prune="auto",
-                 host_fronts=None, prune_r=0):
+                 host_fronts=None, prune_r=0, debug=False):
+        """``debug``: after every eager step, recompute the niche bookkeeping from scratch
+        (niche.check_bookkeeping) and keep the niche trace records in
+        ``self.niche_trace``; raises RuntimeError on the first inconsistency.  Costs host syncs."""
         validate(cfg)
         self.cfg = cfg
+        self.debug = bool(debug)
+        self.niche_trace = []
         self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         n, m, d = cfg.n, cfg.m, cfg.d
         self.problem = problems.ContinuousProblem(cfg.problem, m, d)
@@ -267,6 +272,51 @@ class Engine:
         self._step_dispatch(profile)
         self._gen_dev_synced = False
         self._post_error_copy()
+        if self.debug:
+            from . import niche
+            self.check_errors(block=True)
+            self.niche_trace.append(niche.trace(self))
+            bad = [k for k, ok in niche.check_bookkeeping(self).items() if not ok]
+            if bad:
+                raise RuntimeError(f"niche bookkeeping mismatch at generation {self.generation - 1}: {bad}")
+
+    # ------------------------------------------------------------ snapshots
+    def snapshot(self):
+        """Run-state snapshot: the population, its objectives, the running ideal,
+        the generation counter and the configuration -- everything a generation depends on (the
+        keyed RNG streams are functions of (seed, generation)), so a restored engine continues
+        bit-identically.  Host numpy arrays + plain values."""
+        import dataclasses
+        self.check_errors(block=True)
+        cfg = dataclasses.asdict(self.cfg)
+        return {"format": "manyobj_b200.snapshot/1", "generation": int(self.generation), "config": cfg,
+                "X": self.X.cpu().numpy().copy(), "F": self.F.cpu().numpy().copy(),
+                "ideal": self.ideal.cpu().numpy().copy()}
+
+    def restore(self, snap):
+        """Load a :meth:`snapshot` of a run with the same configuration into this engine."""
+        import dataclasses
+        if snap.get("format") != "manyobj_b200.snapshot/1":
+            raise ConfigError("snapshot", "unknown snapshot format")
+        import json
+
+        def canon(c):   # JSON form: tuples and lists compare equal
+            c = json.loads(json.dumps(c, default=_json_default))
+            c.pop("generations", None)
+            return c
+        if canon(dataclasses.asdict(self.cfg)) != canon(dict(snap["config"])):
+            raise ConfigError("snapshot", "snapshot of a different RunConfig")
+        n, m, d = self.cfg.n, self.cfg.m, self.cfg.d
+        X = torch.as_tensor(np.asarray(snap["X"], np.float32))
+        F = torch.as_tensor(np.asarray(snap["F"], np.float32))
+        if X.shape != (n, d) or F.shape != (n, m):
+            raise ShapeError(f"snapshot population {tuple(X.shape)} / {tuple(F.shape)}")
+        self.XR[self.cur][:n].copy_(X)
+        self.FR[self.cur][:n].copy_(F)
+        self.ideal.copy_(torch.as_tensor(np.asarray(snap["ideal"], np.float32)))
+        self.generation = int(snap["generation"])
+        self._gen_dev_synced = False
+        torch.cuda.synchronize(self.dev)
 
     def _post_error_copy(self):
         self._err_host.copy_(self.info[_lib.INFO["ERROR_FIRST"]: _lib.INFO["ERROR_FIRST"] + 1], non_blocking=True)
@@ -577,5 +627,41 @@ def run(cfg, record=True, profile=False, graph=False, **engine_kw):
     return history, state
 
 
+def save_state(state, path):
+    """Write a run-state snapshot (Engine.snapshot) to ``path`` (numpy .npz; SPEC.md:492's optional binary
+    snapshot of the population)."""
+    import json
+    snap = state.engine.snapshot() if isinstance(state, RunState) else state.snapshot()
+    meta = {"format": snap["format"], "generation": snap["generation"], "config": snap["config"]}
+    np.savez(path, X=snap["X"], F=snap["F"], ideal=snap["ideal"],
+             meta=np.frombuffer(json.dumps(meta, default=_json_default).encode(), dtype=np.uint8))
+
+
+def _json_default(o):
+    import dataclasses
+    if dataclasses.is_dataclass(o):
+        return dataclasses.asdict(o)
+    raise TypeError(repr(o))
+
+
+def load_state(path, cfg=None, **engine_kw):
+    """Resume a run from :func:`save_state`: a new Engine (``engine_kw`` as for initialize) holding the
+    snapshot's population at its generation.  ``cfg`` defaults to the snapshot's configuration."""
+    import json
+    with np.load(path) as z:
+        meta = json.loads(bytes(z["meta"]).decode())
+        snap = {"format": meta["format"], "generation": meta["generation"], "config": meta["config"],
+                "X": z["X"], "F": z["F"], "ideal": z["ideal"]}
+    if cfg is None:
+        c = dict(meta["config"])
+        c["variation"] = VariationConfig(**c["variation"])
+        if c.get("reference_points") is not None:
+            c["reference_points"] = tuple(c["reference_points"])
+        cfg = RunConfig(**c)
+    eng = Engine(cfg, **engine_kw)
+    eng.restore(snap)
+    return _state(eng, {})
+
+
 __all__ = ["RunConfig", "RunState", "Engine", "LocalShards", "initialize", "step", "run", "validate",
-           "build_reference_set", "run_collective"]
+           "build_reference_set", "run_collective", "save_state", "load_state"]

@@ -212,3 +212,111 @@ def perpendicular_distance_matrix(Fn, Z):
 
 __all__ = ["normalize_objectives", "associate", "associate_canonical", "niche_counts", "nearest_selection",
            "build_cache", "batched_random_selection", "niche_select", "perpendicular_distance_matrix", "DROPPED"]
+
+
+# ------------------------------------------------------------------ debug bookkeeping / niche trace
+
+def niche_state(engine):
+    """Views of the niche-selection state the engine's last step left in its workspace (valid until the
+    next step): pi, d, prom (per merged row); rho, rho_p (post-nearest counts), take (cache entries taken)
+    per reference point; the row / reference positions of that generation's shuffles."""
+    cfg = engine.cfg
+    n, m, w = cfg.n, cfg.m, engine.w
+    R = 2 * n
+    off = _lib.niche_offsets(n, m, w, engine.sort_mode, engine.shard_count)
+    ws = engine.ws
+
+    def i32(name, count):
+        return ws[off[name]: off[name] + 4 * count].view(torch.int32)
+    return {"pi": i32("pi", R), "d": ws[off["d"]: off["d"] + 4 * R].view(torch.float32),
+            "prom": ws[off["prom"]: off["prom"] + R].bool(), "rho": i32("rho", w), "rho_p": i32("rho_p", w),
+            "take": i32("take", w), "pos_pop": i32("pos_pop", R), "pos_ref": i32("pos_ref", w)}
+
+
+def trace(engine):
+    """The SPEC debug trace record of the last step's niching: post-nearest counts rho /
+    rho', the per-point takes, the water level L* (the batched loop's iterations collapse into it) and
+    the promoted rows.  A plain dict (host lists), one record per generation."""
+    info = engine.info_dict()
+    st = niche_state(engine)
+    return {"generation": engine.generation - 1, "l": info["l"], "k": info["k"], "nearest": info["nearest"],
+            "level": info["level"], "skipped": info["skipped"], "rho": st["rho"].tolist(),
+            "rho_prime": st["rho_p"].tolist(), "take": st["take"].tolist(),
+            "promoted": torch.nonzero(st["prom"]).flatten().tolist()}
+
+
+def check_bookkeeping(engine):
+    """SPEC.md:406's debug-mode check, in the closed form the engine computes: recompute from scratch
+    (from the final ranks, the association and the promoted flags of the last step) the niche counts over
+    F_s, the nearest-selection outcome, the post-nearest counts rho / rho', the per-point takes against
+    the water level, the cache order (the taken members of a point are its take_j lowest shuffled
+    positions) and the survivor count.  Returns {check: bool}; all True on a consistent step."""
+    info = engine.info_dict()
+    n, w = engine.cfg.n, engine.w
+    out = {"survivors": info["survivors"] == n}
+    if info["skipped"]:
+        return out
+    st = niche_state(engine)
+    l, k = info["l"], info["k"]
+    ranks = engine.ranks
+    prom = st["prom"]
+    orig = torch.where(prom, torch.full_like(ranks, l), ranks)
+    Fs = (orig >= 0) & (orig < l)
+    Fl = orig == l
+    pi = st["pi"].long()
+    rho0 = torch.bincount(pi[Fs], minlength=w)[:w]
+    rhop0 = torch.bincount(pi[Fl], minlength=w)[:w]
+    empty = (rho0 == 0) & (rhop0 > 0)
+    M0 = int(empty.sum())
+    out["final_ranks"] = bool(((ranks < l) & (ranks >= 0)).sum() == n)
+    # nearest candidate of every empty niche: min (d, shuffled position) over its F_l members
+    R = ranks.numel()
+    pos = st["pos_pop"].long()
+    rows = torch.nonzero(Fl).flatten()
+    d = st["d"][rows].double()
+    key = pi[rows] * (R + 1) + pos[rows]               # group by niche, ties by shuffled position
+    order = torch.argsort(key)
+    order = order[torch.sort(d[order], stable=True).indices]
+    grp = pi[rows][order]
+    first = torch.ones_like(grp, dtype=torch.bool)
+    g_sorted, perm = torch.sort(grp, stable=True)
+    first_s = torch.ones_like(g_sorted, dtype=torch.bool)
+    first_s[1:] = g_sorted[1:] != g_sorted[:-1]
+    first[perm] = first_s
+    nearest_rows = rows[order][first & empty[grp]]
+    if M0 > k:   # truncated: the first k empty niches in shuffled reference order take their nearest
+        pos_ref = st["pos_ref"].long()
+        nn = pi[nearest_rows]
+        keep = torch.argsort(pos_ref[nn])[:k]
+        want = torch.zeros_like(prom)
+        want[nearest_rows[keep]] = True
+        out["nearest_truncated"] = bool(torch.equal(want, prom))
+        out["nearest_count"] = info["nearest"] == k
+        return out
+    out["nearest_count"] = info["nearest"] == M0
+    out["nearest_promoted"] = bool(prom[nearest_rows].all())
+    rho_post = rho0 + empty.long()
+    rhop_post = rhop0 - empty.long()
+    out["rho_post_nearest"] = bool(torch.equal(rho_post, st["rho"].long()))
+    out["rho_prime_post_nearest"] = bool(torch.equal(rhop_post, st["rho_p"].long()))
+    take = st["take"].long()
+    per_point = torch.bincount(pi[prom], minlength=w)[:w]
+    out["takes_per_point"] = bool(torch.equal(per_point, empty.long() + take))
+    out["takes_total"] = int(take.sum()) == k - M0
+    L = info["level"]
+    lo = torch.clamp(L - rho_post, min=0)
+    lo = torch.minimum(lo, rhop_post)
+    hi = torch.minimum(torch.clamp(L + 1 - rho_post, min=0), rhop_post)
+    out["water_level"] = bool(((take >= lo) & (take <= hi)).all())
+    # cache order: among the non-nearest F_l members of a point, exactly the take_j lowest positions
+    is_near = torch.zeros_like(prom)
+    is_near[nearest_rows] = True
+    cm = torch.nonzero(Fl & ~is_near).flatten()
+    kk = pi[cm] * (R + 1) + pos[cm]
+    o = torch.argsort(kk)
+    gp = pi[cm][o]
+    start = torch.zeros(w + 1, dtype=torch.long, device=gp.device)
+    start[1:] = torch.cumsum(torch.bincount(gp, minlength=w)[:w], 0)
+    idx = torch.arange(gp.numel(), device=gp.device) - start[gp]
+    out["cache_order"] = bool(torch.equal(prom[cm][o], idx < take[gp]))
+    return out
