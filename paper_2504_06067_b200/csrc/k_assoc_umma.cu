@@ -53,12 +53,12 @@ constexpr int UA_EPI_WARPS = 8;   // 10 warps: <= 3 per SM sub-partition, 168 re
 constexpr int UA_EPI = UA_EPI_WARPS * 32;
 constexpr int UA_THREADS = 64 + UA_EPI;
 constexpr int UA_TMEM_COLS = 512;                // 2 buffers x 2 row tiles x 128 columns
-constexpr int UA_NB = 6;                         // candidate buffer entries per (thread, row tile)
+constexpr int UA_NB = 8;                         // candidate chunks buffered per (thread, row tile)
 constexpr int UA_RING_BYTES = 96 * 1024;
 constexpr int UA_WARM = 8;                       // warm-up tiles per item (running maxima before candidates)
 __host__ __device__ constexpr int ua_ks(int m) { return (3 * m + 15) / 16; }   // K16 steps for K = 3m
 __host__ __device__ constexpr size_t ua_smem(int ks) {                         // > 114 KB: 1 CTA/SM
-  return 1024 + 2 * (size_t)ks * UA_A_STEP + UA_RING_BYTES + 2 * (size_t)UA_NB * UA_EPI * 8 + 32 * UA_EPI * 4;
+  return 1024 + 2 * (size_t)ks * UA_A_STEP + UA_RING_BYTES + 2 * (size_t)UA_NB * UA_EPI * 12;
 }
 
 // byte offset of element (row n, k) in a K-major no-swizzle tile of 8-row x 16-byte core matrices:
@@ -183,18 +183,24 @@ __device__ __forceinline__ void ua_load_fn(const AssocArgs& a, int row, float (&
   }
 }
 
-// canonical key of packed column cg for candidate row `row` (objectives re-read: rare)
+// canonical keys of the packed columns col0 + i, i in the bitmask `qm` (the columns of a 32-column chunk
+// that were within 2 eps of the running maximum when the chunk was seen), for candidate row `row`
+// (objectives re-read: only chunks still within 2 eps of the row's final running maximum get here)
 template <int M>
-__device__ __forceinline__ void ua_exact(const AssocArgs& a, const int32_t* colref, int row, int cg,
-                                         unsigned long long& best) {
-  const int j = __ldg(colref + cg);
-  if (j < 0) return;
+__device__ __forceinline__ void ua_exact_cols(const AssocArgs& a, const int32_t* colref, int row, int col0,
+                                              uint32_t qm, unsigned long long& best) {
   float fn[M];
   ua_load_fn<M>(a, row, fn);
-  const int p = __ldg(a.pos_ref + j);
-  const float tk = ua_canon_dot<M>(fn, a.zs + (int64_t)p * M);
-  const unsigned long long key = ((unsigned long long)f2ord(tk) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
-  best = key > best ? key : best;
+  while (qm) {
+    const int i = __ffs(qm) - 1;
+    qm &= qm - 1u;
+    const int j = __ldg(colref + col0 + i);
+    if (j < 0) continue;
+    const int p = __ldg(a.pos_ref + j);
+    const float tk = ua_canon_dot<M>(fn, a.zs + (int64_t)p * M);
+    const unsigned long long key = ((unsigned long long)f2ord(tk) << 32) | (uint32_t)(0xffffffffu - (uint32_t)p);
+    best = key > best ? key : best;
+  }
 }
 
 template <int M>
@@ -219,9 +225,9 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ua_dyn) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = base;                              // 2 row tiles x KS steps
   uint8_t* sB = base + 2 * ATILE;                  // ring
-  float* sCV = reinterpret_cast<float*>(sB + UA_RING_BYTES);   // candidate values  [rt][NB][thread]
-  int* sCC = reinterpret_cast<int*>(sCV + 2 * UA_NB * UA_EPI); // candidate columns
-  float* sStage = reinterpret_cast<float*>(sCC + 2 * UA_NB * UA_EPI);   // a triggered chunk [32][thread]
+  float* sCV = reinterpret_cast<float*>(sB + UA_RING_BYTES);   // candidate chunks: max t~ [rt][NB][thread]
+  int* sCC = reinterpret_cast<int*>(sCV + 2 * UA_NB * UA_EPI); // candidate chunks: first packed column
+  uint32_t* sCM = reinterpret_cast<uint32_t*>(sCC + 2 * UA_NB * UA_EPI);   // qualifying columns of the chunk
   const uint8_t* tiles = static_cast<const uint8_t*>(a.zumma);
   const int32_t* colref = reinterpret_cast<const int32_t*>(tiles + (int64_t)ntiles * TILE);
   if (threadIdx.x == 0) {
@@ -415,40 +421,37 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const float s = sm[rt][h];
-            if (s >= mxr[rt] - marg[rt]) {   // a column within 2 eps of the best seen: buffer the candidates
+            if (s >= mxr[rt] - marg[rt]) {   // a column within 2 eps of the best seen: remember the chunk
               const float mn = fmaxf(mxr[rt], s), th = mn - marg[rt];
               uint32_t qm = 0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                qm |= (__uint_as_float(u[rt][h][i]) >= th ? 1u : 0u) << i;
-                sStage[i * UA_EPI + et] = __uint_as_float(u[rt][h][i]);   // read back by column index
-              }
-              while (qm) {
-                const int i = __ffs(qm) - 1;
-                qm &= qm - 1u;
-                if (cnt[rt] == UA_NB) {   // full: drop what the new maximum excludes, evaluate the rest
-                  int kept = 0;
-                  for (int b = 0; b < UA_NB; ++b) {
-                    const int idx = (rt * UA_NB + b) * UA_EPI + et;
-                    if (sCV[idx] >= th) {
-                      const int to = (rt * UA_NB + kept) * UA_EPI + et;
-                      sCV[to] = sCV[idx];
-                      sCC[to] = sCC[idx];
-                      ++kept;
-                    }
+              for (int i = 0; i < 32; ++i) qm |= (__uint_as_float(u[rt][h][i]) >= th ? 1u : 0u) << i;
+              if (cnt[rt] == UA_NB) {   // full: drop the chunks the new maximum excludes, evaluate the rest
+                int kept = 0;
+                for (int b2 = 0; b2 < UA_NB; ++b2) {
+                  const int idx = (rt * UA_NB + b2) * UA_EPI + et;
+                  if (sCV[idx] >= th) {
+                    const int to = (rt * UA_NB + kept) * UA_EPI + et;
+                    sCV[to] = sCV[idx];
+                    sCC[to] = sCC[idx];
+                    sCM[to] = sCM[idx];
+                    ++kept;
                   }
-                  if (kept == UA_NB) {
-                    for (int b = 0; b < UA_NB; ++b)
-                      ua_exact<M>(a, colref, row[rt], sCC[(rt * UA_NB + b) * UA_EPI + et], best[rt]);
-                    kept = 0;
-                  }
-                  cnt[rt] = kept;
                 }
-                const int to = (rt * UA_NB + cnt[rt]) * UA_EPI + et;
-                sCV[to] = sStage[i * UA_EPI + et];
-                sCC[to] = t * UA_N + cgp * 64 + h * 32 + i;
-                ++cnt[rt];
+                if (kept == UA_NB) {
+                  for (int b2 = 0; b2 < UA_NB; ++b2) {
+                    const int idx = (rt * UA_NB + b2) * UA_EPI + et;
+                    ua_exact_cols<M>(a, colref, row[rt], sCC[idx], sCM[idx], best[rt]);
+                  }
+                  kept = 0;
+                }
+                cnt[rt] = kept;
               }
+              const int to = (rt * UA_NB + cnt[rt]) * UA_EPI + et;
+              sCV[to] = s;
+              sCC[to] = t * UA_N + cgp * 64 + h * 32;
+              sCM[to] = qm;
+              ++cnt[rt];
               mxr[rt] = mn;
             }
           }
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
         const float th = mxr[rt] - marg[rt];
         for (int b = 0; b < cnt[rt]; ++b) {
           const int idx = (rt * UA_NB + b) * UA_EPI + et;
-          if (sCV[idx] >= th) ua_exact<M>(a, colref, row[rt], sCC[idx], best[rt]);
+          if (sCV[idx] >= th) ua_exact_cols<M>(a, colref, row[rt], sCC[idx], sCM[idx], best[rt]);
         }
         if (best[rt]) atomicMax(&a.akey[row[rt]], best[rt]);
       }

@@ -7,12 +7,8 @@
 // For a 256-row block I of the S-presorted rows and one objective k, the set {i in I : a_ik <= b}
 // is the prefix of I's rows sorted by objective k whose length c is the number of values <= b.
 // So per block and objective we precompute (k_dom_tables):
-//   * the block's sorted values and a bucket table: with Q = 256 global splitters s_0 <= ... <= s_255
-//     of objective k (k_dom_splitters: a sorted sample of the population), bucket q of a value b is
-//     #{t : s_t <= b}, and tab[q] = (#{a_i < s_(q-1)}, #{a_i < s_q}) -- every value below the bucket
-//     is <= b, every value from the next splitter on is > b, so c = lo + #{sorted positions in
-//     [lo, hi) whose value is <= b} (about one comparison per lookup); each row's bucket index per
-//     objective is computed once per generation (qidx), not once per block;
+//   * the sorted values in Eytzinger (BFS) order, 511 slots padded with NaN -> c by 9 branch-free
+//     probes, conflict-free in shared memory (level t of the tree is 2^t contiguous words);
 //   * the 257 prefix masks P_k[c] (256 bits = 8 words each).
 // Then, for a row j, the 256 bits "a_i <= b_j in every objective" are AND_k P_k[c_k(j)]: m searches
 // and m x 8 word ANDs for 256 pairs instead of 256 m-long compare chains (about 1.6 instructions per
@@ -25,8 +21,8 @@
 //
 // k_dom_rank: persistent grid over items (I block, run of J blocks).  The CTA pulls block I's m
 // tables (m x 10,272 B) into shared memory with ONE bulk TMA copy (cp.async.bulk + mbarrier), then
-// sweeps its J blocks, one row j per thread: b_j and its bucket indices from L2, m bucket lookups
-// (unrolled across the m objectives for ILP), the mask ANDs, 8 words stored to row j.  Reverse-direction words of the
+// sweeps its J blocks, one row j per thread: b_j from FS (L2), m Eytzinger searches (unrolled across
+// the m objectives for ILP), the mask ANDs, 8 words stored to row j.  Reverse-direction words of the
 // overlapping tiles are transposed through warp ballots and shared memory.
 #include <cuda_runtime.h>
 
@@ -37,13 +33,10 @@
 namespace mo {
 
 constexpr int DR_BLK = 256;                        // rows per block (= the bit-matrix tile)
-constexpr int DR_Q = 256;                          // global splitters per objective
-constexpr int DR_TAB = 260;                        // bucket table words (q = 0..DR_Q used), padded
-constexpr int DR_SV = DR_BLK;                      // the block's sorted values (NaN last)
-constexpr int DR_MOFF = DR_TAB + DR_SV;            // prefix masks start
+constexpr int DR_EYT = 512;                        // Eytzinger slots (1..511 used)
 constexpr int DR_MASKS = DR_BLK + 1;               // prefix masks c = 0..256
-constexpr int DR_TBL_WORDS = DR_MOFF + DR_MASKS * 8;
-constexpr int DR_TBL_BYTES = DR_TBL_WORDS * 4;     // 10,288 (16-byte multiple)
+constexpr int DR_TBL_WORDS = DR_EYT + DR_MASKS * 8;
+constexpr int DR_TBL_BYTES = DR_TBL_WORDS * 4;     // 10,272 (16-byte multiple)
 static_assert(DR_TBL_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
 
 __host__ __device__ inline int64_t dom_rank_blocks(int64_t R) { return (R + DR_BLK - 1) / DR_BLK; }
@@ -52,41 +45,13 @@ __host__ __device__ inline int64_t dom_rank_blocks(int64_t R) { return (R + DR_B
 // bank groups of a 128-bit shared-memory phase
 __device__ __forceinline__ int mask_slot(int c, int h) { return 2 * c + (h ^ ((c >> 2) & 1)); }
 
-// ------------------------------------------------------------------ splitters
-// grid m: the Q sorted values of objective k at Q evenly spaced rows (NaN last; -0 -> +0)
-__global__ void __launch_bounds__(DR_Q) k_dom_splitters(const float* __restrict__ FS, int R, int m,
-                                                        float* __restrict__ spl) {
-  pdl_wait();
-  __shared__ uint32_t sKey[DR_Q];
-  const int k = blockIdx.x, t = threadIdx.x;
-  const int64_t r = (int64_t)t * R / DR_Q;
-  const float x = FS[r * m + k];
-  sKey[t] = x != x ? 0xffffffffu : f2ord(__fadd_rn(x, 0.0f));
-  __syncthreads();
-  for (int size = 2; size <= DR_Q; size <<= 1)
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const int p = t ^ stride;
-      if (p > t) {
-        const bool up = (t & size) == 0;
-        const uint32_t a = sKey[t], b = sKey[p];
-        if ((a > b) == up) {
-          sKey[t] = b;
-          sKey[p] = a;
-        }
-      }
-      __syncthreads();
-    }
-  spl[k * DR_Q + t] = sKey[t] == 0xffffffffu ? __int_as_float(0x7fc00000) : ord2f(sKey[t]);
-}
-
 // ------------------------------------------------------------------ tables
 // grid (nb, M): block bi, objective k.  vmask[bi*8 + w]: rows of block bi that exist and have no NaN.
 // M = 0: runtime m (the wide-m path, m > 16)
 template <int M>
 __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__ FS, int R,
                                                         uint32_t* __restrict__ tables, uint32_t* __restrict__ vmask,
-                                                        int m_rt, uint32_t* __restrict__ tsum,
-                                                        const float* __restrict__ spl, uint16_t* __restrict__ qidx) {
+                                                        int m_rt, uint32_t* __restrict__ tsum) {
   pdl_wait();
   const int m = M > 0 ? M : m_rt;
   if (tsum && blockIdx.y == 0) {   // this generation's tile summary of block bi's rows starts empty
@@ -131,46 +96,18 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__
     }
   }
   uint32_t* tab = tables + ((int64_t)bi * m + k) * DR_TBL_WORDS;
-  // sorted values; bucket table (lo, hi) = (#{a < s_(q-1)}, #{a < s_q}), a NaN splitter counting every
-  // non-NaN value; this block's rows' bucket indices
-  __shared__ float sVal[DR_BLK], sSpl[DR_Q];
-  __shared__ int sCnt[DR_Q];
-  const bool fin = sKey[t] != 0xffffffffu;
-  sVal[t] = fin ? ord2f(sKey[t]) : __int_as_float(0x7fc00000);
-  sSpl[t] = spl[k * DR_Q + t];
-  const int nonnan = __syncthreads_count(fin);
-  tab[DR_TAB + t] = __float_as_uint(sVal[t]);
-  {
-    const float sp = sSpl[t];
-    int lo = 0, hi = nonnan;
-    if (sp == sp) {
-      while (lo < hi) {   // lower bound: #{a < sp}
-        const int mid = (lo + hi) >> 1;
-        if (sVal[mid] < sp) lo = mid + 1;
-        else hi = mid;
-      }
-    } else {
-      lo = nonnan;
+  // Eytzinger: node n at depth d holds sorted position ((2 (n - 2^d) + 1) << (8 - d)) - 1
+  for (int n = t; n < DR_EYT; n += DR_BLK) {
+    float v = __int_as_float(0x7fc00000);
+    if (n >= 1) {
+      const int d = 31 - __clz(n);
+      const int pos = ((2 * (n - (1 << d)) + 1) << (8 - d)) - 1;
+      if (pos < DR_BLK && sKey[pos] != 0xffffffffu) v = ord2f(sKey[pos]);
     }
-    sCnt[t] = lo;
-  }
-  if (i < R) {   // #{t : s_t <= b}: NaN splitters (last) never count
-    int lo = 0, hi = DR_Q;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sSpl[mid] <= x) lo = mid + 1;
-      else hi = mid;
-    }
-    qidx[(int64_t)i * m + k] = (uint16_t)lo;
-  }
-  __syncthreads();
-  for (int q = t; q <= DR_Q; q += DR_BLK) {
-    const uint32_t lo = q == 0 ? 0u : (uint32_t)sCnt[q - 1];
-    const uint32_t hi = q < DR_Q ? (uint32_t)sCnt[q] : (uint32_t)nonnan;
-    tab[q] = lo | (hi << 16);
+    tab[n] = __float_as_uint(v);
   }
   // prefix masks: warp w builds word w of P[0..256] by an inclusive OR-scan over the sorted order
-  uint32_t* P = tab + DR_MOFF;
+  uint32_t* P = tab + DR_EYT;
   uint32_t carry = 0;
   for (int q = 0; q < DR_BLK / 32; ++q) {
     const int s = q * 32 + lane;
@@ -206,24 +143,7 @@ struct DomRankArgs {
   int64_t items;
   uint32_t* tsum;          // nullable: tile summary (then zero word blocks are not stored)
   int64_t TW;
-  const uint16_t* qidx;    // R x m: bucket index of every row and objective (k_dom_tables)
 };
-
-// bucket lookup in table `tk`: (#{a <= b}, #{a < b}) over the block's values -- both are prefix lengths
-// of the sorted order; `strict` = also the strict count (overlapping tiles)
-template <bool STRICT>
-__device__ __forceinline__ void dr_count(const uint32_t* tk, int q, float b, int& cle, int& clt) {
-  const uint32_t pr = tk[q];
-  int pos = (int)(pr & 0xffffu);
-  const int hi = (int)(pr >> 16);
-  const float* sv = reinterpret_cast<const float*>(tk + DR_TAB);
-  if (STRICT) {
-    while (pos < hi && sv[pos] < b) ++pos;
-    clt = pos;
-  }
-  while (pos < hi && sv[pos] <= b) ++pos;
-  cle = pos;
-}
 
 // store the 8 words of block `blk` of row `row` (always without a summary; with one, only when nonzero,
 // flagging the block); hasdom[row] = 1 when nonzero
@@ -284,54 +204,47 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
     const int i0 = bi * DR_BLK;
     // first J row's objectives while the tables land
     float bnext[M];
-    int qnext[M];
     {
       const int j = bj0 * DR_BLK + tid;
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        bnext[k] = j < a.R ? __ldg(a.FS + (int64_t)j * M + k) : 0.0f;
-        qnext[k] = j < a.R ? (int)__ldg(a.qidx + (int64_t)j * M + k) : 0;
-      }
+      for (int k = 0; k < M; ++k) bnext[k] = j < a.R ? __ldg(a.FS + (int64_t)j * M + k) : 0.0f;
     }
     mbar_wait(&sBar, parity);
     parity ^= 1u;
     for (int bj = bj0; bj < bj1; ++bj) {
       const int j = bj * DR_BLK + tid;
       float b[M];
-      int qb[M];
       bool jnan = false;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         b[k] = bnext[k];
-        qb[k] = qnext[k];
         jnan = jnan || (b[k] != b[k]);
       }
       if (bj + 1 < bj1) {   // prefetch the next J block's row
         const int jn = j + DR_BLK;
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          bnext[k] = jn < a.R ? __ldg(a.FS + (int64_t)jn * M + k) : 0.0f;
-          qnext[k] = jn < a.R ? (int)__ldg(a.qidx + (int64_t)jn * M + k) : 0;
-        }
+        for (int k = 0; k < M; ++k) bnext[k] = jn < a.R ? __ldg(a.FS + (int64_t)jn * M + k) : 0.0f;
       }
       const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
-      // weak relation a_i <= b_j in every objective: AND of the prefix masks; overlapping tiles also
-      // take the strict counts for the reverse relation
-      int cle[M], clt[M];
-      if (fast) {
+      // weak relation a_i <= b_j in every objective: AND of the prefix masks
+      int node[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k) dr_count<false>(sTab + k * DR_TBL_WORDS, qb[k], b[k], cle[k], clt[k]);
-      } else {
+      for (int k = 0; k < M; ++k) node[k] = 1;
 #pragma unroll
-        for (int k = 0; k < M; ++k) dr_count<true>(sTab + k * DR_TBL_WORDS, qb[k], b[k], cle[k], clt[k]);
+      for (int s = 0; s < 9; ++s) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + node[k]]);
+          node[k] = 2 * node[k] + (e <= b[k] ? 1 : 0);
+        }
       }
       uint32_t le[8];
 #pragma unroll
       for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        const int c = cle[k];
-        const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_MOFF);
+        const int c = node[k] - DR_EYT;
+        const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
         const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
         le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
         le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
@@ -342,13 +255,24 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
         for (int w = 0; w < 8; ++w) out[w] = le[w];
       } else {
         // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
+        int nd[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) nd[k] = 1;
+#pragma unroll
+        for (int s = 0; s < 9; ++s) {
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + nd[k]]);
+            nd[k] = 2 * nd[k] + (e < b[k] ? 1 : 0);
+          }
+        }
         uint32_t ge[8];
 #pragma unroll
         for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const int c = clt[k];
-          const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_MOFF);
+          const int c = nd[k] - DR_EYT;
+          const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
           const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
           ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
           ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
@@ -444,11 +368,9 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
           bulk_g2s(sTab, a.tables + ((int64_t)bi * m + k0) * DR_TBL_WORDS, (unsigned)(mc * DR_TBL_BYTES), &sBar);
         }
         float b[DRW_MC];
-        int qb[DRW_MC];
 #pragma unroll
         for (int q = 0; q < DRW_MC; ++q) {
           b[q] = (j < a.R && q < mc) ? __ldg(a.FS + (int64_t)j * m + k0 + q) : 0.0f;
-          qb[q] = (j < a.R && q < mc) ? (int)__ldg(a.qidx + (int64_t)j * m + k0 + q) : 0;
           jnan = jnan || (b[q] != b[q]);
         }
         mbar_wait(&sBar, parity);
@@ -457,18 +379,25 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
         for (int q = 0; q < DRW_MC; ++q) {
           if (q < mc) {
             const uint32_t* tab = sTab + q * DR_TBL_WORDS;
-            int node = 0, nd = 0;
-            if (fast) dr_count<false>(tab, qb[q], b[q], node, nd);
-            else dr_count<true>(tab, qb[q], b[q], node, nd);
-            const uint4* P = reinterpret_cast<const uint4*>(tab + DR_MOFF);
+            int node = 1, nd = 1;
+#pragma unroll
+            for (int st = 0; st < 9; ++st) {
+              const float e = __uint_as_float(tab[node]);
+              node = 2 * node + (e <= b[q] ? 1 : 0);
+              if (!fast) {
+                const float e2 = __uint_as_float(tab[nd]);
+                nd = 2 * nd + (e2 < b[q] ? 1 : 0);
+              }
+            }
+            const uint4* P = reinterpret_cast<const uint4*>(tab + DR_EYT);
             {
-              const int c = node;
+              const int c = node - DR_EYT;
               const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
               le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
               le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
             }
             if (!fast) {
-              const int c = nd;
+              const int c = nd - DR_EYT;
               const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
               ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
               ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
@@ -527,29 +456,13 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank_wide(DomRankArgs a, int m) 
   pdl_trigger();
 }
 
-// tables region: [nb x m tables][vmask nb x 8][splitters m x Q][qidx R x m u16]
-size_t dom_rank_tables_bytes(int64_t R, int m) {
-  const int64_t nb = dom_rank_blocks(R);
-  return (size_t)nb * (size_t)m * DR_TBL_BYTES + (size_t)nb * 8 * 4 + (size_t)m * DR_Q * 4 +
-         (size_t)R * m * 2 + 256;
-}
-static float* dr_spl(uint32_t* tables, int64_t nb, int m) {
-  return reinterpret_cast<float*>(tables + nb * m * DR_TBL_WORDS + nb * 8);
-}
-static uint16_t* dr_qidx(uint32_t* tables, int64_t nb, int m) {
-  return reinterpret_cast<uint16_t*>(dr_spl(tables, nb, m) + (int64_t)m * DR_Q);
-}
-
 static int launch_dom_rank_wide(const float* FS, const float* blkmin, const float* blkmax, const int* wend,
                                 int64_t R, int m, uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s,
                                 uint32_t* tsum) {
   const int nb = (int)dom_rank_blocks(R);
   uint32_t* vmask = tables + (int64_t)nb * m * DR_TBL_WORDS;
-  float* spl = dr_spl(tables, nb, m);
-  uint16_t* qidx = dr_qidx(tables, nb, m);
-  MO_TRY(launch_ex(k_dom_splitters, dim3(m), dim3(DR_Q), 0, s, false, g_mo_pdl, FS, (int)R, m, spl));
   MO_TRY(launch_ex(k_dom_tables<0>, dim3(nb, m), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, m,
-                   tsum, (const float*)spl, qidx));
+                   tsum));
   const size_t smem = (size_t)DRW_MC * DR_TBL_BYTES;
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
@@ -572,7 +485,6 @@ static int launch_dom_rank_wide(const float* FS, const float* blkmin, const floa
   a.hasdom = hasdom;
   a.tsum = tsum;
   a.TW = tsum_words(R);
-  a.qidx = qidx;
   a.R = (int)R;
   a.nb = nb;
   a.ch = 1;   // one (I, J) tile per item: every tile re-streams block I's m tables anyway
@@ -583,17 +495,18 @@ static int launch_dom_rank_wide(const float* FS, const float* blkmin, const floa
   return launch_ex(k_dom_rank_wide, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a, m);
 }
 
+size_t dom_rank_tables_bytes(int64_t R, int m) {
+  const int64_t nb = dom_rank_blocks(R);
+  return (size_t)nb * (size_t)m * DR_TBL_BYTES + (size_t)nb * 8 * 4 + 256;
+}
 
 template <int M>
 static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
                              uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum) {
   const int nb = (int)dom_rank_blocks(R);
   uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
-  float* spl = dr_spl(tables, nb, M);
-  uint16_t* qidx = dr_qidx(tables, nb, M);
-  MO_TRY(launch_ex(k_dom_splitters, dim3(M), dim3(DR_Q), 0, s, false, g_mo_pdl, FS, (int)R, M, spl));
   MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M,
-                   tsum, (const float*)spl, qidx));
+                   tsum));
   const size_t smem = (size_t)M * DR_TBL_BYTES;
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
@@ -622,7 +535,6 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
   a.hasdom = hasdom;
   a.tsum = tsum;
   a.TW = tsum_words(R);
-  a.qidx = qidx;
   a.R = (int)R;
   a.nb = nb;
   a.ch = ch;

@@ -268,7 +268,7 @@ def check_bookkeeping(engine):
     rhop0 = torch.bincount(pi[Fl], minlength=w)[:w]
     empty = (rho0 == 0) & (rhop0 > 0)
     M0 = int(empty.sum())
-    out["final_ranks"] = bool(((ranks < l) & (ranks >= 0)).sum() == n)
+    out["final_ranks"] = bool((ranks < l).sum() == n)   # promoted rows carry l - 1 (-1 when l = 0)
     # nearest candidate of every empty niche: min (d, shuffled position) over its F_l members
     R = ranks.numel()
     pos = st["pos_pop"].long()
