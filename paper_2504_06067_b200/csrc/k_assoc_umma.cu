@@ -501,10 +501,12 @@ int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // items = (256-row tile, reference chunk): ~8 per CTA at the worst-case candidate count R
+  // items = (256-row tile, reference chunk).  Every item restarts its rows' running maxima, and each
+  // new maximum costs a candidate record, so rows keep all their references in one item (chunks = 1)
+  // unless there are too few row tiles for ~2 items per CTA
   const int64_t nrt = ceil_div(R, (int64_t)UA_ROWS);
   const int64_t ntiles = ceil_div((int64_t)a.w, (int64_t)UA_N);
-  int64_t chunks = ceil_div((int64_t)sms * 8, nrt);
+  int64_t chunks = ceil_div((int64_t)sms * 2, nrt);
   if (chunks > ntiles / 8) chunks = ntiles / 8;
   if (chunks < 1) chunks = 1;
   const dim3 grid((unsigned)sms), blk(UA_THREADS);
