@@ -55,7 +55,7 @@ constexpr int UA_THREADS = 64 + UA_EPI;
 constexpr int UA_TMEM_COLS = 512;                // 2 buffers x 2 row tiles x 128 columns
 constexpr int UA_NB = 8;                         // candidate chunks buffered per (thread, row tile)
 constexpr int UA_RING_BYTES = 96 * 1024;
-constexpr int UA_WARM = 8;                       // warm-up tiles per item (running maxima before candidates)
+constexpr int UA_WARM = 32;                      // warm-up tiles per item (running maxima before candidates)
 __host__ __device__ constexpr int ua_ks(int m) { return (3 * m + 15) / 16; }   // K16 steps for K = 3m
 __host__ __device__ constexpr size_t ua_smem(int ks) {                         // > 114 KB: 1 CTA/SM
   return 1024 + 2 * (size_t)ks * UA_A_STEP + UA_RING_BYTES + 2 * (size_t)UA_NB * UA_EPI * 12;
