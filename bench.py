@@ -374,7 +374,10 @@ def run_ours(args, rank, world):
         eng.XR[eng.cur][:n].copy_(hX, non_blocking=True)
         eng.FR[eng.cur][:n].copy_(hF, non_blocking=True)
         eng.ideal.copy_(hI, non_blocking=True)
-        eng.step()
+        if graph:
+            eng.replay_one()      # the public graph-replay generation (engine.run(cfg, graph=True))
+        else:
+            eng.step()
         hX.copy_(eng.X, non_blocking=True)
         hF.copy_(eng.F, non_blocking=True)
         hI.copy_(eng.ideal, non_blocking=True)
@@ -573,7 +576,10 @@ def main():
             "config": cfg_out,
             "clocks": r["clk"],
             "e2e": {"value": reps * 1e3 / r["e2e_ms"], "unit": "generations/s", "h2d_bytes_per_step": r["h2d"],
-                    "d2h_bytes_per_step": r["d2h"]},
+                    "d2h_bytes_per_step": r["d2h"],
+                    "path": ("Engine.replay_one (one CUDA-graph generation)" if r["sort"] == "bits" else
+                             "Engine.step (eager)") + ": pinned host X, F, ideal copied in, survivors X, F, "
+                            "ideal and the info record copied out every generation"},
             "gpu_launches": launches,
             "roofline": roof,
             "phases_ms": {k: round(v, 4) for k, v in kern.items() if isinstance(v, (int, float))},
