@@ -272,6 +272,12 @@ typedef struct mo_step_args {
    * bytes, static).  The association stays bit-identical: tcgen05.mma only
    * selects which references get the canonical FP32 key. */
   const void* zhat_umma;
+  /* Divisions of the Das-Dennis / two-layer reference set
+   * the directions came from (0 = unknown): the tcgen05 filter seeds every
+   * row's running maximum with the key of the lattice point nearest to the
+   * row's simplex projection, a valid lower bound of its maximum. */
+  int32_t ref_H_outer;
+  int32_t ref_H_inner;
 } mo_step_args;
 
 enum { MO_SORT_BITS = 0, MO_SORT_STREAM = 1 };

@@ -45,7 +45,7 @@ class StepArgs(ctypes.Structure):
         ("sort_mode", c_i32), ("shard_rank", c_i32), ("shard_count", c_i32), ("pad2", c_i32),
         ("lattice_z", c_vp), ("lattice_index", c_vp), ("lattice_pos", c_vp), ("lattice_H", c_i32),
         ("lattice_r", c_i32), ("pad3", c_i32),
-        ("zhat_frag", c_vp), ("zhat_umma", c_vp),
+        ("zhat_frag", c_vp), ("zhat_umma", c_vp), ("ref_H_outer", c_i32), ("ref_H_inner", c_i32),
     ]
 
 

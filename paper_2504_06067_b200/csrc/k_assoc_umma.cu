@@ -49,11 +49,12 @@ constexpr int UA_NBUF = 2;                       // accumulator buffers (2 row t
 constexpr int UA_ROWS = 256;                     // candidate rows per item: two M = 128 row tiles
 constexpr int UA_STEP_BYTES = UA_N * 16 * 2;     // 4 KB: 128 directions x K16 FP16 (one MMA K step)
 constexpr int UA_A_STEP = 128 * 16 * 2;          // 4 KB: 128 rows x K16 FP16
-constexpr int UA_EPI_WARPS = 8;   // 10 warps: <= 3 per SM sub-partition, 168 registers each
+constexpr int UA_GROUPS = 2;                     // epilogue groups: group g takes the tiles with counter % 2 == g
+constexpr int UA_EPI_WARPS = 8 * UA_GROUPS;   // 10 warps: <= 3 per SM sub-partition, 168 registers each
 constexpr int UA_EPI = UA_EPI_WARPS * 32;
 constexpr int UA_THREADS = 64 + UA_EPI;
 constexpr int UA_TMEM_COLS = 512;                // 2 buffers x 2 row tiles x 128 columns
-constexpr int UA_NB = 8;                         // candidate chunks buffered per (thread, row tile)
+constexpr int UA_NB = 4;                         // candidate chunks buffered per (thread, row tile)
 constexpr int UA_RING_BYTES = 96 * 1024;
 constexpr int UA_WARM = 32;                      // warm-up tiles per item (running maxima before candidates)
 __host__ __device__ constexpr int ua_ks(int m) { return (3 * m + 15) / 16; }   // K16 steps for K = 3m
@@ -203,6 +204,81 @@ __device__ __forceinline__ void ua_exact_cols(const AssocArgs& a, const int32_t*
   }
 }
 
+// Seed of a row's running maximum: the exact key (FP64) of the reference point nearest to the row's
+// simplex projection u = f / sum(f) on the outer lattice (z = p / Ho) and on the inner layer (z = q /
+// (2 Hi) + 1 / (2m)) of the Das-Dennis / two-layer set -- a point that exists in the set, so its
+// canonical FP32 key is >= this value - 2^-18 ||f|| (FP32 rounding of the key and of the stored unit
+// direction), and its filter value >= that / 2^e - eps: a valid running maximum from the first tile on
+// (no warm-up pass, few new maxima later).  Returns 0 when unknown (f not finite / zero sum).
+template <int M>
+__device__ double ua_lattice_round(const double (&v)[M], int H, int (&p)[M]) {
+  int sum = 0;
+  double fr[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const double fl = floor(v[k]);
+    p[k] = (int)fl;
+    fr[k] = v[k] - fl;
+    sum += p[k];
+  }
+  const int rem = H - sum;   // 0 <= rem < M: give +1 to the rem largest fractional parts
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    int rank = 0;
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) rank += (fr[k2] > fr[k]) || (fr[k2] == fr[k] && k2 < k);
+    p[k] += rank < rem ? 1 : 0;
+  }
+  return 0.0;
+}
+
+template <int M>
+__device__ double ua_guess(const float (&f)[M], int Ho, int Hi) {
+  double S = 0.0;
+#pragma unroll
+  for (int k = 0; k < M; ++k) S += (double)f[k];
+  if (!(S > 0.0) || !isfinite(S)) return 0.0;
+  double best = 0.0;
+  {
+    double v[M];
+    int p[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) v[k] = fmax(0.0, (double)f[k]) / S * Ho;
+    ua_lattice_round<M>(v, Ho, p);
+    double dot = 0.0, nn = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const double z = (double)p[k] / Ho;
+      dot += (double)f[k] * z;
+      nn += z * z;
+    }
+    if (nn > 0.0) best = fmax(best, dot / sqrt(nn));
+  }
+  if (Hi > 0) {
+    double v[M], sv = 0.0;
+    int q[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      v[k] = fmax(0.0, (2.0 * (double)f[k] / S - 1.0 / M) * Hi);
+      sv += v[k];
+    }
+    if (sv > 0.0) {
+#pragma unroll
+      for (int k = 0; k < M; ++k) v[k] = v[k] * Hi / sv;
+      ua_lattice_round<M>(v, Hi, q);
+      double dot = 0.0, nn = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const double z = (double)q[k] / (2.0 * Hi) + 1.0 / (2.0 * M);
+        dot += (double)f[k] * z;
+        nn += z * z;
+      }
+      if (nn > 0.0) best = fmax(best, dot / sqrt(nn));
+    }
+  }
+  return best;
+}
+
 template <int M>
 __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int chunks, int dbg) {
   constexpr int KS = ua_ks(M);
@@ -237,7 +313,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
     }
     for (int b = 0; b < UA_NBUF; ++b) {
       mbar_init(&sTFull[b], 1);
-      mbar_init(&sTEmpty[b], UA_EPI);
+      mbar_init(&sTEmpty[b], UA_EPI / UA_GROUPS);   // buffer b is drained by group b
     }
     mbar_init(&sAReady, UA_EPI);
   }
@@ -260,7 +336,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         const int ch = item % chunks;
         const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
-        const int wu = min(UA_WARM, t1 - t0);
+        const int wu = a.ref_Ho > 0 ? 0 : min(UA_WARM, t1 - t0);
         for (int ti = 0; ti < wu + (t1 - t0); ++ti) {
           const int t = ti < wu ? t0 + ti : t0 + ti - wu;
           mbar_wait(&sEmpty[s], ph ^ 1u);
@@ -287,7 +363,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
         mbar_wait(&sAReady, aph);
         aph ^= 1u;
         tc_fence_after();
-        const int wu = min(UA_WARM, t1 - t0);
+        const int wu = a.ref_Ho > 0 ? 0 : min(UA_WARM, t1 - t0);
         for (int ti = 0; ti < wu + (t1 - t0); ++ti) {
           mbar_wait(&sFull[s], ph);
           mbar_wait(&sTEmpty[buf], tph ^ 1u);
@@ -317,18 +393,19 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
     // ------------------------------------------------------------ epilogue
     const int et = threadIdx.x - 64;        // 0 .. UA_EPI-1
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    const int cgp = (warp - 2) >> 2;        // 64-column half of every 128-column accumulator
+    const int grp = (warp - 2) >> 3;        // tiles with global counter % UA_GROUPS == grp (its own buffer)
+    const int cgp = ((warp - 2) >> 2) & 1;  // 64-column half of every 128-column accumulator
     const int r = q * 32 + lane;            // row within each row tile
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    int buf = 0;
-    unsigned tph = 0;
+    int gt = 0;                             // tiles of all items so far (the MMA issuer's buffer counter)
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int rb = (item / chunks) * UA_ROWS;
       const int ch = item % chunks;
       const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
       int row[2];
       bool act[2];
-      float marg[2];
+      float marg[2], nrm[2];
+      int escale[2];
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt) {
         const int c = rb + rt * 128 + r;
@@ -347,7 +424,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
         const float norm = sqrtf(nn);
         const bool ok = fin && mx > 0.0f && isfinite(norm);
         if (act[rt] && !ok) {
-          if (ch == 0 && cgp == rt) {
+          if (ch == 0 && cgp == rt && grp == 0) {
             a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row[rt];
             atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
           }
@@ -357,7 +434,9 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
         int e = 0;
         if (act[rt]) frexpf(mx, &e);
         marg[rt] = ldexpf(norm, -15 - e);
-        if (cgp == rt) {   // this thread writes row r of A tile rt: [h(f) | h(f) | l(f)] / 2^e, zero-padded
+        escale[rt] = e;
+        nrm[rt] = norm;
+        if (cgp == rt && grp == 0) {   // row r of A tile rt: [h(f) | h(f) | l(f)] / 2^e, zero-padded
           __half hk[16 * KS];
 #pragma unroll
           for (int kp = 0; kp < 16 * KS; ++kp) {
@@ -388,44 +467,59 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core reads
       ua_arrive(&sAReady);
       float mxr[2] = {-__int_as_float(0x7f800000), -__int_as_float(0x7f800000)};
-      int cnt[2] = {0, 0};
-      unsigned long long best[2] = {0ull, 0ull};
-      const int wu = min(UA_WARM, t1 - t0);
-      for (int ti = 0; ti < wu + (t1 - t0); ++ti) {
-        const bool warm = ti < wu || (dbg & 1);   // warm-up pass: running maxima only (dbg 1: always)
-        const int t = warm ? t0 + ti : t0 + ti - wu;
-        mbar_wait(&sTFull[buf], tph);
-        tc_fence_after();
-        // this thread's 64 columns of both row tiles: four loads in flight, one wait, then the buffer is free
-        uint32_t u[2][2][32];
-#pragma unroll
-        for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            ua_ld32(tmem + lane_addr + (uint32_t)(buf * 2 + rt) * UA_N + (uint32_t)(cgp * 64 + h * 32), u[rt][h]);
-        ua_ld_wait();
-        tc_fence_before();
-        ua_arrive(&sTEmpty[buf]);
-        float sm[2][2];
-#pragma unroll
-        for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) sm[rt][h] = max32(u[rt][h]);
+      if (a.ref_Ho > 0) {   // lattice seeds (see ua_guess): t_c >= g - 2^-18 |f|, t~ >= t_c / 2^e - eps
 #pragma unroll
         for (int rt = 0; rt < 2; ++rt) {
           if (!act[rt]) continue;
+          float fn[M];
+          ua_load_fn<M>(a, row[rt], fn);
+          const double g = ua_guess<M>(fn, a.ref_Ho, a.ref_Hi);
+          if (g > 0.0) {
+            // marg = 2 eps in filter units; the seed sits eps + 2^-18 |f| / 2^e below the point's key
+            const double seed = g * (double)ldexpf(1.0f, -escale[rt]) - 0.5 * (double)marg[rt] -
+                                (double)ldexpf(nrm[rt], -18 - escale[rt]);
+            mxr[rt] = (float)seed - fabsf((float)seed) * 1e-6f;   // round down
+          }
+        }
+      }
+      int cnt[2] = {0, 0};
+      unsigned long long best[2] = {0ull, 0ull};
+      const int wu = a.ref_Ho > 0 ? 0 : min(UA_WARM, t1 - t0);
+      for (int ti = 0; ti < wu + (t1 - t0); ++ti, ++gt) {
+        if ((gt & (UA_GROUPS - 1)) != grp) continue;   // the other group's tile
+        const bool warm = ti < wu || (dbg & 1);   // warm-up pass: running maxima only (dbg 1: always)
+        const int t = warm ? t0 + ti : t0 + ti - wu;
+        const int buf = gt & 1;
+        const unsigned tph = (unsigned)(gt >> 1) & 1u;
+        mbar_wait(&sTFull[buf], tph);
+        tc_fence_after();
+        // this thread's 64 columns of row tile 0, then of row tile 1 (two loads in flight each; 64 live
+        // values); the buffer is released once both are in registers
+#pragma unroll
+        for (int rt = 0; rt < 2; ++rt) {
+          uint32_t u[2][32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            ua_ld32(tmem + lane_addr + (uint32_t)(buf * 2 + rt) * UA_N + (uint32_t)(cgp * 64 + h * 32), u[h]);
+          ua_ld_wait();
+          if (rt == 1) {
+            tc_fence_before();
+            ua_arrive(&sTEmpty[buf]);
+          }
+          if (!act[rt]) continue;
+          const float sm0 = max32(u[0]), sm1 = max32(u[1]);
           if (warm) {
-            mxr[rt] = fmaxf(mxr[rt], fmaxf(sm[rt][0], sm[rt][1]));
+            mxr[rt] = fmaxf(mxr[rt], fmaxf(sm0, sm1));
             continue;
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const float s = sm[rt][h];
+            const float s = h ? sm1 : sm0;
             if (s >= mxr[rt] - marg[rt]) {   // a column within 2 eps of the best seen: remember the chunk
               const float mn = fmaxf(mxr[rt], s), th = mn - marg[rt];
               uint32_t qm = 0;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) qm |= (__uint_as_float(u[rt][h][i]) >= th ? 1u : 0u) << i;
+              for (int i = 0; i < 32; ++i) qm |= (__uint_as_float(u[h][i]) >= th ? 1u : 0u) << i;
               if (cnt[rt] == UA_NB) {   // full: drop the chunks the new maximum excludes, evaluate the rest
                 int kept = 0;
                 for (int b2 = 0; b2 < UA_NB; ++b2) {
@@ -455,10 +549,6 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
               mxr[rt] = mn;
             }
           }
-        }
-        if (++buf == UA_NBUF) {
-          buf = 0;
-          tph ^= 1u;
         }
       }
 #pragma unroll

@@ -91,6 +91,7 @@ struct AssocArgs {
   // tcgen05 filter (k_assoc_umma): FP16 reference tiles + packed-column reference indices
   // (mo_pack_refs_f16); preferred over zfrag when set
   const void* zumma;
+  int ref_Ho, ref_Hi;    // divisions of the reference set (0 = unknown): lattice seeds of the running maxima
 };
 
 struct AssocFinalArgs {

@@ -421,6 +421,8 @@ static int niche_phase(const mo_step_args* a, const Layout& L, uint32_t mask, cu
   aa.zfrag = reinterpret_cast<const uint2*>(a->zhat_frag);
   aa.zsT = pa.zsT;
   aa.zumma = a->zhat_umma;
+  aa.ref_Ho = a->ref_H_outer;
+  aa.ref_Hi = a->ref_H_inner;
   if (a->lattice_z && m >= 2 && m <= 5)
     MO_TRY(launch_assoc_lattice(aa, m, R, s));
   else if (use_umma(aa, m))

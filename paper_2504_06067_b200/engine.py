@@ -255,6 +255,9 @@ class Engine:
         a.lattice_r = self.prune_r
         a.zhat_frag = self.zfrag.data_ptr() if self.zfrag is not None else None
         a.zhat_umma = self.zumma.data_ptr() if self.zumma is not None else None
+        Ho, Hi = (cfg.reference_points if cfg.reference_points is not None
+                  else refpoints.choose_divisions(cfg.m, cfg.n))
+        a.ref_H_outer, a.ref_H_inner = int(Ho), int(Hi)
         return a
 
     def _launch(self, cur, generation, phases=_lib.PHASE_ALL, use_dev_gen=False):

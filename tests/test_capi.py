@@ -64,6 +64,7 @@ def test_step_args_layout_matches_header(so):
     assert A.generation_dev.offset == A.workspace_bytes.offset + 8
     assert A.pad3.offset == A.lattice_r.offset + 4 and A.zhat_frag.offset % 8 == 0
     assert A.zhat_umma.offset == A.zhat_frag.offset + 8
-    assert ctypes.sizeof(A) == A.zhat_umma.offset + 8
+    assert A.ref_H_outer.offset == A.zhat_umma.offset + 8 and A.ref_H_inner.offset == A.ref_H_outer.offset + 4
+    assert ctypes.sizeof(A) == A.ref_H_inner.offset + 4
     so.mo_step_args_bytes.restype = ctypes.c_size_t
     assert so.mo_step_args_bytes() == ctypes.sizeof(A)
