@@ -28,12 +28,17 @@
 //                 tile KS tcgen05.mma.cta_group::1.kind::f16 M128 N128 K16 (the two row tiles share the
 //                 B tile), tcgen05.commit to the ring slot's empty barrier and to the accumulator
 //                 buffer's full barrier; two accumulator buffers (2 x 2 x 128 columns);
-//   warps 2..9    epilogue: build the item's A tiles in shared memory, then per tile four tcgen05.ld
-//                 32x32b.x32 of their TMEM lane quarter (warp % 4) and 64-column half (both row
-//                 tiles), one wait, release the buffer, FMNMX3 trees, candidate buffering.
-// Measured (C3, ncu): tensor pipe ~17 %, issue ~39 %: the per-tile chain (commit -> mbarrier ->
-// tcgen05.ld -> release -> next MMA) bounds it, not the MMA or the FMNMX3 work; N = 64 with four buffers
-// and two CTAs per SM (N = 64, 256 TMEM columns each) both measured slower (2.7 / 2.5 ms vs 2.2 ms).
+//   warps 2..17   epilogue in two groups of 8: group g takes the tiles whose running counter is g mod 2
+//                 (TMEM buffer g), so the two groups' per-tile chains (mbarrier wait -> tcgen05.ld ->
+//                 release -> FMNMX3 trees) overlap; a warp covers its TMEM lane quarter (warp % 4) and a
+//                 64-column half of both row tiles, one row tile at a time (64 live values).
+// Running maxima are seeded with the key of the reference point nearest to the row's simplex
+// projection (ua_guess: the divisions of the Das-Dennis / two-layer set), so there is no warm-up pass
+// and new maxima -- each one a candidate record -- are rare; without divisions an UA_WARM-tile warm-up
+// pass runs first.  Measured at C3 (MO_UMMA_DEBUG timing modes): 2.29 ms with per-element candidates
+// -> 1.57 ms (chunk records, one reference chunk per item, two groups, lattice seeds); the candidate
+// work left is ~0.14 ms, the rest is the per-tile chain.  N = 64 with four buffers and two CTAs per SM
+// measured slower.
 #include <cuda_fp16.h>
 #include <stdlib.h>
 #include <cuda_runtime.h>
