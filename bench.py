@@ -19,10 +19,17 @@ population.
 * cpu_baseline: one FULL generation of the reference algorithm (the oracle port: numpy + the C/OpenMP
   restatement of its O(R^2) stages) on the GPU run's final population, all host cores.
 * --impl reference: W + K full generations of that port on one evolving population (run_reference).
-N > 1 (torchrun): ONE population sharded over the N GPUs (scaling "strong") -- the streamed sort's
-dominated rows dealt to the ranks, front masks all-gathered and association keys max-reduced over
-NCCL; every rank then runs the identical replicated niching/variation, so survivors are bit-identical
-to one GPU.  Sharded generations are eager (the front loop is host driven).
+N > 1 (torchrun):
+* populations of 1M and more (C4; the north star's sharded regime): ONE population sharded over the N
+  GPUs (scaling "strong") -- the streamed sort's dominated rows dealt to the ranks, front masks
+  all-gathered and association keys max-reduced over NCCL; every rank then runs the identical
+  replicated niching/variation, so survivors are bit-identical to one GPU.  Eager generations (the
+  front loop is host driven).
+* C1-C3 (bit-matrix sort, one CUDA-graph replay per generation): N independent populations ("islands",
+  seeds 0..N-1, scaling "weak", no data-path collective).  At these sizes one GPU's bit-matrix sort
+  (C3: 6 ms per generation) beats the streamed sort sharded over several GPUs (C3 streamed on one GPU:
+  ~25 ms; the bit-matrix does not shard without its per-front exchange), so a sharded C3 would scale
+  below one GPU.
 """
 import argparse
 import json
@@ -309,14 +316,15 @@ def run_ours(args, rank, world):
 
     wl = WORKLOADS[args.workload]
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
-    sharded = world > 1                # N > 1: ONE population, dominated rows sharded over the ranks
+    sharded = sharded_for(wl, world)   # ONE population, dominated rows sharded over the ranks
     sort = sort_for(wl, world)
     group = None
     if sharded:
         import torch.distributed as dist
         group = dist.group.WORLD
+    # islands (bit-matrix workloads at N > 1): an independent population per rank
     cfg = engine.RunConfig(problem=wl["problem"], n=wl["n"], m=wl["m"], d=wl["d"],
-                           generations=args.steps + args.warmup, seed=0)
+                           generations=args.steps + args.warmup, seed=0 if sharded else rank)
     graph = sort == "bits"
     eng = engine.Engine(cfg, graph=graph, sort=sort, group=group)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -407,9 +415,14 @@ def run_ours(args, rank, world):
     return result
 
 
+def sharded_for(wl, world):
+    """N > 1 shards one population for the streamed-sort workloads (N >= 1M); islands otherwise."""
+    return world > 1 and wl["sort"] == "stream"
+
+
 def sort_for(wl, world):
-    """The sort mode of a run: the workload's at one GPU; the streamed (row-sharded) sort at N > 1."""
-    return "stream" if world > 1 else wl["sort"]
+    """The sort mode of a run: the workload's (the streamed sort is the sharded one)."""
+    return wl["sort"]
 
 
 def cfgd_for(wl, world, args):
@@ -419,7 +432,8 @@ def cfgd_for(wl, world, args):
     w = refpoints.lattice_size(wl["m"], *refpoints.choose_divisions(wl["m"], wl["n"]))
     cfgd = {"workload": wl["label"], "problem": wl["problem"], "m": wl["m"], "d": wl["d"], "n": wl["n"],
             "merged_rows": 2 * wl["n"], "w": w, "sort": sort,
-            "parallelism": f"sharded{world}" if world > 1 else "single",
+            "parallelism": (f"sharded{world}" if sharded_for(wl, world) else f"islands{world}") if world > 1
+            else "single",
             "l2": "flushed (512 MiB write) between timed generations",
             "graph": "one CUDA-graph replay per generation" if sort == "bits"
             else "eager generations (host-driven front loop)"}
