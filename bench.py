@@ -263,10 +263,11 @@ def time_kernels(torch, eng, _lib):
     for _ in range(7):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        if tb:     # the engine's kernels and configuration: rank-mask tables + sweep with the tile summary
+        if tb:     # the engine's kernels and configuration: rank-mask tables + sweep (+ tile summary, m >= 4)
             _lib.check(L.mo_dominance_bits_ranked(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
                                                   _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),
-                                                  _lib.ptr(tables), tb, _lib.ptr(tsum), _lib.stream_ptr()), "dom")
+                                                  _lib.ptr(tables), tb, _lib.ptr(tsum) if m >= 4 else None,
+                                                  _lib.stream_ptr()), "dom")
         else:
             _lib.check(L.mo_dominance_bits_sorted(_lib.ptr(ps["FS"]), _lib.ptr(ps["blkmin"]), _lib.ptr(ps["blkmax"]),
                                                   _lib.ptr(ps["wend"]), R, m, _lib.ptr(bits), _lib.ptr(hasdom),

@@ -768,38 +768,43 @@ __device__ __forceinline__ int64_t peel_row_summary(const PeelArgs& a, int64_t j
   for (;;) {
     const bool scanning = active && blocked_at < 0 && (sw0 << 5) < tlim;
     if (__ballot_sync(MO_FULL, scanning) == 0) break;
-    int64_t hit = INT64_MAX;
+    uint32_t f = 0;
     if (scanning) {
       const int64_t swi = sw0 + l8;
       if ((swi << 5) < tlim) {
-        uint32_t f = __ldcg(a.tsum + j * a.TW + swi);
+        f = __ldcg(a.tsum + j * a.TW + swi);
         if (swi == (t0 >> 5)) f &= 0xffffffffu << (t0 & 31);              // blocks before the resume block
         const int64_t rem = tlim - (swi << 5);
         if (rem < 32) f &= (1u << rem) - 1u;
-        while (f) {
-          const int b = __ffs(f) - 1;
-          f &= f - 1u;
-          const int64_t t = (swi << 5) + b;
-          const uint4* bw = reinterpret_cast<const uint4*>(a.bits + j * a.W + t * 8);
-          const uint4* rw = reinterpret_cast<const uint4*>(a.ranked + t * 8);
-          const uint4 b0 = __ldg(bw), b1 = __ldg(bw + 1);
-          const uint4 r0 = __ldcg(rw), r1 = __ldcg(rw + 1);
-          const uint32_t h = (b0.x & ~r0.x) | (b0.y & ~r0.y) | (b0.z & ~r0.z) | (b0.w & ~r0.w) |
-                             (b1.x & ~r1.x) | (b1.y & ~r1.y) | (b1.z & ~r1.z) | (b1.w & ~r1.w);
-          if (h) {
-            hit = t;
-            break;
-          }
-        }
       }
     }
-    // smallest blocking block of the 8-lane group
+    // the group's 8 summary words in block order; the 8 lanes split each nonzero word's flagged blocks
+    // (dense rows: up to 4 blocks per lane per word, in parallel), and the first word with an unranked
+    // dominator ends the scan at its smallest such block
+    int64_t hit = INT64_MAX;
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t wk = __shfl_sync(MO_FULL, f, k, 8);
+      if (wk == 0u || hit != INT64_MAX) continue;   // uniform within the 8-lane group
+      const int nbits = __popc(wk);
+      int64_t tmin = INT64_MAX;
+      for (int r = l8; r < nbits; r += 8) {
+        const int bpos = (int)__fns(wk, 0, r + 1);
+        const int64_t t = ((sw0 + k) << 5) + bpos;
+        const uint4* bw = reinterpret_cast<const uint4*>(a.bits + j * a.W + t * 8);
+        const uint4* rw = reinterpret_cast<const uint4*>(a.ranked + t * 8);
+        const uint4 b0 = __ldg(bw), b1 = __ldg(bw + 1);
+        const uint4 r0 = __ldcg(rw), r1 = __ldcg(rw + 1);
+        const uint32_t h = (b0.x & ~r0.x) | (b0.y & ~r0.y) | (b0.z & ~r0.z) | (b0.w & ~r0.w) |
+                           (b1.x & ~r1.x) | (b1.y & ~r1.y) | (b1.z & ~r1.z) | (b1.w & ~r1.w);
+        if (h && t < tmin) tmin = t;
+      }
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      const int64_t oh = __shfl_xor_sync(MO_FULL, hit, o, 8);
-      hit = oh < hit ? oh : hit;
+      for (int o = 4; o > 0; o >>= 1) {
+        const int64_t ot = __shfl_xor_sync(gmask, tmin, o, 8);
+        tmin = ot < tmin ? ot : tmin;
+      }
+      hit = tmin;
     }
-    (void)gmask;
     if (scanning) {
       if (hit != INT64_MAX)
         blocked_at = hit;

@@ -326,7 +326,9 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   ps.hasdom = hasdom;
   MO_TRY(launch_presort(ps, s));
   // rank-mask kernels: only nonzero 256-bit word blocks are stored, flagged in the tile summary that the
-  // peel walks (MO_NO_TSUM=1: full stores and the word-by-word peel)
+  // peel walks (MO_NO_TSUM=1: full stores and the word-by-word peel).  m <= 3 populations have dense
+  // dominance (many dominators per row, many fronts: DTLZ3 m=3 N=16k 21 fronts): there the full stores
+  // and the contiguous word peel are faster (1,617 vs 928 generations/s), so the summary is for m >= 4
   static int no_tsum = -1;
   if (no_tsum < 0) {
     const char* e = getenv("MO_NO_TSUM");
@@ -334,7 +336,7 @@ static int sort_phase(const mo_step_args* a, const Layout& L, cudaStream_t s) {
   }
   uint32_t* tsum = nullptr;
   if (use_dom_rank(a->m, R)) {
-    tsum = no_tsum ? nullptr : at<uint32_t>(ws, L.tsum);
+    tsum = (no_tsum || a->m <= 3) ? nullptr : at<uint32_t>(ws, L.tsum);
     MO_TRY(launch_dom_rank(ps.FS, ps.blkmin, ps.blkmax, ps.wend, R, a->m, bits, hasdom, at<uint32_t>(ws, L.dtab), s,
                            tsum));
   } else {
