@@ -18,12 +18,6 @@
 
 namespace mo {
 
-__device__ __forceinline__ void atomic_min_float(float* addr, float v) {
-  if (v >= 0.0f)
-    atomicMin(reinterpret_cast<int*>(addr), __float_as_int(v));
-  else
-    atomicMax(reinterpret_cast<unsigned*>(addr), __float_as_uint(v));
-}
 
 
 // One block = ppb <= VARY_PAIRS mating pairs, VARY_THREADS threads.  Phase 1: one
