@@ -18,6 +18,6 @@ tags).  The oracle is pinned against every one of them
 (``tests/golden/spec_examples.json``, produced by
 ``tests/golden/make_golden.py``; checked by ``tests/test_oracle_golden.py``).
 Beyond those examples the bit-level arithmetic (FP32 canonical association,
-FP64 intercept solve, Philox streams, Feistel shuffles) is pinned by this
+FP64 intercept solve, Philox streams, keyed swap-or-not shuffles) is pinned by this
 oracle itself — see DESIGN.md §"Pinned semantics".
 """
