@@ -279,52 +279,91 @@ __device__ __forceinline__ void prep_extremes_rt(const PrepArgs& a, int R, int l
 }
 
 // phase 1 of k_prep for m = M (register arrays): ASF extreme-point keys and column maxima of the
-// translated candidate rows (rank in [0, l]), merged by warp reductions + one atomic per warp.  The keys
-// are stored complemented (atomicMax of ~key: 0 is neutral, so a zeroed workspace needs no reset node;
-// phase 2 restores 0 after reading).  build_cand: also append the candidates to cand (engine path:
-// phase 0's list pass and its grid barrier are folded in here).
+// translated candidate rows (rank in [0, l]).  Each thread keeps its best key per axis and its column
+// maxima across its rows; warp, then block reductions (shared memory) leave one atomic per CTA per
+// axis / column -- per-warp atomics on these 2M addresses serialised at C3 (6k warps x 2M atomics).
+// The keys are stored complemented (atomicMax of ~key: 0 is neutral, so a zeroed workspace needs no
+// reset node; phase 2 restores 0 after reading).  build_cand: also append the candidates to cand
+// (engine path: phase 0's list pass and its grid barrier are folded in here), one atomic per CTA and
+// row chunk.
 template <int M>
-__device__ __forceinline__ void prep_extremes(const PrepArgs& a, int R, int l, int gthreads, bool build_cand) {
-  const int tid = threadIdx.x, lane = tid & 31;
+__device__ __forceinline__ void prep_extremes(const PrepArgs& a, int R, int l, int gthreads, bool build_cand,
+                                              double* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // scratch: k_prep's (not yet used) system buffer -- 8 warps x M keys, 8 x M column maxima, counters
+  unsigned long long (*sKey)[M] = reinterpret_cast<unsigned long long (*)[M]>(scratch);
+  uint32_t (*sCol)[M] = reinterpret_cast<uint32_t (*)[M]>(scratch + 8 * M);
+  int* sCnt = reinterpret_cast<int*>(scratch + 16 * M);
+  int& sBase = sCnt[8];
   float idl[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) idl[k] = __ldcg(a.ideal + k);
+  unsigned long long best[M];
+  uint32_t cmax[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    best[k] = ~0ull;
+    cmax[k] = 0u;
+  }
   for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
     const int row = base + tid;
     const bool act = row < R && a.ranks[row] >= 0 && a.ranks[row] <= l;
-    if (build_cand) {
-      const int slot = warp_alloc(a.ctl, act ? 1 : 0);   // candidate order is immaterial
-      if (act) a.cand[slot] = row;
+    if (build_cand) {   // candidate order is immaterial: one atomic per CTA and chunk
+      const unsigned bal = __ballot_sync(MO_FULL, act);
+      if (lane == 0) sCnt[warp] = __popc(bal);
+      __syncthreads();
+      if (tid == 0) {
+        int tot = 0;
+        for (int w = 0; w < nw; ++w) {
+          const int c = sCnt[w];
+          sCnt[w] = tot;
+          tot += c;
+        }
+        sBase = tot ? atomicAdd(a.ctl, tot) : 0;
+      }
+      __syncthreads();
+      if (act) a.cand[sBase + sCnt[warp] + __popc(bal & ((1u << lane) - 1u))] = row;
+      __syncthreads();   // sCnt / sBase are rewritten by the next chunk
     }
-    float ft[M], q[M];
-    int pp = 0;
     if (act) {
-      pp = __ldcg(a.pos_pop + row);
+      const int pp = __ldcg(a.pos_pop + row);
+      float ft[M], q[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         ft[k] = __fsub_rn(a.F[(int64_t)row * M + k], idl[k]);
         q[k] = __fdiv_rn(ft[k], ASF_EPS);
+        cmax[k] = max(cmax[k], f2ord(ft[k]));
       }
-    }
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      uint32_t v = act ? f2ord(ft[k]) : 0u;
-      v = warp_max_u32(v);
-      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
-    }
-#pragma unroll
-    for (int ax = 0; ax < M; ++ax) {
-      unsigned long long key = ~0ull;
-      if (act) {
+      for (int ax = 0; ax < M; ++ax) {
         float s = ft[ax];  // w_ax,ax = 1: f / 1 is exact
 #pragma unroll
         for (int k = 0; k < M; ++k)
           if (k != ax) s = fmaxf(s, q[k]);
-        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+        const unsigned long long key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+        best[ax] = key < best[ax] ? key : best[ax];
       }
-      key = warp_min_u64(key);
-      if (lane == 0 && key != ~0ull) atomicMax(&a.ext_key[ax], ~key);
     }
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const unsigned long long kv = warp_min_u64(best[k]);
+    const uint32_t cv = warp_max_u32(cmax[k]);
+    if (lane == 0) {
+      sKey[warp][k] = kv;
+      sCol[warp][k] = cv;
+    }
+  }
+  __syncthreads();
+  if (tid < M) {
+    unsigned long long kv = ~0ull;
+    uint32_t cv = 0u;
+    for (int w = 0; w < nw; ++w) {
+      kv = sKey[w][tid] < kv ? sKey[w][tid] : kv;
+      cv = max(cv, sCol[w][tid]);
+    }
+    if (kv != ~0ull) atomicMax(&a.ext_key[tid], ~kv);
+    if (cv) atomicMax(&a.colmax[tid], cv);
   }
 }
 
@@ -396,7 +435,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
   // ---- phase 1: ASF extreme points + column maxima of translated candidates
   switch (m) {
 #define MO_PX_CASE(MM) \
-  case MM: prep_extremes<MM>(a, R, l, gthreads, fused); break;
+  case MM: prep_extremes<MM>(a, R, l, gthreads, fused, sA); break;
     MO_PX_CASE(1) MO_PX_CASE(2) MO_PX_CASE(3) MO_PX_CASE(4) MO_PX_CASE(5) MO_PX_CASE(6) MO_PX_CASE(7)
     MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
     MO_PX_CASE(15) MO_PX_CASE(16)
