@@ -1267,6 +1267,7 @@ __global__ void k_assoc_final_rt(AssocFinalArgs a) {
 
 
 constexpr int SELECT_THREADS = 512;
+constexpr int SEL_BIG = 1024;   // partial buckets above this many candidates are selected block-wide
 
 __device__ __forceinline__ int warp_bitonic_asc(int v) {
   const int lane = threadIdx.x & 31;
@@ -1299,6 +1300,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
   __shared__ int sh[40];
   __shared__ int sHist[2][LVL_BINS];
   __shared__ int sRes[4];
+  __shared__ int sSel[(SELECT_THREADS / 32) * 256];   // per-warp radix bins of the P7 top-t select
   const int tid = threadIdx.x, lane = tid & 31;
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int gwarp = gtid >> 5, nwarps = gthreads >> 5;
@@ -1361,6 +1363,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       // ---- P2: all empty niches take their nearest; post-nearest counts; level histogram
       for (int q = tid; q < 2 * LVL_BINS; q += blockDim.x) (&sHist[0][0])[q] = 0;
       __syncthreads();
+      int maxe = 0;   // largest end level rho_j + c_j of an active niche (bounds the water level)
       for (int j = gtid; j < w; j += gthreads) {
         int r = __ldcg(a.rho + j), c = __ldcg(a.rho_p + j);
         if (c == 0) continue;
@@ -1372,9 +1375,12 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
           a.rho_p[j] = c;
         }
         if (c == 0) continue;
+        maxe = max(maxe, r + c);
         if (r < LVL_BINS) atomicAdd(&sHist[0][r], 1);
         if (r + c < LVL_BINS) atomicAdd(&sHist[1][r + c], 1);
       }
+      maxe = (int)warp_max_u32((uint32_t)maxe);
+      if (lane == 0 && maxe >= LVL_BINS) atomicMax(&a.sctl[SCTL_MAXE], maxe);
       __syncthreads();
       for (int q = tid; q < 2 * LVL_BINS; q += blockDim.x) {
         const int v = (&sHist[0][0])[q];
@@ -1415,46 +1421,72 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         if (lane == 0) {
           sRes[0] = (int)Lstar;
           sRes[1] = (int)before;
+          sRes[2] = (int)carryT;   // takes below level LVL_BINS (when the level lies beyond the window)
         }
       }
       __syncthreads();
       int L = sRes[0];
       long long before = sRes[1];
       if (L < 0) {
-        // rare: level beyond the window -> block-cooperative binary search over all j
-        __shared__ unsigned long long sAcc;
-        long long lo = LVL_BINS, hi = 0x7fffffff;
-        while (lo < hi) {
-          const long long mid = (lo + hi) / 2;
+        // level beyond the histogram window (a few crowded niches, e.g. DTLZ3 m = 10 late in a run):
+        // grid-cooperative 32-ary search for X = min{x : U(x) >= k'} with U(x) = sum_j clamp(x - rho_j,
+        // 0, c_j) the takes below level x; lane i of every warp evaluates candidate x_i, each warp
+        // streams 32 niches per coalesced load and broadcasts them by shuffles; one global accumulator
+        // per candidate (three rotating sets of 32), one grid barrier per pass, ~log32(max level) passes.
+        // Then L* = X - 1 and before = U(X - 1).
+        __shared__ unsigned long long sAcc[32];
+        __shared__ long long sSearch[3];
+        unsigned long long* acc = reinterpret_cast<unsigned long long*>(a.lvl + 2 * LVL_BINS);
+        long long lo = LVL_BINS + 1, hi = __ldcg(a.sctl + SCTL_MAXE), Ulo = sRes[2];
+        for (int pass = 0; lo < hi; ++pass) {
+          unsigned long long* cur = acc + (pass % 3) * 32;
+          if (blockIdx.x == 0 && tid < 32) acc[((pass + 1) % 3) * 32 + tid] = 0ull;   // next pass's set
+          if (tid < 32) sAcc[tid] = 0ull;
+          __syncthreads();
+          const long long x = lo + (hi - lo) * lane / 32;
           unsigned long long part = 0;
-          for (int j = tid; j < w; j += blockDim.x) {
-            const int c = __ldcg(a.rho_p + j);
-            if (c == 0) continue;
-            const long long t = mid + 1 - __ldcg(a.rho + j);
-            part += t < 0 ? 0 : (t > c ? c : t);
+          for (int base = gwarp * 32; base < w; base += nwarps * 32) {
+            const int j = base + lane;
+            const int c = j < w ? __ldcg(a.rho_p + j) : 0;
+            const int r = c > 0 ? __ldcg(a.rho + j) : 0;
+#pragma unroll 8
+            for (int q = 0; q < 32; ++q) {
+              const int cq = __shfl_sync(MO_FULL, c, q), rq = __shfl_sync(MO_FULL, r, q);
+              const long long t0 = x - rq;
+              part += t0 <= 0 ? 0ull : (unsigned long long)(t0 > cq ? cq : t0);
+            }
           }
-          if (tid == 0) sAcc = 0;
+          if (part) atomicAdd(&sAcc[lane], part);
           __syncthreads();
-          atomicAdd(&sAcc, part);
+          if (tid < 32 && sAcc[tid]) atomicAdd(cur + tid, sAcc[tid]);
+          grid_sync(a.g.bar);
+          if (tid < 32) {
+            const long long u = (long long)__ldcg(cur + tid);
+            const unsigned ge = __ballot_sync(MO_FULL, u >= k_rem);   // a suffix of the lanes (U, x_i monotone)
+            const int f = ge ? __ffs(ge) - 1 : 32;
+            const long long xf = __shfl_sync(MO_FULL, x, f & 31);
+            const long long xp = __shfl_sync(MO_FULL, x, (f + 31) & 31);   // x_{f-1} (x_31 when f = 32)
+            const long long up = __shfl_sync(MO_FULL, u, (f + 31) & 31);
+            if (tid == 0) {
+              long long nlo = lo, nhi = hi, nU = Ulo;
+              if (f < 32) nhi = xf;
+              if (f > 0) {
+                nlo = xp + 1;
+                nU = up;
+              }
+              sSearch[0] = nlo;
+              sSearch[1] = nhi;
+              sSearch[2] = nU;
+            }
+          }
           __syncthreads();
-          const long long T = (long long)sAcc;
+          lo = sSearch[0];
+          hi = sSearch[1];
+          Ulo = sSearch[2];
           __syncthreads();
-          if (T >= k_rem) hi = mid; else lo = mid + 1;
         }
-        L = (int)lo;
-        unsigned long long part = 0;
-        for (int j = tid; j < w; j += blockDim.x) {
-          const int c = __ldcg(a.rho_p + j);
-          if (c == 0) continue;
-          const long long t = (long long)L - __ldcg(a.rho + j);
-          part += t < 0 ? 0 : (t > c ? c : t);
-        }
-        if (tid == 0) sAcc = 0;
-        __syncthreads();
-        atomicAdd(&sAcc, part);
-        __syncthreads();
-        before = (long long)sAcc;
-        __syncthreads();
+        L = (int)(lo - 1);
+        before = Ulo;
       }
       const int need = (int)(k_rem - before);
       level = L;
@@ -1509,25 +1541,146 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       for (int j = gwarp; j < w; j += nwarps) {
         const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
         if (t == 0 || t >= c) continue;
+        if (c > SEL_BIG) continue;   // crowded niche: a whole block below
         const int* bk = a.bucket + __ldcg(a.bstart + j);
         if (c <= 32) {
           int v = lane < c ? __ldcg(bk + lane) : 0x7fffffff;
           v = warp_bitonic_asc(v);
           if (lane < t) a.prom[a.perm_pop[v]] = 1;
         } else {
-          // smallest x with #{pos <= x} >= t (positions are distinct)
-          int lo = 0, hi = R - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            int cnt = 0;
-            for (int q = lane; q < c; q += 32) cnt += __ldcg(bk + q) <= mid;
-            cnt = warp_sum(cnt);
-            if (cnt >= t) hi = mid; else lo = mid + 1;
+          // the t-th smallest of the c distinct positions (< R) by an 8-bit-digit radix select in this
+          // warp's shared-memory bins: ceil(log2(R) / 8) passes over the bucket instead of a binary
+          // search of log2(R) passes (crowded niches hold thousands of candidates late in a run)
+          int* bins = sSel + (tid >> 5) * 256;
+          const int nbits = 32 - __clz(max(R - 1, 1));
+          int prefix = 0, need = t;
+          for (int shift = nbits; shift > 0;) {
+            const int b = min(8, shift);
+            shift -= b;
+            const int hiShift = shift + b;   // bits >= hiShift are fixed in prefix
+#pragma unroll
+            for (int q = 0; q < 8; ++q) bins[lane * 8 + q] = 0;
+            __syncwarp();
+            for (int q = lane; q < c; q += 32) {
+              const int v = __ldcg(bk + q);
+              if (hiShift >= 31 || (v >> hiShift) == (prefix >> hiShift))
+                atomicAdd(&bins[(v >> shift) & ((1 << b) - 1)], 1);
+            }
+            __syncwarp();
+            int cnt[8], sum = 0;   // lane owns bins [8 lane, 8 lane + 8)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              cnt[q] = bins[lane * 8 + q];
+              sum += cnt[q];
+            }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(MO_FULL, incl, o);
+              if (lane >= o) incl += y;
+            }
+            const unsigned hit = __ballot_sync(MO_FULL, incl >= need);
+            const int fl = __ffs(hit) - 1;   // the lane whose bins reach `need` (always exists)
+            int digit = 0, below = 0;
+            if (lane == fl) {
+              int run = incl - sum;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (run + cnt[q] >= need) {
+                  digit = lane * 8 + q;
+                  below = run;
+                  break;
+                }
+                run += cnt[q];
+              }
+            }
+            digit = __shfl_sync(MO_FULL, digit, fl);
+            below = __shfl_sync(MO_FULL, below, fl);
+            prefix |= digit << shift;
+            need -= below;
+            __syncwarp();
           }
           for (int q = lane; q < c; q += 32) {
             const int v = __ldcg(bk + q);
-            if (v <= lo) a.prom[a.perm_pop[v]] = 1;
+            if (v <= prefix) a.prom[a.perm_pop[v]] = 1;
           }
+        }
+      }
+      // crowded niches (> SEL_BIG bucketed candidates): the same radix select by a whole block, the
+      // candidates of 512 reference points at a time compacted through shared memory
+      {
+        int* bins = &sHist[0][0];          // free after P2
+        int* list = &sHist[1][0];
+        __shared__ int sNbig, sDigit, sBelow;
+        for (int base = blockIdx.x * SELECT_THREADS; base < w; base += gridDim.x * SELECT_THREADS) {
+          if (tid == 0) sNbig = 0;
+          __syncthreads();
+          {
+            const int j = base + tid;
+            if (j < w) {
+              const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
+              if (t > 0 && t < c && c > SEL_BIG) list[atomicAdd(&sNbig, 1)] = j;
+            }
+          }
+          __syncthreads();
+          const int nbig = sNbig;
+          for (int e = 0; e < nbig; ++e) {
+            const int j = list[e];
+            const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
+            const int* bk = a.bucket + __ldcg(a.bstart + j);
+            const int nbits = 32 - __clz(max(R - 1, 1));
+            int prefix = 0, need = t;
+            for (int shift = nbits; shift > 0;) {
+              const int b = min(8, shift);
+              shift -= b;
+              const int hiShift = shift + b;
+              if (tid < 256) bins[tid] = 0;
+              __syncthreads();
+              for (int q = tid; q < c; q += SELECT_THREADS) {
+                const int v = __ldcg(bk + q);
+                if (hiShift >= 31 || (v >> hiShift) == (prefix >> hiShift))
+                  atomicAdd(&bins[(v >> shift) & ((1 << b) - 1)], 1);
+              }
+              __syncthreads();
+              if (tid < 32) {
+                int cnt[8], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  cnt[q] = bins[lane * 8 + q];
+                  sum += cnt[q];
+                }
+                int incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                  const int y = __shfl_up_sync(MO_FULL, incl, o);
+                  if (lane >= o) incl += y;
+                }
+                const unsigned hit = __ballot_sync(MO_FULL, incl >= need);
+                const int fl = __ffs(hit) - 1;
+                if (lane == fl) {
+                  int run = incl - sum;
+#pragma unroll
+                  for (int q = 0; q < 8; ++q) {
+                    if (run + cnt[q] >= need) {
+                      sDigit = lane * 8 + q;
+                      sBelow = run;
+                      break;
+                    }
+                    run += cnt[q];
+                  }
+                }
+              }
+              __syncthreads();
+              prefix |= sDigit << shift;
+              need -= sBelow;
+              __syncthreads();
+            }
+            for (int q = tid; q < c; q += SELECT_THREADS) {
+              const int v = __ldcg(bk + q);
+              if (v <= prefix) a.prom[a.perm_pop[v]] = 1;
+            }
+          }
+          __syncthreads();   // list / sNbig reuse
         }
       }
       grid_sync(a.g.bar);

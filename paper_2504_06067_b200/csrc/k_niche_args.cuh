@@ -38,7 +38,7 @@ struct PrepArgs {
   int* fill;
   unsigned long long* near_key;
   uint8_t* prom;
-  int* lvl;   // 2 * LVL_BINS level histogram
+  int* lvl;   // LVL_WORDS: level histograms + level-search accumulators
   int* sctl;  // 16 select counters
   const int* lat_index;  // nullable: lattice index of every reference point (lattice-pruned association)
   int* lat_pos;          // lat_pos[lat_index[j]] = shuffled position of j
@@ -59,7 +59,10 @@ struct PrepArgs {
 };
 
 constexpr int LVL_BINS = 1024;
-enum { SCTL_M0 = 0, SCTL_ALLOC = 1 };
+// lvl region: the two level histograms, then 3 x 32 u64 accumulators of the 32-ary level search
+// (levels beyond the histogram window)
+constexpr int LVL_WORDS = 2 * LVL_BINS + 3 * 32 * 2;
+enum { SCTL_M0 = 0, SCTL_ALLOC = 1, SCTL_MAXE = 2 };
 
 enum { PREP_FULL = 0, PREP_PERMS_CAND = 1, PREP_PERMS = 2 };
 
@@ -132,7 +135,7 @@ struct SelectArgs {
   int* bucket;    // shuffled positions of the bucketed candidates (R)
   unsigned long long* near_key;
   uint8_t* prom;
-  int* lvl;       // 2 * LVL_BINS
+  int* lvl;       // LVL_WORDS
   int* sctl;
   uint8_t* selected;
   const float* XR;  // compaction sources (nullable)

@@ -112,7 +112,7 @@ static Layout make_layout(int64_t R, int64_t w, int m, int sort_mode = MO_SORT_B
   L.pctl = bump(c, 16 * 4);
   L.kept = bump(c, (size_t)(w + 1) * 4);
   L.fill = bump(c, (size_t)(w + 1) * 4);
-  L.lvl = bump(c, (size_t)2 * LVL_BINS * 4);
+  L.lvl = bump(c, (size_t)LVL_WORDS * 4);
   L.sctl = bump(c, 16 * 4);
   L.mate = bump(c, (size_t)(R + 16) * 4);   // [0..7] two tags, [8] counter, [16..): two n-slot mating buffers
   // rank-mask dominance tables (k_dom_rank.cu): per 256-row block and objective, Eytzinger values +

@@ -53,7 +53,7 @@ __device__ inline void gen_prologue(const PrepArgs& a, uint32_t gen, int gtid, i
       }
   }
   if (a.lvl)
-    for (int q = gtid; q < 2 * LVL_BINS; q += gthreads) a.lvl[q] = 0;
+    for (int q = gtid; q < LVL_WORDS; q += gthreads) a.lvl[q] = 0;
   if (a.sctl && gtid < 16) a.sctl[gtid] = 0;
   if (gtid == 0 && a.fb_ctl) {
     a.fb_ctl[0] = 0;

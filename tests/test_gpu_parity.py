@@ -348,6 +348,38 @@ def test_niche_select_bit_exact(M, seed, R, m, w_target):
     assert ginfo["NEAREST"] == len(info["nearest"])
 
 
+@pytest.mark.parametrize("seed,R,w,f0,f1,n", [(0, 40000, 8, 0, 30000, 20000), (1, 40000, 16, 5000, 30000, 20000),
+                                               (2, 12000, 3, 3000, 6000, 6000), (3, 200000, 40, 20000, 150000, 100000)])
+def test_niche_select_crowded_levels(M, seed, R, w, f0, f1, n):
+    """Crowded niches (thousands of members per reference point, as DTLZ3 m=10 late in a run): the water
+    level lies beyond k_select's 1024-bin histogram window (grid-cooperative 32-ary level search) and the
+    partially taken buckets hold thousands of candidates (radix top-t select)."""
+    rs = np.random.default_rng(seed)
+    ranks = np.full(R, 2, np.int32)
+    ranks[:f0] = 0
+    ranks[f0:f0 + f1] = 1 if f0 else 0
+    rs.shuffle(ranks)
+    sp = Odom.split_fronts(ranks, n)
+    assert not sp.infeasible if hasattr(sp, "infeasible") else True
+    p = 1.0 / np.arange(1, w + 1)
+    pi = rs.choice(w, size=R, p=p / p.sum()).astype(np.int32)
+    d = rs.random(R).astype(np.float32)
+    cand = ranks <= sp.l
+    pi[~cand] = -1
+    d[~cand] = 0
+    F = rs.random((R, 3)).astype(np.float32)
+    zh = np.ones((w, 3), np.float32) / np.sqrt(3)
+    gen = 7
+    sel, info = Oniche.select(F, ranks, sp, np.full(3, np.inf, np.float32), zh, seed, gen,
+                              associate_fn=lambda Fn, z, pos_ref, rows: (pi, d))
+    assert not info["skipped"]
+    gsel, granks, ginfo = M.niche.niche_select(pi, d, ranks, sp, n, w, seed, gen)
+    assert ginfo["LEVEL"] >= 1024, ginfo            # the instance exercises the search beyond the window
+    assert np.array_equal(np_(gsel), sel)
+    assert int(np_(gsel).sum()) == n
+    assert ginfo["NEAREST"] == len(info["nearest"])
+
+
 # ------------------------------------------------------------------- engine
 
 def _gpu_state_to_oracle(eng):
