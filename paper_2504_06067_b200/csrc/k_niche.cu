@@ -1305,6 +1305,7 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int gwarp = gtid >> 5, nwarps = gthreads >> 5;
   const int R = a.R, w = a.w;
+  int* plist = reinterpret_cast<int*>(a.near_key);   // P5 -> P7 list of partially taken points
   if (a.reset_ctl && gtid == 0) *a.reset_ctl = 0;   // k_assoc_final (the last reader) has completed
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   const int l = __ldcg(a.info + MO_INFO_L);
@@ -1519,6 +1520,9 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         const bool part = c > 0 && t > 0 && t < c;
         const int off = warp_alloc(&a.sctl[SCTL_ALLOC], part ? c : 0);   // bucket order is immaterial
         if (part) a.bstart[j] = off;
+        // the partially taken points, listed for P7 (near_key is dead after P2 and reset by the prologue)
+        const int slot = warp_alloc(&a.sctl[SCTL_NPART], part ? 1 : 0);
+        if (part) plist[slot] = j;
       }
       grid_sync(a.g.bar);
       trace_mark(a.trace, 29);
@@ -1538,9 +1542,10 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
       grid_sync(a.g.bar);
       trace_mark(a.trace, 30);
       // ---- P7: the take_j smallest shuffled positions of every partial bucket (warp per point)
-      for (int j = gwarp; j < w; j += nwarps) {
+      const int npart = __ldcg(a.sctl + SCTL_NPART);
+      for (int e = gwarp; e < npart; e += nwarps) {
+        const int j = __ldcg(plist + e);
         const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
-        if (t == 0 || t >= c) continue;
         if (c > SEL_BIG) continue;   // crowded niche: a whole block below
         const int* bk = a.bucket + __ldcg(a.bstart + j);
         if (c <= 32) {
@@ -1612,15 +1617,12 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         int* bins = &sHist[0][0];          // free after P2
         int* list = &sHist[1][0];
         __shared__ int sNbig, sDigit, sBelow;
-        for (int base = blockIdx.x * SELECT_THREADS; base < w; base += gridDim.x * SELECT_THREADS) {
+        for (int base = blockIdx.x * SELECT_THREADS; base < npart; base += gridDim.x * SELECT_THREADS) {
           if (tid == 0) sNbig = 0;
           __syncthreads();
-          {
-            const int j = base + tid;
-            if (j < w) {
-              const int t = __ldcg(a.take + j), c = __ldcg(a.rho_p + j);
-              if (t > 0 && t < c && c > SEL_BIG) list[atomicAdd(&sNbig, 1)] = j;
-            }
+          if (base + tid < npart) {
+            const int j = __ldcg(plist + base + tid);
+            if (__ldcg(a.rho_p + j) > SEL_BIG) list[atomicAdd(&sNbig, 1)] = j;
           }
           __syncthreads();
           const int nbig = sNbig;
@@ -1934,7 +1936,9 @@ int launch_select(const SelectArgs& a, cudaStream_t s) {
   int blocks = select_grid_blocks();
   // ~128 rows per CTA (one CTA per SM at C2): the phases are latency-bound, and more CTAs in flight beat
   // the extra barrier arrivals (C2: 64 -> 44 us, rows/CTA 1024 -> 128)
-  int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), 128);
+  const int64_t rows = a.R > a.w ? a.R : a.w;
+  int need = (int)ceil_div(rows, (int64_t)128);
+  if (rows <= 2048) need = 1;   // C1-sized: one CTA, every grid barrier is a __syncthreads
   if (blocks > need) blocks = need < 1 ? 1 : need;
   return launch_coop(k_select, blocks, SELECT_THREADS, a, s);
 }

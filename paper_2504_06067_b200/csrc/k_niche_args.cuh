@@ -62,7 +62,7 @@ constexpr int LVL_BINS = 1024;
 // lvl region: the two level histograms, then 3 x 32 u64 accumulators of the 32-ary level search
 // (levels beyond the histogram window)
 constexpr int LVL_WORDS = 2 * LVL_BINS + 3 * 32 * 2;
-enum { SCTL_M0 = 0, SCTL_ALLOC = 1, SCTL_MAXE = 2 };
+enum { SCTL_M0 = 0, SCTL_ALLOC = 1, SCTL_MAXE = 2, SCTL_NPART = 3 };
 
 enum { PREP_FULL = 0, PREP_PERMS_CAND = 1, PREP_PERMS = 2 };
 
