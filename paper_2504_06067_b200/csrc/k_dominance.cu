@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   const int gtid = blockIdx.x * blockDim.x + tid, gthreads = gridDim.x * blockDim.x;
   const int R = a.R, m = a.m;
   const int NB = presort_buckets(R);
+  // row loops of P0 / P3: wide rows (m > 16) are dealt round-robin over the CTAs (row b + G t) so the
+  // strided row reads spread over every SM's L1 instead of the first few CTAs'
+  const int rstart = m > 16 ? (int)blockIdx.x + (int)gridDim.x * tid : gtid;
   trace_mark(a.trace, 0);
   // P0: sums, keys, key range; clear bucket counts and fill cursors
   if (tid == 0) {
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
   }
   __syncthreads();
   unsigned kmin = 0xffffffffu, kmax = 0u;
-  for (int i = gtid; i < R; i += gthreads) {
+  for (int i = rstart; i < R; i += gthreads) {
     const float* f = a.F + (int64_t)i * m;
     float s = f[0];
     for (int k = 1; k < m; ++k) s = __fadd_rn(s, f[k]);
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(PRESORT_THREADS) k_presort(PresortArgs a) {
     for (int pos = gtid; pos < R; pos += gthreads) a.tkey[__ldcg(a.valA + pos)] = __ldcg(a.keyA + pos);
     grid_sync(a.g.bar);
   } else {
-    for (int i = gtid; i < R; i += gthreads) {
+    for (int i = rstart; i < R; i += gthreads) {
       const uint32_t q = __ldcg(a.keyA + i);
       const int pos = atomicAdd(&a.fill[q], 1);
       a.perm[pos] = i;
@@ -700,7 +703,8 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
     small_max = e ? atoi(e) : 2048;
     if (small_max > PS_MAXR) small_max = PS_MAXR;
   }
-  if (!args.stable && args.R <= small_max) {
+  // (and wide rows: the one-CTA version reads R x m strided values through a single SM)
+  if (!args.stable && args.R <= small_max && (int64_t)args.R * args.m <= 32768) {
     static bool attr = false;
     if (!attr) {
       if (cudaFuncSetAttribute(k_presort_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -717,6 +721,7 @@ int launch_presort(const PresortArgs& args, cudaStream_t s) {
   const int64_t by_rows = ceil_div((int64_t)args.R, (int64_t)(PRESORT_THREADS / 2));
   const int64_t by_buckets = ceil_div((int64_t)NB, (int64_t)(PRESORT_THREADS * 4));
   int blocks = (int)(by_rows > by_buckets ? by_rows : by_buckets);
+  if (args.m > 16) blocks = (int)ceil_div((int64_t)args.R, (int64_t)8);   // wide rows: ~8 rows per CTA
   if (blocks > maxb) blocks = maxb;
   if (blocks < 1) blocks = 1;
   if (!args.in_step) {

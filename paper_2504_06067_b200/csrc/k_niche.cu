@@ -231,50 +231,66 @@ __device__ void gauss_solve_block(double* A, double* rhs, int m, int* singular, 
 
 // phase 1 of k_prep for runtime m (wide m > 16): the same keys and column maxima as prep_extremes<M>.
 // The ASF of axis ax is max(ft[ax], max_{k != ax} q[k]) (fmaxf: exact, NaN-ignoring, order-free), so
-// one pass finds the largest q and the largest q outside its index and every axis takes one of them.
-__device__ __forceinline__ void prep_extremes_rt(const PrepArgs& a, int R, int l, int gthreads, bool build_cand,
-                                                 int m) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int base = blockIdx.x * blockDim.x; base < R; base += gthreads) {   // uniform trip count
-    const int row = base + tid;
-    const bool act = row < R && a.ranks[row] >= 0 && a.ranks[row] <= l;
-    if (build_cand) {
-      const int slot = warp_alloc(a.ctl, act ? 1 : 0);
-      if (act) a.cand[slot] = row;
-    }
-    const float* f = a.F + (int64_t)(act ? row : 0) * m;
-    int pp = 0;
-    float top1 = __int_as_float(0x7fc00000), top2 = top1;
-    int i1 = -1;
-    if (act) {
-      pp = __ldcg(a.pos_pop + row);
-      for (int k = 0; k < m; ++k) {
-        const float q = __fdiv_rn(__fsub_rn(f[k], __ldcg(a.ideal + k)), ASF_EPS);
-        if (q > top1 || top1 != top1) {          // new maximum (NaN q never enters)
-          if (q == q) {
-            top2 = top1;
-            top1 = q;
-            i1 = k;
-          }
-        } else {
-          top2 = fmaxf(top2, q);
+// one pass finds the largest q (first index) and the largest q outside its index and every axis takes
+// one of them.  A warp per candidate row (coalesced row reads, the top-2 merged across lanes), the
+// column maxima and complemented keys reduced in shared memory (scratch: k_prep's not yet used system
+// buffer), one atomic per CTA and axis.
+__device__ __forceinline__ void prep_extremes_rt(const PrepArgs& a, int R, int l, bool build_cand, int m,
+                                                 double* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, nwb = blockDim.x >> 5;
+  uint32_t* sCol = reinterpret_cast<uint32_t*>(scratch);                       // MO_MAX_M
+  unsigned long long* sKey = reinterpret_cast<unsigned long long*>(scratch + MO_MAX_M / 2);
+  for (int k = tid; k < m; k += blockDim.x) {
+    sCol[k] = 0u;
+    sKey[k] = 0ull;
+  }
+  __syncthreads();
+  const float QNAN = __int_as_float(0x7fc00000);
+  for (int row = blockIdx.x * nwb + (tid >> 5); row < R; row += gridDim.x * nwb) {   // warp-uniform
+    const int r = a.ranks[row];
+    if (!(r >= 0 && r <= l)) continue;
+    if (build_cand && lane == 0) a.cand[atomicAdd(a.ctl, 1)] = row;   // candidate order is immaterial
+    const float* f = a.F + (int64_t)row * m;
+    const int pp = __ldcg(a.pos_pop + row);
+    float t1 = QNAN, t2 = QNAN;   // largest q (first index i1) and the largest q at any other index
+    int i1 = 0x7fffffff;
+    for (int k = lane; k < m; k += 32) {
+      const float q = __fdiv_rn(__fsub_rn(f[k], __ldcg(a.ideal + k)), ASF_EPS);
+      if (q > t1 || t1 != t1) {
+        if (q == q) {
+          t2 = t1;
+          t1 = q;
+          i1 = k;
         }
+      } else {
+        t2 = fmaxf(t2, q);
       }
     }
-    for (int k = 0; k < m; ++k) {
-      uint32_t v = act ? f2ord(__fsub_rn(f[k], __ldcg(a.ideal + k))) : 0u;
-      v = warp_max_u32(v);
-      if (lane == 0 && v) atomicMax(&a.colmax[k], v);
-    }
-    for (int ax = 0; ax < m; ++ax) {
-      unsigned long long key = ~0ull;
-      if (act) {
-        const float s = fmaxf(__fsub_rn(f[ax], __ldcg(a.ideal + ax)), ax == i1 ? top2 : top1);
-        key = ((unsigned long long)f2ord(s) << 32) | (uint32_t)pp;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float b1 = __shfl_xor_sync(MO_FULL, t1, o), b2 = __shfl_xor_sync(MO_FULL, t2, o);
+      const int bi = __shfl_xor_sync(MO_FULL, i1, o);
+      if (b1 != b1) continue;                       // nothing on the other side
+      if (t1 != t1 || b1 > t1 || (b1 == t1 && bi < i1)) {
+        t2 = t1 != t1 ? b2 : fmaxf(b2, fmaxf(t2, t1));
+        t1 = b1;
+        i1 = bi;
+      } else {
+        t2 = fmaxf(t2, fmaxf(b2, b1));
       }
-      key = warp_min_u64(key);
-      if (lane == 0 && key != ~0ull) atomicMax(&a.ext_key[ax], ~key);
     }
+    for (int k = lane; k < m; k += 32) {
+      const float ft = __fsub_rn(f[k], __ldcg(a.ideal + k));
+      const uint32_t c = f2ord(ft);
+      if (c) atomicMax(&sCol[k], c);
+      const float sv = fmaxf(ft, k == i1 ? t2 : t1);
+      const unsigned long long key = ((unsigned long long)f2ord(sv) << 32) | (uint32_t)pp;
+      atomicMax(&sKey[k], ~key);
+    }
+  }
+  __syncthreads();
+  for (int k = tid; k < m; k += blockDim.x) {
+    if (sCol[k]) atomicMax(&a.colmax[k], sCol[k]);
+    if (sKey[k]) atomicMax(&a.ext_key[k], sKey[k]);
   }
 }
 
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     MO_PX_CASE(8) MO_PX_CASE(9) MO_PX_CASE(10) MO_PX_CASE(11) MO_PX_CASE(12) MO_PX_CASE(13) MO_PX_CASE(14)
     MO_PX_CASE(15) MO_PX_CASE(16)
 #undef MO_PX_CASE
-    default: prep_extremes_rt(a, R, l, gthreads, fused, m);   // wide m (launch_prep: m <= MO_MAX_M)
+    default: prep_extremes_rt(a, R, l, fused, m, sA);   // wide m (launch_prep: m <= MO_MAX_M)
   }
   // phase 2 runs in the last block to finish phase 1
   if (!grid_last(a.bar)) return;
@@ -453,11 +469,25 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     __shared__ double sFb0[MAXM], sGF0[MAXM];
     double* sFb = big ? sA + MO_MAX_M : sFb0;
     double* A = big ? a.solveA : sA;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int r = e / m, c = e - r * m;
-      const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
-      const int row = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
-      A[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
+    if (big) {
+      // extreme rows first (two dependent loads each), then the m x m loads independent and coalesced
+      int* sRowX = reinterpret_cast<int*>(sA + 3 * MO_MAX_M);   // after rhs / fallbacks / solve scratch
+      for (int r = tid; r < m; r += blockDim.x) {
+        const unsigned long long ck = __ldcg(a.ext_key + r);
+        sRowX[r] = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
+      }
+      __syncthreads();
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int r = e / m, c = e - r * m;
+        A[e] = (double)__fsub_rn(a.F[(int64_t)sRowX[r] * m + c], __ldcg(a.ideal + c));
+      }
+    } else {
+      for (int e = tid; e < m * m; e += blockDim.x) {
+        const int r = e / m, c = e - r * m;
+        const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
+        const int row = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
+        A[e] = (double)__fsub_rn(a.F[(int64_t)row * m + c], __ldcg(a.ideal + c));
+      }
     }
     for (int k = tid; k < m; k += blockDim.x) {
       const double mx = (double)ord2f(__ldcg(a.colmax + k));
@@ -1691,17 +1721,21 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
   }
   // ---- P8: survivors = fronts < l + promoted (or fronts <= l when niching was skipped);
   //          promoted rank = l - 1 (A-8); stable compaction in merged-row order (A-9)
+  // wide rows (d + m >= 64, e.g. PAPER Appendix D d = 1000): the emitting thread only records the slot
+  // and the block's warps copy its chunk's survivors row by row, coalesced
+  const bool wide_copy = a.X_next && a.dvars + a.m >= 64;
+  auto survives = [&](int64_t i) {
+    const int r = a.ranks[i];
+    return skipped ? (r >= 0 && r <= l) : ((r >= 0 && r < l) || __ldcg(a.prom + i) != 0);
+  };
   const int nsurv = grid_scan(
-      a.g, R,
-      [&](int64_t i) {
-        const int r = a.ranks[i];
-        const bool s = skipped ? (r >= 0 && r <= l) : ((r >= 0 && r < l) || __ldcg(a.prom + i) != 0);
-        return (int)s;
-      },
+      a.g, R, [&](int64_t i) { return (int)survives(i); },
       [&](int64_t i, int pre) {
         // survivor `pre` <- merged row i, copied by the emitting thread (the rows are L2-resident; no
         // barrier + second pass for a separate gather)
-        if (a.X_next) {
+        if (wide_copy) {
+          a.bucket[i] = pre;   // bucket (P6 / P7) is dead here
+        } else if (a.X_next) {
           const int d = a.dvars, mm = a.m;
           const float* xs = a.XR + i * d;
           float* xd = a.X_next + (int64_t)pre * d;
@@ -1710,6 +1744,30 @@ __global__ void __launch_bounds__(SELECT_THREADS) k_select(SelectArgs a) {
         }
       },
       sh);
+  if (wide_copy) {
+    // this block's chunk of the scan, SELECT_THREADS rows at a time: its survivors listed in shared
+    // memory (sSel is free after P7), then the (row, element) space copied by the whole block
+    __shared__ int sNl;
+    const int64_t chunk = ceil_div((int64_t)R, (int64_t)gridDim.x);
+    const int64_t lo = min((int64_t)blockIdx.x * chunk, (int64_t)R), hi = min(lo + chunk, (int64_t)R);
+    const int d = a.dvars, mm = a.m, rowlen = a.dvars + a.m;
+    for (int64_t w0 = lo; w0 < hi; w0 += SELECT_THREADS) {
+      if (tid == 0) sNl = 0;
+      __syncthreads();   // (first window: the slot records of this chunk are visible block-wide)
+      const int64_t e = w0 + tid;
+      if (e < hi && survives(e)) sSel[atomicAdd(&sNl, 1)] = (int)e;
+      __syncthreads();
+      const int nl = sNl;
+      for (int t = tid; t < nl * rowlen; t += SELECT_THREADS) {   // nl <= 512: fits in int
+        const int li = t / rowlen, v = t - li * rowlen;
+        const int64_t i = sSel[li];
+        const int64_t dst = __ldcg(a.bucket + i);
+        if (v < d) a.X_next[dst * d + v] = a.XR[i * d + v];
+        else a.F_next[dst * mm + (v - d)] = a.FR[i * mm + (v - d)];
+      }
+      __syncthreads();
+    }
+  }
   trace_mark(a.trace, 35);
   // No grid barrier after the P8 compaction scan: other blocks may still be in grid_scan's second
   // pass re-reading ranks[] of their chunks while this loop rewrites promoted rows to l-1.  That is
@@ -1769,6 +1827,7 @@ int launch_prep(const PrepArgs& a, cudaStream_t s) {
   }
   int blocks = prep_grid_blocks();
   int need = (int)ceil_div((int64_t)(a.R > a.w ? a.R : a.w), 256);
+  if (a.m > 16) need = (int)ceil_div((int64_t)a.R, (int64_t)32);   // wide m: a warp per row, ~4 rows per warp
   if (blocks > need) blocks = need < 1 ? 1 : need;
   return launch_coop(k_prep, blocks, 256, a, s);
 }
@@ -1938,7 +1997,13 @@ int launch_select(const SelectArgs& a, cudaStream_t s) {
   // the extra barrier arrivals (C2: 64 -> 44 us, rows/CTA 1024 -> 128)
   const int64_t rows = a.R > a.w ? a.R : a.w;
   int need = (int)ceil_div(rows, (int64_t)128);
-  if (rows <= 2048) need = 1;   // C1-sized: one CTA, every grid barrier is a __syncthreads
+  // C1-sized: one CTA, every grid barrier is a __syncthreads (not for wide rows: the survivor copy)
+  if (rows <= 2048 && a.dvars + a.m < 64) need = 1;
+  // wide rows: enough CTAs for the survivor copy (~32K copied values per CTA)
+  if (a.X_next && a.dvars + a.m >= 64) {
+    const int64_t copy = ceil_div((int64_t)a.n * (a.dvars + a.m), (int64_t)32768);
+    if (copy > need) need = (int)copy;
+  }
   if (blocks > need) blocks = need < 1 ? 1 : need;
   return launch_coop(k_select, blocks, SELECT_THREADS, a, s);
 }

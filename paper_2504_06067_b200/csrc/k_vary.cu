@@ -153,8 +153,22 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   }
   __syncthreads();
   if (tb) trace_mark_any(pro.trace, 43);
-  // Phase 3b: one thread per (child, objective)
-  const int etasks = nch * m;
+  // Phase 3b: one thread per (child, objective); wide m: one thread per child, all m objectives by
+  // running prefix products (O(m) transcendentals per child instead of O(m^2))
+  if (m > 16) {
+    for (int cl = tid; cl < nch; cl += VARY_THREADS) {
+      const int child = 2 * q0 + cl;
+      float* fo = Fo + (int64_t)child * m;
+      dtlz_eval_prefix(problem, Xo + (int64_t)child * d, m, shG[cl], [&](int j, float f) {
+        fo[j] = f;
+        if (ideal) {
+          if (j < 16) atomic_min_float(&shMin[j], f);
+          else atomic_min_float(&ideal[j], f);
+        }
+      });
+    }
+  }
+  const int etasks = m > 16 ? 0 : nch * m;
   for (int e = tid; e < etasks; e += VARY_THREADS) {
     const int cl = e / m, j = e - cl * m;
     const int child = 2 * q0 + cl;

@@ -146,4 +146,36 @@ __device__ inline float dtlz_eval_obj(int problem, const float* __restrict__ x, 
   return (float)val;
 }
 
+// All m objectives of one row in O(m) (wide m): every product of dtlz_eval_obj is a left fold over the
+// same leading factors, so after t factors the running prefix is objective (m-1-t)'s partial product and
+// out(j, f_j) receives bit-identical values (same factors, same order, same sin / cos calls).
+template <class Out>
+__device__ inline void dtlz_eval_prefix(int problem, const float* __restrict__ x, int m, double g, Out out) {
+  const double PI = 3.141592653589793;
+  if (problem == 7) {
+    for (int j = 0; j < m; ++j) out(j, dtlz_eval_obj(problem, x, m, j, g));
+    return;
+  }
+  if (problem == 1) {
+    double P = 0.5 * (1.0 + g);
+    for (int t = 0; t < m - 1; ++t) {
+      out(m - 1 - t, (float)(P * (1.0 - (double)x[t])));
+      P = P * (double)x[t];
+    }
+    out(0, (float)P);
+    return;
+  }
+  const double hp = PI / 2.0;
+  double P = 1.0 + g;
+  for (int t = 0; t < m - 1; ++t) {
+    double xi = (double)x[t];
+    if (problem == 4) xi = pow(xi, 100.0);
+    const double th = ((problem == 5 || problem == 6) && t > 0) ? PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * xi)
+                                                                 : xi * hp;
+    out(m - 1 - t, (float)(P * sin(th)));
+    P = P * cos(th);
+  }
+  out(0, (float)P);
+}
+
 }  // namespace mo

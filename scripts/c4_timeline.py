@@ -33,6 +33,12 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(2):
         eng.step()
     torch.cuda.synchronize()
+import ctypes  # noqa: E402
+from paper_2504_06067_b200 import _lib  # noqa: E402
+off = ctypes.c_int64(0)
+_lib.check(_lib.lib().mo_stream_stats_offset(n, 3, eng.w, eng.sort_mode, eng.shard_count, ctypes.byref(off)), "stats")
+st = eng.ws[off.value: off.value + 32].view(torch.int64).cpu().tolist()
+print(json.dumps({"count_pairs_le": st[0], "count_pairs_full": st[1], "dec_pairs_le": st[2], "dec_pairs_full": st[3]}))
 ks = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 agg = {}
 for e in ks:
