@@ -458,6 +458,22 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
 #undef MO_PX_CASE
     default: prep_extremes_rt(a, R, l, fused, m, sA);   // wide m (launch_prep: m <= MO_MAX_M)
   }
+  if (big) {
+    // m > 64: the m x m system lives in global memory; every block loads a slice of it (one more grid
+    // barrier) instead of the last block alone -- a single CTA's load -> store round trips over 262K
+    // values took ~0.3 ms at m = 512
+    grid_sync(a.bar);
+    int* sRowX = reinterpret_cast<int*>(sA + 3 * MO_MAX_M);   // after rhs / fallbacks / solve scratch
+    for (int r = tid; r < m; r += blockDim.x) {
+      const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
+      sRowX[r] = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
+    }
+    __syncthreads();
+    for (int e = gtid; e < m * m; e += gthreads) {
+      const int r = e / m, c = e - r * m;
+      a.solveA[e] = (double)__fsub_rn(__ldg(a.F + (int64_t)sRowX[r] * m + c), __ldcg(a.ideal + c));
+    }
+  }
   // phase 2 runs in the last block to finish phase 1
   if (!grid_last(a.bar)) return;
   trace_mark_any(a.trace, 18);
@@ -469,19 +485,7 @@ __global__ void __launch_bounds__(256) k_prep(PrepArgs a) {
     __shared__ double sFb0[MAXM], sGF0[MAXM];
     double* sFb = big ? sA + MO_MAX_M : sFb0;
     double* A = big ? a.solveA : sA;
-    if (big) {
-      // extreme rows first (two dependent loads each), then the m x m loads independent and coalesced
-      int* sRowX = reinterpret_cast<int*>(sA + 3 * MO_MAX_M);   // after rhs / fallbacks / solve scratch
-      for (int r = tid; r < m; r += blockDim.x) {
-        const unsigned long long ck = __ldcg(a.ext_key + r);
-        sRowX[r] = ck ? __ldcg(a.perm_pop + (uint32_t)(~ck & 0xffffffffull)) : 0;
-      }
-      __syncthreads();
-      for (int e = tid; e < m * m; e += blockDim.x) {
-        const int r = e / m, c = e - r * m;
-        A[e] = (double)__fsub_rn(a.F[(int64_t)sRowX[r] * m + c], __ldcg(a.ideal + c));
-      }
-    } else {
+    if (!big) {   // (m > 64: loaded by every block before grid_last)
       for (int e = tid; e < m * m; e += blockDim.x) {
         const int r = e / m, c = e - r * m;
         const unsigned long long ck = __ldcg(a.ext_key + r);   // complemented key; 0 = no candidate
@@ -1248,47 +1252,54 @@ __global__ void k_assoc_final(AssocFinalArgs a) {
 }
 
 // k_assoc_final for runtime m (wide m > 16): identical arithmetic, objectives re-read from F (L1)
-__global__ void k_assoc_final_rt(AssocFinalArgs a) {
+// Wide m: a warp per candidate row -- Fn_k and the direction z_k staged by the lanes (coalesced) in a
+// per-warp shared-memory slice, then lane 0 runs the same sequential FP32 folds (t, then s2) as
+// k_assoc_final<M>, so the results are bit-identical while the loads and divides are spread over 32
+// lanes.
+constexpr int AFW_WARPS = 4;
+__global__ void __launch_bounds__(AFW_WARPS * 32) k_assoc_final_rt(AssocFinalArgs a) {
+  __shared__ float sF[AFW_WARPS][MO_MAX_M], sZ[AFW_WARPS][MO_MAX_M];
   pdl_wait();
   if (__ldcg(a.info + MO_INFO_ERROR) != 0) return;
   if (__ldcg(a.info + MO_INFO_SKIPPED) != 0) return;
   const int ncand = __ldcg(a.ctl);
-  const int base = blockIdx.x * blockDim.x;
-  if (base >= ncand) return;
-  const int c = base + threadIdx.x;
-  const bool act = c < ncand;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int m = a.m;
-  const int row = act ? __ldcg(a.cand + c) : 0;
-  auto fn = [&](int k) {
-    float v = a.F[(int64_t)row * m + k];
-    if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
-    if (a.a32) v = __fdiv_rn(v, a.a32[k]);
-    return v;
-  };
-  if (act && a.Fn_out)
-    for (int k = 0; k < m; ++k) a.Fn_out[(int64_t)row * m + k] = fn(k);
-  if (a.fn_only) return;
-  int j = 0;
-  if (act) {
+  float* fw = sF[w];
+  float* zw = sZ[w];
+  const int l = a.ranks ? __ldcg(a.info + MO_INFO_L) : 0;
+  for (int c = blockIdx.x * AFW_WARPS + w; c < ncand; c += gridDim.x * AFW_WARPS) {   // warp-uniform
+    const int row = __ldcg(a.cand + c);
+    for (int k = lane; k < m; k += 32) {
+      float v = a.F[(int64_t)row * m + k];
+      if (a.ideal) v = __fsub_rn(v, a.ideal[k]);
+      if (a.a32) v = __fdiv_rn(v, a.a32[k]);
+      fw[k] = v;
+      if (a.Fn_out) a.Fn_out[(int64_t)row * m + k] = v;
+    }
+    if (a.fn_only) continue;
     const unsigned long long key = __ldcg(a.akey + row);
     const int p = (int)(0xffffffffu - (uint32_t)(key & 0xffffffffull));
-    const float* z = a.zs + (int64_t)p * m;
-    float t = __fmul_rn(fn(0), z[0]);
-    for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fn(k), z[k]));
-    float s2 = 0.0f;
-    for (int k = 0; k < m; ++k) {
-      const float e = __fsub_rn(fn(k), __fmul_rn(t, z[k]));
-      s2 = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s2, __fmul_rn(e, e));
+    for (int k = lane; k < m; k += 32) zw[k] = a.zs[(int64_t)p * m + k];
+    __syncwarp();
+    if (lane == 0) {
+      float t = __fmul_rn(fw[0], zw[0]);
+      for (int k = 1; k < m; ++k) t = __fadd_rn(t, __fmul_rn(fw[k], zw[k]));
+      float s2 = 0.0f;
+      for (int k = 0; k < m; ++k) {
+        const float e = __fsub_rn(fw[k], __fmul_rn(t, zw[k]));
+        s2 = k == 0 ? __fmul_rn(e, e) : __fadd_rn(s2, __fmul_rn(e, e));
+      }
+      const int j = a.perm_ref[p];
+      a.pi[row] = j;
+      a.d[row] = __fsqrt_rn(s2);
+      if (a.ranks) {
+        const int r = a.ranks[row];
+        if (r < l) atomicAdd(a.rho + j, 1);
+        if (r == l) atomicAdd(a.rho_p + j, 1);
+      }
     }
-    j = a.perm_ref[p];
-    a.pi[row] = j;
-    a.d[row] = __fsqrt_rn(s2);
-  }
-  if (a.ranks) {
-    const int l = __ldcg(a.info + MO_INFO_L);
-    const int r = act ? a.ranks[row] : -1;
-    warp_agg_add(a.rho, j, act && r < l);
-    warp_agg_add(a.rho_p, j, act && r == l);
+    __syncwarp();   // the slices are rewritten by the next row
   }
 }
 
@@ -1986,7 +1997,8 @@ int launch_assoc_final(const AssocFinalArgs& a, int64_t R, cudaStream_t s) {
 #undef MO_AF_CASE
     default:
       if (a.m > MO_MAX_M) return MO_ERR_PARAM;
-      return launch_ex(k_assoc_final_rt, grid, blk, 0, s, false, g_mo_pdl, a);
+      return launch_ex(k_assoc_final_rt, dim3((unsigned)ceil_div(R, (int64_t)AFW_WARPS)), dim3(AFW_WARPS * 32), 0, s,
+                       false, g_mo_pdl, a);
   }
 }
 

@@ -155,7 +155,46 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   if (tb) trace_mark_any(pro.trace, 43);
   // Phase 3b: one thread per (child, objective); wide m: one thread per child, all m objectives by
   // running prefix products (O(m) transcendentals per child instead of O(m^2))
-  if (m > 16) {
+  if (m > 16 && problem != 7) {
+    // the factors (cos, sin or x, 1 - x of the first m-1 variables) of 32 variables at a time for every
+    // child by all threads, then one thread per child extends its running prefix product over them
+    __shared__ double shC[2 * VARY_PAIRS][32], shS[2 * VARY_PAIRS][32];
+    double P = 0.0;
+    const int cl0 = tid;   // the child this thread folds (tid < nch)
+    if (cl0 < nch) P = problem == 1 ? 0.5 * (1.0 + shG[cl0]) : 1.0 + shG[cl0];
+    for (int t0 = 0; t0 < m - 1; t0 += 32) {
+      for (int e = tid; e < nch * 32; e += VARY_THREADS) {
+        const int cl = e >> 5, u = e & 31, t = t0 + u;
+        if (t < m - 1) {
+          double cf, sf;
+          dtlz_factors(problem, Xo + (int64_t)(2 * q0 + cl) * d, t, shG[cl], cf, sf);
+          shC[cl][u] = cf;
+          shS[cl][u] = sf;
+        }
+      }
+      __syncthreads();
+      if (cl0 < nch) {
+        const int child = 2 * q0 + cl0;
+        float* fo = Fo + (int64_t)child * m;
+        for (int u = 0; u < 32 && t0 + u < m - 1; ++u) {
+          const int j = m - 1 - (t0 + u);
+          const float f = (float)(P * shS[cl0][u]);
+          P = P * shC[cl0][u];
+          fo[j] = f;
+          if (ideal) {
+            if (j < 16) atomic_min_float(&shMin[j], f);
+            else atomic_min_float(&ideal[j], f);
+          }
+        }
+        if (t0 + 32 >= m - 1) {   // last chunk: f_0 = the full product
+          const float f = (float)P;
+          fo[0] = f;
+          if (ideal) atomic_min_float(&shMin[0], f);
+        }
+      }
+      __syncthreads();
+    }
+  } else if (m > 16) {
     for (int cl = tid; cl < nch; cl += VARY_THREADS) {
       const int child = 2 * q0 + cl;
       float* fo = Fo + (int64_t)child * m;

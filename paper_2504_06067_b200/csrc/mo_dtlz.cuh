@@ -146,6 +146,24 @@ __device__ inline float dtlz_eval_obj(int problem, const float* __restrict__ x, 
   return (float)val;
 }
 
+// Factor pair of variable t < m-1 for the prefix form below: cf multiplies the running prefix,
+// sf closes objective m-1-t (DTLZ1: x_t and 1 - x_t; DTLZ2-6: cos and sin of the same angle).
+__device__ inline void dtlz_factors(int problem, const float* __restrict__ x, int t, double g, double& cf,
+                                    double& sf) {
+  const double PI = 3.141592653589793;
+  if (problem == 1) {
+    cf = (double)x[t];
+    sf = 1.0 - (double)x[t];
+    return;
+  }
+  double xi = (double)x[t];
+  if (problem == 4) xi = pow(xi, 100.0);
+  const double th = ((problem == 5 || problem == 6) && t > 0) ? PI / (4.0 * (1.0 + g)) * (1.0 + 2.0 * g * xi)
+                                                               : xi * (PI / 2.0);
+  cf = cos(th);
+  sf = sin(th);
+}
+
 // All m objectives of one row in O(m) (wide m): every product of dtlz_eval_obj is a left fold over the
 // same leading factors, so after t factors the running prefix is objective (m-1-t)'s partial product and
 // out(j, f_j) receives bit-identical values (same factors, same order, same sin / cos calls).
