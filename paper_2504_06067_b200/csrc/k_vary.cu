@@ -27,6 +27,9 @@ namespace mo {
 // objective) evaluates DTLZ in FP64 and lowers the block's column minima.
 constexpr int VARY_PAIRS = 16;
 constexpr int VARY_THREADS = 256;
+#ifndef MO_VARY_FACTOR_M
+#define MO_VARY_FACTOR_M 5
+#endif
 
 __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const float* __restrict__ X, int n, int d,
                                                             int m, uint64_t seed, uint32_t gen_val,
@@ -153,9 +156,10 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
   }
   __syncthreads();
   if (tb) trace_mark_any(pro.trace, 43);
-  // Phase 3b: one thread per (child, objective); wide m: one thread per child, all m objectives by
-  // running prefix products (O(m) transcendentals per child instead of O(m^2))
-  if (m > 16 && problem != 7) {
+  // Phase 3b: one thread per (child, objective) for small m; from MO_VARY_FACTOR_M objectives on, the
+  // factors of the running prefix products by all threads, then one thread per child folds them
+  // (O(m) transcendentals per child instead of O(m^2), bit-identical)
+  if (m >= MO_VARY_FACTOR_M && problem != 7) {
     // the factors (cos, sin or x, 1 - x of the first m-1 variables) of 32 variables at a time for every
     // child by all threads, then one thread per child extends its running prefix product over them
     __shared__ double shC[2 * VARY_PAIRS][32], shS[2 * VARY_PAIRS][32];
@@ -163,14 +167,13 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
     const int cl0 = tid;   // the child this thread folds (tid < nch)
     if (cl0 < nch) P = problem == 1 ? 0.5 * (1.0 + shG[cl0]) : 1.0 + shG[cl0];
     for (int t0 = 0; t0 < m - 1; t0 += 32) {
-      for (int e = tid; e < nch * 32; e += VARY_THREADS) {
-        const int cl = e >> 5, u = e & 31, t = t0 + u;
-        if (t < m - 1) {
-          double cf, sf;
-          dtlz_factors(problem, Xo + (int64_t)(2 * q0 + cl) * d, t, shG[cl], cf, sf);
-          shC[cl][u] = cf;
-          shS[cl][u] = sf;
-        }
+      const int cw = min(32, m - 1 - t0);   // variables in this chunk
+      for (int e = tid; e < nch * cw; e += VARY_THREADS) {
+        const int cl = e / cw, u = e - cl * cw;
+        double cf, sf;
+        dtlz_factors(problem, Xo + (int64_t)(2 * q0 + cl) * d, t0 + u, shG[cl], cf, sf);
+        shC[cl][u] = cf;
+        shS[cl][u] = sf;
       }
       __syncthreads();
       if (cl0 < nch) {
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(VARY_THREADS) k_vary_eval(int problem, const f
       });
     }
   }
-  const int etasks = m > 16 ? 0 : nch * m;
+  const int etasks = (m > 16 || (m >= MO_VARY_FACTOR_M && problem != 7)) ? 0 : nch * m;
   for (int e = tid; e < etasks; e += VARY_THREADS) {
     const int cl = e / m, j = e - cl * m;
     const int child = 2 * q0 + cl;
