@@ -26,6 +26,8 @@
 // overlapping tiles are transposed through warp ballots and shared memory.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "mo_common.cuh"
 #include "k_dominance_args.cuh"
 #include "mo_async.cuh"
@@ -54,6 +56,8 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__
                                                         int m_rt, uint32_t* __restrict__ tsum) {
   pdl_wait();
   const int m = M > 0 ? M : m_rt;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+    vmask[(int64_t)gridDim.x * 8] = 0u;   // k_dom_rank's chunk counter (in the tables' slack)
   if (tsum && blockIdx.y == 0) {   // this generation's tile summary of block bi's rows starts empty
     const int64_t TW = tsum_words(R);
     const int64_t r0 = (int64_t)blockIdx.x * DR_BLK, r1 = min((int64_t)R, r0 + DR_BLK);
@@ -143,6 +147,9 @@ struct DomRankArgs {
   int64_t items;
   uint32_t* tsum;          // nullable: tile summary (then zero word blocks are not stored)
   int64_t TW;
+  int ordered_and;         // S-separated tiles: AND the prefixes shortest first with early exit
+  int64_t pairs;           // k_dom_rank<M>: tiles of the block upper triangle (row-major), chunks of ch
+  unsigned* next;          // k_dom_rank<M>: chunk counter (zeroed by k_dom_tables)
 };
 
 // store the 8 words of block `blk` of row `row` (always without a summary; with one, only when nonzero,
@@ -179,6 +186,72 @@ __device__ __forceinline__ void dr_decode(int64_t t, int nb, int ch, int& bi, in
   bj1 = min(nb, bj0 + ch);
 }
 
+// le = AND_k P_k[c_k] (c_k = node[k] - DR_EYT): a_i <= b_j in every objective
+// tile t of the row-major upper block triangle (row bi holds tiles (bi, bi..nb-1), offset
+// off(bi) = bi nb - bi (bi - 1) / 2) -> block row bi and the J run [bj0, bj1) up to the row end or t1
+__device__ __forceinline__ void dr_tile_decode(int64_t t, int64_t t1, int nb, int& bi, int& bj0, int& bj1) {
+  int lo = 0, hi = nb - 1;   // largest bi with off(bi) <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int64_t)mid * nb - (int64_t)mid * (mid - 1) / 2 <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  bi = lo;
+  bj0 = bi + (int)(t - ((int64_t)bi * nb - (int64_t)bi * (bi - 1) / 2));
+  bj1 = (int)min((int64_t)nb, (int64_t)bj0 + (t1 - t));
+}
+
+template <int M>
+__device__ __forceinline__ void dr_and_all(const uint32_t* sTab, const int* node, uint32_t* le) {
+#pragma unroll
+  for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+#pragma unroll
+  for (int k = 0; k < M; ++k) {
+    const int c = node[k] - DR_EYT;
+    const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
+    const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+    le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
+    le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+  }
+}
+
+// The same set for S-separated tiles, where only le is needed and ~96 % of the (row, block) results
+// are empty (C3): the prefixes are ANDed shortest first (keys c << 4 | k, sorted by a static
+// odd-even transposition network) and a lane stops once its AND is empty, so the later mask gathers
+// run with fewer active lanes -- fewer shared-memory wavefronts and bank conflicts.
+template <int M>
+__device__ __forceinline__ void dr_and_shortest_first(const uint32_t* sTab, const int* node, uint32_t* out) {
+  uint32_t key[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) key[k] = ((uint32_t)(node[k] - DR_EYT) << 4) | (uint32_t)k;
+#pragma unroll
+  for (int p = 0; p < M; ++p) {
+#pragma unroll
+    for (int q = p & 1; q + 1 < M; q += 2) {
+      const uint32_t lo = min(key[q], key[q + 1]), hi = max(key[q], key[q + 1]);
+      key[q] = lo;
+      key[q + 1] = hi;
+    }
+  }
+  uint32_t le[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+  bool nz = (key[0] >> 4) != 0u;   // an empty prefix empties the AND
+#pragma unroll
+  for (int s = 0; s < M; ++s) {
+    if (nz) {
+      const int c = (int)(key[s] >> 4), k = (int)(key[s] & 15u);
+      const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
+      const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+      le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
+      le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+      nz = (le[0] | le[1] | le[2] | le[3] | le[4] | le[5] | le[6] | le[7]) != 0u;
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 8; ++w) out[w] = nz ? le[w] : 0u;
+}
+
 template <int M>
 __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
   pdl_wait();
@@ -189,135 +262,146 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
   if (tid == 0) mbar_init(&sBar, 1);
   __syncthreads();
   unsigned parity = 0;
-  for (int64_t item = blockIdx.x; item < a.items; item += gridDim.x) {
-    int bi, bj0, bj1;
-    dr_decode(item, a.nb, a.ch, bi, bj0, bj1);
-    __syncthreads();   // the previous item is done with sTab / sT
-    if (tid == 0) {
-      mbar_expect_tx(&sBar, (unsigned)(M * DR_TBL_BYTES));
-      bulk_g2s(sTab, a.tables + (int64_t)bi * M * DR_TBL_WORDS, (unsigned)(M * DR_TBL_BYTES), &sBar);
-    }
-    uint32_t vI[8];
-#pragma unroll
-    for (int w = 0; w < 8; ++w) vI[w] = __ldg(a.vmask + (int64_t)bi * 8 + w);
-    const float smaxI = __ldg(a.blkmax + bi);
-    const int i0 = bi * DR_BLK;
-    // first J row's objectives while the tables land
-    float bnext[M];
-    {
-      const int j = bj0 * DR_BLK + tid;
-#pragma unroll
-      for (int k = 0; k < M; ++k) bnext[k] = j < a.R ? __ldg(a.FS + (int64_t)j * M + k) : 0.0f;
-    }
-    mbar_wait(&sBar, parity);
-    parity ^= 1u;
-    for (int bj = bj0; bj < bj1; ++bj) {
-      const int j = bj * DR_BLK + tid;
-      float b[M];
-      bool jnan = false;
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        b[k] = bnext[k];
-        jnan = jnan || (b[k] != b[k]);
-      }
-      if (bj + 1 < bj1) {   // prefetch the next J block's row
-        const int jn = j + DR_BLK;
-#pragma unroll
-        for (int k = 0; k < M; ++k) bnext[k] = jn < a.R ? __ldg(a.FS + (int64_t)jn * M + k) : 0.0f;
-      }
-      const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
-      // weak relation a_i <= b_j in every objective: AND of the prefix masks
-      int node[M];
-#pragma unroll
-      for (int k = 0; k < M; ++k) node[k] = 1;
-#pragma unroll
-      for (int s = 0; s < 9; ++s) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) {
-          const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + node[k]]);
-          node[k] = 2 * node[k] + (e <= b[k] ? 1 : 0);
+  __shared__ int sChunk;
+  int cur_bi = -1;   // block whose tables are in sTab
+  for (;;) {
+    __syncthreads();   // the previous chunk is done with sTab / sT / sChunk
+    if (tid == 0) sChunk = (int)atomicAdd(a.next, 1u);
+    __syncthreads();
+    const int64_t chunk = sChunk;
+    if (chunk >= a.items) break;
+    // chunks are taken from the END of the row-major tile order first: the short block rows at the
+    // end (a diagonal tile and a table load every few tiles) are the costliest per tile
+    const int64_t t0 = (a.items - 1 - chunk) * a.ch, t1 = min(a.pairs, t0 + a.ch);
+    for (int64_t t = t0; t < t1;) {
+      int bi, bj0, bj1;
+      dr_tile_decode(t, t1, a.nb, bi, bj0, bj1);
+      t += bj1 - bj0;
+      const bool load = bi != cur_bi;   // CTA-uniform
+      if (load) {
+        __syncthreads();   // everyone is done with the previous block's tables
+        if (tid == 0) {
+          mbar_expect_tx(&sBar, (unsigned)(M * DR_TBL_BYTES));
+          bulk_g2s(sTab, a.tables + (int64_t)bi * M * DR_TBL_WORDS, (unsigned)(M * DR_TBL_BYTES), &sBar);
         }
       }
-      uint32_t le[8];
+      uint32_t vI[8];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+      for (int w = 0; w < 8; ++w) vI[w] = __ldg(a.vmask + (int64_t)bi * 8 + w);
+      const float smaxI = __ldg(a.blkmax + bi);
+      const int i0 = bi * DR_BLK;
+      // first J row's objectives while the tables land
+      float bnext[M];
+      {
+        const int j = bj0 * DR_BLK + tid;
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const int c = node[k] - DR_EYT;
-        const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
-        const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
-        le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
-        le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+        for (int k = 0; k < M; ++k) bnext[k] = j < a.R ? __ldg(a.FS + (int64_t)j * M + k) : 0.0f;
       }
-      uint32_t out[8];
-      if (fast) {
+      if (load) {
+        mbar_wait(&sBar, parity);
+        parity ^= 1u;
+        cur_bi = bi;
+      }
+      for (int bj = bj0; bj < bj1; ++bj) {
+        const int j = bj * DR_BLK + tid;
+        float b[M];
+        bool jnan = false;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) out[w] = le[w];
-      } else {
-        // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
-        int nd[M];
+        for (int k = 0; k < M; ++k) {
+          b[k] = bnext[k];
+          jnan = jnan || (b[k] != b[k]);
+        }
+        if (bj + 1 < bj1) {   // prefetch the next J block's row
+          const int jn = j + DR_BLK;
 #pragma unroll
-        for (int k = 0; k < M; ++k) nd[k] = 1;
+          for (int k = 0; k < M; ++k) bnext[k] = jn < a.R ? __ldg(a.FS + (int64_t)jn * M + k) : 0.0f;
+        }
+        const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
+        // weak relation a_i <= b_j in every objective: AND of the prefix masks
+        int node[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) node[k] = 1;
 #pragma unroll
         for (int s = 0; s < 9; ++s) {
 #pragma unroll
           for (int k = 0; k < M; ++k) {
-            const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + nd[k]]);
-            nd[k] = 2 * nd[k] + (e < b[k] ? 1 : 0);
+            const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + node[k]]);
+            node[k] = 2 * node[k] + (e <= b[k] ? 1 : 0);
           }
         }
-        uint32_t ge[8];
+        uint32_t out[8], le[8];
+        const bool ordered = fast && M >= 4 && a.ordered_and;   // CTA-uniform
+        if (ordered) dr_and_shortest_first<M>(sTab, node, out);
+        else dr_and_all<M>(sTab, node, le);
+        if (fast && !ordered) {
 #pragma unroll
-        for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
+          for (int w = 0; w < 8; ++w) out[w] = le[w];
+        } else if (!fast) {
+          // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
+          int nd[M];
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          const int c = nd[k] - DR_EYT;
-          const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
-          const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
-          ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
-          ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
-        }
+          for (int k = 0; k < M; ++k) nd[k] = 1;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) out[w] = le[w] & ~ge[w];   // i dominates j
-        if (bi != bj) {
-          // j dominates i: transpose the per-j masks into rows i (word bj*8 + warp) by ballots
-          const bool jok = j < a.R;
+          for (int s = 0; s < 9; ++s) {
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const uint32_t rev = jok ? (ge[w] & ~le[w]) : 0u;
-            uint32_t mine = 0;
-#pragma unroll
-            for (int b2 = 0; b2 < 32; ++b2) {
-              const uint32_t bal = __ballot_sync(MO_FULL, (rev >> b2) & 1u);
-              mine = lane == b2 ? bal : mine;
+            for (int k = 0; k < M; ++k) {
+              const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + nd[k]]);
+              nd[k] = 2 * nd[k] + (e < b[k] ? 1 : 0);
             }
-            sT[(w * 32 + lane) * 9 + warp] = mine;   // row i = w*32 + lane, word warp of block bj
           }
-        }
-      }
-      if (j < a.R) dr_store(a, j, bi, out);
-      if (fast && !a.tsum) {
-        // rows i of I's last S bucket may share it with rows of J: their words of block bj lie below
-        // wend and are read by the peel, so they must hold zeros (no j of a fast tile dominates an i)
-        const int ilast = min(a.R, i0 + DR_BLK) - 1;
-        if (__ldg(a.wend + ilast) > bj * 8) {
-          const int i = i0 + tid;
-          if (i < a.R && __ldg(a.wend + i) > bj * 8) {
-            uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
-            dst[0] = make_uint4(0u, 0u, 0u, 0u);
-            dst[1] = make_uint4(0u, 0u, 0u, 0u);
-          }
-        }
-      } else if (!fast && bi != bj) {
-        __syncthreads();
-        const int i = i0 + tid;
-        if (i < a.R) {
-          uint32_t sw[8];
+          uint32_t ge[8];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) sw[w] = sT[tid * 9 + w];
-          dr_store(a, i, bj, sw);
+          for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const int c = nd[k] - DR_EYT;
+            const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
+            const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+            ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
+            ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
+          }
+#pragma unroll
+          for (int w = 0; w < 8; ++w) out[w] = le[w] & ~ge[w];   // i dominates j
+          if (bi != bj) {
+            // j dominates i: transpose the per-j masks into rows i (word bj*8 + warp) by ballots
+            const bool jok = j < a.R;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              const uint32_t rev = jok ? (ge[w] & ~le[w]) : 0u;
+              uint32_t mine = 0;
+#pragma unroll
+              for (int b2 = 0; b2 < 32; ++b2) {
+                const uint32_t bal = __ballot_sync(MO_FULL, (rev >> b2) & 1u);
+                mine = lane == b2 ? bal : mine;
+              }
+              sT[(w * 32 + lane) * 9 + warp] = mine;   // row i = w*32 + lane, word warp of block bj
+            }
+          }
         }
-        __syncthreads();
+        if (j < a.R) dr_store(a, j, bi, out);
+        if (fast && !a.tsum) {
+          // rows i of I's last S bucket may share it with rows of J: their words of block bj lie below
+          // wend and are read by the peel, so they must hold zeros (no j of a fast tile dominates an i)
+          const int ilast = min(a.R, i0 + DR_BLK) - 1;
+          if (__ldg(a.wend + ilast) > bj * 8) {
+            const int i = i0 + tid;
+            if (i < a.R && __ldg(a.wend + i) > bj * 8) {
+              uint4* dst = reinterpret_cast<uint4*>(a.bits + (int64_t)i * a.W + (int64_t)bj * 8);
+              dst[0] = make_uint4(0u, 0u, 0u, 0u);
+              dst[1] = make_uint4(0u, 0u, 0u, 0u);
+            }
+          }
+        } else if (!fast && bi != bj) {
+          __syncthreads();
+          const int i = i0 + tid;
+          if (i < a.R) {
+            uint32_t sw[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) sw[w] = sT[tid * 9 + w];
+            dr_store(a, i, bj, sw);
+          }
+          __syncthreads();
+        }
       }
     }
   }
@@ -485,6 +569,7 @@ static int launch_dom_rank_wide(const float* FS, const float* blkmin, const floa
   a.hasdom = hasdom;
   a.tsum = tsum;
   a.TW = tsum_words(R);
+  a.ordered_and = getenv("MO_DOM_PLAIN_AND") == nullptr;   // A/B switch for measurements
   a.R = (int)R;
   a.nb = nb;
   a.ch = 1;   // one (I, J) tile per item: every tile re-streams block I's m tables anyway
@@ -520,10 +605,11 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
   }
   const int64_t slots = (int64_t)sms * per_sm;
   const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
-  // ~4 items per resident CTA: each item re-loads block I's tables (M x 10 KB), so runs of J blocks
-  // amortise the copy while the item count keeps the triangular work balanced
-  int ch = (int)ceil_div(pairs, 4 * slots);
-  ch = ch < 1 ? 1 : (ch > nb ? nb : ch);
+  // equal chunks of consecutive tiles, ~12 per resident CTA, pulled from a counter: a chunk re-loads
+  // block I's tables (M x 10 KB) only where it enters a new block row, and the dynamic schedule keeps
+  // the SMs evenly loaded (static round-robin over per-row runs of 1..ch tiles left SMs 40 % idle)
+  int64_t ch = ceil_div(pairs, 12 * slots);
+  ch = ch < 2 ? 2 : ch;
   DomRankArgs a;
   a.FS = FS;
   a.blkmin = blkmin;
@@ -535,12 +621,14 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
   a.hasdom = hasdom;
   a.tsum = tsum;
   a.TW = tsum_words(R);
+  a.ordered_and = getenv("MO_DOM_PLAIN_AND") == nullptr;   // A/B switch for measurements
   a.R = (int)R;
   a.nb = nb;
-  a.ch = ch;
+  a.ch = (int)ch;
   a.W = words_per_row(R);
-  int64_t items = 0;
-  for (int bi = 0; bi < nb; ++bi) items += (nb - bi + ch - 1) / ch;
+  a.pairs = pairs;
+  a.next = vmask + (int64_t)nb * 8;
+  const int64_t items = ceil_div(pairs, ch);
   a.items = items;
   const int64_t grid = items < slots ? items : slots;
   return launch_ex(k_dom_rank<M>, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a);
