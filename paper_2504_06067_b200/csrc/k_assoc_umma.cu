@@ -18,8 +18,8 @@
 // canonical keys are computed (a full buffer is pruned, then evaluated); rows with ||f|| = 0 or
 // non-finite values go to the sliced FP32 fallback (fb_cand), as in the bf16 mma.sync filter.
 //
-// CTA (one per SM, warp-specialised, persistent over items = (256 candidate rows, a chunk of reference
-// tiles)):
+// CTA (one per SM, warp-specialised, persistent over an equal contiguous share of the (256 candidate
+// rows, reference tile) units, walked as segments of consecutive reference tiles of one row pair):
 //   warp 0        producer: 1-D bulk copies (cp.async.bulk + mbarrier complete_tx) of the pre-packed
 //                 reference tiles (128 directions x KS K16 steps of FP16, UMMA K-major no-swizzle
 //                 core-matrix layout, 4 KB per step) into a shared-memory ring (a warm-up prefix of
@@ -284,8 +284,16 @@ __device__ double ua_guess(const float (&f)[M], int Ho, int Hi) {
   return best;
 }
 
+// next segment of a CTA's unit range: row tile pair rti, reference tiles [t0, t1); advances u
+__device__ __forceinline__ void ua_segment(int64_t& u, int64_t u_end, int ntiles, int& rti, int& t0, int& t1) {
+  rti = (int)(u / ntiles);
+  t0 = (int)(u - (int64_t)rti * ntiles);
+  t1 = (int)min((int64_t)ntiles, (int64_t)t0 + (u_end - u));
+  u += t1 - t0;
+}
+
 template <int M>
-__global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int chunks, int dbg) {
+__global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int dbg) {
   constexpr int KS = ua_ks(M);
   constexpr int TILE = KS * UA_STEP_BYTES;          // one packed reference tile
   constexpr int ATILE = KS * UA_A_STEP;             // one row tile of A
@@ -299,9 +307,12 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
   const int ncand = __ldcg(a.ctl);
   const int nrt = (ncand + UA_ROWS - 1) / UA_ROWS;
   const int ntiles = (a.w + UA_N - 1) / UA_N;
-  const int per_chunk = (ntiles + chunks - 1) / chunks;
-  const int items = nrt * chunks;
-  if ((int)blockIdx.x >= items) return;   // CTA-uniform, before any barrier / TMEM use
+  // this CTA's equal, contiguous share of the nrt x ntiles (row tile pair, reference tile) units,
+  // walked as segments (row tile pair, reference tiles [t0, t1)); a row tile pair split between CTAs
+  // merges its keys by the atomicMax below
+  const int64_t units = (int64_t)nrt * ntiles;
+  const int64_t u_begin = units * blockIdx.x / gridDim.x, u_end = units * (blockIdx.x + 1) / gridDim.x;
+  if (u_begin >= u_end) return;   // CTA-uniform, before any barrier / TMEM use
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ua_dyn) + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = base;                              // 2 row tiles x KS steps
@@ -338,9 +349,9 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
     if (lane == 0) {
       int s = 0;
       unsigned ph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int ch = item % chunks;
-        const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
+      for (int64_t u = u_begin; u < u_end;) {
+        int rti, t0, t1;
+        ua_segment(u, u_end, ntiles, rti, t0, t1);
         const int wu = a.ref_Ho > 0 ? 0 : min(UA_WARM, t1 - t0);
         for (int ti = 0; ti < wu + (t1 - t0); ++ti) {
           const int t = ti < wu ? t0 + ti : t0 + ti - wu;
@@ -362,9 +373,9 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
       int buf = 0;
       unsigned tph = 0;
       const uint32_t abase = smem_addr(sA), bbase = smem_addr(sB);
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int ch = item % chunks;
-        const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
+      for (int64_t u = u_begin; u < u_end;) {
+        int rti, t0, t1;
+        ua_segment(u, u_end, ntiles, rti, t0, t1);
         mbar_wait(&sAReady, aph);
         aph ^= 1u;
         tc_fence_after();
@@ -403,10 +414,10 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
     const int r = q * 32 + lane;            // row within each row tile
     const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
     int gt = 0;                             // tiles of all items so far (the MMA issuer's buffer counter)
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
-      const int rb = (item / chunks) * UA_ROWS;
-      const int ch = item % chunks;
-      const int t0 = ch * per_chunk, t1 = min(ntiles, t0 + per_chunk);
+    for (int64_t u = u_begin; u < u_end;) {
+      int rti, t0, t1;
+      ua_segment(u, u_end, ntiles, rti, t0, t1);
+      const int rb = rti * UA_ROWS;
       int row[2];
       bool act[2];
       float marg[2], nrm[2];
@@ -429,7 +440,7 @@ __global__ void __launch_bounds__(UA_THREADS, 1) k_assoc_umma(AssocArgs a, int c
         const float norm = sqrtf(nn);
         const bool ok = fin && mx > 0.0f && isfinite(norm);
         if (act[rt] && !ok) {
-          if (ch == 0 && cgp == rt && grp == 0) {
+          if (t0 == 0 && cgp == rt && grp == 0) {   // once per row: the segment with tile 0
             a.fb_cand[atomicAdd(a.fb_ctl, 1)] = row[rt];
             atomicAdd(const_cast<int*>(a.info) + MO_INFO_ASSOC_FALLBACK, 1);
           }
@@ -596,14 +607,6 @@ int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // items = (256-row tile, reference chunk).  Every item restarts its rows' running maxima, and each
-  // new maximum costs a candidate record, so rows keep all their references in one item (chunks = 1)
-  // unless there are too few row tiles for ~2 items per CTA
-  const int64_t nrt = ceil_div(R, (int64_t)UA_ROWS);
-  const int64_t ntiles = ceil_div((int64_t)a.w, (int64_t)UA_N);
-  int64_t chunks = ceil_div((int64_t)sms * 2, nrt);
-  if (chunks > ntiles / 8) chunks = ntiles / 8;
-  if (chunks < 1) chunks = 1;
   const dim3 grid((unsigned)sms), blk(UA_THREADS);
   switch (m) {
 #define MO_UA_CASE(MM)                                                                                      \
@@ -614,7 +617,7 @@ int launch_assoc_umma(const AssocArgs& a, int m, int64_t R, cudaStream_t s) {
         return MO_ERR_CUDA;                                                                                 \
       attr[MM] = true;                                                                                      \
     }                                                                                                       \
-    MO_TRY(launch_ex(k_assoc_umma<MM>, grid, blk, ua_smem(ua_ks(MM)), s, false, g_mo_pdl, a, (int)chunks, dbg)); \
+    MO_TRY(launch_ex(k_assoc_umma<MM>, grid, blk, ua_smem(ua_ks(MM)), s, false, g_mo_pdl, a, dbg));          \
     break;
     MO_UA_CASE(2) MO_UA_CASE(3) MO_UA_CASE(4) MO_UA_CASE(5) MO_UA_CASE(6) MO_UA_CASE(7) MO_UA_CASE(8)
     MO_UA_CASE(9) MO_UA_CASE(10) MO_UA_CASE(11) MO_UA_CASE(12) MO_UA_CASE(13) MO_UA_CASE(14)
