@@ -148,6 +148,7 @@ struct DomRankArgs {
   uint32_t* tsum;          // nullable: tile summary (then zero word blocks are not stored)
   int64_t TW;
   int ordered_and;         // S-separated tiles: AND the prefixes shortest first with early exit
+  uint32_t two;            // 2, opaque to the compiler (see dr_search)
   int64_t pairs;           // k_dom_rank<M>: tiles of the block upper triangle (row-major), chunks of ch
   unsigned* next;          // k_dom_rank<M>: chunk counter (zeroed by k_dom_tables)
 };
@@ -184,6 +185,38 @@ __device__ __forceinline__ void dr_decode(int64_t t, int nb, int ch, int& bi, in
   const int64_t off = t - (Gn - dr_G(nb - bi, ch));
   bj0 = bi + (int)off * ch;
   bj1 = min(nb, bj0 + ch);
+}
+
+// The m Eytzinger searches of one row: node[k] = 512 + #{values of objective k <= b[k]} (STRICT: < b[k]).
+// The walk carries shared addresses, ad = base + 4 node, so a probe is one load, one compare, one
+// select of two constants and one multiply-add: ad' = 2 ad - base + 4 [go] = base + 4 (2 node + go);
+// the per-objective table offset k * DR_TBL_BYTES folds into the load's immediate.  `two` (= 2) comes
+// from the kernel arguments so that ptxas keeps the multiply-add on the FMA pipe (IMAD) instead of an
+// ALU IADD3: the sweep is ALU-pipe bound, and the compare and select already sit there.
+template <int M, bool STRICT>
+__device__ __forceinline__ void dr_search(uint32_t base, uint32_t two, const float* b, int* node) {
+  const uint32_t c0 = 0u - base, c1 = 4u - base;
+  uint32_t ad[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) ad[k] = base + 4u;
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      float e;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e) : "r"(ad[k] + (uint32_t)(k * DR_TBL_BYTES)));
+      if (STRICT)
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p mad.lo.u32 %0, %0, %3, %4;\n\t"
+            "@!p mad.lo.u32 %0, %0, %3, %5;\n\t}"
+            : "+r"(ad[k]) : "f"(e), "f"(b[k]), "r"(two), "r"(c1), "r"(c0));
+      else
+        asm("{\n\t.reg .pred p;\n\tsetp.le.f32 p, %1, %2;\n\t@p mad.lo.u32 %0, %0, %3, %4;\n\t"
+            "@!p mad.lo.u32 %0, %0, %3, %5;\n\t}"
+            : "+r"(ad[k]) : "f"(e), "f"(b[k]), "r"(two), "r"(c1), "r"(c0));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) node[k] = (int)((ad[k] - base) >> 2);
 }
 
 // le = AND_k P_k[c_k] (c_k = node[k] - DR_EYT): a_i <= b_j in every objective
@@ -253,7 +286,7 @@ __device__ __forceinline__ void dr_and_shortest_first(const uint32_t* sTab, cons
 }
 
 template <int M>
-__global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
+__global__ void __launch_bounds__(DR_BLK, 2) k_dom_rank(DomRankArgs a) {
   pdl_wait();
   extern __shared__ __align__(128) uint32_t sTab[];   // M tables of block I
   __shared__ __align__(8) uint64_t sBar;
@@ -319,16 +352,7 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
         const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
         // weak relation a_i <= b_j in every objective: AND of the prefix masks
         int node[M];
-#pragma unroll
-        for (int k = 0; k < M; ++k) node[k] = 1;
-#pragma unroll
-        for (int s = 0; s < 9; ++s) {
-#pragma unroll
-          for (int k = 0; k < M; ++k) {
-            const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + node[k]]);
-            node[k] = 2 * node[k] + (e <= b[k] ? 1 : 0);
-          }
-        }
+        dr_search<M, false>(smem_addr(sTab), a.two, b, node);
         uint32_t out[8], le[8];
         const bool ordered = fast && M >= 4 && a.ordered_and;   // CTA-uniform
         if (ordered) dr_and_shortest_first<M>(sTab, node, out);
@@ -339,16 +363,7 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_rank(DomRankArgs a) {
         } else if (!fast) {
           // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
           int nd[M];
-#pragma unroll
-          for (int k = 0; k < M; ++k) nd[k] = 1;
-#pragma unroll
-          for (int s = 0; s < 9; ++s) {
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
-              const float e = __uint_as_float(sTab[k * DR_TBL_WORDS + nd[k]]);
-              nd[k] = 2 * nd[k] + (e < b[k] ? 1 : 0);
-            }
-          }
+          dr_search<M, true>(smem_addr(sTab), a.two, b, nd);
           uint32_t ge[8];
 #pragma unroll
           for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
@@ -585,14 +600,9 @@ size_t dom_rank_tables_bytes(int64_t R, int m) {
   return (size_t)nb * (size_t)m * DR_TBL_BYTES + (size_t)nb * 8 * 4 + 256;
 }
 
+// resident CTAs of k_dom_rank<M> per SM (attributes set once per instantiation)
 template <int M>
-static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
-                             uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum) {
-  const int nb = (int)dom_rank_blocks(R);
-  uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
-  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M,
-                   tsum));
-  const size_t smem = (size_t)M * DR_TBL_BYTES;
+static int dom_rank_slots(size_t smem, int64_t& slots) {
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
     if (cudaFuncSetAttribute(k_dom_rank<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -603,13 +613,34 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dom_rank<M>, DR_BLK, smem);
     if (per_sm < 1) per_sm = 1;
   }
-  const int64_t slots = (int64_t)sms * per_sm;
-  const int64_t pairs = (int64_t)nb * (nb + 1) / 2;
-  // equal chunks of consecutive tiles, ~12 per resident CTA, pulled from a counter: a chunk re-loads
-  // block I's tables (M x 10 KB) only where it enters a new block row, and the dynamic schedule keeps
-  // the SMs evenly loaded (static round-robin over per-row runs of 1..ch tiles left SMs 40 % idle)
-  int64_t ch = ceil_div(pairs, 12 * slots);
+  slots = (int64_t)sms * per_sm;
+  return MO_OK;
+}
+
+template <int M>
+static int launch_dom_rank_mg(DomRankArgs a, cudaStream_t s) {
+  const size_t smem = (size_t)M * DR_TBL_BYTES;
+  int64_t slots = 0;
+  if (const int e = dom_rank_slots<M>(smem, slots)) return e;
+  // equal chunks of consecutive tiles, ~12 per resident CTA, pulled from a counter: a chunk
+  // re-loads block I's tables (M x 10 KB) only where it enters a new block row, and the dynamic
+  // schedule keeps the SMs evenly loaded (static round-robin over per-row runs of 1..ch tiles left SMs
+  // 40 % idle)
+  int64_t ch = ceil_div(a.pairs, 12 * slots);
   ch = ch < 2 ? 2 : ch;
+  a.ch = (int)ch;
+  a.items = ceil_div(a.pairs, ch);
+  const int64_t grid = a.items < slots ? a.items : slots;
+  return launch_ex(k_dom_rank<M>, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a);
+}
+
+template <int M>
+static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R,
+                             uint32_t* bits, uint8_t* hasdom, uint32_t* tables, cudaStream_t s, uint32_t* tsum) {
+  const int nb = (int)dom_rank_blocks(R);
+  uint32_t* vmask = tables + (int64_t)nb * M * DR_TBL_WORDS;
+  MO_TRY(launch_ex(k_dom_tables<M>, dim3(nb, M), dim3(DR_BLK), 0, s, false, g_mo_pdl, FS, (int)R, tables, vmask, M,
+                   tsum));
   DomRankArgs a;
   a.FS = FS;
   a.blkmin = blkmin;
@@ -622,16 +653,13 @@ static int launch_dom_rank_m(const float* FS, const float* blkmin, const float* 
   a.tsum = tsum;
   a.TW = tsum_words(R);
   a.ordered_and = getenv("MO_DOM_PLAIN_AND") == nullptr;   // A/B switch for measurements
+  a.two = 2u;
   a.R = (int)R;
   a.nb = nb;
-  a.ch = (int)ch;
   a.W = words_per_row(R);
-  a.pairs = pairs;
+  a.pairs = (int64_t)nb * (nb + 1) / 2;
   a.next = vmask + (int64_t)nb * 8;
-  const int64_t items = ceil_div(pairs, ch);
-  a.items = items;
-  const int64_t grid = items < slots ? items : slots;
-  return launch_ex(k_dom_rank<M>, dim3((unsigned)grid), dim3(DR_BLK), smem, s, false, g_mo_pdl, a);
+  return launch_dom_rank_mg<M>(a, s);
 }
 
 int launch_dom_rank(const float* FS, const float* blkmin, const float* blkmax, const int* wend, int64_t R, int m,
