@@ -31,6 +31,7 @@
 #include "mo_common.cuh"
 #include "k_dominance_args.cuh"
 #include "mo_async.cuh"
+#include "mo_sortnet.cuh"
 
 namespace mo {
 
@@ -39,7 +40,7 @@ constexpr int DR_EYT = 512;                        // Eytzinger slots (1..511 us
 constexpr int DR_MASKS = DR_BLK + 1;               // prefix masks c = 0..256
 constexpr int DR_TBL_WORDS = DR_EYT + DR_MASKS * 8;
 constexpr int DR_TBL_BYTES = DR_TBL_WORDS * 4;     // 10,272 (16-byte multiple)
-static_assert(DR_TBL_BYTES % 16 == 0, "bulk copies move 16-byte multiples");
+static_assert(DR_TBL_BYTES % 32 == 0, "bulk copies move 16-byte multiples; prefix-mask slot pairs are 32-byte aligned");
 
 __host__ __device__ inline int64_t dom_rank_blocks(int64_t R) { return (R + DR_BLK - 1) / DR_BLK; }
 
@@ -248,34 +249,43 @@ __device__ __forceinline__ void dr_and_all(const uint32_t* sTab, const int* node
   }
 }
 
+__host__ __device__ constexpr int dr_pow2(int m) { return m <= 1 ? 1 : 2 * dr_pow2((m + 1) / 2); }
+
 // The same set for S-separated tiles, where only le is needed and ~96 % of the (row, block) results
-// are empty (C3): the prefixes are ANDed shortest first (keys c << 4 | k, sorted by a static
-// odd-even transposition network) and a lane stops once its AND is empty, so the later mask gathers
-// run with fewer active lanes -- fewer shared-memory wavefronts and bank conflicts.
+// are empty (C3): the prefixes are ANDed shortest first and a lane stops once its AND is empty, so the
+// later mask gathers run with fewer active lanes -- fewer shared-memory wavefronts and bank conflicts.
+// Sort keys are c << 18 | (byte offset of half 0 of P_k[c] in the tables), so the loop needs no
+// swizzle arithmetic: half 1 sits at offset ^ 16 (mask_slot pairs the slots 2c, 2c + 1 and every table
+// starts on a 32-byte boundary).  Batcher's odd-even merge network over the keys padded to a power of
+// two with all-ones keys (the compiler folds the comparators that touch padding): 32 comparators at
+// m = 10 instead of 45 for odd-even transposition; the sweep is ALU-pipe bound.
 template <int M>
-__device__ __forceinline__ void dr_and_shortest_first(const uint32_t* sTab, const int* node, uint32_t* out) {
-  uint32_t key[M];
+__device__ __forceinline__ void dr_and_shortest_first(uint32_t sbase, const int* node, uint32_t* out) {
+  constexpr int N = dr_pow2(M);
+  uint32_t key[N];
 #pragma unroll
-  for (int k = 0; k < M; ++k) key[k] = ((uint32_t)(node[k] - DR_EYT) << 4) | (uint32_t)k;
-#pragma unroll
-  for (int p = 0; p < M; ++p) {
-#pragma unroll
-    for (int q = p & 1; q + 1 < M; q += 2) {
-      const uint32_t lo = min(key[q], key[q + 1]), hi = max(key[q], key[q + 1]);
-      key[q] = lo;
-      key[q + 1] = hi;
+  for (int k = 0; k < N; ++k) {
+    if (k < M) {
+      const uint32_t c = (uint32_t)(node[k] - DR_EYT);
+      key[k] = (c << 18) | (uint32_t)(k * DR_TBL_BYTES + DR_EYT * 4 + 16 * mask_slot((int)c, 0));
+    } else {
+      key[k] = 0xffffffffu;
     }
   }
+  sortnet<N>(key);
   uint32_t le[8];
 #pragma unroll
   for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
-  bool nz = (key[0] >> 4) != 0u;   // an empty prefix empties the AND
+  bool nz = (key[0] >> 18) != 0u;   // an empty prefix empties the AND
 #pragma unroll
   for (int s = 0; s < M; ++s) {
     if (nz) {
-      const int c = (int)(key[s] >> 4), k = (int)(key[s] & 15u);
-      const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
-      const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
+      const uint32_t off = key[s] & 0x3ffffu;
+      uint4 h0, h1;
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(h0.x), "=r"(h0.y), "=r"(h0.z), "=r"(h0.w) : "r"(sbase + off));
+      asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(h1.x), "=r"(h1.y), "=r"(h1.z), "=r"(h1.w) : "r"(sbase + (off ^ 16u)));
       le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
       le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
       nz = (le[0] | le[1] | le[2] | le[3] | le[4] | le[5] | le[6] | le[7]) != 0u;
@@ -355,7 +365,7 @@ __global__ void __launch_bounds__(DR_BLK, 2) k_dom_rank(DomRankArgs a) {
         dr_search<M, false>(smem_addr(sTab), a.two, b, node);
         uint32_t out[8], le[8];
         const bool ordered = fast && M >= 4 && a.ordered_and;   // CTA-uniform
-        if (ordered) dr_and_shortest_first<M>(sTab, node, out);
+        if (ordered) dr_and_shortest_first<M>(smem_addr(sTab), node, out);
         else dr_and_all<M>(sTab, node, le);
         if (fast && !ordered) {
 #pragma unroll
