@@ -284,7 +284,7 @@ def time_kernels(torch, eng, _lib):
 # (workload, sort) -> (kernel name prefix, committed `ncu --set full` raw export under profiles/)
 TRAFFIC_CAPTURES = {
     ("c2", "bits"): ("k_dom_rank<5", "r02_ncu_full_c2_domrank_raw.csv"),
-    ("c3", "bits"): ("k_dom_rank<10", "r02_ncu_full_c3_domrank_raw.csv"),
+    ("c3", "bits"): ("k_dom_rank<10", "r02c_ncu_full_c3_domrank_raw.csv"),
     ("c4", "stream"): ("k_stream_tiles<3, 0>", "r01_ncu_full_c4_count_raw.csv"),
 }
 _UNITS = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -574,7 +574,9 @@ def main():
                 "peak_source": "measured: k_peak_smem conflict-free ld.shared.v4 bandwidth (148 SMs x 128 B/clk "
                                "nominal); MEASURED_PEAKS.json has HBM and tensor peaks only",
                 "algorithmic": (f"{pairs:.4e} (row, 256-row block) pairs x m = {m} x (32 B mask + 36 B search) = "
-                                f"{smem_bytes:.4e} B of shared-memory reads per launch")}
+                                f"{smem_bytes:.4e} B of shared-memory reads per launch"),
+                "binding_unit": ("ALU pipe (ncu --set full at C3 after the load-balanced schedule: ALU ~80 % of "
+                                 "peak, issue ~70 %); frac is against the shared-memory read roofline")}
         launches = K * (8 + assoc_kernels)   # + k_dom_tables
     roof["traffic"] = traffic
     roof["traffic_note"] = ("DRAM bytes per launch (read + write) of the dominant kernel from the committed ncu "
