@@ -88,7 +88,17 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "20", "-f", self.path],
                                          stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
-            time.sleep(0.3)   # let the sampler start before the timed region
+            # the timed region must see samples: wait for nvidia-smi's first line (its start-up can take
+            # well over the 20 ms period on a fresh box), then one more period
+            t0 = time.time()
+            while time.time() - t0 < 10.0:
+                try:
+                    if os.path.getsize(self.path) > 0:
+                        break
+                except OSError:
+                    pass
+                time.sleep(0.02)
+            time.sleep(0.05)
         except FileNotFoundError:
             self.proc = None
         return self

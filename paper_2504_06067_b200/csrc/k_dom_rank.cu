@@ -188,16 +188,15 @@ __device__ __forceinline__ void dr_decode(int64_t t, int nb, int ch, int& bi, in
   bj1 = min(nb, bj0 + ch);
 }
 
-// The m Eytzinger searches of one row: node[k] = 512 + #{values of objective k <= b[k]} (STRICT: < b[k]).
-// The walk carries shared addresses, ad = base + 4 node, so a probe is one load, one compare, one
+// The m Eytzinger searches of one row, returned as shared addresses ad[k] = base + 4 node[k] with
+// node[k] = 512 + #{values of objective k <= b[k]} (STRICT: < b[k]).  The walk carries the addresses, so a probe is one load, one compare, one
 // select of two constants and one multiply-add: ad' = 2 ad - base + 4 [go] = base + 4 (2 node + go);
 // the per-objective table offset k * DR_TBL_BYTES folds into the load's immediate.  `two` (= 2) comes
 // from the kernel arguments so that ptxas keeps the multiply-add on the FMA pipe (IMAD) instead of an
 // ALU IADD3: the sweep is ALU-pipe bound, and the compare and select already sit there.
 template <int M, bool STRICT>
-__device__ __forceinline__ void dr_search(uint32_t base, uint32_t two, const float* b, int* node) {
+__device__ __forceinline__ void dr_search(uint32_t base, uint32_t two, const float* b, uint32_t* ad) {
   const uint32_t c0 = 0u - base, c1 = 4u - base;
-  uint32_t ad[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) ad[k] = base + 4u;
 #pragma unroll
@@ -216,11 +215,8 @@ __device__ __forceinline__ void dr_search(uint32_t base, uint32_t two, const flo
             : "+r"(ad[k]) : "f"(e), "f"(b[k]), "r"(two), "r"(c1), "r"(c0));
     }
   }
-#pragma unroll
-  for (int k = 0; k < M; ++k) node[k] = (int)((ad[k] - base) >> 2);
 }
 
-// le = AND_k P_k[c_k] (c_k = node[k] - DR_EYT): a_i <= b_j in every objective
 // tile t of the row-major upper block triangle (row bi holds tiles (bi, bi..nb-1), offset
 // off(bi) = bi nb - bi (bi - 1) / 2) -> block row bi and the J run [bj0, bj1) up to the row end or t1
 __device__ __forceinline__ void dr_tile_decode(int64_t t, int64_t t1, int nb, int& bi, int& bj0, int& bj1) {
@@ -235,17 +231,22 @@ __device__ __forceinline__ void dr_tile_decode(int64_t t, int64_t t1, int nb, in
   bj1 = (int)min((int64_t)nb, (int64_t)bj0 + (t1 - t));
 }
 
-template <int M>
-__device__ __forceinline__ void dr_and_all(const uint32_t* sTab, const int* node, uint32_t* le) {
-#pragma unroll
-  for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+// le = AND_k P_k[c_k] (c_k = node[k] - DR_EYT, from the search addresses): a_i <= b_j (INV: the
+// complement of the strict prefixes, a_i >= b_j) in every objective
+template <int M, bool INV>
+__device__ __forceinline__ void dr_and_all(const uint32_t* sTab, uint32_t base, const uint32_t* ad, uint32_t* le) {
 #pragma unroll
   for (int k = 0; k < M; ++k) {
-    const int c = node[k] - DR_EYT;
+    const int c = (int)((ad[k] - base) >> 2) - DR_EYT;
     const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
     const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
-    le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
-    le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+    if (INV) {
+      le[0] &= ~h0.x; le[1] &= ~h0.y; le[2] &= ~h0.z; le[3] &= ~h0.w;
+      le[4] &= ~h1.x; le[5] &= ~h1.y; le[6] &= ~h1.z; le[7] &= ~h1.w;
+    } else {
+      le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
+      le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
+    }
   }
 }
 
@@ -260,14 +261,16 @@ __host__ __device__ constexpr int dr_pow2(int m) { return m <= 1 ? 1 : 2 * dr_po
 // two with all-ones keys (the compiler folds the comparators that touch padding): 32 comparators at
 // m = 10 instead of 45 for odd-even transposition; the sweep is ALU-pipe bound.
 template <int M>
-__device__ __forceinline__ void dr_and_shortest_first(uint32_t sbase, const int* node, uint32_t* out) {
+__device__ __forceinline__ void dr_and_shortest_first(uint32_t sbase, const uint32_t* ad, uint32_t* out) {
   constexpr int N = dr_pow2(M);
   uint32_t key[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) {
     if (k < M) {
-      const uint32_t c = (uint32_t)(node[k] - DR_EYT);
-      key[k] = (c << 18) | (uint32_t)(k * DR_TBL_BYTES + DR_EYT * 4 + 16 * mask_slot((int)c, 0));
+      // q = ad - base - 2048 = 4c: c << 18 | 16 slot0 = q (2^16 + 8) + (q & 16) with slot0 = 2c + ((c >> 2) & 1)
+      // (mask_slot), and the table offset K has bit 4 clear -- one IADD, one LOP3, one IMAD
+      const uint32_t q = ad[k] - (sbase + DR_EYT * 4u);
+      key[k] = q * 65544u + ((q & 16u) | (uint32_t)(k * DR_TBL_BYTES + DR_EYT * 4));
     } else {
       key[k] = 0xffffffffu;
     }
@@ -361,30 +364,29 @@ __global__ void __launch_bounds__(DR_BLK, 2) k_dom_rank(DomRankArgs a) {
         }
         const bool fast = bi < bj && smaxI < __ldg(a.blkmin + bj);   // CTA-uniform
         // weak relation a_i <= b_j in every objective: AND of the prefix masks
-        int node[M];
-        dr_search<M, false>(smem_addr(sTab), a.two, b, node);
+        const uint32_t sbase = smem_addr(sTab);
+        uint32_t ad[M];
+        dr_search<M, false>(sbase, a.two, b, ad);
         uint32_t out[8], le[8];
         const bool ordered = fast && M >= 4 && a.ordered_and;   // CTA-uniform
-        if (ordered) dr_and_shortest_first<M>(smem_addr(sTab), node, out);
-        else dr_and_all<M>(sTab, node, le);
+        if (ordered) {
+          dr_and_shortest_first<M>(sbase, ad, out);
+        } else {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
+          dr_and_all<M, false>(sTab, sbase, ad, le);
+        }
         if (fast && !ordered) {
 #pragma unroll
           for (int w = 0; w < 8; ++w) out[w] = le[w];
         } else if (!fast) {
           // reverse weak relation a_i >= b_j: complement of the strict prefix #{a_i < b_j}
-          int nd[M];
-          dr_search<M, true>(smem_addr(sTab), a.two, b, nd);
+          uint32_t nd[M];
+          dr_search<M, true>(sbase, a.two, b, nd);
           uint32_t ge[8];
 #pragma unroll
           for (int w = 0; w < 8; ++w) ge[w] = jnan ? 0u : vI[w];
-#pragma unroll
-          for (int k = 0; k < M; ++k) {
-            const int c = nd[k] - DR_EYT;
-            const uint4* P = reinterpret_cast<const uint4*>(sTab + k * DR_TBL_WORDS + DR_EYT);
-            const uint4 h0 = P[mask_slot(c, 0)], h1 = P[mask_slot(c, 1)];
-            ge[0] &= ~h0.x; ge[1] &= ~h0.y; ge[2] &= ~h0.z; ge[3] &= ~h0.w;
-            ge[4] &= ~h1.x; ge[5] &= ~h1.y; ge[6] &= ~h1.z; ge[7] &= ~h1.w;
-          }
+          dr_and_all<M, true>(sTab, sbase, nd, ge);
 #pragma unroll
           for (int w = 0; w < 8; ++w) out[w] = le[w] & ~ge[w];   // i dominates j
           if (bi != bj) {
