@@ -276,10 +276,11 @@ __device__ __forceinline__ void dr_and_shortest_first(uint32_t sbase, const uint
     }
   }
   sortnet<N>(key);
+  bool nz = (key[0] >> 18) != 0u;   // an empty prefix empties the AND
+  const uint32_t ones = nz ? 0xffffffffu : 0u;
   uint32_t le[8];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) le[w] = 0xffffffffu;
-  bool nz = (key[0] >> 18) != 0u;   // an empty prefix empties the AND
+  for (int w = 0; w < 8; ++w) le[w] = ones;
 #pragma unroll
   for (int s = 0; s < M; ++s) {
     if (nz) {
@@ -291,11 +292,12 @@ __device__ __forceinline__ void dr_and_shortest_first(uint32_t sbase, const uint
                    : "=r"(h1.x), "=r"(h1.y), "=r"(h1.z), "=r"(h1.w) : "r"(sbase + (off ^ 16u)));
       le[0] &= h0.x; le[1] &= h0.y; le[2] &= h0.z; le[3] &= h0.w;
       le[4] &= h1.x; le[5] &= h1.y; le[6] &= h1.z; le[7] &= h1.w;
-      nz = (le[0] | le[1] | le[2] | le[3] | le[4] | le[5] | le[6] | le[7]) != 0u;
+      // the shortest prefix alone (c >= 1) is never empty; from the second objective on, stop at empty
+      if (s > 0) nz = (le[0] | le[1] | le[2] | le[3] | le[4] | le[5] | le[6] | le[7]) != 0u;
     }
   }
 #pragma unroll
-  for (int w = 0; w < 8; ++w) out[w] = nz ? le[w] : 0u;
+  for (int w = 0; w < 8; ++w) out[w] = le[w];   // zero whenever the walk stopped early
 }
 
 template <int M>
