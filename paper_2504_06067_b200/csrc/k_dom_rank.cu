@@ -81,25 +81,41 @@ __global__ void __launch_bounds__(DR_BLK) k_dom_tables(const float* __restrict__
     const uint32_t bal = __ballot_sync(MO_FULL, ok);
     if (lane == 0) vmask[(int64_t)bi * 8 + warp] = bal;
   }
-  __syncthreads();
-  // bitonic sort of (key, idx), ascending
+  // bitonic sort of (key, idx), ascending, one element per thread: strides < 32 exchange through warp
+  // shuffles, only the 6 stages with stride >= 32 go through shared memory (12 barriers instead of 36).
+  // Ties may land in any order: every count c the sweep looks up (#{a <= b}, #{a < b}) ends on a
+  // tie-group boundary, where the prefix P[c] does not depend on the order inside the group.
+  uint32_t key = sKey[t];
+  int idx = t;
+#pragma unroll
   for (int size = 2; size <= DR_BLK; size <<= 1) {
+#pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const int p = t ^ stride;
-      if (p > t) {
-        const bool up = (t & size) == 0;
-        const uint32_t a = sKey[t], b = sKey[p];
-        if ((a > b) == up) {
-          sKey[t] = b;
-          sKey[p] = a;
-          const int ia = sIdx[t];
-          sIdx[t] = sIdx[p];
-          sIdx[p] = ia;
-        }
+      uint32_t ok;
+      int oi;
+      if (stride >= 32) {
+        __syncthreads();   // previous readers of sKey / sIdx are done
+        sKey[t] = key;
+        sIdx[t] = idx;
+        __syncthreads();
+        ok = sKey[t ^ stride];
+        oi = sIdx[t ^ stride];
+      } else {
+        ok = __shfl_xor_sync(MO_FULL, key, stride);
+        oi = __shfl_xor_sync(MO_FULL, idx, stride);
       }
-      __syncthreads();
+      const bool up = (t & size) == 0, lower = (t & stride) == 0;
+      const uint32_t lo = lower ? key : ok, hi = lower ? ok : key;
+      if (up ? lo > hi : lo < hi) {   // both partners decide on the same (lo, hi): they swap together
+        key = ok;
+        idx = oi;
+      }
     }
   }
+  __syncthreads();
+  sKey[t] = key;
+  sIdx[t] = idx;
+  __syncthreads();
   uint32_t* tab = tables + ((int64_t)bi * m + k) * DR_TBL_WORDS;
   // Eytzinger: node n at depth d holds sorted position ((2 (n - 2^d) + 1) << (8 - d)) - 1
   for (int n = t; n < DR_EYT; n += DR_BLK) {
